@@ -1,0 +1,228 @@
+"""CPU oracle for the gsplat hot path (arXiv 2409.06765) -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2409_06765_b200`` never imports it, and the two share no code: this
+wrapper marshals numpy arrays into ``liboracle`` (``gs_oracle.c``) and nothing
+else.  See the header of ``gs_oracle.c`` for what each function follows in the
+paper, and DESIGN.md "Oracle pins" for what pins each one.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gs_oracle.c")
+_LIB = os.path.join(_HERE, "libgs_oracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-Wall"]
+
+
+def build(force: bool = False) -> str:
+    """Compile gs_oracle.c (plain C, OpenMP) into oracle/libgs_oracle.so."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class OrOpts(ct.Structure):
+    _fields_ = [
+        ("near_plane", ct.c_double), ("far_plane", ct.c_double), ("eps2d", ct.c_double),
+        ("alpha_max", ct.c_double), ("alpha_min", ct.c_double), ("t_min", ct.c_double),
+        ("amb_rel_alpha", ct.c_double), ("amb_rel_t", ct.c_double),
+        ("tile_size", ct.c_int32), ("antialiased", ct.c_int32), ("sh_degree", ct.c_int32),
+        ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("pad_", ct.c_int32),
+    ]
+
+
+@dataclass
+class Options:
+    """Constants of the method.  Duplicated, not shared, with the
+    CUDA path's gs_options; tests/test_constants.py cross-checks the two tables."""
+    near_plane: float = 0.01       # S:196, Q18
+    far_plane: float = 1e10
+    eps2d: float = 0.3
+    alpha_max: float = 0.99        # north_star "opacity saturation at 0.99" (Q13)
+    alpha_min: float = 1.0 / 255.0  # Q14
+    t_min: float = 1e-4            # Q15
+    amb_rel_alpha: float = 1e-4    # ambiguity margins for parity masks
+    amb_rel_t: float = 1e-3
+    tile_size: int = 16
+    antialiased: int = 0
+    sh_degree: int = 3
+    bbox_mode: int = 0
+    fov_clamp: int = 1
+
+    def c(self) -> OrOpts:
+        return OrOpts(self.near_plane, self.far_plane, self.eps2d, self.alpha_max, self.alpha_min,
+                      self.t_min, self.amb_rel_alpha, self.amb_rel_t, self.tile_size, self.antialiased,
+                      self.sh_degree, self.bbox_mode, self.fov_clamp, 0)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ct.CDLL(build())
+        P = ct.c_void_p
+        i64, i32, dbl = ct.c_int64, ct.c_int32, ct.c_double
+        _lib.or_project.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32, P, P] + [P] * 9
+        _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
+        _lib.or_isect.restype = i64
+        _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 9 + [P] * 6
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 9 + [P] * 6
+        _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6
+        _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
+        _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
+        _lib.or_quat_to_rotmat.argtypes = [P, P]
+        _lib.or_num_threads.restype = i32
+        _lib.or_set_num_threads.argtypes = [i32]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ct.c_void_p)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def num_threads() -> int:
+    return lib().or_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    lib().or_set_num_threads(int(n))
+
+
+def sh_basis(deg, d):
+    Y = np.zeros(16)
+    lib().or_sh_basis(deg, float(d[0]), float(d[1]), float(d[2]), _p(Y))
+    return Y[: (deg + 1) ** 2]
+
+
+def sh_basis_grad(deg, d):
+    g = np.zeros((16, 3))
+    lib().or_sh_basis_grad(deg, float(d[0]), float(d[1]), float(d[2]), _p(g))
+    return g[: (deg + 1) ** 2]
+
+
+def quat_to_rotmat(q):
+    R = np.zeros((3, 3))
+    lib().or_quat_to_rotmat(_p(_f64(q)), _p(R))
+    return R
+
+
+def _scene_arrays(scene):
+    means = _f32(scene["means"]); quats = _f32(scene["quats"]); scales = _f32(scene["scales"])
+    opac = _f32(scene["opacities"]); colors = _f32(scene["colors"])
+    viewmats = _f32(scene["viewmats"]); Ks = _f32(scene["Ks"])
+    return means, quats, scales, opac, colors, viewmats, Ks
+
+
+def project(scene, opts: Options):
+    """F1-F15 for every (camera, Gaussian).  Returns dense [C, N, ...] arrays."""
+    means, quats, scales, opac, colors, viewmats, Ks = _scene_arrays(scene)
+    N, C = means.shape[0], viewmats.shape[0]
+    W, H = int(scene["width"]), int(scene["height"])
+    K = colors.shape[1] if colors.ndim == 3 else 1
+    out = dict(
+        radii=np.zeros((C, N, 2), np.int32), mean2d_f=np.zeros((C, N, 2), np.float32),
+        depth_f=np.zeros((C, N), np.float32), mean2d=np.zeros((C, N, 2)), depth=np.zeros((C, N)),
+        conic=np.zeros((C, N, 3)), comp=np.zeros((C, N)), opac_eff=np.zeros((C, N)),
+        rgb=np.zeros((C, N, 3)))
+    o = opts.c()
+    lib().or_project(ct.byref(o), N, C, W, H, _p(means), _p(quats), _p(scales), _p(opac), _p(colors), K,
+                     _p(viewmats), _p(Ks), _p(out["radii"]), _p(out["mean2d_f"]), _p(out["depth_f"]),
+                     _p(out["mean2d"]), _p(out["depth"]), _p(out["conic"]), _p(out["comp"]),
+                     _p(out["opac_eff"]), _p(out["rgb"]))
+    return out
+
+
+def isect(proj, C, N, W, H, opts: Options):
+    """I1-I4 by brute-force enumeration + sort.  Returns keys (u64), ids (i32), offsets."""
+    o = opts.c()
+    radii, m2, d = proj["radii"], proj["mean2d_f"], proj["depth_f"]
+    M = lib().or_isect(ct.byref(o), C, N, W, H, _p(radii), _p(m2), _p(d), 0, None, None, None)
+    TS = opts.tile_size
+    TX, TY = (W + TS - 1) // TS, (H + TS - 1) // TS
+    keys = np.zeros(max(M, 1), np.uint64)
+    ids = np.zeros(max(M, 1), np.int32)
+    offs = np.zeros(C * TX * TY + 1, np.int32)
+    M2 = lib().or_isect(ct.byref(o), C, N, W, H, _p(radii), _p(m2), _p(d), M, _p(keys), _p(ids), _p(offs))
+    assert M2 == M
+    return keys[:M], ids[:M], offs
+
+
+def render_fwd(proj, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None):
+    o = opts.c()
+    bg = None if backgrounds is None else _f64(backgrounds)
+    tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
+    out = dict(rgb=np.zeros((C, H, W, 3)), alpha=np.zeros((C, H, W)), T=np.zeros((C, H, W)),
+               last_gid=np.zeros((C, H, W), np.int64), ambig=np.zeros((C, H, W), np.uint8),
+               ncontrib=np.zeros((C, H, W), np.int32))
+    lib().or_render_fwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
+                        _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
+                        _p(tm), _p(out["rgb"]), _p(out["alpha"]), _p(out["T"]), _p(out["last_gid"]),
+                        _p(out["ambig"]), _p(out["ncontrib"]))
+    return out
+
+
+def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds=None, tile_mask=None):
+    """B1-B6.  Returns v2d [C,N,9] (v_mean2d 2, v_conic 3, v_rgb 3, v_opac_eff 1), the
+    per-element condition floor a2d (sum of |per-pixel terms|), g_ambig and the T-replay error."""
+    o = opts.c()
+    bg = None if backgrounds is None else _f64(backgrounds)
+    tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
+    v_img = _f64(v_img)
+    va = None if v_alpha is None else _f64(v_alpha)
+    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); amb = np.zeros((C, N), np.uint8)
+    err = ct.c_double(0)
+    lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
+                        _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
+                        _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(amb), ct.byref(err))
+    return dict(v2d=v2d, a2d=a2d, g_ambig=amb, T_replay_err=err.value)
+
+
+def project_bwd(scene, proj, v2d, opts: Options):
+    """P1-P9, summed over cameras.  Returns v_means, v_quats, v_scales, v_opacities, v_colors (f64)."""
+    means, quats, scales, opac, colors, viewmats, Ks = _scene_arrays(scene)
+    N, C = means.shape[0], viewmats.shape[0]
+    W, H = int(scene["width"]), int(scene["height"])
+    K = colors.shape[1] if colors.ndim == 3 else 1
+    o = opts.c()
+    out = dict(v_means=np.zeros((N, 3)), v_quats=np.zeros((N, 4)), v_scales=np.zeros((N, 3)),
+               v_opacities=np.zeros(N), v_colors=np.zeros(colors.shape))
+    lib().or_project_bwd(ct.byref(o), N, C, W, H, _p(means), _p(quats), _p(scales), _p(opac), _p(colors), K,
+                         _p(viewmats), _p(Ks), _p(proj["radii"]), _p(_f64(v2d)), _p(out["v_means"]),
+                         _p(out["v_quats"]), _p(out["v_scales"]), _p(out["v_opacities"]), _p(out["v_colors"]))
+    return out
+
+
+def forward_backward(scene, opts: Options, v_img, v_alpha=None, backgrounds=None, tile_mask=None,
+                     with_isect=True):
+    """The whole path: project -> isect -> render fwd -> render bwd -> project bwd."""
+    C, N = scene["viewmats"].shape[0], scene["means"].shape[0]
+    W, H = int(scene["width"]), int(scene["height"])
+    proj = project(scene, opts)
+    res = dict(proj=proj)
+    if with_isect:
+        res["keys"], res["ids"], res["offsets"] = isect(proj, C, N, W, H, opts)
+    res["fwd"] = render_fwd(proj, C, N, W, H, opts, backgrounds, tile_mask)
+    res["bwd"] = render_bwd(proj, C, N, W, H, opts, v_img, v_alpha, backgrounds, tile_mask)
+    res["grads"] = project_bwd(scene, proj, res["bwd"]["v2d"], opts)
+    return res

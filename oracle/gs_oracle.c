@@ -1,0 +1,958 @@
+/*
+ * oracle/gs_oracle.c -- the CPU ORACLE for the gsplat hot path (arXiv 2409.06765).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2409_06765_b200/) never imports, links or executes anything in oracle/,
+ * and this file shares no code, header, table or constant generator with it.
+ *
+ * What it is: a plain, slow, deliberately unblocked implementation of what the
+ * method computes, following the paper step by step.  Citations are to
+ * /root/reference/PAPER.md by line ("P:534") and to SURVEY.md Appendix A step
+ * names (F1..F15, I1..I4, R1..R3, B1..B6, P1..P9), which restate the paper.
+ *
+ *  - Values and gradients are computed in fp64 (the paper fixes no precision).
+ *  - Integer decisions that the GPU takes in fp32 -- radii, the projected mean and
+ *    the depth bits that form tile keys -- are taken here in fp32 with the op
+ *    order written down in DESIGN.md ("key path", reading Q28), so keys, sort
+ *    order and tile ranges can be compared bit-exactly.  Compile with
+ *    -ffp-contract=off (no FMA contraction) so every fp32 op rounds once.
+ *  - Compositing uses NO tiles as an accelerator: every pixel walks the camera's
+ *    whole global depth-sorted visible list ("sorted by depth") and keeps a
+ *    splat only if the pixel's 16x16 tile lies inside the splat's 3-sigma tile
+ *    rectangle ("include it in a tile bin if its bounding box intersects
+ *    with the tile"), which is part of the method's definition.
+ *
+ * Parity status of each function is stated in DESIGN.md section "Oracle pins".
+ * Parity unpinned: the SH basis signs (Q22) -- only magnitudes are pinned by the
+ * orthonormality quadrature test.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef struct {
+    double near_plane;   /* 0.01 : cull iff depth <  near (Q18, pinned by Fig. 1)     */
+    double far_plane;    /* 1e10 : cull iff depth >  far                                  */
+    double eps2d;        /* 0.3  : low-pass s                                     */
+    double alpha_max;    /* 0.99 : opacity saturation (north_star; Q13)                   */
+    double alpha_min;    /* 1/255: skip iff alpha < alpha_min (Q14)                       */
+    double t_min;        /* 1e-4 : stop iff T*(1-alpha) <= t_min, exclusive (Q15)         */
+    double amb_rel_alpha;/* ambiguity margin (relative) around alpha_min / alpha_max      */
+    double amb_rel_t;    /* ambiguity margin (relative) around t_min                      */
+    int32_t tile_size;   /* 16                                                    */
+    int32_t antialiased; /* 0 classic | 1 compensated opacity                 */
+    int32_t sh_degree;   /* -1 direct RGB colors | 0..3 spherical harmonics               */
+    int32_t bbox_mode;   /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3*sqrt(lambda_max)   */
+    int32_t fov_clamp;   /* 1 clamp t_x/t_z, t_y/t_z for J only (Q27)                     */
+    int32_t pad_;
+} or_opts;
+
+/* ------------------------------------------------------------------------- */
+/* Spherical harmonics, real basis up to degree 3 ([bk]).  */
+/* P:505 writes c = SH((mu - t)/||mu - t||); P:476 says colour is SH-encoded.  */
+/* ------------------------------------------------------------------------- */
+static const double SH_C0 = 0.28209479177387814;
+static const double SH_C1 = 0.4886025119029199;
+static const double SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                -1.0925484305920792, 0.5462742152960396};
+static const double SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                                -0.5900435899266435};
+
+/* Y[j] for j < (deg+1)^2 at unit direction (x,y,z). */
+static void sh_basis(int deg, double x, double y, double z, double *Y)
+{
+    Y[0] = SH_C0;
+    if (deg < 1) return;
+    Y[1] = -SH_C1 * y;
+    Y[2] = SH_C1 * z;
+    Y[3] = -SH_C1 * x;
+    if (deg < 2) return;
+    double xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = SH_C2[0] * x * y;
+    Y[5] = SH_C2[1] * y * z;
+    Y[6] = SH_C2[2] * (2.0 * zz - xx - yy);
+    Y[7] = SH_C2[3] * x * z;
+    Y[8] = SH_C2[4] * (xx - yy);
+    if (deg < 3) return;
+    Y[9]  = SH_C3[0] * y * (3.0 * xx - yy);
+    Y[10] = SH_C3[1] * x * y * z;
+    Y[11] = SH_C3[2] * y * (4.0 * zz - xx - yy);
+    Y[12] = SH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    Y[13] = SH_C3[4] * x * (4.0 * zz - xx - yy);
+    Y[14] = SH_C3[5] * z * (xx - yy);
+    Y[15] = SH_C3[6] * x * (xx - 3.0 * yy);
+}
+
+/* dY[j][0..2] = dY_j / d(x,y,z), the partial derivatives of the polynomials above
+ * (treating x,y,z as independent; the normalisation is chained separately, P7). */
+static void sh_basis_grad(int deg, double x, double y, double z, double dY[16][3])
+{
+    memset(dY, 0, sizeof(double) * 16 * 3);
+    if (deg < 1) return;
+    dY[1][1] = -SH_C1;
+    dY[2][2] = SH_C1;
+    dY[3][0] = -SH_C1;
+    if (deg < 2) return;
+    double xx = x * x, yy = y * y, zz = z * z;
+    dY[4][0] = SH_C2[0] * y;              dY[4][1] = SH_C2[0] * x;
+    dY[5][1] = SH_C2[1] * z;              dY[5][2] = SH_C2[1] * y;
+    dY[6][0] = SH_C2[2] * (-2.0 * x);     dY[6][1] = SH_C2[2] * (-2.0 * y);  dY[6][2] = SH_C2[2] * (4.0 * z);
+    dY[7][0] = SH_C2[3] * z;              dY[7][2] = SH_C2[3] * x;
+    dY[8][0] = SH_C2[4] * (2.0 * x);      dY[8][1] = SH_C2[4] * (-2.0 * y);
+    if (deg < 3) return;
+    dY[9][0]  = SH_C3[0] * (6.0 * x * y);
+    dY[9][1]  = SH_C3[0] * (3.0 * xx - 3.0 * yy);
+    dY[10][0] = SH_C3[1] * y * z;  dY[10][1] = SH_C3[1] * x * z;  dY[10][2] = SH_C3[1] * x * y;
+    dY[11][0] = SH_C3[2] * (-2.0 * x * y);
+    dY[11][1] = SH_C3[2] * (4.0 * zz - xx - 3.0 * yy);
+    dY[11][2] = SH_C3[2] * (8.0 * y * z);
+    dY[12][0] = SH_C3[3] * (-6.0 * x * z);
+    dY[12][1] = SH_C3[3] * (-6.0 * y * z);
+    dY[12][2] = SH_C3[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+    dY[13][0] = SH_C3[4] * (4.0 * zz - 3.0 * xx - yy);
+    dY[13][1] = SH_C3[4] * (-2.0 * x * y);
+    dY[13][2] = SH_C3[4] * (8.0 * x * z);
+    dY[14][0] = SH_C3[5] * (2.0 * x * z);
+    dY[14][1] = SH_C3[5] * (-2.0 * y * z);
+    dY[14][2] = SH_C3[5] * (xx - yy);
+    dY[15][0] = SH_C3[6] * (3.0 * xx - 3.0 * yy);
+    dY[15][1] = SH_C3[6] * (-6.0 * x * y);
+}
+
+/* exported for the quadrature / FD pins */
+void or_sh_basis(int32_t deg, double x, double y, double z, double *Y) { sh_basis(deg, x, y, z, Y); }
+void or_sh_basis_grad(int32_t deg, double x, double y, double z, double *dY)
+{
+    double g[16][3];
+    sh_basis_grad(deg, x, y, z, g);
+    memcpy(dY, g, sizeof g);
+}
+
+/* ------------------------------------------------------------------------- */
+/* F1: quaternion (w,x,y,z), Hamilton, to rotation matrix.          */
+/* ------------------------------------------------------------------------- */
+static void quat_to_rot(double w, double x, double y, double z, double R[3][3])
+{
+    R[0][0] = 1.0 - 2.0 * (y * y + z * z);
+    R[0][1] = 2.0 * (x * y - w * z);
+    R[0][2] = 2.0 * (x * z + w * y);
+    R[1][0] = 2.0 * (x * y + w * z);
+    R[1][1] = 1.0 - 2.0 * (x * x + z * z);
+    R[1][2] = 2.0 * (y * z - w * x);
+    R[2][0] = 2.0 * (x * z - w * y);
+    R[2][1] = 2.0 * (y * z + w * x);
+    R[2][2] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+void or_quat_to_rotmat(const double *q, double *R9)
+{
+    double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    double R[3][3];
+    quat_to_rot(q[0] / n, q[1] / n, q[2] / n, q[3] / n, R);
+    memcpy(R9, R, sizeof R);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Key path: fp32, fixed op order (reading Q28).  Produces radii,   */
+/* the fp32 projected mean and depth; decides visibility (F4, F9, F12, F13).  */
+/* Every expression below is one IEEE op per operator, left to right.         */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int   visible;
+    int   rx, ry;
+    float mx, my, depth;
+} keypath_t;
+
+static keypath_t key_path_f32(const or_opts *o, int W, int H, const float *mu, const float *q,
+                              const float *s, const float *vm /*4x4*/, const float *Kc /*3x3*/)
+{
+    keypath_t kp = {0, 0, 0, 0.f, 0.f, 0.f};
+    /* KP1 (F3): t = W mu + w */
+    float tx = ((vm[0] * mu[0] + vm[1] * mu[1]) + vm[2] * mu[2]) + vm[3];
+    float ty = ((vm[4] * mu[0] + vm[5] * mu[1]) + vm[6] * mu[2]) + vm[7];
+    float tz = ((vm[8] * mu[0] + vm[9] * mu[1]) + vm[10] * mu[2]) + vm[11];
+    /* KP2 (F4): depth, near/far (strict, Q18) */
+    if (!(tz >= (float)o->near_plane) || tz > (float)o->far_plane) return kp;
+    /* KP3 (F1): q_hat = q / ||q|| */
+    float qn2 = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+    if (!(qn2 > 0.f) || !isfinite(qn2)) return kp;
+    float qn = sqrtf(qn2);
+    float w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
+    /* KP4 (F1): R(q_hat) */
+    float R[3][3];
+    R[0][0] = 1.f - 2.f * (y * y + z * z);
+    R[0][1] = 2.f * (x * y - w * z);
+    R[0][2] = 2.f * (x * z + w * y);
+    R[1][0] = 2.f * (x * y + w * z);
+    R[1][1] = 1.f - 2.f * (x * x + z * z);
+    R[1][2] = 2.f * (y * z - w * x);
+    R[2][0] = 2.f * (x * z - w * y);
+    R[2][1] = 2.f * (y * z + w * x);
+    R[2][2] = 1.f - 2.f * (x * x + y * y);
+    /* KP5 (F2): M = R diag(s) ; KP6: Sigma = M M^T */
+    float M[3][3], S[3][3];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) M[i][j] = R[i][j] * s[j];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) S[i][j] = (M[i][0] * M[j][0] + M[i][1] * M[j][1]) + M[i][2] * M[j][2];
+    /* KP7 (F5): Sigma_c = Wr Sigma Wr^T, via A = Wr Sigma */
+    float Wr[3][3] = {{vm[0], vm[1], vm[2]}, {vm[4], vm[5], vm[6]}, {vm[8], vm[9], vm[10]}};
+    float A[3][3], Sc[3][3];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) A[i][j] = (Wr[i][0] * S[0][j] + Wr[i][1] * S[1][j]) + Wr[i][2] * S[2][j];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) Sc[i][j] = (A[i][0] * Wr[j][0] + A[i][1] * Wr[j][1]) + A[i][2] * Wr[j][2];
+    /* KP8 (F6): J with focals (Q4) and optional frustum clamp (Q27) */
+    float fx = Kc[0], fy = Kc[4], cx = Kc[2], cy = Kc[5];
+    float txc = tx, tyc = ty;
+    if (o->fov_clamp) {
+        float tanx = (0.5f * (float)W) / fx, tany = (0.5f * (float)H) / fy;
+        float lxp = ((float)W - cx) / fx + 0.3f * tanx, lxn = cx / fx + 0.3f * tanx;
+        float lyp = ((float)H - cy) / fy + 0.3f * tany, lyn = cy / fy + 0.3f * tany;
+        float u = tx / tz, v = ty / tz;
+        float uc = fminf(lxp, fmaxf(-lxn, u)), vc = fminf(lyp, fmaxf(-lyn, v));
+        txc = tz * uc;
+        tyc = tz * vc;
+    }
+    float J[2][3];
+    J[0][0] = fx / tz; J[0][1] = 0.f; J[0][2] = -(fx * txc) / (tz * tz);
+    J[1][0] = 0.f; J[1][1] = fy / tz; J[1][2] = -(fy * tyc) / (tz * tz);
+    /* KP9 (F7): Sigma' = J Sigma_c J^T via B = J Sigma_c */
+    float B[2][3], Sp[2][2];
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 3; j++) B[i][j] = (J[i][0] * Sc[0][j] + J[i][1] * Sc[1][j]) + J[i][2] * Sc[2][j];
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 2; j++) Sp[i][j] = (B[i][0] * J[j][0] + B[i][1] * J[j][1]) + B[i][2] * J[j][2];
+    /* KP10 (F8): low-pass */
+    float a = Sp[0][0] + (float)o->eps2d, b = Sp[0][1], c = Sp[1][1] + (float)o->eps2d;
+    /* KP11 (F9): det */
+    float det = a * c - b * b;
+    if (!(det > 0.f)) return kp;
+    /* KP12 (F12): radii */
+    int rx, ry;
+    if (o->bbox_mode == 0) {
+        rx = (int)ceilf(3.f * sqrtf(a));
+        ry = (int)ceilf(3.f * sqrtf(c));
+    } else {
+        float m = 0.5f * (a + c);
+        float lam = m + sqrtf(fmaxf(0.f, m * m - det));
+        rx = ry = (int)ceilf(3.f * sqrtf(lam));
+    }
+    /* KP13 (F11): mu' = f t/t_z + c */
+    float mx = (fx * tx) / tz + cx;
+    float my = (fy * ty) / tz + cy;
+    /* KP14 (F13): off-screen cull (Q19) */
+    if (mx + (float)rx <= 0.f || mx - (float)rx >= (float)W || my + (float)ry <= 0.f ||
+        my - (float)ry >= (float)H)
+        return kp;
+    if (!isfinite(mx) || !isfinite(my)) return kp;
+    kp.visible = 1; kp.rx = rx; kp.ry = ry; kp.mx = mx; kp.my = my; kp.depth = tz;
+    return kp;
+}
+
+/* I1 (Q20): tile rectangle [x0,x1) x [y0,y1) in fp32, /tile is exact. */
+static void tile_rect(int tile, int TX, int TY, float mx, float my, int rx, int ry,
+                      int *x0, int *x1, int *y0, int *y1)
+{
+    float ft = (float)tile;
+    int a0 = (int)floorf((mx - (float)rx) / ft), a1 = (int)ceilf((mx + (float)rx) / ft);
+    int b0 = (int)floorf((my - (float)ry) / ft), b1 = (int)ceilf((my + (float)ry) / ft);
+    *x0 = a0 < 0 ? 0 : (a0 > TX ? TX : a0);
+    *x1 = a1 < 0 ? 0 : (a1 > TX ? TX : a1);
+    *y0 = b0 < 0 ? 0 : (b0 > TY ? TY : b0);
+    *y1 = b1 < 0 ? 0 : (b1 > TY ? TY : b1);
+}
+
+/* ------------------------------------------------------------------------- */
+/* fp64 values path, F1..F15, for one (c,n).                                   */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    /* inputs promoted */
+    double mu[3], qraw[4], qn, qh[4], s[3], o;
+    double Wr[3][3], w[3], fx, fy, cx, cy;
+    /* intermediates */
+    double R[3][3], M[3][3], Sig[3][3], t[3], Sc[3][3];
+    double u, v, uc, vc, txc, tyc;
+    int clamp_x, clamp_y;
+    double J[2][3], Sp[2][2], Spb[2][2], det, detb, comp;
+    double conic[3];
+    double mean2d[2];
+    double campos[3], e[3], enorm, dir[3];
+    double raw[3], rgb[3];
+    double opac_eff;
+} proj64_t;
+
+static void project64(const or_opts *o, int W, int H, const float *mu, const float *q, const float *s,
+                      float op, const float *colors, int K, const float *vm, const float *Kc, proj64_t *P)
+{
+    for (int i = 0; i < 3; i++) P->mu[i] = mu[i], P->s[i] = s[i];
+    for (int i = 0; i < 4; i++) P->qraw[i] = q[i];
+    P->o = op;
+    for (int i = 0; i < 3; i++) {
+        for (int j = 0; j < 3; j++) P->Wr[i][j] = vm[4 * i + j];
+        P->w[i] = vm[4 * i + 3];
+    }
+    P->fx = Kc[0]; P->fy = Kc[4]; P->cx = Kc[2]; P->cy = Kc[5];
+    /* F1 */
+    P->qn = sqrt(P->qraw[0] * P->qraw[0] + P->qraw[1] * P->qraw[1] + P->qraw[2] * P->qraw[2] +
+                 P->qraw[3] * P->qraw[3]);
+    for (int i = 0; i < 4; i++) P->qh[i] = P->qraw[i] / P->qn;
+    quat_to_rot(P->qh[0], P->qh[1], P->qh[2], P->qh[3], P->R);
+    /* F2: M = R S, Sigma = M M^T */
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) P->M[i][j] = P->R[i][j] * P->s[j];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) {
+            double acc = 0;
+            for (int k = 0; k < 3; k++) acc += P->M[i][k] * P->M[j][k];
+            P->Sig[i][j] = acc;
+        }
+    /* F3: t = W mu + w ("t = T_cw q") */
+    for (int i = 0; i < 3; i++) {
+        double acc = P->w[i];
+        for (int k = 0; k < 3; k++) acc += P->Wr[i][k] * P->mu[k];
+        P->t[i] = acc;
+    }
+    /* F5: Sigma_c = W Sigma W^T (Fig. P:423) */
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) {
+            double acc = 0;
+            for (int k = 0; k < 3; k++)
+                for (int l = 0; l < 3; l++) acc += P->Wr[i][k] * P->Sig[k][l] * P->Wr[j][l];
+            P->Sc[i][j] = acc;
+        }
+    /* F6: J (P:695-709 with focals; Q4) with frustum clamp for J only (Q27) */
+    double tz = P->t[2];
+    P->u = P->t[0] / tz; P->v = P->t[1] / tz;
+    P->uc = P->u; P->vc = P->v; P->clamp_x = P->clamp_y = 0;
+    if (o->fov_clamp) {
+        double tanx = 0.5 * W / P->fx, tany = 0.5 * H / P->fy;
+        double lxp = (W - P->cx) / P->fx + 0.3 * tanx, lxn = P->cx / P->fx + 0.3 * tanx;
+        double lyp = (H - P->cy) / P->fy + 0.3 * tany, lyn = P->cy / P->fy + 0.3 * tany;
+        if (P->u > lxp) { P->uc = lxp; P->clamp_x = 1; }
+        if (P->u < -lxn) { P->uc = -lxn; P->clamp_x = 1; }
+        if (P->v > lyp) { P->vc = lyp; P->clamp_y = 1; }
+        if (P->v < -lyn) { P->vc = -lyn; P->clamp_y = 1; }
+    }
+    P->txc = tz * P->uc; P->tyc = tz * P->vc;
+    P->J[0][0] = P->fx / tz; P->J[0][1] = 0; P->J[0][2] = -P->fx * P->txc / (tz * tz);
+    P->J[1][0] = 0; P->J[1][1] = P->fy / tz; P->J[1][2] = -P->fy * P->tyc / (tz * tz);
+    /* F7: Sigma' = J Sigma_c J^T */
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 2; j++) {
+            double acc = 0;
+            for (int k = 0; k < 3; k++)
+                for (int l = 0; l < 3; l++) acc += P->J[i][k] * P->Sc[k][l] * P->J[j][l];
+            P->Sp[i][j] = acc;
+        }
+    /* F8: + s I in both modes (Q6) */
+    P->Spb[0][0] = P->Sp[0][0] + o->eps2d; P->Spb[0][1] = P->Sp[0][1];
+    P->Spb[1][0] = P->Sp[1][0];            P->Spb[1][1] = P->Sp[1][1] + o->eps2d;
+    /* F9: determinants and the A.4 compensation (Q7) */
+    P->det = P->Sp[0][0] * P->Sp[1][1] - P->Sp[0][1] * P->Sp[1][0];
+    P->detb = P->Spb[0][0] * P->Spb[1][1] - P->Spb[0][1] * P->Spb[1][0];
+    if (o->antialiased) {
+        double r = P->det / P->detb;
+        P->comp = sqrt(r > 0 ? r : 0);
+    } else {
+        P->comp = 1.0;
+    }
+    /* F10: conic = (Sigma'+sI)^-1 packed (A, B, C) */
+    P->conic[0] = P->Spb[1][1] / P->detb;
+    P->conic[1] = -P->Spb[0][1] / P->detb;
+    P->conic[2] = P->Spb[0][0] / P->detb;
+    /* F11: P:790-791 */
+    P->mean2d[0] = P->fx * P->t[0] / tz + P->cx;
+    P->mean2d[1] = P->fy * P->t[1] / tz + P->cy;
+    /* F14: colour (SH basis [bk], Q22) */
+    if (o->sh_degree >= 0) {
+        /* campos = -Wr^T w */
+        for (int i = 0; i < 3; i++) {
+            double acc = 0;
+            for (int k = 0; k < 3; k++) acc -= P->Wr[k][i] * P->w[k];
+            P->campos[i] = acc;
+        }
+        for (int i = 0; i < 3; i++) P->e[i] = P->mu[i] - P->campos[i];
+        P->enorm = sqrt(P->e[0] * P->e[0] + P->e[1] * P->e[1] + P->e[2] * P->e[2]);
+        for (int i = 0; i < 3; i++) P->dir[i] = P->e[i] / P->enorm;
+        double Y[16];
+        int nb = (o->sh_degree + 1) * (o->sh_degree + 1);
+        sh_basis(o->sh_degree, P->dir[0], P->dir[1], P->dir[2], Y);
+        for (int ch = 0; ch < 3; ch++) {
+            double acc = 0.5;
+            for (int j = 0; j < nb; j++) acc += Y[j] * (double)colors[(int64_t)j * 3 + ch];
+            P->raw[ch] = acc;
+            P->rgb[ch] = acc > 0 ? acc : 0;
+        }
+    } else {
+        for (int ch = 0; ch < 3; ch++) P->raw[ch] = P->rgb[ch] = colors[ch];
+    }
+    (void)K;
+    /* F15 */
+    P->opac_eff = P->o * P->comp;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Exported: projection over all (c, n).                                       */
+/* ------------------------------------------------------------------------- */
+int or_project(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H, const float *means,
+               const float *quats, const float *scales, const float *opacities, const float *colors,
+               int32_t K, const float *viewmats, const float *Ks,
+               int32_t *radii, float *mean2d_f, float *depth_f,
+               double *mean2d, double *depth, double *conic, double *comp, double *opac_eff, double *rgb)
+{
+    int64_t stride = o->sh_degree >= 0 ? (int64_t)K * 3 : 3;
+#pragma omp parallel for schedule(static)
+    for (int64_t idx = 0; idx < (int64_t)C * N; idx++) {
+        int64_t c = idx / N, n = idx % N;
+        const float *vm = viewmats + 16 * c, *Kc = Ks + 9 * c;
+        keypath_t kp = key_path_f32(o, W, H, means + 3 * n, quats + 4 * n, scales + 3 * n, vm, Kc);
+        radii[2 * idx] = kp.visible ? kp.rx : 0;
+        radii[2 * idx + 1] = kp.visible ? kp.ry : 0;
+        mean2d_f[2 * idx] = kp.visible ? kp.mx : 0.f;
+        mean2d_f[2 * idx + 1] = kp.visible ? kp.my : 0.f;
+        depth_f[idx] = kp.visible ? kp.depth : 0.f;
+        if (!kp.visible) {
+            mean2d[2 * idx] = mean2d[2 * idx + 1] = 0;
+            depth[idx] = 0; conic[3 * idx] = conic[3 * idx + 1] = conic[3 * idx + 2] = 0;
+            comp[idx] = 0; opac_eff[idx] = 0; rgb[3 * idx] = rgb[3 * idx + 1] = rgb[3 * idx + 2] = 0;
+            continue;
+        }
+        proj64_t P;
+        project64(o, W, H, means + 3 * n, quats + 4 * n, scales + 3 * n, opacities[n], colors + stride * n,
+                  K, vm, Kc, &P);
+        mean2d[2 * idx] = P.mean2d[0]; mean2d[2 * idx + 1] = P.mean2d[1];
+        depth[idx] = P.t[2];
+        for (int i = 0; i < 3; i++) conic[3 * idx + i] = P.conic[i], rgb[3 * idx + i] = P.rgb[i];
+        comp[idx] = P.comp;
+        opac_eff[idx] = P.opac_eff;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* I1-I4 by brute force: enumerate every (c, n, tile) with the tile inside the */
+/* rectangle, key = (c << (32+B)) | (tile << 32) | bits(depth),    */
+/* value = c*N + n, then sort by (key, value) and take lower bounds.           */
+/* Returns M; writes outputs only when M <= cap.                               */
+/* ------------------------------------------------------------------------- */
+typedef struct { uint64_t key; int32_t id; } kv_t;
+static int kv_cmp(const void *a, const void *b)
+{
+    const kv_t *x = a, *y = b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+
+static int tile_bits(int ntiles)
+{
+    int B = 0;
+    while ((1LL << B) < ntiles) B++;
+    return B;
+}
+
+int64_t or_isect(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
+                 const float *mean2d_f, const float *depth_f, int64_t cap, uint64_t *keys, int32_t *ids,
+                 int32_t *tile_offsets)
+{
+    int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
+    int B = tile_bits(TX * TY);
+    int64_t M = 0;
+    for (int64_t idx = 0; idx < (int64_t)C * N; idx++) {
+        if (radii[2 * idx] <= 0 || radii[2 * idx + 1] <= 0) continue;
+        int x0, x1, y0, y1;
+        tile_rect(T, TX, TY, mean2d_f[2 * idx], mean2d_f[2 * idx + 1], radii[2 * idx], radii[2 * idx + 1],
+                  &x0, &x1, &y0, &y1);
+        M += (int64_t)(x1 - x0) * (y1 - y0);
+    }
+    if (M > cap) return M;
+    kv_t *kv = (kv_t *)malloc(sizeof(kv_t) * (M > 0 ? M : 1));
+    int64_t m = 0;
+    for (int64_t idx = 0; idx < (int64_t)C * N; idx++) {
+        if (radii[2 * idx] <= 0 || radii[2 * idx + 1] <= 0) continue;
+        int64_t c = idx / N;
+        int x0, x1, y0, y1;
+        tile_rect(T, TX, TY, mean2d_f[2 * idx], mean2d_f[2 * idx + 1], radii[2 * idx], radii[2 * idx + 1],
+                  &x0, &x1, &y0, &y1);
+        uint32_t dbits;
+        memcpy(&dbits, &depth_f[idx], 4);
+        for (int ty = y0; ty < y1; ty++)
+            for (int tx = x0; tx < x1; tx++) {
+                uint64_t tile = (uint64_t)(ty * TX + tx);
+                kv[m].key = ((uint64_t)c << (32 + B)) | (tile << 32) | (uint64_t)dbits;
+                kv[m].id = (int32_t)idx;
+                m++;
+            }
+    }
+    qsort(kv, M, sizeof(kv_t), kv_cmp);
+    for (int64_t i = 0; i < M; i++) keys[i] = kv[i].key, ids[i] = kv[i].id;
+    /* I4: offsets[c*TT + t] = first index whose (cam, tile) >= (c, t); offsets[end] = M */
+    int64_t ntot = (int64_t)C * TX * TY;
+    int64_t k = 0;
+    for (int64_t bin = 0; bin < ntot; bin++) {
+        int64_t c = bin / (TX * TY), t = bin % (TX * TY);
+        uint64_t lo = ((uint64_t)c << (32 + B)) | ((uint64_t)t << 32);
+        while (k < M && keys[k] < lo) k++;
+        tile_offsets[bin] = (int32_t)k;
+    }
+    tile_offsets[ntot] = (int32_t)M;
+    free(kv);
+    return M;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Rendering.  Per camera: the visible set sorted by (fp32 depth bits, n)      */
+/* ("sorts them per tile by depth"; tie-break Q16).                      */
+/* ------------------------------------------------------------------------- */
+typedef struct { uint32_t dbits; int32_t n; } dn_t;
+static int dn_cmp(const void *a, const void *b)
+{
+    const dn_t *x = a, *y = b;
+    if (x->dbits != y->dbits) return x->dbits < y->dbits ? -1 : 1;
+    return (x->n > y->n) - (x->n < y->n);
+}
+
+typedef struct {
+    int64_t count;       /* visible splats of this camera */
+    int32_t *n;          /* sorted Gaussian indices */
+    int32_t *rect;       /* [count][4] tile rectangle x0,x1,y0,y1 */
+} camlist_t;
+
+static void build_camlist(const or_opts *o, int64_t c, int64_t N, int W, int H, const int32_t *radii,
+                          const float *mean2d_f, const float *depth_f, camlist_t *L)
+{
+    int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
+    int64_t cnt = 0;
+    for (int64_t n = 0; n < N; n++)
+        if (radii[2 * (c * N + n)] > 0 && radii[2 * (c * N + n) + 1] > 0) cnt++;
+    dn_t *tmp = (dn_t *)malloc(sizeof(dn_t) * (cnt > 0 ? cnt : 1));
+    int64_t m = 0;
+    for (int64_t n = 0; n < N; n++) {
+        int64_t idx = c * N + n;
+        if (radii[2 * idx] > 0 && radii[2 * idx + 1] > 0) {
+            memcpy(&tmp[m].dbits, &depth_f[idx], 4);
+            tmp[m].n = (int32_t)n;
+            m++;
+        }
+    }
+    qsort(tmp, cnt, sizeof(dn_t), dn_cmp);
+    L->count = cnt;
+    L->n = (int32_t *)malloc(sizeof(int32_t) * (cnt > 0 ? cnt : 1));
+    L->rect = (int32_t *)malloc(sizeof(int32_t) * 4 * (cnt > 0 ? cnt : 1));
+    for (int64_t i = 0; i < cnt; i++) {
+        int64_t idx = c * N + tmp[i].n;
+        L->n[i] = tmp[i].n;
+        tile_rect(T, TX, TY, mean2d_f[2 * idx], mean2d_f[2 * idx + 1], radii[2 * idx], radii[2 * idx + 1],
+                  &L->rect[4 * i], &L->rect[4 * i + 1], &L->rect[4 * i + 2], &L->rect[4 * i + 3]);
+    }
+    free(tmp);
+}
+
+static void free_camlist(camlist_t *L)
+{
+    free(L->n);
+    free(L->rect);
+}
+
+/* One pixel's forward walk, R1-R3.  Optionally records the composited
+ * sequence (index into the camera list, alpha, T before, G, sigma) for B1-B6. */
+typedef struct {
+    int64_t li;      /* list index */
+    double alpha, T, G, sigma, dx, dy;
+} contrib_t;
+
+typedef struct {
+    double rgb[3], T;
+    int64_t last_li;  /* -1 if none */
+    int64_t end_li;   /* exclusive end of the evaluated part of the list */
+    int ambig;
+    int64_t ncontrib;
+} pixres_t;
+
+static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, int64_t N, int px, int py,
+                              const double *mean2d, const double *conic, const double *opac_eff,
+                              const double *rgb, contrib_t *rec, int64_t rec_cap)
+{
+    pixres_t r = {{0, 0, 0}, 1.0, -1, L->count, 0, 0};
+    int tx = px / o->tile_size, ty = py / o->tile_size;
+    double p[2] = {px + 0.5, py + 0.5};            /* R1: pixel centre */
+    double T = 1.0;
+    for (int64_t i = 0; i < L->count; i++) {
+        const int32_t *rc = &L->rect[4 * i];
+        if (tx < rc[0] || tx >= rc[1] || ty < rc[2] || ty >= rc[3]) continue;   /* tile predicate */
+        int64_t g = c * N + L->n[i];
+        double dx = mean2d[2 * g] - p[0], dy = mean2d[2 * g + 1] - p[1];     /* Delta = mu' - p (Q21) */
+        const double *Y = &conic[3 * g];
+        double sigma = 0.5 * (Y[0] * dx * dx + Y[2] * dy * dy) + Y[1] * dx * dy;
+        if (sigma < 0) continue;
+        double G = exp(-sigma);
+        double raw = opac_eff[g] * G;
+        if (fabs(raw - o->alpha_min) <= o->amb_rel_alpha * o->alpha_min) r.ambig = 1;
+        if (fabs(raw - o->alpha_max) <= o->amb_rel_alpha * o->alpha_max) r.ambig = 1;
+        double alpha = raw < o->alpha_max ? raw : o->alpha_max;
+        if (alpha < o->alpha_min) continue;                                   /* Q14 */
+        double nT = T * (1.0 - alpha);
+        if (fabs(nT - o->t_min) <= o->amb_rel_t * o->t_min) r.ambig = 1;
+        if (nT <= o->t_min) { r.end_li = i + 1; break; }                      /* Q15 */
+        if (rec && r.ncontrib < rec_cap) {
+            contrib_t *e = &rec[r.ncontrib];
+            e->li = i; e->alpha = alpha; e->T = T; e->G = G; e->sigma = sigma; e->dx = dx; e->dy = dy;
+        }
+        for (int ch = 0; ch < 3; ch++) r.rgb[ch] += rgb[3 * g + ch] * alpha * T;
+        T = nT;
+        r.last_li = i;
+        r.ncontrib++;
+    }
+    r.T = T;
+    return r;
+}
+
+static int tile_selected(const uint8_t *tile_mask, int64_t c, int TX, int TY, int px, int py, int T)
+{
+    if (!tile_mask) return 1;
+    return tile_mask[c * TX * TY + (py / T) * TX + (px / T)] != 0;
+}
+
+/* R1-R3 for every (selected) pixel.  out_last_gid = flat id c*N+n of the last
+ * composited splat, -1 if none. Unselected pixels get rgb=bg, T=1, gid=-1. */
+int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
+                  const float *mean2d_f, const float *depth_f, const double *mean2d, const double *conic,
+                  const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
+                  double *out_rgb, double *out_alpha, double *out_T, int64_t *out_last_gid,
+                  uint8_t *out_ambig, int32_t *out_ncontrib)
+{
+    int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
+    for (int64_t c = 0; c < C; c++) {
+        camlist_t L;
+        build_camlist(o, c, N, W, H, radii, mean2d_f, depth_f, &L);
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t pix = 0; pix < (int64_t)W * H; pix++) {
+            int px = (int)(pix % W), py = (int)(pix / W);
+            int64_t oi = c * W * H + pix;
+            const double *b = bg ? bg + 3 * c : NULL;
+            if (!tile_selected(tile_mask, c, TX, TY, px, py, T)) {
+                for (int ch = 0; ch < 3; ch++) out_rgb[3 * oi + ch] = b ? b[ch] : 0.0;
+                out_alpha[oi] = 0; out_T[oi] = 1; out_last_gid[oi] = -1;
+                if (out_ambig) out_ambig[oi] = 0;
+                if (out_ncontrib) out_ncontrib[oi] = 0;
+                continue;
+            }
+            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d, conic, opac_eff, rgb, NULL, 0);
+            for (int ch = 0; ch < 3; ch++) out_rgb[3 * oi + ch] = r.rgb[ch] + r.T * (b ? b[ch] : 0.0);  /* R3, Q25 */
+            out_alpha[oi] = 1.0 - r.T;
+            out_T[oi] = r.T;
+            out_last_gid[oi] = r.last_li >= 0 ? c * N + L.n[r.last_li] : -1;
+            if (out_ambig) out_ambig[oi] = (uint8_t)r.ambig;
+            if (out_ncontrib) out_ncontrib[oi] = (int32_t)r.ncontrib;
+        }
+        free_camlist(&L);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* B1-B6.  Per pixel: replay the forward to find the composited    */
+/* sequence, then walk it back to front with the paper's recurrences           */
+/* T_{n-1} = T_n/(1-alpha_{n-1}) and S.  Per-pixel terms are   */
+/* written to per-pixel slots and summed serially in pixel order.              */
+/* v2d layout per flat id g, 9 doubles:                                        */
+/*   [0,1] v_mean2d  [2,3,4] v_conic (A,B,C)  [5,6,7] v_rgb  [8] v_opac_eff     */
+/* a2d: same layout, sum over pixels of |term| (the condition floor)*/
+/* g_ambig[g] = 1 if g was evaluated at an ambiguous pixel.                     */
+/* T_replay_err (optional) = max |T_replayed - T_forward| over all steps.      */
+/* ------------------------------------------------------------------------- */
+typedef struct { int32_t g; double v[9]; } term_t;
+
+int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
+                  const float *mean2d_f, const float *depth_f, const double *mean2d, const double *conic,
+                  const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
+                  const double *v_img, const double *v_alpha_img, double *v2d, double *a2d,
+                  uint8_t *g_ambig, double *T_replay_err)
+{
+    int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
+    memset(v2d, 0, sizeof(double) * 9 * C * N);
+    if (a2d) memset(a2d, 0, sizeof(double) * 9 * C * N);
+    if (g_ambig) memset(g_ambig, 0, (size_t)C * N);
+    double max_err = 0;
+    for (int64_t c = 0; c < C; c++) {
+        camlist_t L;
+        build_camlist(o, c, N, W, H, radii, mean2d_f, depth_f, &L);
+        int64_t P = (int64_t)W * H;
+        int32_t *cnt = (int32_t *)calloc(P, sizeof(int32_t));
+        /* pass 1: composited count per pixel */
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t pix = 0; pix < P; pix++) {
+            int px = (int)(pix % W), py = (int)(pix / W);
+            if (!tile_selected(tile_mask, c, TX, TY, px, py, T)) continue;
+            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d, conic, opac_eff, rgb, NULL, 0);
+            cnt[pix] = (int32_t)r.ncontrib;
+            if (r.ambig && g_ambig) {
+                /* mark every splat this pixel evaluated (in-tile, up to termination) */
+                int tx = px / T, ty = py / T;
+                for (int64_t i = 0; i < r.end_li; i++) {
+                    const int32_t *rc = &L.rect[4 * i];
+                    if (tx < rc[0] || tx >= rc[1] || ty < rc[2] || ty >= rc[3]) continue;
+                    int64_t g = c * N + L.n[i];
+#pragma omp atomic write
+                    g_ambig[g] = 1;
+                }
+            }
+        }
+        int64_t *off = (int64_t *)malloc(sizeof(int64_t) * (P + 1));
+        off[0] = 0;
+        for (int64_t pix = 0; pix < P; pix++) off[pix + 1] = off[pix] + cnt[pix];
+        int64_t tot = off[P];
+        term_t *terms = (term_t *)malloc(sizeof(term_t) * (tot > 0 ? tot : 1));
+        double *errs = (double *)calloc(P, sizeof(double));
+        /* pass 2: per-pixel backward */
+#pragma omp parallel
+        {
+            int64_t cap = 1024;
+            contrib_t *rec = (contrib_t *)malloc(sizeof(contrib_t) * cap);
+#pragma omp for schedule(dynamic, 64)
+            for (int64_t pix = 0; pix < P; pix++) {
+                if (cnt[pix] == 0) continue;
+                int px = (int)(pix % W), py = (int)(pix / W);
+                if (cnt[pix] > cap) {
+                    cap = cnt[pix];
+                    rec = (contrib_t *)realloc(rec, sizeof(contrib_t) * cap);
+                }
+                pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d, conic, opac_eff, rgb, rec, cap);
+                int64_t oi = c * P + pix;
+                const double *vC = &v_img[3 * oi];
+                double vA = v_alpha_img ? v_alpha_img[oi] : 0.0;
+                const double *b = bg ? bg + 3 * c : NULL;
+                double bgdot = b ? (b[0] * vC[0] + b[1] * vC[1] + b[2] * vC[2]) : 0.0;
+                double Tfin = r.T;
+                double Tn = Tfin;                /* B1 */
+                double S[3] = {0, 0, 0};
+                double err = 0;
+                for (int64_t k = r.ncontrib - 1; k >= 0; k--) {
+                    const contrib_t *e = &rec[k];
+                    int64_t g = c * N + L.n[e->li];
+                    double alpha = e->alpha;
+                    double ra = 1.0 / (1.0 - alpha);
+                    Tn = Tn * ra;                /* B2: T_{n-1} = T_n / (1 - alpha_{n-1}) */
+                    double d = fabs(Tn - e->T);
+                    if (d > err) err = d;
+                    double fac = alpha * Tn;
+                    term_t *tm = &terms[off[pix] + k];
+                    tm->g = (int32_t)g;
+                    for (int ch = 0; ch < 3; ch++) tm->v[5 + ch] = fac * vC[ch];   /* B3 */
+                    double v_alpha = 0;                                            /* B4 */
+                    for (int ch = 0; ch < 3; ch++) v_alpha += (rgb[3 * g + ch] * Tn - S[ch] * ra) * vC[ch];
+                    v_alpha += -Tfin * ra * bgdot + Tfin * ra * vA;
+                    for (int ch = 0; ch < 3; ch++) S[ch] += rgb[3 * g + ch] * fac;  /* B5 */
+                    double raw = opac_eff[g] * e->G;
+                    if (raw < o->alpha_max) {                                    /* B6 (Q24) */
+                        tm->v[8] = e->G * v_alpha;
+                        double v_sigma = -opac_eff[g] * e->G * v_alpha;
+                        const double *Y = &conic[3 * g];
+                        tm->v[2] = v_sigma * 0.5 * e->dx * e->dx;
+                        tm->v[3] = v_sigma * e->dx * e->dy;
+                        tm->v[4] = v_sigma * 0.5 * e->dy * e->dy;
+                        tm->v[0] = v_sigma * (Y[0] * e->dx + Y[1] * e->dy);
+                        tm->v[1] = v_sigma * (Y[1] * e->dx + Y[2] * e->dy);
+                    } else {
+                        tm->v[8] = tm->v[0] = tm->v[1] = tm->v[2] = tm->v[3] = tm->v[4] = 0;
+                    }
+                }
+                errs[pix] = err;
+            }
+            free(rec);
+        }
+        /* pass 3: serial reduction in pixel order */
+        for (int64_t i = 0; i < tot; i++) {
+            int32_t g = terms[i].g;
+            for (int j = 0; j < 9; j++) {
+                v2d[9 * (int64_t)g + j] += terms[i].v[j];
+                if (a2d) a2d[9 * (int64_t)g + j] += fabs(terms[i].v[j]);
+            }
+        }
+        for (int64_t pix = 0; pix < P; pix++)
+            if (errs[pix] > max_err) max_err = errs[pix];
+        free(errs); free(terms); free(off); free(cnt);
+        free_camlist(&L);
+    }
+    if (T_replay_err) *T_replay_err = max_err;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* P1-P9: projection backward, summed over cameras (Q30).          */
+/* v2d is the 9-double layout of or_render_bwd.  Outputs fully overwritten:    */
+/* v_means [N,3], v_quats [N,4], v_scales [N,3], v_opac [N],                   */
+/* v_colors [N,K,3] (SH) or [N,3] (direct).                                    */
+/* ------------------------------------------------------------------------- */
+int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H, const float *means,
+                   const float *quats, const float *scales, const float *opacities, const float *colors,
+                   int32_t K, const float *viewmats, const float *Ks, const int32_t *radii, const double *v2d,
+                   double *v_means, double *v_quats, double *v_scales, double *v_opac, double *v_colors)
+{
+    int64_t stride = o->sh_degree >= 0 ? (int64_t)K * 3 : 3;
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; n++) {
+        double gm[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gs[3] = {0, 0, 0}, go = 0;
+        double *gc = &v_colors[stride * n];
+        for (int64_t j = 0; j < stride; j++) gc[j] = 0;
+        for (int64_t c = 0; c < C; c++) {
+            int64_t idx = c * N + n;
+            if (radii[2 * idx] <= 0 || radii[2 * idx + 1] <= 0) continue;
+            const double *vg = &v2d[9 * idx];
+            proj64_t P;
+            project64(o, W, H, means + 3 * n, quats + 4 * n, scales + 3 * n, opacities[n],
+                      colors + stride * n, K, viewmats + 16 * c, Ks + 9 * c, &P);
+            /* P1: o_eff = o * comp */
+            go += vg[8] * P.comp;
+            double v_comp = vg[8] * P.o;
+            /* P2: Y = Spb^-1, G_Y = [[vA, vB/2],[vB/2, vC]], v_Spb = -Y G_Y Y */
+            double Y[2][2] = {{P.conic[0], P.conic[1]}, {P.conic[1], P.conic[2]}};
+            double GY[2][2] = {{vg[2], 0.5 * vg[3]}, {0.5 * vg[3], vg[4]}};
+            double YG[2][2], vSp[2][2];
+            for (int i = 0; i < 2; i++)
+                for (int j = 0; j < 2; j++) YG[i][j] = Y[i][0] * GY[0][j] + Y[i][1] * GY[1][j];
+            for (int i = 0; i < 2; i++)
+                for (int j = 0; j < 2; j++) vSp[i][j] = -(YG[i][0] * Y[0][j] + YG[i][1] * Y[1][j]);
+            /* P3 (AA only): d comp / d Sigma' = comp/2 (Sigma'^-1 - Spb^-1) (derived from P:281) */
+            if (o->antialiased && P.det > 0) {
+                double Si[2][2] = {{P.Sp[1][1] / P.det, -P.Sp[0][1] / P.det},
+                                   {-P.Sp[1][0] / P.det, P.Sp[0][0] / P.det}};
+                for (int i = 0; i < 2; i++)
+                    for (int j = 0; j < 2; j++) vSp[i][j] += v_comp * 0.5 * P.comp * (Si[i][j] - Y[i][j]);
+            }
+            /* P4: v_Sc = J^T vSp J; v_J = vSp J Sc^T + vSp^T J Sc (Q11) */
+            double vSc[3][3], vJ[2][3];
+            for (int i = 0; i < 3; i++)
+                for (int j = 0; j < 3; j++) {
+                    double acc = 0;
+                    for (int k = 0; k < 2; k++)
+                        for (int l = 0; l < 2; l++) acc += P.J[k][i] * vSp[k][l] * P.J[l][j];
+                    vSc[i][j] = acc;
+                }
+            for (int i = 0; i < 2; i++)
+                for (int j = 0; j < 3; j++) {
+                    double acc = 0;
+                    for (int k = 0; k < 2; k++)
+                        for (int l = 0; l < 3; l++)
+                            acc += vSp[i][k] * P.J[k][l] * P.Sc[j][l] + vSp[k][i] * P.J[k][l] * P.Sc[l][j];
+                    vJ[i][j] = acc;
+                }
+            /* P5: v_t through J (exact derivative with the clamp of Q27)
+             * and through mu' (re-derived from P:790-791, Q10) */
+            double tx = P.t[0], ty = P.t[1], tz = P.t[2];
+            double fx = P.fx, fy = P.fy, tz2 = tz * tz, tz3 = tz2 * tz;
+            double vt[3] = {0, 0, 0};
+            vt[2] += -fx / tz2 * vJ[0][0] - fy / tz2 * vJ[1][1];
+            if (!P.clamp_x) {
+                vt[0] += -fx / tz2 * vJ[0][2];
+                vt[2] += 2.0 * fx * tx / tz3 * vJ[0][2];
+            } else {
+                vt[2] += fx * P.txc / tz3 * vJ[0][2];
+            }
+            if (!P.clamp_y) {
+                vt[1] += -fy / tz2 * vJ[1][2];
+                vt[2] += 2.0 * fy * ty / tz3 * vJ[1][2];
+            } else {
+                vt[2] += fy * P.tyc / tz3 * vJ[1][2];
+            }
+            vt[0] += fx / tz * vg[0];
+            vt[1] += fy / tz * vg[1];
+            vt[2] += -(fx * tx / tz2) * vg[0] - (fy * ty / tz2) * vg[1];
+            /* P6: v_mu += W^T v_t, v_Sigma = W^T v_Sc W */
+            for (int i = 0; i < 3; i++)
+                for (int k = 0; k < 3; k++) gm[i] += P.Wr[k][i] * vt[k];
+            double vS[3][3];
+            for (int i = 0; i < 3; i++)
+                for (int j = 0; j < 3; j++) {
+                    double acc = 0;
+                    for (int k = 0; k < 3; k++)
+                        for (int l = 0; l < 3; l++) acc += P.Wr[k][i] * vSc[k][l] * P.Wr[l][j];
+                    vS[i][j] = acc;
+                }
+            /* P7: colour */
+            const double *vrgb = &vg[5];
+            if (o->sh_degree >= 0) {
+                int deg = o->sh_degree, nb = (deg + 1) * (deg + 1);
+                double Yb[16], dY[16][3];
+                sh_basis(deg, P.dir[0], P.dir[1], P.dir[2], Yb);
+                sh_basis_grad(deg, P.dir[0], P.dir[1], P.dir[2], dY);
+                double vraw[3];
+                for (int ch = 0; ch < 3; ch++) vraw[ch] = P.raw[ch] > 0 ? vrgb[ch] : 0.0;
+                double vdir[3] = {0, 0, 0};
+                for (int j = 0; j < nb; j++) {
+                    double shv = 0;
+                    for (int ch = 0; ch < 3; ch++) {
+                        gc[3 * j + ch] += Yb[j] * vraw[ch];
+                        shv += (double)colors[stride * n + 3 * j + ch] * vraw[ch];
+                    }
+                    for (int d = 0; d < 3; d++) vdir[d] += dY[j][d] * shv;
+                }
+                /* dir = e/|e|, d dir/d mu = (I - dir dir^T)/|e| */
+                double dd = P.dir[0] * vdir[0] + P.dir[1] * vdir[1] + P.dir[2] * vdir[2];
+                for (int i = 0; i < 3; i++) gm[i] += (vdir[i] - P.dir[i] * dd) / P.enorm;
+            } else {
+                for (int ch = 0; ch < 3; ch++) gc[ch] += vrgb[ch];
+            }
+            /* P8: Sigma = M M^T -> v_M = (vS + vS^T) M; M = R S -> v_R = v_M S, v_s */
+            double vM[3][3];
+            for (int i = 0; i < 3; i++)
+                for (int j = 0; j < 3; j++) {
+                    double acc = 0;
+                    for (int k = 0; k < 3; k++) acc += (vS[i][k] + vS[k][i]) * P.M[k][j];
+                    vM[i][j] = acc;
+                }
+            for (int j = 0; j < 3; j++) {
+                double acc = 0;
+                for (int i = 0; i < 3; i++) acc += P.R[i][j] * vM[i][j];
+                gs[j] += acc;
+            }
+            double vR[3][3];
+            for (int i = 0; i < 3; i++)
+                for (int j = 0; j < 3; j++) vR[i][j] = vM[i][j] * P.s[j];
+            /* P9: dR/d(w,x,y,z) at q_hat, then the normalisation */
+            double w = P.qh[0], x = P.qh[1], y = P.qh[2], z = P.qh[3];
+            double dRw[3][3] = {{0, -z, y}, {z, 0, -x}, {-y, x, 0}};
+            double dRx[3][3] = {{0, y, z}, {y, -2 * x, -w}, {z, w, -2 * x}};
+            double dRy[3][3] = {{-2 * y, x, w}, {x, 0, z}, {-w, z, -2 * y}};
+            double dRz[3][3] = {{-2 * z, -w, x}, {w, -2 * z, y}, {x, y, 0}};
+            double vqh[4] = {0, 0, 0, 0};
+            for (int i = 0; i < 3; i++)
+                for (int j = 0; j < 3; j++) {
+                    vqh[0] += 2.0 * dRw[i][j] * vR[i][j];
+                    vqh[1] += 2.0 * dRx[i][j] * vR[i][j];
+                    vqh[2] += 2.0 * dRy[i][j] * vR[i][j];
+                    vqh[3] += 2.0 * dRz[i][j] * vR[i][j];
+                }
+            double dot = vqh[0] * P.qh[0] + vqh[1] * P.qh[1] + vqh[2] * P.qh[2] + vqh[3] * P.qh[3];
+            for (int i = 0; i < 4; i++) gq[i] += (vqh[i] - dot * P.qh[i]) / P.qn;
+        }
+        for (int i = 0; i < 3; i++) v_means[3 * n + i] = gm[i], v_scales[3 * n + i] = gs[i];
+        for (int i = 0; i < 4; i++) v_quats[4 * n + i] = gq[i];
+        v_opac[n] = go;
+    }
+    return 0;
+}
+
+int or_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void or_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
