@@ -1,0 +1,381 @@
+"""Benchmark of the gsplat hot path on B200 (BASELINE.json metric: megapixels/s of
+forward+backward, and the fraction of the roofline of the dominant kernel).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step = one pass of the whole hot path over one batch of synthetic views:
+gs_project -> gs_isect_tiles -> gs_rasterize_fwd -> gs_rasterize_bwd -> gs_project_bwd
+(+ one NCCL all-reduce of the flat parameter gradient when N > 1).  At N=1 the workload
+is BASELINE configs[1] ("garden1m": 1M Gaussians, SH degree 3, one 1297x840 view); with
+N ranks every rank renders its own view of the same scene (weak scaling).  Inputs are
+seeded synthetic scenes shaped like Mip-NeRF 360 (synth/scenes.py, DESIGN.md recipe).
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py runs it)
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "megapixels/sec fwd+bwd at 1/2/4/8 B200; fraction of HBM roofline"
+UNIT = "MP/s"
+SMS = 148
+FP32_LANES_PER_SM = 128
+# algorithmic FP32 instructions per pair
+OPS_EVAL = 13        # eval_alpha: 2 FSUB, 4 FMUL, 2 FFMA, 2 FSETP, MUFU.EX2, FMUL, FMNMX
+OPS_FWD_CONTRIB = 7  # 1-alpha, T*, compare, w, 3 FFMA
+OPS_BWD_CONTRIB = 36  # B2-B6 per composited pair
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm_gbs=float(d["hbm_gbs"]), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)), src="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7 and r[0].isdigit()]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def build_scene(cfg_name, world, rank, views_per_gpu):
+    from synth import scenes as S
+    cfg = S.CONFIGS[cfg_name]
+    # every rank draws the same Gaussians (same seed) and its own contiguous block of views
+    sc = S.mipnerf_like_scene(cfg["N"], cfg["width"], cfg["height"], views=views_per_gpu, sh_degree=cfg["sh_degree"],
+                              seed=cfg["seed"], view_offset=rank * views_per_gpu)
+    v_img, _ = S.image_grads(cfg["seed"] + rank, views_per_gpu, cfg["height"], cfg["width"])
+    return sc, v_img
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2409_06765_b200 import Engine, _lib as L
+
+    world, rank, local = _dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    cfg_name = args.config
+    sc, v_img = build_scene(cfg_name, world, rank, args.views_per_gpu)
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    keys = ["means", "quats", "scales", "opacities", "colors", "viewmats", "Ks"]
+    host = {k: torch.from_numpy(np.ascontiguousarray(sc[k], np.float32)).pin_memory() for k in keys}
+    host_v = torch.from_numpy(v_img).pin_memory()
+    params = tuple(host[k].to(dev) for k in keys)
+    v_dev = host_v.to(dev)
+    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # size the intersection capacity once (one sync), outside any timed region
+    eng.run_checked(params, v_dev)
+    torch.cuda.synchronize(dev)
+    M = eng.n_isect
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+
+    def step():
+        eng.step(params, v_dev)
+        if world > 1:
+            dist.all_reduce(eng.flat_grad)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-timed region: K steps, L2 flushed between steps (outside the events) ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        se = stage_ev[i]
+        se[0].record(stream)
+        eng.project(*params)
+        se[1].record(stream)
+        eng.isect()
+        se[2].record(stream)
+        eng.rasterize_fwd()
+        se[3].record(stream)
+        eng.rasterize_bwd(v_dev)
+        se[4].record(stream)
+        eng.project_bwd(*params)
+        se[5].record(stream)
+        if world > 1:
+            dist.all_reduce(eng.flat_grad)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(np.sum(step_ms))
+    names = ["project", "isect", "raster_fwd", "raster_bwd", "project_bwd"]
+    stage_ms = {n: float(np.mean([stage_ev[i][j].elapsed_time(stage_ev[i][j + 1]) for i in range(args.steps)]))
+                for j, n in enumerate(names)}
+    if int(eng.overflow.item()) != 0:
+        raise RuntimeError("intersection capacity overflowed inside the timed region")
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    mp_per_step = C * W * H / 1e6 * world
+    value = mp_per_step / (ms_per_step / 1e3)
+
+    # ---- work counts for the roofline (outside the timed region) ----
+    n_eval = torch.zeros((C, H, W), dtype=torch.int32, device=dev)
+    n_con = torch.zeros_like(n_eval)
+    L.gs_rasterize_stats(eng.opts, C, N, W, H, eng.splats, eng.isect_ids, eng.tile_offsets, n_eval, n_con)
+    torch.cuda.synchronize(dev)
+    E_f = int(n_eval.sum().item())
+    E_c = int(n_con.sum().item())
+    # pairs the backward walks per pixel: from its last composited index back to the range start
+    TX, TY = L.tiles(W, H)
+    ys = torch.arange(H, device=dev).view(H, 1) // 16
+    xs = torch.arange(W, device=dev).view(1, W) // 16
+    tile = (ys * TX + xs).view(1, H, W) + torch.arange(C, device=dev).view(C, 1, 1) * (TX * TY)
+    start = eng.tile_offsets[tile.long()]
+    E_b = int((eng.last_ids - start + 1).clamp(min=0).sum().item())
+    V = int((eng.radii[..., 0] > 0).sum().item())
+
+    peaks = _peaks()
+    clk_mhz = peaks["sm_max_mhz"]
+    alu_peak = SMS * FP32_LANES_PER_SM * clk_mhz * 1e6 / 1e12          # T FP32 instr/s
+    alu = {
+        "raster_fwd": (OPS_EVAL * E_f + OPS_FWD_CONTRIB * E_c) / 1e12,
+        "raster_bwd": (OPS_EVAL * E_b + OPS_BWD_CONTRIB * E_c) / 1e12,
+    }
+    # algorithmic HBM bytes per launch (SURVEY 8d formulas)
+    Kc = 16 if sc["sh_degree"] == 3 else (sc["sh_degree"] + 1) ** 2
+    P = C * W * H
+    hbm = {
+        "project": N * 44 + N * 12 * Kc + C * N * (48 + 8),
+        "isect": C * N * 8 + V * 8 * 2 * 4 + M * 8 + M * 8 * 2 * 2 + M * 4,
+        "project_bwd": C * N * (48 + 8) + N * (44 + 12 * Kc) + N * (44 + 12 * Kc),
+    }
+    dom = max(stage_ms, key=stage_ms.get)
+    if dom in alu:
+        ach = alu[dom] / (stage_ms[dom] / 1e3)
+        roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2),
+                "unit": "T FP32 instr/s", "frac": round(ach / alu_peak, 4), "traffic": None,
+                "peak_src": f"{SMS} SMs x {FP32_LANES_PER_SM} FP32 lanes x {clk_mhz:.0f} MHz ({peaks['src']})",
+                "work": {"E_eval": E_f, "E_contrib": E_c, "E_bwd": E_b}}
+    else:
+        ach = hbm[dom] / (stage_ms[dom] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_src": peaks["src"]}
+    per_stage = {}
+    for n_, ms in stage_ms.items():
+        d = {"ms": round(ms, 4)}
+        if n_ in hbm:
+            d["hbm_frac"] = round(hbm[n_] / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)
+        if n_ in alu:
+            d["alu_frac"] = round(alu[n_] / (ms / 1e3) / alu_peak, 4)
+        per_stage[n_] = d
+
+    # ---- end to end through the public API with HOST buffers (pinned), every step ----
+    e2e = None
+    if not args.no_e2e:
+        out_host = torch.empty(eng.out_rgb.shape, dtype=torch.float32).pin_memory()
+        grad_host = torch.empty(eng.flat_grad.shape, dtype=torch.float32).pin_memory()
+        dev_params = list(params)
+        bi = sum(t.numel() * 4 for t in host.values()) + host_v.numel() * 4
+        bo = out_host.numel() * 4 + grad_host.numel() * 4
+        e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()
+            e_ev[i][0].record(stream)
+            for dst, k in zip(dev_params, keys):
+                dst.copy_(host[k], non_blocking=True)
+            v_dev.copy_(host_v, non_blocking=True)
+            eng.step(tuple(dev_params), v_dev)
+            if world > 1:
+                dist.all_reduce(eng.flat_grad)
+            out_host.copy_(eng.out_rgb, non_blocking=True)
+            grad_host.copy_(eng.flat_grad, non_blocking=True)
+            e_ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = float(np.sum([a.elapsed_time(b) for a, b in e_ev]))
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": round(mp_per_step / (e_ms / args.steps / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "ms_per_step": round(e_ms / args.steps, 4)}
+
+    tile_passes = (max(1, (C * TX * TY - 1).bit_length()) + 7) // 8
+    launches = 1 + 3 + 3 * 4 + 3 + 3 * tile_passes + 2 + 1 + 1 + 1
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(sc, v_img, budget_s=args.cpu_budget)
+
+    res = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Mip-NeRF-360-shaped scene)",
+        "config": {"workload": f"{cfg_name}: {N} Gaussians SH{sc['sh_degree']}, {args.views_per_gpu} view(s) of "
+                               f"{W}x{H} per GPU (BASELINE configs[1])", "global_batch_views": C * world,
+                   "width": W, "height": H, "n_gaussians": N, "parallelism": f"views dp{world}",
+                   "l2": "flushed between steps (256 MiB write outside the per-step events)",
+                   "V_visible": V, "M_isect": M, "pairs_eval": E_f, "pairs_contrib": E_c},
+        "roofline": roof, "stages": per_stage, "gpu_launches": launches * args.steps,
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_baseline(sc, v_img, budget_s=15.0, min_tiles=2):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload:
+    full projection + projection backward of every Gaussian, compositing forward and
+    backward on a seeded subset of tiles (v_img masked to those tiles)."""
+    import oracle
+    from synth import scenes as S
+    oracle.build()
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    o = oracle.Options(sh_degree=sc["sh_degree"])
+
+    def run(n_tiles):
+        mask = S.tile_subset_mask(0, C, W, H, n_tiles)
+        t0 = time.perf_counter()
+        p = oracle.project(sc, o)
+        f = oracle.render_fwd(p, C, N, W, H, o, tile_mask=mask)
+        b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64), tile_mask=mask)
+        oracle.project_bwd(sc, p, b["v2d"], o)
+        dt = time.perf_counter() - t0
+        px = int(np.repeat(np.repeat(mask, 16, 1), 16, 2)[:, :H, :W].sum())
+        return dt, px
+
+    dt, px = run(min_tiles)
+    n = max(min_tiles, int(min_tiles * budget_s / max(dt, 1e-3)))
+    TT = ((W + 15) // 16) * ((H + 15) // 16)
+    n = min(n, TT)
+    if n > min_tiles:
+        dt, px = run(n)
+    return {"value": round(px / 1e6 / dt, 6), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{n} of {((W + 15) // 16) * ((H + 15) // 16)} tiles per view ({px} px) composited fwd+bwd, "
+                      f"plus projection fwd+bwd of all {N} Gaussians; {dt:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    sc, v_img = build_scene(args.config, 1, 0, args.views_per_gpu)
+    C, W, H = sc["viewmats"].shape[0], sc["width"], sc["height"]
+    per = max(1.0, args.cpu_budget / max(1, args.steps + args.warmup))
+    vals = []
+    cpu = None
+    for i in range(args.warmup + args.steps):
+        cpu = cpu_baseline(sc, v_img, budget_s=per)
+        if i >= args.warmup:
+            vals.append(cpu["value"])
+    v = float(np.mean(vals))
+    res = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(C * W * H / 1e6 / v * 1e3, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded Mip-NeRF-360-shaped scene)",
+           "config": {"workload": f"{args.config} (oracle on a bounded tile sample)", "width": W, "height": H},
+           "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": cpu["cores"], "kind": "oracle",
+                            "sample": cpu["sample"]},
+           "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="garden1m")
+    ap.add_argument("--views-per-gpu", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * gs.h -- C-ABI of libgsplat_b200: the B200 (sm_100a) hot path of the differentiable
+ * tile-based 3D Gaussian Splatting rasterizer described in "gsplat: An Open-Source
+ * Library for Gaussian Splatting" (arXiv 2409.06765).
+ *
+ * Citations "P:n" are lines of the paper text; step names F*, I*, R*, B*,
+ * P* are SURVEY.md Appendix A, which restates the paper step by step; "Qn" are the
+ * readings of ambiguous passages listed in DESIGN.md.
+ *
+ * The calls follow the paper's user-level statement (Fig. 1)
+ *     rgb, alpha, meta = rasterization(means, quats, scales, opacities, colors,
+ *                                      viewmats, Ks, width, height)
+ * split into the four stages of the method:
+ *     gs_project        projection of every (camera, Gaussian)          (App. B.1)
+ *     gs_isect_tiles    tile keys, on-device radix sort, tile ranges      (App. B.2)
+ *     gs_rasterize_fwd  front-to-back alpha compositing per pixel         (App. B.2)
+ *     gs_rasterize_bwd  back-to-front gradient walk per pixel             (App. C.2)
+ *     gs_project_bwd    gradients back through the projection             (App. C.3-C.4)
+ *
+ * CONVENTIONS (all entry points)
+ *  - Every array argument is a DEVICE pointer to C-contiguous row-major storage
+ *    (fp32 unless stated), 16-byte aligned.  The caller allocates every buffer,
+ *    outputs and workspace alike; the library allocates nothing and keeps no mutable
+ *    global state (re-entrant, thread-safe).  Ownership never transfers.
+ *  - Every call is asynchronous and stream-ordered on `stream` (a cudaStream_t passed
+ *    as void*; NULL = the legacy default stream).  No call synchronizes the host.
+ *  - Outputs are fully overwritten.  Gradient outputs are zero-filled by the library
+ *    before accumulation.
+ *  - Argument errors return GS_ERR_INVALID_ARGUMENT (NULL required pointer, N < 0,
+ *    C < 1, width/height < 1, misaligned pointer, sh_degree > 3, K < (d+1)^2, too small
+ *    workspace); tile_size != 16 returns GS_ERR_UNSUPPORTED; a failed launch returns
+ *    GS_ERR_CUDA (gs_last_error() holds the CUDA message, per thread).  Per-element
+ *    degeneracies (zero/non-finite quaternion, depth outside [near, far], det <= 0,
+ *    off-screen) are never errors: the element is culled (radii = 0).
+ *  - Gaussian parameters are ACTIVATED values (scales > 0, opacities in
+ *    [0,1]); quaternions (w,x,y,z) need not be normalised (F1 normalises).
+ *    Gradients are with respect to the arguments as passed (Q8).
+ *  - viewmats [C,4,4] map world to camera (t = W mu + w, Q1), OpenCV axes; Ks [C,3,3]
+ *    = [[fx,0,cx],[0,fy,cy],[0,0,1]] (Q2); pixel (i,j) has centre (i+0.5, j+0.5).
+ */
+#ifndef GSPLAT_B200_GS_H
+#define GSPLAT_B200_GS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GS_API __attribute__((visibility("default")))
+#else
+#define GS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GS_OK = 0,
+    GS_ERR_INVALID_ARGUMENT = 1,
+    GS_ERR_UNSUPPORTED = 2,
+    GS_ERR_CAPACITY = 3,
+    GS_ERR_CUDA = 4
+} gs_status;
+
+/* Method constants (gs_default_options fills the defaults). */
+typedef struct gs_options {
+    float near_plane;   /* 0.01  cull iff depth < near (strict; Q18, Fig. 1)          */
+    float far_plane;    /* 1e10  cull iff depth > far                                     */
+    float eps2d;        /* 0.3   low-pass s added to Sigma' in both modes  */
+    float alpha_max;    /* 0.99  opacity saturation (north_star; Q13)                     */
+    float alpha_min;    /* 1/255 skip a splat at a pixel iff alpha < alpha_min (Q14)       */
+    float t_min;        /* 1e-4  stop iff T(1-alpha) <= t_min, not composited (Q15)        */
+    int32_t tile_size;  /* 16 only                                                */
+    int32_t antialiased;/* 0 classic | 1 opacity x sqrt(det S'/det(S'+sI))     */
+    int32_t sh_degree;  /* -1: colors are RGB [N,3]; 0..3: colors are SH [N,K,3]   */
+    int32_t bbox_mode;  /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3 sqrt(lambda_max)     */
+    int32_t fov_clamp;  /* 1 clamp t_x/t_z, t_y/t_z to the widened frustum for J only (Q27)*/
+    int32_t reserved;   /* must be 0                                                      */
+} gs_options;
+
+/* ---- Projected splat record ------------------------------------------------------
+ * gs_project writes one 48-byte record per (camera c, Gaussian n) at
+ * splats[(c*N + n)*GS_SPLAT_FLOATS + k]:
+ *   k=0,1  mean2d (mu'_x, mu'_y), pixel coordinates (F11)
+ *   k=2    opac_eff = opacity * comp (F15)
+ *   k=3    depth = t_z (F4)
+ *   k=4..6 conic (A, B, C) = (Sigma' + s I)^-1 = [[A,B],[B,C]] (F10)
+ *   k=7    comp (1 in classic mode)
+ *   k=8..10 rgb (F14)
+ *   k=11   0
+ * Culled records (radii == 0) are all zeros.  gs_rasterize_bwd writes gradients in the
+ * SAME slot layout (v_mean2d in 0,1; v_opac_eff in 2; v_conic in 4..6; v_rgb in 8..10;
+ * slot 3 = d/d depth (0 unless depth rendering), slots 7 and 11 = absgrad |v_mean2d|
+ * sums (NEXT-1, 0 unless requested)). */
+#define GS_SPLAT_FLOATS 12
+
+GS_API void gs_default_options(gs_options* opt);
+GS_API const char* gs_status_string(int32_t status);
+GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
+GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
+#define GS_ABI_VERSION 1
+
+/* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
+ * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
+ *      colors [N,K,3] (sh_degree >= 0, K >= (d+1)^2) or [N,3] (sh_degree = -1; K ignored),
+ *      viewmats [C,4,4], Ks [C,3,3].
+ * Out: radii [C,N,2] int32 (per-axis pixel radius; 0 = culled),
+ *      splats [C,N,GS_SPLAT_FLOATS] (record layout above).
+ * The fp32 "key path" (mean2d, depth, radii) uses a fixed IEEE op order without FMA
+ * contraction (Q28) so tile keys are reproducible bit for bit. */
+GS_API gs_status gs_project(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
+                     const float* means, const float* quats, const float* scales,
+                     const float* opacities, const float* colors, int32_t K,
+                     const float* viewmats, const float* Ks,
+                     int32_t* radii, float* splats, void* stream);
+
+/* ---- Stage 2: tile intersection + on-device radix sort + tile ranges (I1-I4)
+ * Each visible (c,n) is binned into every 16x16 tile its 3-sigma rectangle touches
+ * (Q20).  The result is ordered by (camera, tile, depth, c*N+n) ascending (Q16).
+ * In : radii, splats from gs_project (reads mean2d and depth).
+ * Out: *M (device int64)        total number of intersections (may exceed M_capacity)
+ *      *overflow (device int32) 1 iff *M > M_capacity (then the outputs are truncated
+ *                               and must be recomputed with a larger capacity)
+ *      isect_ids [M_capacity]   flat id c*N+n of each intersection, in sorted order
+ *      isect_keys [M_capacity]  (optional, NULL to skip) the 64-bit key
+ *                               (c << (32+B)) | (tile << 32) | bits(depth_f32),
+ *                               B = ceil(log2(TX*TY))
+ *      tile_offsets [C*TY*TX+1] int32: intersections of tile t of camera c are
+ *                               [tile_offsets[c*TY*TX+t], tile_offsets[c*TY*TX+t+1])
+ * workspace: at least gs_isect_workspace_size(C, N, width, height, M_capacity) bytes,
+ * 256-byte aligned, contents undefined on entry and exit. */
+GS_API size_t gs_isect_workspace_size(int32_t C, int64_t N, int32_t width, int32_t height, int64_t M_capacity);
+GS_API gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                         const int32_t* radii, const float* splats, int64_t M_capacity,
+                         int64_t* M, int32_t* overflow, int32_t* isect_ids, uint64_t* isect_keys,
+                         int32_t* tile_offsets, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- Stage 3: forward composite (R1-R3) ---------------------------------
+ * Per pixel p = (i+0.5, j+0.5), front to back over its tile's range:
+ *   sigma = 1/2 (A dx^2 + C dy^2) + B dx dy, (dx,dy) = mu' - p; alpha = min(alpha_max,
+ *   opac_eff exp(-sigma)); skip alpha < alpha_min; stop when T(1-alpha) <= t_min;
+ *   color += rgb alpha T; T *= (1 - alpha).  out = color + T bg.
+ * In : splats, isect_ids, tile_offsets; backgrounds [C,3] or NULL (black).
+ * Out: out_rgb [C,H,W,3], out_alpha [C,H,W] (= 1 - T), out_T [C,H,W] (final
+ *      transmittance, saved for the backward: P:605), last_ids [C,H,W] int32 (index into
+ *      isect_ids of the last composited splat; tile_offsets[tile]-1 if none). */
+GS_API gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                           const float* splats, const float* backgrounds, const int32_t* isect_ids,
+                           const int32_t* tile_offsets, float* out_rgb, float* out_alpha, float* out_T,
+                           int32_t* last_ids, void* stream);
+
+/* ---- Diagnostics (not on the hot path): per-pixel work counts of stage 3 ---------
+ * Runs the forward walk of gs_rasterize_fwd and writes, per pixel, n_eval [C,H,W] (pairs
+ * whose alpha was evaluated, up to and including the terminating one) and n_contrib
+ * [C,H,W] (pairs composited).  bench.py uses the sums as the algorithmic work of K6/K7. */
+GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                                    const float* splats, const int32_t* isect_ids, const int32_t* tile_offsets,
+                                    int32_t* n_eval, int32_t* n_contrib, void* stream);
+
+/* ---- Stage 4a: backward composite (B1-B6) -------------------------------
+ * Back to front from last_ids with T_{n-1} = T_n/(1-alpha_{n-1}) and the S
+ * recurrence; per-(c,n) sums over pixels are accumulated with fp32 atomics.
+ * In : as gs_rasterize_fwd plus out_T, last_ids, v_out_rgb [C,H,W,3],
+ *      v_out_alpha [C,H,W] or NULL.
+ * Out: v_splats [C,N,GS_SPLAT_FLOATS] (zero-filled here, then accumulated; slot layout
+ *      above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 7, 11. */
+GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                           const float* splats, const float* backgrounds, const int32_t* isect_ids,
+                           const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
+                           const float* v_out_rgb, const float* v_out_alpha, int32_t absgrad,
+                           float* v_splats, void* stream);
+
+/* ---- Stage 4b: projection backward (P1-P9) -------------------------------
+ * In : the gs_project inputs, its radii output, v_splats from gs_rasterize_bwd.
+ * Out: v_means [N,3], v_quats [N,4], v_scales [N,3], v_opacities [N],
+ *      v_colors (same shape as colors).  Summed over the C cameras inside one thread per
+ *      Gaussian (deterministic; Q30); Gaussians culled in every camera get zeros. */
+GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
+                         const float* means, const float* quats, const float* scales,
+                         const float* opacities, const float* colors, int32_t K,
+                         const float* viewmats, const float* Ks, const int32_t* radii,
+                         const float* v_splats, float* v_means, float* v_quats, float* v_scales,
+                         float* v_opacities, float* v_colors, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSPLAT_B200_GS_H */

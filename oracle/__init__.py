@@ -52,8 +52,8 @@ class Options:
     alpha_max: float = 0.99        # north_star "opacity saturation at 0.99" (Q13)
     alpha_min: float = 1.0 / 255.0  # Q14
     t_min: float = 1e-4            # Q15
-    amb_rel_alpha: float = 1e-4    # ambiguity margins for parity masks
-    amb_rel_t: float = 1e-3
+    amb_rel_alpha: float = 1e-6    # ambiguity margins for parity masks (Q28b):
+    amb_rel_t: float = 1e-3        #   ex2.approx ulps on alpha; fp32 T product on T
     tile_size: int = 16
     antialiased: int = 0
     sh_degree: int = 3
@@ -75,11 +75,11 @@ def lib():
         _lib = ct.CDLL(build())
         P = ct.c_void_p
         i64, i32, dbl = ct.c_int64, ct.c_int32, ct.c_double
-        _lib.or_project.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32, P, P] + [P] * 9
+        _lib.or_project.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32, P, P] + [P] * 10
         _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
         _lib.or_isect.restype = i64
-        _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 9 + [P] * 6
-        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 9 + [P] * 6
+        _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6
         _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6
         _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
@@ -142,13 +142,14 @@ def project(scene, opts: Options):
     K = colors.shape[1] if colors.ndim == 3 else 1
     out = dict(
         radii=np.zeros((C, N, 2), np.int32), mean2d_f=np.zeros((C, N, 2), np.float32),
-        depth_f=np.zeros((C, N), np.float32), mean2d=np.zeros((C, N, 2)), depth=np.zeros((C, N)),
+        depth_f=np.zeros((C, N), np.float32), dec=np.zeros((C, N, 4), np.float32),
+        mean2d=np.zeros((C, N, 2)), depth=np.zeros((C, N)),
         conic=np.zeros((C, N, 3)), comp=np.zeros((C, N)), opac_eff=np.zeros((C, N)),
         rgb=np.zeros((C, N, 3)))
     o = opts.c()
     lib().or_project(ct.byref(o), N, C, W, H, _p(means), _p(quats), _p(scales), _p(opac), _p(colors), K,
                      _p(viewmats), _p(Ks), _p(out["radii"]), _p(out["mean2d_f"]), _p(out["depth_f"]),
-                     _p(out["mean2d"]), _p(out["depth"]), _p(out["conic"]), _p(out["comp"]),
+                     _p(out["dec"]), _p(out["mean2d"]), _p(out["depth"]), _p(out["conic"]), _p(out["comp"]),
                      _p(out["opac_eff"]), _p(out["rgb"]))
     return out
 
@@ -176,7 +177,7 @@ def render_fwd(proj, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None
                last_gid=np.zeros((C, H, W), np.int64), ambig=np.zeros((C, H, W), np.uint8),
                ncontrib=np.zeros((C, H, W), np.int32))
     lib().or_render_fwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
-                        _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
+                        _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(out["rgb"]), _p(out["alpha"]), _p(out["T"]), _p(out["last_gid"]),
                         _p(out["ambig"]), _p(out["ncontrib"]))
     return out
@@ -193,7 +194,7 @@ def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds
     v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); amb = np.zeros((C, N), np.uint8)
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
-                        _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
+                        _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(amb), ct.byref(err))
     return dict(v2d=v2d, a2d=a2d, g_ambig=amb, T_replay_err=err.value)
 

@@ -167,12 +167,15 @@ typedef struct {
     int   visible;
     int   rx, ry;
     float mx, my, depth;
+    /* decision path (Q28b): the fp32 conic and effective opacity the kernel's threshold
+     * decisions are taken from */
+    float conic[3], opac;
 } keypath_t;
 
 static keypath_t key_path_f32(const or_opts *o, int W, int H, const float *mu, const float *q,
-                              const float *s, const float *vm /*4x4*/, const float *Kc /*3x3*/)
+                              const float *s, float op, const float *vm /*4x4*/, const float *Kc /*3x3*/)
 {
-    keypath_t kp = {0, 0, 0, 0.f, 0.f, 0.f};
+    keypath_t kp = {0, 0, 0, 0.f, 0.f, 0.f, {0.f, 0.f, 0.f}, 0.f};
     /* KP1 (F3): t = W mu + w */
     float tx = ((vm[0] * mu[0] + vm[1] * mu[1]) + vm[2] * mu[2]) + vm[3];
     float ty = ((vm[4] * mu[0] + vm[5] * mu[1]) + vm[6] * mu[2]) + vm[7];
@@ -253,6 +256,16 @@ static keypath_t key_path_f32(const or_opts *o, int W, int H, const float *mu, c
         return kp;
     if (!isfinite(mx) || !isfinite(my)) return kp;
     kp.visible = 1; kp.rx = rx; kp.ry = ry; kp.mx = mx; kp.my = my; kp.depth = tz;
+    /* KP15 (F9, F10, F15 in fp32): conic and effective opacity for the decisions */
+    kp.conic[0] = c / det;
+    kp.conic[1] = -b / det;
+    kp.conic[2] = a / det;
+    float comp = 1.f;
+    if (o->antialiased) {
+        float det_raw = Sp[0][0] * Sp[1][1] - Sp[0][1] * Sp[0][1];
+        comp = sqrtf(fmaxf(0.f, det_raw / det));
+    }
+    kp.opac = op * comp;
     return kp;
 }
 
@@ -404,7 +417,7 @@ static void project64(const or_opts *o, int W, int H, const float *mu, const flo
 int or_project(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H, const float *means,
                const float *quats, const float *scales, const float *opacities, const float *colors,
                int32_t K, const float *viewmats, const float *Ks,
-               int32_t *radii, float *mean2d_f, float *depth_f,
+               int32_t *radii, float *mean2d_f, float *depth_f, float *dec,
                double *mean2d, double *depth, double *conic, double *comp, double *opac_eff, double *rgb)
 {
     int64_t stride = o->sh_degree >= 0 ? (int64_t)K * 3 : 3;
@@ -412,7 +425,9 @@ int or_project(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H, con
     for (int64_t idx = 0; idx < (int64_t)C * N; idx++) {
         int64_t c = idx / N, n = idx % N;
         const float *vm = viewmats + 16 * c, *Kc = Ks + 9 * c;
-        keypath_t kp = key_path_f32(o, W, H, means + 3 * n, quats + 4 * n, scales + 3 * n, vm, Kc);
+        keypath_t kp = key_path_f32(o, W, H, means + 3 * n, quats + 4 * n, scales + 3 * n, opacities[n], vm, Kc);
+        for (int i = 0; i < 3; i++) dec[4 * idx + i] = kp.visible ? kp.conic[i] : 0.f;
+        dec[4 * idx + 3] = kp.visible ? kp.opac : 0.f;
         radii[2 * idx] = kp.visible ? kp.rx : 0;
         radii[2 * idx + 1] = kp.visible ? kp.ry : 0;
         mean2d_f[2 * idx] = kp.visible ? kp.mx : 0.f;
@@ -565,6 +580,7 @@ static void free_camlist(camlist_t *L)
 typedef struct {
     int64_t li;      /* list index */
     double alpha, T, G, sigma, dx, dy;
+    int clamped;     /* alpha saturated at alpha_max (decision path) */
 } contrib_t;
 
 typedef struct {
@@ -575,37 +591,64 @@ typedef struct {
     int64_t ncontrib;
 } pixres_t;
 
+/* Decision path (reading Q28b).  The three threshold decisions of R2 -- skip when
+ * alpha < alpha_min (Q14), saturate at alpha_max (Q13), stop when T(1-alpha) <= t_min
+ * (Q15) -- decide which splats a pixel composites, i.e. they decide an integer.  They
+ * are therefore taken in the kernel's precision: the exponent -sigma*log2(e) is formed
+ * in fp32 from the fp32 conic and fp32 pixel offset with the kernel's op order (conic
+ * pre-scaled by -log2(e)/2, -log2(e), -log2(e)/2; p = fma(b', dx dy, fma(a', dx^2, c' dy^2))),
+ * then exponentiated exactly (the kernel's ex2.approx differs by a few ulp, which the
+ * ambiguity margins cover).  Values are still fp64.  Returns o_f32 * 2^p, or -1 when
+ * p > 0 (sigma < 0, skipped). */
+static double decision_raw(const float *dec4, const float *m2f, int px, int py)
+{
+    const float ka = -0.5f * 1.4426950408889634f, kb = -1.4426950408889634f;
+    float a = ka * dec4[0], b = kb * dec4[1], cc = ka * dec4[2];
+    float dx = m2f[0] - ((float)px + 0.5f), dy = m2f[1] - ((float)py + 0.5f);
+    float p = fmaf(b, dx * dy, fmaf(a, dx * dx, cc * (dy * dy)));
+    if (p > 0.f) return -1.0;
+    return (double)dec4[3] * exp2((double)p);
+}
+
 static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, int64_t N, int px, int py,
-                              const double *mean2d, const double *conic, const double *opac_eff,
-                              const double *rgb, contrib_t *rec, int64_t rec_cap)
+                              const float *mean2d_f, const float *dec, const double *mean2d,
+                              const double *conic, const double *opac_eff, const double *rgb, contrib_t *rec,
+                              int64_t rec_cap)
 {
     pixres_t r = {{0, 0, 0}, 1.0, -1, L->count, 0, 0};
     int tx = px / o->tile_size, ty = py / o->tile_size;
     double p[2] = {px + 0.5, py + 0.5};            /* R1: pixel centre */
-    double T = 1.0;
+    const double amax = (float)o->alpha_max, amin = (float)o->alpha_min, tmin = (float)o->t_min;
+    double T = 1.0, Tdec = 1.0;
     for (int64_t i = 0; i < L->count; i++) {
         const int32_t *rc = &L->rect[4 * i];
         if (tx < rc[0] || tx >= rc[1] || ty < rc[2] || ty >= rc[3]) continue;   /* tile predicate */
         int64_t g = c * N + L->n[i];
+        /* decisions (kernel precision) */
+        double raw_d = decision_raw(&dec[4 * g], &mean2d_f[2 * g], px, py);
+        if (raw_d < 0) continue;                                              /* sigma < 0 */
+        if (fabs(raw_d - amin) <= o->amb_rel_alpha * amin) r.ambig = 1;
+        if (fabs(raw_d - amax) <= o->amb_rel_alpha * amax) r.ambig = 1;
+        int clamped = !(raw_d < amax);
+        double alpha_d = clamped ? amax : raw_d;
+        if (alpha_d < amin) continue;                                         /* Q14 */
+        double nT_d = Tdec * (1.0 - alpha_d);
+        if (fabs(nT_d - tmin) <= o->amb_rel_t * tmin) r.ambig = 1;
+        if (nT_d <= tmin) { r.end_li = i + 1; break; }                        /* Q15 */
+        /* values (fp64) */
         double dx = mean2d[2 * g] - p[0], dy = mean2d[2 * g + 1] - p[1];     /* Delta = mu' - p (Q21) */
         const double *Y = &conic[3 * g];
         double sigma = 0.5 * (Y[0] * dx * dx + Y[2] * dy * dy) + Y[1] * dx * dy;
-        if (sigma < 0) continue;
         double G = exp(-sigma);
-        double raw = opac_eff[g] * G;
-        if (fabs(raw - o->alpha_min) <= o->amb_rel_alpha * o->alpha_min) r.ambig = 1;
-        if (fabs(raw - o->alpha_max) <= o->amb_rel_alpha * o->alpha_max) r.ambig = 1;
-        double alpha = raw < o->alpha_max ? raw : o->alpha_max;
-        if (alpha < o->alpha_min) continue;                                   /* Q14 */
-        double nT = T * (1.0 - alpha);
-        if (fabs(nT - o->t_min) <= o->amb_rel_t * o->t_min) r.ambig = 1;
-        if (nT <= o->t_min) { r.end_li = i + 1; break; }                      /* Q15 */
+        double alpha = clamped ? o->alpha_max : opac_eff[g] * G;
         if (rec && r.ncontrib < rec_cap) {
             contrib_t *e = &rec[r.ncontrib];
             e->li = i; e->alpha = alpha; e->T = T; e->G = G; e->sigma = sigma; e->dx = dx; e->dy = dy;
+            e->clamped = clamped;
         }
         for (int ch = 0; ch < 3; ch++) r.rgb[ch] += rgb[3 * g + ch] * alpha * T;
-        T = nT;
+        T = T * (1.0 - alpha);
+        Tdec = nT_d;
         r.last_li = i;
         r.ncontrib++;
     }
@@ -622,7 +665,8 @@ static int tile_selected(const uint8_t *tile_mask, int64_t c, int TX, int TY, in
 /* R1-R3 for every (selected) pixel.  out_last_gid = flat id c*N+n of the last
  * composited splat, -1 if none. Unselected pixels get rgb=bg, T=1, gid=-1. */
 int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
-                  const float *mean2d_f, const float *depth_f, const double *mean2d, const double *conic,
+                  const float *mean2d_f, const float *depth_f, const float *dec, const double *mean2d,
+                  const double *conic,
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   double *out_rgb, double *out_alpha, double *out_T, int64_t *out_last_gid,
                   uint8_t *out_ambig, int32_t *out_ncontrib)
@@ -643,7 +687,7 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 if (out_ncontrib) out_ncontrib[oi] = 0;
                 continue;
             }
-            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d, conic, opac_eff, rgb, NULL, 0);
+            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL, 0);
             for (int ch = 0; ch < 3; ch++) out_rgb[3 * oi + ch] = r.rgb[ch] + r.T * (b ? b[ch] : 0.0);  /* R3, Q25 */
             out_alpha[oi] = 1.0 - r.T;
             out_T[oi] = r.T;
@@ -663,14 +707,16 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
 /* written to per-pixel slots and summed serially in pixel order.              */
 /* v2d layout per flat id g, 9 doubles:                                        */
 /*   [0,1] v_mean2d  [2,3,4] v_conic (A,B,C)  [5,6,7] v_rgb  [8] v_opac_eff     */
-/* a2d: same layout, sum over pixels of |term| (the condition floor)*/
+/* a2d: same layout, sum over pixels of |term| with B4's v_alpha replaced by the */
+/* sum of the magnitudes of its parts (the fp32 condition floor)    */
 /* g_ambig[g] = 1 if g was evaluated at an ambiguous pixel.                     */
 /* T_replay_err (optional) = max |T_replayed - T_forward| over all steps.      */
 /* ------------------------------------------------------------------------- */
-typedef struct { int32_t g; double v[9]; } term_t;
+typedef struct { int32_t g; double v[9], va[9]; } term_t;
 
 int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
-                  const float *mean2d_f, const float *depth_f, const double *mean2d, const double *conic,
+                  const float *mean2d_f, const float *depth_f, const float *dec, const double *mean2d,
+                  const double *conic,
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   const double *v_img, const double *v_alpha_img, double *v2d, double *a2d,
                   uint8_t *g_ambig, double *T_replay_err)
@@ -690,7 +736,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
         for (int64_t pix = 0; pix < P; pix++) {
             int px = (int)(pix % W), py = (int)(pix / W);
             if (!tile_selected(tile_mask, c, TX, TY, px, py, T)) continue;
-            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d, conic, opac_eff, rgb, NULL, 0);
+            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL, 0);
             cnt[pix] = (int32_t)r.ncontrib;
             if (r.ambig && g_ambig) {
                 /* mark every splat this pixel evaluated (in-tile, up to termination) */
@@ -723,7 +769,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     cap = cnt[pix];
                     rec = (contrib_t *)realloc(rec, sizeof(contrib_t) * cap);
                 }
-                pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d, conic, opac_eff, rgb, rec, cap);
+                pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, rec, cap);
                 int64_t oi = c * P + pix;
                 const double *vC = &v_img[3 * oi];
                 double vA = v_alpha_img ? v_alpha_img[oi] : 0.0;
@@ -745,12 +791,18 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     term_t *tm = &terms[off[pix] + k];
                     tm->g = (int32_t)g;
                     for (int ch = 0; ch < 3; ch++) tm->v[5 + ch] = fac * vC[ch];   /* B3 */
+                    for (int ch = 0; ch < 3; ch++) tm->va[5 + ch] = fabs(tm->v[5 + ch]);
                     double v_alpha = 0;                                            /* B4 */
                     for (int ch = 0; ch < 3; ch++) v_alpha += (rgb[3 * g + ch] * Tn - S[ch] * ra) * vC[ch];
                     v_alpha += -Tfin * ra * bgdot + Tfin * ra * vA;
+                    /* magnitude of B4 before its internal cancellation (c T vs S/(1-alpha)):
+                     * the condition floor a2d of the v_alpha-dependent gradients uses it */
+                    double v_alpha_abs = fabs(Tfin * ra * bgdot) + fabs(Tfin * ra * vA);
+                    for (int ch = 0; ch < 3; ch++)
+                        v_alpha_abs += fabs(rgb[3 * g + ch] * Tn * vC[ch]) + fabs(S[ch] * ra * vC[ch]);
+
                     for (int ch = 0; ch < 3; ch++) S[ch] += rgb[3 * g + ch] * fac;  /* B5 */
-                    double raw = opac_eff[g] * e->G;
-                    if (raw < o->alpha_max) {                                    /* B6 (Q24) */
+                    if (!e->clamped) {                                           /* B6 (Q24) */
                         tm->v[8] = e->G * v_alpha;
                         double v_sigma = -opac_eff[g] * e->G * v_alpha;
                         const double *Y = &conic[3 * g];
@@ -759,8 +811,16 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                         tm->v[4] = v_sigma * 0.5 * e->dy * e->dy;
                         tm->v[0] = v_sigma * (Y[0] * e->dx + Y[1] * e->dy);     /* P:630 */
                         tm->v[1] = v_sigma * (Y[1] * e->dx + Y[2] * e->dy);
+                        double vsa = opac_eff[g] * e->G * v_alpha_abs;
+                        tm->va[8] = e->G * v_alpha_abs;
+                        tm->va[2] = vsa * 0.5 * e->dx * e->dx;
+                        tm->va[3] = vsa * fabs(e->dx * e->dy);
+                        tm->va[4] = vsa * 0.5 * e->dy * e->dy;
+                        tm->va[0] = vsa * (fabs(Y[0] * e->dx) + fabs(Y[1] * e->dy));
+                        tm->va[1] = vsa * (fabs(Y[1] * e->dx) + fabs(Y[2] * e->dy));
                     } else {
                         tm->v[8] = tm->v[0] = tm->v[1] = tm->v[2] = tm->v[3] = tm->v[4] = 0;
+                        tm->va[8] = tm->va[0] = tm->va[1] = tm->va[2] = tm->va[3] = tm->va[4] = 0;
                     }
                 }
                 errs[pix] = err;
@@ -772,7 +832,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
             int32_t g = terms[i].g;
             for (int j = 0; j < 9; j++) {
                 v2d[9 * (int64_t)g + j] += terms[i].v[j];
-                if (a2d) a2d[9 * (int64_t)g + j] += fabs(terms[i].v[j]);
+                if (a2d) a2d[9 * (int64_t)g + j] += terms[i].va[j];
             }
         }
         for (int64_t pix = 0; pix < P; pix++)

@@ -1,0 +1,180 @@
+"""ctypes binding of libgsplat_b200 (include/gs.h) -- argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; this module converts torch
+tensors to device pointers and the current CUDA stream to a cudaStream_t.  It fails
+loudly when the shared library is missing or a tensor is not a contiguous CUDA tensor of
+the expected dtype: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
+SPLAT_FLOATS = 12
+ABI_VERSION = 1
+
+GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
+
+
+class GsOptions(ct.Structure):
+    _fields_ = [
+        ("near_plane", ct.c_float), ("far_plane", ct.c_float), ("eps2d", ct.c_float),
+        ("alpha_max", ct.c_float), ("alpha_min", ct.c_float), ("t_min", ct.c_float),
+        ("tile_size", ct.c_int32), ("antialiased", ct.c_int32), ("sh_degree", ct.c_int32),
+        ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("reserved", ct.c_int32),
+    ]
+
+
+class GsError(RuntimeError):
+    pass
+
+
+_lib = None
+
+# name -> (restype, argtypes)
+_P, _I32, _I64, _SZ = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_size_t
+SIGNATURES = {
+    "gs_default_options": (None, [_P]),
+    "gs_status_string": (ct.c_char_p, [_I32]),
+    "gs_last_error": (ct.c_char_p, []),
+    "gs_abi_version": (_I32, []),
+    "gs_project": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
+    "gs_isect_workspace_size": (_SZ, [_I32, _I64, _I32, _I32, _I64]),
+    "gs_isect_tiles": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "gs_rasterize_fwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "gs_rasterize_stats": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P]),
+    "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
+    "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
+                              _P, _P, _P]),
+}
+
+
+def lib():
+    """Load libgsplat_b200.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise GsError(f"{LIB_PATH} is missing: build it with `python -m paper_2409_06765_b200.build` "
+                          "(there is no CPU fallback)")
+        L = ct.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        if L.gs_abi_version() != ABI_VERSION:
+            raise GsError("libgsplat_b200 ABI mismatch")
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = lib().gs_last_error().decode()
+        raise GsError(f"{what}: {GS_STATUS.get(status, status)} {msg}")
+
+
+def options(sh_degree=3, antialiased=False, near_plane=0.01, far_plane=1e10, eps2d=0.3, alpha_max=0.99,
+            alpha_min=1.0 / 255.0, t_min=1e-4, tile_size=16, bbox_mode=0, fov_clamp=True) -> GsOptions:
+    o = GsOptions()
+    lib().gs_default_options(ct.byref(o))
+    o.near_plane, o.far_plane, o.eps2d = near_plane, far_plane, eps2d
+    o.alpha_max, o.alpha_min, o.t_min = alpha_max, alpha_min, t_min
+    o.tile_size, o.antialiased, o.sh_degree = tile_size, int(bool(antialiased)), int(sh_degree)
+    o.bbox_mode, o.fov_clamp = int(bbox_mode), int(bool(fov_clamp))
+    return o
+
+
+def ptr(t, dtype=torch.float32, name="tensor"):
+    """Device pointer of a contiguous CUDA tensor of `dtype` (None -> NULL)."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise GsError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise GsError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise GsError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def tiles(width, height, tile=16):
+    return (width + tile - 1) // tile, (height + tile - 1) // tile
+
+
+# ------------------------------------------------------------------------------------
+# Thin wrappers with the C names.  All tensors are caller-allocated.
+# ------------------------------------------------------------------------------------
+def gs_project(o, means, quats, scales, opacities, colors, K, viewmats, Ks, width, height, radii, splats,
+               stream=None):
+    N, C = means.shape[0], viewmats.shape[0]
+    check(lib().gs_project(ct.byref(o), N, C, width, height, ptr(means, name="means"), ptr(quats, name="quats"),
+                           ptr(scales, name="scales"), ptr(opacities, name="opacities"), ptr(colors, name="colors"),
+                           K, ptr(viewmats, name="viewmats"), ptr(Ks, name="Ks"),
+                           ptr(radii, torch.int32, "radii"), ptr(splats, name="splats"), stream_ptr(stream)),
+          "gs_project")
+
+
+def gs_isect_workspace_size(C, N, width, height, cap):
+    return int(lib().gs_isect_workspace_size(C, N, width, height, cap))
+
+
+def gs_isect_tiles(o, C, N, width, height, radii, splats, cap, M, overflow, isect_ids, isect_keys, tile_offsets,
+                   workspace, stream=None):
+    check(lib().gs_isect_tiles(ct.byref(o), C, N, width, height, ptr(radii, torch.int32, "radii"),
+                               ptr(splats, name="splats"), cap, ptr(M, torch.int64, "M"),
+                               ptr(overflow, torch.int32, "overflow"), ptr(isect_ids, torch.int32, "isect_ids"),
+                               ptr(isect_keys, torch.int64, "isect_keys"),
+                               ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(workspace, torch.uint8, "ws"),
+                               workspace.numel(), stream_ptr(stream)),
+          "gs_isect_tiles")
+
+
+def gs_rasterize_fwd(o, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_rgb, out_alpha,
+                     out_T, last_ids, stream=None):
+    check(lib().gs_rasterize_fwd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
+                                 ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
+                                 ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_rgb, name="out_rgb"),
+                                 ptr(out_alpha, name="out_alpha"), ptr(out_T, name="out_T"),
+                                 ptr(last_ids, torch.int32, "last_ids"), stream_ptr(stream)),
+          "gs_rasterize_fwd")
+
+
+def gs_rasterize_stats(o, C, N, width, height, splats, isect_ids, tile_offsets, n_eval, n_contrib, stream=None):
+    check(lib().gs_rasterize_stats(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
+                                   ptr(isect_ids, torch.int32, "isect_ids"),
+                                   ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(n_eval, torch.int32, "n_eval"),
+                                   ptr(n_contrib, torch.int32, "n_contrib"), stream_ptr(stream)),
+          "gs_rasterize_stats")
+
+
+def gs_rasterize_bwd(o, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T, last_ids,
+                     v_out_rgb, v_out_alpha, absgrad, v_splats, stream=None):
+    check(lib().gs_rasterize_bwd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
+                                 ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
+                                 ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_T, name="out_T"),
+                                 ptr(last_ids, torch.int32, "last_ids"), ptr(v_out_rgb, name="v_out_rgb"),
+                                 ptr(v_out_alpha, name="v_out_alpha"), int(bool(absgrad)),
+                                 ptr(v_splats, name="v_splats"), stream_ptr(stream)),
+          "gs_rasterize_bwd")
+
+
+def gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, width, height, radii, v_splats,
+                   v_means, v_quats, v_scales, v_opacities, v_colors, stream=None):
+    N, C = means.shape[0], viewmats.shape[0]
+    check(lib().gs_project_bwd(ct.byref(o), N, C, width, height, ptr(means, name="means"), ptr(quats, name="quats"),
+                               ptr(scales, name="scales"), ptr(opacities, name="opacities"),
+                               ptr(colors, name="colors"), K, ptr(viewmats, name="viewmats"), ptr(Ks, name="Ks"),
+                               ptr(radii, torch.int32, "radii"), ptr(v_splats, name="v_splats"),
+                               ptr(v_means, name="v_means"), ptr(v_quats, name="v_quats"),
+                               ptr(v_scales, name="v_scales"), ptr(v_opacities, name="v_opacities"),
+                               ptr(v_colors, name="v_colors"), stream_ptr(stream)),
+          "gs_project_bwd")

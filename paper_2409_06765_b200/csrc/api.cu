@@ -1,0 +1,180 @@
+// C-ABI entry points of libgsplat_b200 (include/gs.h): argument validation and dispatch to
+// the stage launchers.  No allocation, no host synchronisation, no global mutable state
+// except the per-thread last-error string.
+#include <stdio.h>
+#include <string.h>
+
+#include "gs_internal.cuh"
+
+namespace gsb {
+static thread_local char g_err[512] = "";
+void set_last_error(const char* where, cudaError_t e) {
+    snprintf(g_err, sizeof g_err, "%s: %s", where, cudaGetErrorString(e));
+}
+}  // namespace gsb
+
+namespace {
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+inline bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+gs_status check_opts(const gs_options* o) {
+    if (!o) return GS_ERR_INVALID_ARGUMENT;
+    if (o->tile_size != GS_TILE) return GS_ERR_UNSUPPORTED;
+    if (o->sh_degree < -1 || o->sh_degree > 3) return GS_ERR_INVALID_ARGUMENT;
+    if (!(o->eps2d >= 0.f) || !(o->alpha_max > 0.f) || !(o->alpha_max < 1.f) || !(o->alpha_min >= 0.f) ||
+        !(o->t_min >= 0.f) || !(o->near_plane > 0.f))
+        return GS_ERR_INVALID_ARGUMENT;
+    if (o->bbox_mode < 0 || o->bbox_mode > 1 || o->reserved != 0) return GS_ERR_INVALID_ARGUMENT;
+    return GS_OK;
+}
+
+gs_status check_dims(int64_t N, int32_t C, int32_t W, int32_t H) {
+    if (N < 0 || C < 1 || W < 1 || H < 1) return GS_ERR_INVALID_ARGUMENT;
+    if ((int64_t)C * N >= (int64_t)1 << 31) return GS_ERR_INVALID_ARGUMENT;   // flat ids are int32
+    const int64_t TT = (int64_t)((W + GS_TILE - 1) / GS_TILE) * ((H + GS_TILE - 1) / GS_TILE);
+    if (TT * C >= (int64_t)1 << 31) return GS_ERR_INVALID_ARGUMENT;
+    return GS_OK;
+}
+
+}  // namespace
+
+#define GS_TRY(x)                     \
+    do {                              \
+        gs_status st_ = (x);          \
+        if (st_ != GS_OK) return st_; \
+    } while (0)
+#define GS_REQ(cond)                                        \
+    do {                                                    \
+        if (!(cond)) return GS_ERR_INVALID_ARGUMENT;        \
+    } while (0)
+
+extern "C" {
+
+void gs_default_options(gs_options* o) {
+    if (!o) return;
+    o->near_plane = 0.01f;
+    o->far_plane = 1e10f;
+    o->eps2d = 0.3f;
+    o->alpha_max = 0.99f;
+    o->alpha_min = 1.f / 255.f;
+    o->t_min = 1e-4f;
+    o->tile_size = GS_TILE;
+    o->antialiased = 0;
+    o->sh_degree = 3;
+    o->bbox_mode = 0;
+    o->fov_clamp = 1;
+    o->reserved = 0;
+}
+
+const char* gs_status_string(int32_t s) {
+    switch (s) {
+        case GS_OK: return "ok";
+        case GS_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case GS_ERR_UNSUPPORTED: return "unsupported";
+        case GS_ERR_CAPACITY: return "capacity exceeded";
+        case GS_ERR_CUDA: return "cuda error";
+        default: return "unknown status";
+    }
+}
+
+const char* gs_last_error(void) { return gsb::g_err; }
+int32_t gs_abi_version(void) { return GS_ABI_VERSION; }
+
+gs_status gs_project(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height, const float* means,
+                     const float* quats, const float* scales, const float* opacities, const float* colors, int32_t K,
+                     const float* viewmats, const float* Ks, int32_t* radii, float* splats, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    if (N == 0) return GS_OK;
+    GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && splats);
+    GS_REQ(aligned16(quats) && aligned16(splats) && aligned8(radii) && aligned4(means) && aligned4(scales) &&
+           aligned4(opacities) && aligned4(colors) && aligned4(viewmats) && aligned4(Ks));
+    if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
+    return gsb::launch_project_fwd(*opt, N, C, width, height, means, quats, scales, opacities, colors,
+                                   opt->sh_degree >= 0 ? K : 1, viewmats, Ks, radii, splats,
+                                   static_cast<cudaStream_t>(stream));
+}
+
+size_t gs_isect_workspace_size(int32_t C, int64_t N, int32_t width, int32_t height, int64_t M_capacity) {
+    if (C < 1 || N < 0 || width < 1 || height < 1 || M_capacity < 0) return 0;
+    return gsb::isect_workspace_bytes(C, N, width, height, M_capacity);
+}
+
+gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                         const int32_t* radii, const float* splats, int64_t M_capacity, int64_t* M, int32_t* overflow,
+                         int32_t* isect_ids, uint64_t* isect_keys, int32_t* tile_offsets, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(M_capacity >= 0 && M_capacity < ((int64_t)1 << 31) - 1);
+    GS_REQ(M && overflow && tile_offsets && workspace);
+    GS_REQ(N == 0 || (radii && splats));
+    GS_REQ(M_capacity == 0 || isect_ids);
+    GS_REQ(aligned8(M) && aligned4(overflow) && aligned4(tile_offsets) && aligned4(isect_ids) &&
+           aligned8(isect_keys) && (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
+    GS_REQ(N == 0 || (aligned8(radii) && aligned16(splats)));
+    GS_REQ(workspace_bytes >= gsb::isect_workspace_bytes(C, N, width, height, M_capacity));
+    return gsb::launch_isect(*opt, C, N, width, height, radii, splats, M_capacity, M, overflow, isect_ids, isect_keys,
+                             tile_offsets, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                           const float* splats, const float* backgrounds, const int32_t* isect_ids,
+                           const int32_t* tile_offsets, float* out_rgb, float* out_alpha, float* out_T,
+                           int32_t* last_ids, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(tile_offsets && out_rgb && out_alpha && out_T && last_ids);
+    GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(backgrounds) && aligned4(out_rgb) &&
+           aligned4(out_alpha) && aligned4(out_T) && aligned4(last_ids));
+    return gsb::launch_raster_fwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_rgb,
+                                  out_alpha, out_T, last_ids, static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                             const float* splats, const int32_t* isect_ids, const int32_t* tile_offsets,
+                             int32_t* n_eval, int32_t* n_contrib, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(tile_offsets && n_eval && n_contrib);
+    GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(n_eval) && aligned4(n_contrib));
+    return gsb::launch_raster_stats(*opt, C, N, width, height, splats, isect_ids, tile_offsets, n_eval, n_contrib,
+                                    static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                           const float* splats, const float* backgrounds, const int32_t* isect_ids,
+                           const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
+                           const float* v_out_rgb, const float* v_out_alpha, int32_t absgrad, float* v_splats,
+                           void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(tile_offsets && out_T && last_ids && v_out_rgb && (v_splats || N == 0));
+    GS_REQ(aligned16(splats) && aligned16(v_splats) && aligned4(isect_ids) && aligned4(backgrounds) &&
+           aligned4(out_T) && aligned4(last_ids) && aligned4(v_out_rgb) && aligned4(v_out_alpha));
+    return gsb::launch_raster_bwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T,
+                                  last_ids, v_out_rgb, v_out_alpha, absgrad, v_splats,
+                                  static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
+                         const float* means, const float* quats, const float* scales, const float* opacities,
+                         const float* colors, int32_t K, const float* viewmats, const float* Ks, const int32_t* radii,
+                         const float* v_splats, float* v_means, float* v_quats, float* v_scales, float* v_opacities,
+                         float* v_colors, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    if (N == 0) return GS_OK;
+    GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && v_splats && v_means &&
+           v_quats && v_scales && v_opacities && v_colors);
+    GS_REQ(aligned16(quats) && aligned16(v_quats) && aligned16(v_splats) && aligned8(radii) && aligned4(means) &&
+           aligned4(v_means) && aligned4(colors) && aligned4(v_colors) && aligned4(scales) && aligned4(v_scales));
+    if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
+    return gsb::launch_project_bwd(*opt, N, C, width, height, means, quats, scales, opacities, colors,
+                                   opt->sh_degree >= 0 ? K : 1, viewmats, Ks, radii, v_splats, v_means, v_quats,
+                                   v_scales, v_opacities, v_colors, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

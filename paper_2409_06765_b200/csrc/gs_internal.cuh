@@ -1,0 +1,61 @@
+// Internal declarations shared by the sm_100a kernels of libgsplat_b200.
+// (The oracle in /oracle shares nothing with this file.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gs.h"
+
+#define GS_TILE 16
+#define GS_BLOCK_PIXELS (GS_TILE * GS_TILE)
+
+// Launch-error capture: returns GS_ERR_CUDA from the enclosing gs_status function.
+namespace gsb {
+void set_last_error(const char* where, cudaError_t e);
+}
+#define GS_LAUNCH_CHECK(where)                                   \
+    do {                                                         \
+        cudaError_t e_ = cudaGetLastError();                     \
+        if (e_ != cudaSuccess) {                                 \
+            gsb::set_last_error(where, e_);                      \
+            return GS_ERR_CUDA;                                  \
+        }                                                        \
+    } while (0)
+
+namespace gsb {
+
+__host__ __device__ inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+inline int tile_bits(int ntiles) {
+    int B = 0;
+    while ((1LL << B) < ntiles) B++;
+    return B;
+}
+
+// ---- stage launchers (defined in project.cu / isect.cu / raster.cu) ----
+gs_status launch_project_fwd(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                             const float* quats, const float* scales, const float* opac,
+                             const float* colors, int K, const float* viewmats, const float* Ks,
+                             int32_t* radii, float* splats, cudaStream_t s);
+gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                             const float* quats, const float* scales, const float* opac,
+                             const float* colors, int K, const float* viewmats, const float* Ks,
+                             const int32_t* radii, const float* v_splats, float* v_means,
+                             float* v_quats, float* v_scales, float* v_opac, float* v_colors,
+                             cudaStream_t s);
+size_t isect_workspace_bytes(int C, int64_t N, int W, int H, int64_t cap);
+gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, const int32_t* radii,
+                       const float* splats, int64_t cap, int64_t* M, int32_t* overflow, int32_t* ids,
+                       uint64_t* keys, int32_t* tile_offsets, void* ws, size_t ws_bytes, cudaStream_t s);
+gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
+                            const float* bg, const int32_t* ids, const int32_t* offs, float* out_rgb,
+                            float* out_alpha, float* out_T, int32_t* last_ids, cudaStream_t s);
+gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
+                              const int32_t* ids, const int32_t* offs, int32_t* n_eval, int32_t* n_contrib,
+                              cudaStream_t s);
+gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
+                            const float* bg, const int32_t* ids, const int32_t* offs, const float* out_T,
+                            const int32_t* last_ids, const float* v_rgb, const float* v_alpha,
+                            int absgrad, float* v_splats, cudaStream_t s);
+
+}  // namespace gsb

@@ -1,0 +1,540 @@
+// Stage 2: tile intersection, on-device radix sort, tile ranges -- I1..I4 of SURVEY
+// Appendix A, restating App. B.2 of arXiv 2409.06765.
+//
+// The method orders intersections by (camera, tile, depth) (ties by flat id, Q16).
+// Instead of one 48-bit LSD sort over all M intersections, this B200 design sorts in
+// two levels, which yields the identical order:
+//   1. compact the V visible (c,n) items, in (c,n) order                   [K2a, K2b]
+//   2. stable LSD radix sort of the V items by fp32 depth bits (4 x 8 bit)   [K4]
+//   3. per sorted item: tile rectangle (I1) and count, device scan -> M      [K2c, K2d]
+//   4. load-balanced emission of (cam*TT + tile, c*N+n) in depth order       [K3]
+//   5. stable LSD radix sort of the M pairs by the ceil(log2(C*TT))-bit
+//      (camera, tile) key -- 2 passes at 1-MP, <= 15 views                   [K4]
+//   6. tile ranges by boundary detection                                     [K5]
+// Step 5 being stable keeps step 2's (depth, id) order inside each tile.  Traffic per
+// intersection is ~40 B instead of ~144 B for a 6-pass 64-bit sort.  All counts live in
+// device memory, so the stage never synchronises the host; grids are sized for the
+// capacities and blocks past the live count exit at once.
+//
+// Radix pass (K4) = three kernels: per-block digit histogram (warp-aggregated shared
+// atomics), one block per digit scanning that digit's row across blocks (coalesced), and
+// a scatter that ranks the block's 4096 keys stably in shared memory (per-warp running
+// digit counters + match.any), reorders them by digit there, and writes each digit run
+// with consecutive threads (coalesced 32-byte sectors instead of 256 scattered streams).
+//
+// Compiled with -fmad=false: the tile rectangle (Q20) is evaluated in fp32 with the
+// same op order as the oracle so keys match bit for bit.
+#include "gs_internal.cuh"
+
+namespace gsb {
+namespace {
+
+constexpr int kT = 256;              // threads per block
+constexpr int kWarps = kT / 32;
+constexpr int kItems = 16;           // items per thread
+constexpr int kTile = kT * kItems;   // items per block (4096)
+constexpr int kScanThreads = 1024;
+constexpr int kEmit = 2048;          // output positions per emission block
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// I1 (Q20): half-open tile rectangle [x0,x1) x [y0,y1) in fp32.
+__device__ __forceinline__ int4 tile_rect(float mx, float my, int rx, int ry, int TX, int TY) {
+    const float ft = (float)GS_TILE;
+    int a0 = (int)floorf((mx - (float)rx) / ft), a1 = (int)ceilf((mx + (float)rx) / ft);
+    int b0 = (int)floorf((my - (float)ry) / ft), b1 = (int)ceilf((my + (float)ry) / ft);
+    return make_int4(clampi(a0, 0, TX), clampi(a1, 0, TX), clampi(b0, 0, TY), clampi(b1, 0, TY));
+}
+
+// ---------------------------------------------------------------------------------------
+// Block-wide exclusive scan of one int per thread.  Returns the exclusive prefix; *total
+// receives the block sum.  s_warp needs 33 ints.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < nw ? s_warp[lane] : 0;
+        int wx = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, wx, o);
+            if (lane >= o) wx += y;
+        }
+        if (lane < nw) s_warp[lane] = wx - w;
+        if (lane == 31) s_warp[32] = wx;
+    }
+    __syncthreads();
+    int res = x - v + s_warp[warp];
+    *total = s_warp[32];
+    __syncthreads();
+    return res;
+}
+
+// Single-block in-place exclusive scan of nb = ceil(n / kTile) block sums (n = *d_n or
+// n_host, clamped to cap).  Coalesced rounds of 1024.  Writes totals / overflow.
+__global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, const int* d_n, int64_t n_host,
+                                                               int64_t cap, int* total_i32, int64_t* total_i64,
+                                                               int32_t* overflow, int64_t ovf_cap, int* clamped_n) {
+    __shared__ int s_warp[33];
+    const int n = (int)min(d_n ? (int64_t)*d_n : n_host, cap);
+    const int nb = div_up(n, kTile);
+    int carry = 0;
+    for (int r = 0; r < nb; r += kScanThreads) {
+        const int i = r + threadIdx.x;
+        const int v = i < nb ? data[i] : 0;
+        int tot;
+        const int ex = block_exclusive_scan(v, s_warp, &tot);
+        if (i < nb) data[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        if (total_i32) *total_i32 = carry;
+        if (total_i64) *total_i64 = carry;
+        if (overflow) *overflow = (int64_t)carry > ovf_cap ? 1 : 0;
+        if (clamped_n) *clamped_n = (int)min((int64_t)carry, ovf_cap);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2a / K2b: stable compaction of the visible (c,n) items.  Thread t owns kItems
+// consecutive items of its block's tile.
+__global__ void __launch_bounds__(kT) k_vis_count(const int2* __restrict__ radii, int64_t n_items, int* blocksum) {
+    __shared__ int s_warp[33];
+    const int64_t i0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int64_t i = i0 + k;
+        if (i < n_items) {
+            const int2 r = radii[i];
+            cnt += (r.x > 0 && r.y > 0) ? 1 : 0;
+        }
+    }
+    int tot;
+    block_exclusive_scan(cnt, s_warp, &tot);
+    if (threadIdx.x == 0) blocksum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ radii, const float* __restrict__ splats,
+                                                   int64_t n_items, const int* __restrict__ blockoff,
+                                                   uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+    __shared__ int s_warp[33];
+    const int64_t i0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    unsigned vis = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int64_t i = i0 + k;
+        if (i < n_items) {
+            const int2 r = radii[i];
+            if (r.x > 0 && r.y > 0) vis |= 1u << k;
+        }
+    }
+    int tot;
+    int pos = blockoff[blockIdx.x] + block_exclusive_scan(__popc(vis), s_warp, &tot);
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        if (vis & (1u << k)) {
+            const int64_t i = i0 + k;
+            out_key[pos] = __float_as_uint(splats[i * GS_SPLAT_FLOATS + 3]);   // depth >= near > 0 (Q17)
+            out_val[pos] = (int32_t)i;
+            pos++;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K4: one pass of a stable LSD radix sort (8-bit digit at `shift`).
+// hist layout: hist[d * nb_max + b] = count of digit d in block b (digit-major rows).
+__global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
+                                                   int shift, int* hist, int nb_max) {
+    __shared__ int s_hist[256];
+    const int n = (int)min((int64_t)*d_n, cap);
+    const int nb = div_up(n, kTile);
+    if ((int)blockIdx.x >= nb) return;
+    s_hist[threadIdx.x] = 0;
+    __syncthreads();
+    const int base = blockIdx.x * kTile;
+    const int lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (int k = 0; k < kItems; k++) {
+        const int i = base + k * kT + threadIdx.x;
+        const unsigned d = i < n ? (keys[i] >> shift) & 255u : 256u + lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[d], __popc(peers));
+    }
+    __syncthreads();
+    hist[threadIdx.x * nb_max + blockIdx.x] = s_hist[threadIdx.x];
+}
+
+// One block per digit: exclusive scan of that digit's row over the live blocks; the
+// row total goes to rowtot[d].
+__global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, const int* d_n, int64_t cap,
+                                                        int* rowtot) {
+    __shared__ int s_warp[33];
+    const int n = (int)min((int64_t)*d_n, cap);
+    const int nb = div_up(n, kTile);
+    int* row = hist + (int64_t)blockIdx.x * nb_max;
+    int carry = 0;
+    for (int r = 0; r < nb; r += kT) {
+        const int i = r + threadIdx.x;
+        const int v = i < nb ? row[i] : 0;
+        int tot;
+        const int ex = block_exclusive_scan(v, s_warp, &tot);
+        if (i < nb) row[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict__ keys_in,
+                                                      const int32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+                                                      int32_t* __restrict__ vals_out, const int* d_n, int64_t cap,
+                                                      int shift, const int* __restrict__ hist, int nb_max,
+                                                      const int* __restrict__ rowtot) {
+    __shared__ int s_cnt[kWarps][256];    // per-warp running digit counts, then per-warp offsets
+    __shared__ int s_dstart[256];         // start of digit d inside this block's sorted tile
+    __shared__ int s_goff[256];           // global start of digit d for this block
+    __shared__ int s_warp[33];
+    __shared__ uint32_t s_k[kTile];
+    __shared__ int32_t s_v[kTile];
+    const int n = (int)min((int64_t)*d_n, cap);
+    const int nb = div_up(n, kTile);
+    if ((int)blockIdx.x >= nb) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int w = 0; w < kWarps; w++) s_cnt[w][threadIdx.x] = 0;
+    __syncthreads();
+    // 1. per-warp stable ranks over the warp's contiguous slice of 512 items
+    const int base = blockIdx.x * kTile + warp * (kTile / kWarps);
+    uint32_t key[kItems];
+    int32_t val[kItems];
+    int rank[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int i = base + k * 32 + lane;
+        const bool valid = i < n;
+        key[k] = valid ? keys_in[i] : 0u;
+        val[k] = valid ? vals_in[i] : 0;
+        const unsigned d = valid ? (key[k] >> shift) & 255u : 256u + lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        int b = 0;
+        if (valid) b = s_cnt[warp][d];
+        __syncwarp();
+        if (valid && (__ffs(peers) - 1) == lane) s_cnt[warp][d] = b + __popc(peers);
+        __syncwarp();
+        rank[k] = valid ? b + __popc(peers & lt_mask) : -1;
+    }
+    __syncthreads();
+    // 2. per digit: exclusive offsets across warps, block digit totals, digit starts
+    {
+        const int d = threadIdx.x;
+        int run = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; w++) {
+            const int c = s_cnt[w][d];
+            s_cnt[w][d] = run;
+            run += c;
+        }
+        int tot;
+        const int start = block_exclusive_scan(run, s_warp, &tot);   // digits in ascending order
+        s_dstart[d] = start;
+        // global start: rows scanned per digit + digit base (exclusive scan of row totals)
+        int dbase;
+        int dummy;
+        dbase = block_exclusive_scan(rowtot[d], s_warp, &dummy);
+        s_goff[d] = dbase + hist[d * nb_max + blockIdx.x];
+    }
+    __syncthreads();
+    // 3. reorder the tile by digit in shared memory
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        if (rank[k] >= 0) {
+            const unsigned d = (key[k] >> shift) & 255u;
+            const int p = s_dstart[d] + s_cnt[warp][d] + rank[k];
+            s_k[p] = key[k];
+            s_v[p] = val[k];
+        }
+    }
+    __syncthreads();
+    // 4. coalesced write-out of the digit runs
+    const int nloc = min(kTile, n - blockIdx.x * kTile);
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int j = k * kT + threadIdx.x;
+        if (j < nloc) {
+            const uint32_t kk = s_k[j];
+            const unsigned d = (kk >> shift) & 255u;
+            const int pos = s_goff[d] + (j - s_dstart[d]);
+            keys_out[pos] = kk;
+            vals_out[pos] = s_v[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2c: tile rectangle and tile count of every depth-sorted visible item (stored for the
+// emission), plus per-block sums.
+struct TileGeom {
+    int TX, TY, TT;
+    int64_t N;
+};
+
+__global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ radii, const float* __restrict__ splats,
+                                                    const int32_t* __restrict__ vis_val, const int* d_V, TileGeom g,
+                                                    int4* __restrict__ ent_rect, int* __restrict__ ent_cnt,
+                                                    int* blocksum) {
+    __shared__ int s_warp[33];
+    const int V = *d_V;
+    const int nb = div_up(V, kTile);
+    if ((int)blockIdx.x >= nb) return;
+    const int base = blockIdx.x * kTile;
+    int cnt = 0;
+    for (int k = 0; k < kItems; k++) {
+        const int j = base + k * kT + threadIdx.x;
+        if (j < V) {
+            const int32_t id = vis_val[j];
+            const int2 r = radii[id];
+            const float2 m = *reinterpret_cast<const float2*>(splats + (int64_t)id * GS_SPLAT_FLOATS);
+            const int4 rc = tile_rect(m.x, m.y, r.x, r.y, g.TX, g.TY);
+            const int c = (rc.y - rc.x) * (rc.w - rc.z);
+            ent_rect[j] = rc;
+            ent_cnt[j] = c;
+            cnt += c;
+        }
+    }
+    int tot;
+    block_exclusive_scan(cnt, s_warp, &tot);
+    if (threadIdx.x == 0) blocksum[blockIdx.x] = tot;
+}
+
+// K2d: exclusive offsets of the per-item counts (ent_off[V] = M), in item order.
+__global__ void __launch_bounds__(kT) k_tiles_offsets(const int* __restrict__ ent_cnt, const int* d_V,
+                                                      const int* __restrict__ blockoff, int* __restrict__ ent_off) {
+    __shared__ int s_warp[33];
+    const int V = *d_V;
+    const int nb = div_up(V, kTile);
+    if ((int)blockIdx.x >= nb) return;
+    const int j0 = blockIdx.x * kTile + threadIdx.x * kItems;
+    int c[kItems];
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        c[k] = (j0 + k < V) ? ent_cnt[j0 + k] : 0;
+        sum += c[k];
+    }
+    int tot;
+    int run = blockoff[blockIdx.x] + block_exclusive_scan(sum, s_warp, &tot);
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        if (j0 + k < V) ent_off[j0 + k] = run;
+        run += c[k];
+    }
+    if (j0 <= V - 1 && V - 1 < j0 + kItems) ent_off[V] = run;   // owner of the last item: run = M
+}
+
+// K3: load-balanced emission.  Block b writes output positions [b*kEmit, (b+1)*kEmit):
+// each position finds its item by binary search over the item offsets staged in shared
+// memory, so writes are perfectly coalesced whatever the per-splat tile counts.
+__global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_rect, const int* __restrict__ ent_off,
+                                                   const int32_t* __restrict__ vis_val, const int* d_V,
+                                                   const int* d_nsort, TileGeom g, uint32_t* __restrict__ out_key,
+                                                   int32_t* __restrict__ out_val) {
+    __shared__ int s_off[kEmit + 1];
+    __shared__ int s_lo, s_hi;
+    const int n = *d_nsort;
+    const int V = *d_V;
+    const int o0 = blockIdx.x * kEmit;
+    if (o0 >= n) return;
+    const int o1 = min(n, o0 + kEmit);
+    if (threadIdx.x < 2) {
+        // item owning position o (largest j with ent_off[j] <= o)
+        const int o = threadIdx.x == 0 ? o0 : o1 - 1;
+        int lo = 0, hi = V - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (ent_off[mid] <= o) lo = mid; else hi = mid - 1;
+        }
+        if (threadIdx.x == 0) s_lo = lo; else s_hi = lo;
+    }
+    __syncthreads();
+    // ne <= kEmit unless zero-count items (empty rectangles) interleave; then search globally
+    const int e0 = s_lo, ne = s_hi - s_lo + 1;
+    const bool staged = ne <= kEmit;
+    if (staged)
+        for (int k = threadIdx.x; k <= ne; k += kT) s_off[k] = ent_off[e0 + k];
+    __syncthreads();
+    const int* offp = staged ? s_off : ent_off + e0;
+    for (int o = o0 + threadIdx.x; o < o1; o += kT) {
+        int lo = 0, hi = ne - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (offp[mid] <= o) lo = mid; else hi = mid - 1;
+        }
+        const int j = e0 + lo;
+        const int kk = o - offp[lo];
+        const int4 rc = ent_rect[j];
+        const int w = rc.y - rc.x;
+        const int ty = rc.z + kk / w, tx = rc.x + kk % w;
+        const int32_t id = vis_val[j];
+        out_key[o] = (uint32_t)(id / g.N) * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
+        out_val[o] = id;
+    }
+}
+
+// K5: tile ranges.  offsets[b] = first sorted index with key >= b; offsets[nbins] = M.
+__global__ void k_ranges_fill(int32_t* offsets, int nbins, const int* d_n) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b <= nbins) offsets[b] = *d_n;
+}
+
+__global__ void k_ranges(const uint32_t* __restrict__ keys, const int* d_n, int32_t* offsets) {
+    const int n = *d_n;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    const int64_t prev = i > 0 ? (int64_t)keys[i - 1] : -1;
+    for (int64_t b = prev + 1; b <= (int64_t)k; b++) offsets[b] = i;
+}
+
+__global__ void k_keys64(const uint32_t* __restrict__ keys32, const int32_t* __restrict__ ids,
+                         const float* __restrict__ splats, const int* d_n, int TT, int B, uint64_t* out) {
+    const int n = *d_n;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys32[i];
+    const uint64_t cam = k / (uint32_t)TT, tile = k % (uint32_t)TT;
+    const uint32_t dbits = __float_as_uint(splats[(int64_t)ids[i] * GS_SPLAT_FLOATS + 3]);
+    out[i] = (cam << (32 + B)) | (tile << 32) | (uint64_t)dbits;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct WsLayout {
+    size_t off_scalars, off_blocksum, off_rowtot, off_hist, off_vk, off_vv, off_ak, off_av, off_rect, off_cnt,
+        off_eoff, off_ka, off_va, off_kb, off_vb, total;
+    int nb_max;
+};
+
+WsLayout ws_layout(int C, int64_t N, int64_t cap) {
+    WsLayout L;
+    const int64_t n_items = (int64_t)C * N;
+    const int64_t big = n_items > cap ? n_items : cap;
+    L.nb_max = div_up(big > 0 ? big : 1, kTile);
+    size_t o = 0;
+    L.off_scalars = o; o = align256(o + 64);
+    L.off_blocksum = o; o = align256(o + sizeof(int) * (size_t)(L.nb_max + 1));
+    L.off_rowtot = o; o = align256(o + sizeof(int) * 256);
+    L.off_hist = o; o = align256(o + sizeof(int) * 256 * (size_t)L.nb_max);
+    L.off_vk = o; o = align256(o + 4 * (size_t)(n_items + 1));
+    L.off_vv = o; o = align256(o + 4 * (size_t)(n_items + 1));
+    L.off_ak = o; o = align256(o + 4 * (size_t)(n_items + 1));
+    L.off_av = o; o = align256(o + 4 * (size_t)(n_items + 1));
+    L.off_rect = o; o = align256(o + 16 * (size_t)(n_items + 1));
+    L.off_cnt = o; o = align256(o + 4 * (size_t)(n_items + 1));
+    L.off_eoff = o; o = align256(o + 4 * (size_t)(n_items + 2));
+    L.off_ka = o; o = align256(o + 4 * (size_t)(cap + 1));
+    L.off_va = o; o = align256(o + 4 * (size_t)(cap + 1));
+    L.off_kb = o; o = align256(o + 4 * (size_t)(cap + 1));
+    L.off_vb = o; o = align256(o + 4 * (size_t)(cap + 1));
+    L.total = o;
+    return L;
+}
+
+struct KV {
+    uint32_t* k;
+    int32_t* v;
+};
+
+// Runs ceil(bits/8) stable 8-bit LSD passes over `a` (live count *d_n <= cap), ping-ponging
+// with `b`.  The last pass writes its values to `final_vals` when given.  Returns the
+// buffers holding the sorted result.
+KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
+              int nb_max, cudaStream_t s) {
+    const int passes = bits <= 0 ? 0 : div_up(bits, 8);
+    KV in = a, out = b;
+    for (int p = 0; p < passes; p++) {
+        int32_t* vdst = (p == passes - 1 && final_vals) ? final_vals : out.v;
+        k_radix_hist<<<nb_max, kT, 0, s>>>(in.k, d_n, cap, 8 * p, hist, nb_max);
+        k_radix_scan_rows<<<256, kT, 0, s>>>(hist, nb_max, d_n, cap, rowtot);
+        k_radix_scatter<<<nb_max, kT, 0, s>>>(in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max, rowtot);
+        KV next_in{out.k, vdst};
+        out = in;
+        in = next_in;
+    }
+    return in;
+}
+
+}  // namespace
+
+size_t isect_workspace_bytes(int C, int64_t N, int W, int H, int64_t cap) {
+    (void)W; (void)H;
+    return ws_layout(C, N, cap).total;
+}
+
+gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, const int32_t* radii, const float* splats,
+                       int64_t cap, int64_t* M, int32_t* overflow, int32_t* ids, uint64_t* keys, int32_t* tile_offsets,
+                       void* ws, size_t ws_bytes, cudaStream_t s) {
+    (void)o;
+    const WsLayout L = ws_layout(C, N, cap);
+    if (ws_bytes < L.total) return GS_ERR_INVALID_ARGUMENT;
+    char* w = static_cast<char*>(ws);
+    int* scal = reinterpret_cast<int*>(w + L.off_scalars);
+    int* d_V = scal + 0;
+    int* d_nsort = scal + 1;
+    int* blocksum = reinterpret_cast<int*>(w + L.off_blocksum);
+    int* rowtot = reinterpret_cast<int*>(w + L.off_rowtot);
+    int* hist = reinterpret_cast<int*>(w + L.off_hist);
+    KV vis{reinterpret_cast<uint32_t*>(w + L.off_vk), reinterpret_cast<int32_t*>(w + L.off_vv)};
+    KV alt{reinterpret_cast<uint32_t*>(w + L.off_ak), reinterpret_cast<int32_t*>(w + L.off_av)};
+    int4* ent_rect = reinterpret_cast<int4*>(w + L.off_rect);
+    int* ent_cnt = reinterpret_cast<int*>(w + L.off_cnt);
+    int* ent_off = reinterpret_cast<int*>(w + L.off_eoff);
+    KV ia{reinterpret_cast<uint32_t*>(w + L.off_ka), reinterpret_cast<int32_t*>(w + L.off_va)};
+    KV ib{reinterpret_cast<uint32_t*>(w + L.off_kb), reinterpret_cast<int32_t*>(w + L.off_vb)};
+
+    const int64_t n_items = (int64_t)C * N;
+    const int TX = div_up(W, GS_TILE), TY = div_up(H, GS_TILE), TT = TX * TY;
+    const int nbins = C * TT;
+    const int B = tile_bits(TT);
+    TileGeom g{TX, TY, TT, N};
+    const int2* r2 = reinterpret_cast<const int2*>(radii);
+    const int nb_items = div_up(n_items > 0 ? n_items : 1, kTile);
+
+    // 1. stable compaction of the visible (c,n) items (K2a, K2b)
+    k_vis_count<<<nb_items, kT, 0, s>>>(r2, n_items, blocksum);
+    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, nullptr, n_items, INT64_MAX, d_V, nullptr, nullptr, 0,
+                                                 nullptr);
+    k_vis_compact<<<nb_items, kT, 0, s>>>(r2, splats, n_items, blocksum, vis.k, vis.v);
+    GS_LAUNCH_CHECK("isect/compact");
+    // 2. stable sort by fp32 depth bits (K4, 4 passes)
+    KV dsorted = radix_sort(vis, alt, nullptr, d_V, n_items, 32, hist, rowtot, L.nb_max, s);
+    GS_LAUNCH_CHECK("isect/depth-sort");
+    // 3. tile rectangles, counts, offsets, M, overflow, clamped count (K2c, K2d)
+    k_tiles_count<<<nb_items, kT, 0, s>>>(r2, splats, dsorted.v, d_V, g, ent_rect, ent_cnt, blocksum);
+    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, d_V, 0, INT64_MAX, nullptr, M, overflow, cap, d_nsort);
+    k_tiles_offsets<<<nb_items, kT, 0, s>>>(ent_cnt, d_V, blocksum, ent_off);
+    // 4. load-balanced emission in depth order (K3)
+    if (cap > 0) k_tiles_emit<<<div_up(cap, kEmit), kT, 0, s>>>(ent_rect, ent_off, dsorted.v, d_V, d_nsort, g, ia.k, ia.v);
+    GS_LAUNCH_CHECK("isect/emit");
+    // 5. stable sort by (camera, tile) (K4); values land in the caller's isect_ids
+    const int kbits = tile_bits(nbins) > 0 ? tile_bits(nbins) : 1;
+    KV sorted = radix_sort(ia, ib, ids, d_nsort, cap, kbits, hist, rowtot, L.nb_max, s);
+    GS_LAUNCH_CHECK("isect/tile-sort");
+    // 6. tile ranges (K5)
+    k_ranges_fill<<<div_up(nbins + 1, 256), 256, 0, s>>>(tile_offsets, nbins, d_nsort);
+    if (cap > 0) k_ranges<<<div_up(cap, 256), 256, 0, s>>>(sorted.k, d_nsort, tile_offsets);
+    if (keys && cap > 0) k_keys64<<<div_up(cap, 256), 256, 0, s>>>(sorted.k, sorted.v, splats, d_nsort, TT, B, keys);
+    GS_LAUNCH_CHECK("isect/ranges");
+    return GS_OK;
+}
+
+}  // namespace gsb

@@ -1,0 +1,338 @@
+// K8: projection backward -- P1..P9 of SURVEY Appendix A, restating App. C.3-C.4
+// of arXiv 2409.06765, with the readings Q10 (mu' -> t re-derived from the
+// pinhole map P:790), Q11 (dL/dT symmetric form), Q27 (exact derivative of the clamped J)
+// and the A.4 compensation gradient (P3, derived from P:281).
+//
+// Design (B200): one thread per Gaussian; the thread recomputes the forward quantities
+// in registers, loops over the C cameras of the call and sums their contributions
+// (no atomics: deterministic, Q30), then writes every parameter gradient once
+// (44 B + 12K B per Gaussian, vector stores for SH).  HBM-bound (DESIGN.md roofline K8).
+#include "gs_internal.cuh"
+#include "sh.cuh"
+
+namespace gsb {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct PBParams {
+    int64_t N;
+    int C, W, H, K;
+    float eps2d;
+    int antialiased, fov_clamp;
+    int vec_colors;   // v_colors base 16B-aligned and K*3 % 4 == 0
+    const float* means;
+    const float* quats;
+    const float* scales;
+    const float* opac;
+    const float* colors;
+    const float* viewmats;
+    const float* Ks;
+    const int32_t* radii;
+    const float* v_splats;
+    float* v_means;
+    float* v_quats;
+    float* v_scales;
+    float* v_opac;
+    float* v_colors;
+};
+
+template <int DEG>
+__global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
+    const int64_t n = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (n >= p.N) return;
+    constexpr int NB = DEG < 0 ? 1 : (DEG + 1) * (DEG + 1);
+
+    const float mu[3] = {p.means[3 * n], p.means[3 * n + 1], p.means[3 * n + 2]};
+    const float4 q4 = reinterpret_cast<const float4*>(p.quats)[n];
+    const float s[3] = {p.scales[3 * n], p.scales[3 * n + 1], p.scales[3 * n + 2]};
+    const float op = p.opac[n];
+    const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+    const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
+    float R[3][3];
+    R[0][0] = 1.f - 2.f * (qy * qy + qz * qz); R[0][1] = 2.f * (qx * qy - qw * qz); R[0][2] = 2.f * (qx * qz + qw * qy);
+    R[1][0] = 2.f * (qx * qy + qw * qz); R[1][1] = 1.f - 2.f * (qx * qx + qz * qz); R[1][2] = 2.f * (qy * qz - qw * qx);
+    R[2][0] = 2.f * (qx * qz - qw * qy); R[2][1] = 2.f * (qy * qz + qw * qx); R[2][2] = 1.f - 2.f * (qx * qx + qy * qy);
+    float M[3][3], Sig[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) M[i][j] = R[i][j] * s[j];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) Sig[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
+
+    float g_mu[3] = {0.f, 0.f, 0.f}, g_S[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+    float g_op = 0.f;
+    float coef[NB * 3];
+    float g_coef[NB * 3];
+#pragma unroll
+    for (int i = 0; i < NB * 3; i++) g_coef[i] = 0.f;
+    bool coef_loaded = false;
+    bool seen = false;
+
+    for (int c = 0; c < p.C; c++) {
+        const int64_t idx = (int64_t)c * p.N + n;
+        const int2 rad = reinterpret_cast<const int2*>(p.radii)[idx];
+        if (rad.x <= 0 || rad.y <= 0) continue;
+        seen = true;
+        const float4* vr = reinterpret_cast<const float4*>(p.v_splats + idx * GS_SPLAT_FLOATS);
+        const float4 v0 = vr[0], v1 = vr[1], v2 = vr[2];
+        const float* vm = p.viewmats + 16 * (int64_t)c;
+        const float* Kc = p.Ks + 9 * (int64_t)c;
+        float Wr[3][3], w[3];
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+#pragma unroll
+            for (int j = 0; j < 3; j++) Wr[i][j] = vm[4 * i + j];
+            w[i] = vm[4 * i + 3];
+        }
+        const float fx = Kc[0], fy = Kc[4], cx = Kc[2], cy = Kc[5];
+        float t[3];
+#pragma unroll
+        for (int i = 0; i < 3; i++) t[i] = Wr[i][0] * mu[0] + Wr[i][1] * mu[1] + Wr[i][2] * mu[2] + w[i];
+        const float tz = t[2];
+        // Sigma_c = Wr Sigma Wr^T
+        float A[3][3], Sc[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) A[i][j] = Wr[i][0] * Sig[0][j] + Wr[i][1] * Sig[1][j] + Wr[i][2] * Sig[2][j];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) Sc[i][j] = A[i][0] * Wr[j][0] + A[i][1] * Wr[j][1] + A[i][2] * Wr[j][2];
+        // J with clamp (Q27)
+        float txc = t[0], tyc = t[1];
+        bool clx = false, cly = false;
+        if (p.fov_clamp) {
+            const float Wf = (float)p.W, Hf = (float)p.H;
+            const float tanx = 0.5f * Wf / fx, tany = 0.5f * Hf / fy;
+            const float lxp = (Wf - cx) / fx + 0.3f * tanx, lxn = cx / fx + 0.3f * tanx;
+            const float lyp = (Hf - cy) / fy + 0.3f * tany, lyn = cy / fy + 0.3f * tany;
+            const float u = t[0] / tz, v = t[1] / tz;
+            clx = (u > lxp) || (u < -lxn);
+            cly = (v > lyp) || (v < -lyn);
+            txc = tz * fminf(lxp, fmaxf(-lxn, u));
+            tyc = tz * fminf(lyp, fmaxf(-lyn, v));
+        }
+        const float J[2][3] = {{fx / tz, 0.f, -fx * txc / (tz * tz)}, {0.f, fy / tz, -fy * tyc / (tz * tz)}};
+        float B[2][3], Sp[2][2];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) B[i][j] = J[i][0] * Sc[0][j] + J[i][1] * Sc[1][j] + J[i][2] * Sc[2][j];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) Sp[i][j] = B[i][0] * J[j][0] + B[i][1] * J[j][1] + B[i][2] * J[j][2];
+        const float a = Sp[0][0] + p.eps2d, b = Sp[0][1], cc = Sp[1][1] + p.eps2d;
+        const float detb = a * cc - b * b;
+        const float Y00 = cc / detb, Y01 = -b / detb, Y11 = a / detb;
+        float comp = 1.f, det_raw = 0.f;
+        if (p.antialiased) {
+            det_raw = Sp[0][0] * Sp[1][1] - Sp[0][1] * Sp[0][1];
+            comp = sqrtf(fmaxf(0.f, det_raw / detb));
+        }
+        // ---- P1: o_eff = o * comp
+        const float v_oeff = v0.z;
+        g_op += v_oeff * comp;
+        const float v_comp = v_oeff * op;
+        // ---- P2: v_Spb = -Y G_Y Y, G_Y = [[vA, vB/2],[vB/2, vC]]
+        const float gA = v1.x, gB = 0.5f * v1.y, gC = v1.z;
+        const float YG00 = Y00 * gA + Y01 * gB, YG01 = Y00 * gB + Y01 * gC;
+        const float YG10 = Y01 * gA + Y11 * gB, YG11 = Y01 * gB + Y11 * gC;
+        float vS00 = -(YG00 * Y00 + YG01 * Y01);
+        float vS01 = -(YG00 * Y01 + YG01 * Y11);
+        float vS11 = -(YG10 * Y01 + YG11 * Y11);
+        // ---- P3 (AA): + v_comp * comp/2 * (Sigma'^-1 - Spb^-1)
+        if (p.antialiased && det_raw > 0.f) {
+            const float k = v_comp * 0.5f * comp;
+            vS00 += k * (Sp[1][1] / det_raw - Y00);
+            vS01 += k * (-Sp[0][1] / det_raw - Y01);
+            vS11 += k * (Sp[0][0] / det_raw - Y11);
+        }
+        const float vSp[2][2] = {{vS00, vS01}, {vS01, vS11}};
+        // ---- P4: v_Sc = J^T vSp J; v_J = 2 vSp J Sc (Q11)
+        float vSc[3][3], vJ[2][3];
+        float PJ[2][3];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) PJ[i][j] = vSp[i][0] * J[0][j] + vSp[i][1] * J[1][j];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) vSc[i][j] = J[0][i] * PJ[0][j] + J[1][i] * PJ[1][j];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) vJ[i][j] = 2.f * (PJ[i][0] * Sc[0][j] + PJ[i][1] * Sc[1][j] + PJ[i][2] * Sc[2][j]);
+        // ---- P5: v_t through J (exact with clamp Q27) and mu' (Q10)
+        const float rz = 1.f / tz, rz2 = rz * rz, rz3 = rz2 * rz;
+        float vt0 = 0.f, vt1 = 0.f, vt2 = -fx * rz2 * vJ[0][0] - fy * rz2 * vJ[1][1];
+        if (!clx) {
+            vt0 += -fx * rz2 * vJ[0][2];
+            vt2 += 2.f * fx * t[0] * rz3 * vJ[0][2];
+        } else {
+            vt2 += fx * txc * rz3 * vJ[0][2];
+        }
+        if (!cly) {
+            vt1 += -fy * rz2 * vJ[1][2];
+            vt2 += 2.f * fy * t[1] * rz3 * vJ[1][2];
+        } else {
+            vt2 += fy * tyc * rz3 * vJ[1][2];
+        }
+        vt0 += fx * rz * v0.x;
+        vt1 += fy * rz * v0.y;
+        vt2 -= fx * t[0] * rz2 * v0.x + fy * t[1] * rz2 * v0.y;
+        // ---- P6: v_mu += W^T v_t; v_Sigma += W^T v_Sc W
+#pragma unroll
+        for (int i = 0; i < 3; i++) g_mu[i] += Wr[0][i] * vt0 + Wr[1][i] * vt1 + Wr[2][i] * vt2;
+        float T1[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) T1[i][j] = vSc[i][0] * Wr[0][j] + vSc[i][1] * Wr[1][j] + vSc[i][2] * Wr[2][j];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) g_S[i][j] += Wr[0][i] * T1[0][j] + Wr[1][i] * T1[1][j] + Wr[2][i] * T1[2][j];
+        // ---- P7: colour
+        if (DEG < 0) {
+            g_coef[0] += v2.x;
+            g_coef[1] += v2.y;
+            g_coef[2] += v2.z;
+        } else {
+            if (!coef_loaded) {
+                const float* src = p.colors + n * (int64_t)p.K * 3;
+#pragma unroll
+                for (int i = 0; i < NB * 3; i++) coef[i] = src[i];
+                coef_loaded = true;
+            }
+            float campos[3];
+#pragma unroll
+            for (int i = 0; i < 3; i++) campos[i] = -(Wr[0][i] * w[0] + Wr[1][i] * w[1] + Wr[2][i] * w[2]);
+            const float ex = mu[0] - campos[0], ey = mu[1] - campos[1], ez = mu[2] - campos[2];
+            const float en = sqrtf(ex * ex + ey * ey + ez * ez);
+            const float dx = ex / en, dy = ey / en, dz = ez / en;
+            float Yb[NB];
+            sh_eval_basis<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, Yb);
+            float raw0 = 0.5f, raw1 = 0.5f, raw2 = 0.5f;
+#pragma unroll
+            for (int j = 0; j < NB; j++) {
+                raw0 += Yb[j] * coef[3 * j];
+                raw1 += Yb[j] * coef[3 * j + 1];
+                raw2 += Yb[j] * coef[3 * j + 2];
+            }
+            const float vr0 = raw0 > 0.f ? v2.x : 0.f, vr1 = raw1 > 0.f ? v2.y : 0.f, vr2 = raw2 > 0.f ? v2.z : 0.f;
+            float wj[NB];
+#pragma unroll
+            for (int j = 0; j < NB; j++) {
+                g_coef[3 * j] += Yb[j] * vr0;
+                g_coef[3 * j + 1] += Yb[j] * vr1;
+                g_coef[3 * j + 2] += Yb[j] * vr2;
+                wj[j] = coef[3 * j] * vr0 + coef[3 * j + 1] * vr1 + coef[3 * j + 2] * vr2;
+            }
+            if (DEG > 0) {
+                float gx = 0.f, gy = 0.f, gz = 0.f;
+                sh_basis_vjp<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, wj, gx, gy, gz);
+                const float dd = dx * gx + dy * gy + dz * gz;
+                const float ren = 1.f / en;
+                g_mu[0] += (gx - dx * dd) * ren;
+                g_mu[1] += (gy - dy * dd) * ren;
+                g_mu[2] += (gz - dz * dd) * ren;
+            }
+        }
+        (void)cy;
+        (void)cx;
+    }
+
+    // ---- P8: v_M = (vS + vS^T) M; v_s_j = (R^T v_M)_jj; v_R = v_M S
+    float vM[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            vM[i][j] = (g_S[i][0] + g_S[0][i]) * M[0][j] + (g_S[i][1] + g_S[1][i]) * M[1][j] +
+                       (g_S[i][2] + g_S[2][i]) * M[2][j];
+    float gsc[3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) gsc[j] = R[0][j] * vM[0][j] + R[1][j] * vM[1][j] + R[2][j] * vM[2][j];
+    float vR[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) vR[i][j] = vM[i][j] * s[j];
+    // ---- P9: dR/d(w,x,y,z) at q_hat, then the normalisation
+    const float w_ = qw, x_ = qx, y_ = qy, z_ = qz;
+    float vqw = 2.f * (-z_ * vR[0][1] + y_ * vR[0][2] + z_ * vR[1][0] - x_ * vR[1][2] - y_ * vR[2][0] + x_ * vR[2][1]);
+    float vqx = 2.f * (y_ * vR[0][1] + z_ * vR[0][2] + y_ * vR[1][0] - 2.f * x_ * vR[1][1] - w_ * vR[1][2] +
+                       z_ * vR[2][0] + w_ * vR[2][1] - 2.f * x_ * vR[2][2]);
+    float vqy = 2.f * (-2.f * y_ * vR[0][0] + x_ * vR[0][1] + w_ * vR[0][2] + x_ * vR[1][0] + z_ * vR[1][2] -
+                       w_ * vR[2][0] + z_ * vR[2][1] - 2.f * y_ * vR[2][2]);
+    float vqz = 2.f * (-2.f * z_ * vR[0][0] - w_ * vR[0][1] + x_ * vR[0][2] + w_ * vR[1][0] - 2.f * z_ * vR[1][1] +
+                       y_ * vR[1][2] + x_ * vR[2][0] + y_ * vR[2][1]);
+    const float dot = vqw * w_ + vqx * x_ + vqy * y_ + vqz * z_;
+    const float rq = 1.f / qn;
+    float4 oq = make_float4((vqw - dot * w_) * rq, (vqx - dot * x_) * rq, (vqy - dot * y_) * rq, (vqz - dot * z_) * rq);
+    if (!seen) {   // culled in every camera (includes zero / non-finite quaternions): zeros
+        oq = make_float4(0.f, 0.f, 0.f, 0.f);
+        gsc[0] = gsc[1] = gsc[2] = 0.f;
+    }
+    reinterpret_cast<float4*>(p.v_quats)[n] = oq;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        p.v_means[3 * n + i] = g_mu[i];
+        p.v_scales[3 * n + i] = gsc[i];
+    }
+    p.v_opac[n] = g_op;
+    if (DEG < 0) {
+#pragma unroll
+        for (int i = 0; i < 3; i++) p.v_colors[3 * n + i] = g_coef[i];
+    } else {
+        float* dst = p.v_colors + n * (int64_t)p.K * 3;
+        if (p.vec_colors && (NB * 3) % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < NB * 3 / 4; i++)
+                reinterpret_cast<float4*>(dst)[i] =
+                    make_float4(g_coef[4 * i], g_coef[4 * i + 1], g_coef[4 * i + 2], g_coef[4 * i + 3]);
+            for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
+        } else {
+#pragma unroll
+            for (int i = 0; i < NB * 3; i++) dst[i] = g_coef[i];
+            for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
+        }
+    }
+}
+
+}  // namespace
+
+gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                             const float* quats, const float* scales, const float* opac,
+                             const float* colors, int K, const float* viewmats, const float* Ks,
+                             const int32_t* radii, const float* v_splats, float* v_means,
+                             float* v_quats, float* v_scales, float* v_opac, float* v_colors,
+                             cudaStream_t s) {
+    if (N == 0) return GS_OK;
+    PBParams p;
+    p.N = N; p.C = C; p.W = W; p.H = H; p.K = K;
+    p.eps2d = o.eps2d; p.antialiased = o.antialiased; p.fov_clamp = o.fov_clamp;
+    p.means = means; p.quats = quats; p.scales = scales; p.opac = opac; p.colors = colors;
+    p.viewmats = viewmats; p.Ks = Ks; p.radii = radii; p.v_splats = v_splats;
+    p.vec_colors = ((reinterpret_cast<uintptr_t>(v_colors) & 15u) == 0) && ((K * 3) % 4 == 0);
+    p.v_means = v_means; p.v_quats = v_quats; p.v_scales = v_scales; p.v_opac = v_opac; p.v_colors = v_colors;
+    const int grid = div_up(N, kThreads);
+    switch (o.sh_degree) {
+        case -1: k_project_bwd<-1><<<grid, kThreads, 0, s>>>(p); break;
+        case 0: k_project_bwd<0><<<grid, kThreads, 0, s>>>(p); break;
+        case 1: k_project_bwd<1><<<grid, kThreads, 0, s>>>(p); break;
+        case 2: k_project_bwd<2><<<grid, kThreads, 0, s>>>(p); break;
+        default: k_project_bwd<3><<<grid, kThreads, 0, s>>>(p); break;
+    }
+    GS_LAUNCH_CHECK("k_project_bwd");
+    return GS_OK;
+}
+
+}  // namespace gsb

@@ -1,0 +1,144 @@
+"""Preallocated execution of the whole hot path through the C-ABI.
+
+`Engine` owns every device buffer of one (N, C, width, height, SH) problem shape and runs
+the five stages of include/gs.h on a CUDA stream without any host synchronisation:
+
+    gs_project -> gs_isect_tiles -> gs_rasterize_fwd      (forward)
+    gs_rasterize_bwd -> gs_project_bwd                     (backward)
+
+The intersection count M is data dependent.  The engine keeps an M capacity; the
+isect stage writes M and an overflow flag on the device, and `ensure_capacity()` (one
+small device->host read) grows the capacity and tells the caller to re-run when the
+flag is set.  In steady state (bench.py, CUDA-graph replay) the flag is checked after
+the timed region only.  Parameter gradients land in ONE flat fp32 buffer (`flat_grad`)
+so the data-parallel gradient sum is a single collective.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib as L
+
+
+def _align4(n):
+    return (n + 3) // 4 * 4
+
+
+class Engine:
+    def __init__(self, N, C, width, height, sh_degree=3, K=None, antialiased=False, M_capacity=None,
+                 device="cuda", absgrad=False, with_keys=False, **opt_kwargs):
+        self.N, self.C, self.W, self.H = int(N), int(C), int(width), int(height)
+        self.sh_degree = int(sh_degree)
+        self.K = (K if K is not None else (self.sh_degree + 1) ** 2) if self.sh_degree >= 0 else 1
+        self.absgrad = bool(absgrad)
+        self.with_keys = bool(with_keys)
+        self.device = torch.device(device)
+        self.opts = L.options(sh_degree=self.sh_degree, antialiased=antialiased, **opt_kwargs)
+        self.TX, self.TY = L.tiles(self.W, self.H)
+        dev = self.device
+        C, N, W, H = self.C, self.N, self.W, self.H
+        self.radii = torch.zeros((C, N, 2), dtype=torch.int32, device=dev)
+        self.splats = torch.zeros((C, N, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
+        self.v_splats = torch.zeros_like(self.splats)
+        self.M = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.tile_offsets = torch.zeros(C * self.TX * self.TY + 1, dtype=torch.int32, device=dev)
+        self.out_rgb = torch.zeros((C, H, W, 3), dtype=torch.float32, device=dev)
+        self.out_alpha = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
+        self.out_T = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
+        self.last_ids = torch.zeros((C, H, W), dtype=torch.int32, device=dev)
+        # flat gradient buffer: [quats 4N | means 3N | scales 3N | opacities N | colors 3KN],
+        # each section 16-byte aligned (float4 stores in K8)
+        ncol = 3 * self.K * N if self.sh_degree >= 0 else 3 * N
+        sizes = [4 * N, 3 * N, 3 * N, N, ncol]
+        offs = [0]
+        for s in sizes[:-1]:
+            offs.append(offs[-1] + _align4(s))
+        self.flat_grad = torch.zeros(offs[-1] + _align4(sizes[-1]), dtype=torch.float32, device=dev)
+        fg = self.flat_grad
+        self.v_quats = fg[offs[0]:offs[0] + sizes[0]].view(N, 4)
+        self.v_means = fg[offs[1]:offs[1] + sizes[1]].view(N, 3)
+        self.v_scales = fg[offs[2]:offs[2] + sizes[2]].view(N, 3)
+        self.v_opacities = fg[offs[3]:offs[3] + sizes[3]].view(N)
+        colshape = (N, self.K, 3) if self.sh_degree >= 0 else (N, 3)
+        self.v_colors = fg[offs[4]:offs[4] + sizes[4]].view(*colshape)
+        self.cap = 0
+        self.isect_ids = None
+        self.isect_keys = None
+        self.workspace = None
+        self._alloc_isect(M_capacity if M_capacity is not None else max(1 << 16, 4 * C * N))
+
+    # ------------------------------------------------------------------------------
+    def _alloc_isect(self, cap):
+        cap = int(cap)
+        if cap <= self.cap and self.isect_ids is not None:
+            return
+        self.cap = cap
+        self.isect_ids = torch.zeros(max(cap, 1), dtype=torch.int32, device=self.device)
+        self.isect_keys = torch.zeros(max(cap, 1), dtype=torch.int64, device=self.device) if self.with_keys else None
+        ws = L.gs_isect_workspace_size(self.C, self.N, self.W, self.H, cap)
+        self.workspace = torch.empty(ws + 256, dtype=torch.uint8, device=self.device)
+        # the C-ABI wants a 256-byte aligned workspace
+        off = (-self.workspace.data_ptr()) % 256
+        self.workspace_view = self.workspace[off:off + ws]
+
+    def ensure_capacity(self, headroom=1.25) -> bool:
+        """Reads M and the overflow flag (one D->H sync).  Returns True when the last
+        isect overflowed; the capacity is then grown and the caller must re-run."""
+        if int(self.overflow.item()) == 0:
+            return False
+        self._alloc_isect(math.ceil(int(self.M.item()) * headroom) + 1024)
+        return True
+
+    @property
+    def n_isect(self) -> int:
+        return int(self.M.item())
+
+    # ------------------------------------------------------------------------------
+    def project(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
+        L.gs_project(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W, self.H,
+                     self.radii, self.splats, stream)
+
+    def isect(self, stream=None):
+        L.gs_isect_tiles(self.opts, self.C, self.N, self.W, self.H, self.radii, self.splats, self.cap, self.M,
+                         self.overflow, self.isect_ids, self.isect_keys, self.tile_offsets, self.workspace_view,
+                         stream)
+
+    def rasterize_fwd(self, backgrounds=None, stream=None):
+        L.gs_rasterize_fwd(self.opts, self.C, self.N, self.W, self.H, self.splats, backgrounds, self.isect_ids,
+                           self.tile_offsets, self.out_rgb, self.out_alpha, self.out_T, self.last_ids, stream)
+
+    def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, stream=None):
+        L.gs_rasterize_bwd(self.opts, self.C, self.N, self.W, self.H, self.splats, backgrounds, self.isect_ids,
+                           self.tile_offsets, self.out_T, self.last_ids, v_rgb, v_alpha, self.absgrad,
+                           self.v_splats, stream)
+
+    def project_bwd(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
+        L.gs_project_bwd(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W, self.H,
+                         self.radii, self.v_splats, self.v_means, self.v_quats, self.v_scales, self.v_opacities,
+                         self.v_colors, stream)
+
+    def forward(self, means, quats, scales, opacities, colors, viewmats, Ks, backgrounds=None, stream=None):
+        self.project(means, quats, scales, opacities, colors, viewmats, Ks, stream)
+        self.isect(stream)
+        self.rasterize_fwd(backgrounds, stream)
+
+    def backward(self, means, quats, scales, opacities, colors, viewmats, Ks, v_rgb, v_alpha=None,
+                 backgrounds=None, stream=None):
+        self.rasterize_bwd(v_rgb, v_alpha, backgrounds, stream)
+        self.project_bwd(means, quats, scales, opacities, colors, viewmats, Ks, stream)
+
+    def step(self, params, v_rgb, v_alpha=None, backgrounds=None, stream=None):
+        """One pass of the whole hot path (forward + backward) over one batch of views.
+        params = (means, quats, scales, opacities, colors, viewmats, Ks)."""
+        self.forward(*params, backgrounds=backgrounds, stream=stream)
+        self.backward(*params, v_rgb, v_alpha, backgrounds, stream)
+
+    def run_checked(self, params, v_rgb, v_alpha=None, backgrounds=None):
+        """step() with capacity growth (syncs once to read the overflow flag)."""
+        while True:
+            self.step(params, v_rgb, v_alpha, backgrounds)
+            if not self.ensure_capacity():
+                return

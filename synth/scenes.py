@@ -57,7 +57,7 @@ def orbit_cameras(n_views, width, height, seed, radius=3.2, view_offset=0):
     elev = rng.uniform(10.0, 35.0, size=total)
     viewmats, Ks = [], []
     for v in range(view_offset, view_offset + n_views):
-        az = 2.0 * np.pi * v / max(total, 8)
+        az = 2.0 * np.pi * v / 8.0
         el = np.deg2rad(elev[v])
         pos = radius * np.array([np.cos(el) * np.sin(az), np.sin(el), -np.cos(el) * np.cos(az)])
         viewmats.append(_lookat_viewmat(pos))

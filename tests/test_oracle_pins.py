@@ -30,6 +30,8 @@ def _splat2d(means2d, conics, opac, rgb, depths, radii, C=1):
     return dict(radii=np.array(radii, np.int32).reshape(C, n, 2),
                 mean2d_f=np.array(means2d, np.float32).reshape(C, n, 2),
                 depth_f=np.array(depths, np.float32).reshape(C, n),
+                dec=np.concatenate([np.array(conics, np.float32).reshape(C, n, 3),
+                                    np.array(opac, np.float32).reshape(C, n, 1)], axis=-1),
                 mean2d=np.array(means2d, np.float64).reshape(C, n, 2),
                 conic=np.array(conics, np.float64).reshape(C, n, 3),
                 opac_eff=np.array(opac, np.float64).reshape(C, n),
