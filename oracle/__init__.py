@@ -79,7 +79,7 @@ def lib():
         _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
         _lib.or_isect.restype = i64
         _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6
-        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7
         _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6
         _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
@@ -184,19 +184,23 @@ def render_fwd(proj, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None
 
 
 def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds=None, tile_mask=None):
-    """B1-B6.  Returns v2d [C,N,9] (v_mean2d 2, v_conic 3, v_rgb 3, v_opac_eff 1), the
-    per-element condition floor a2d (sum of |per-pixel terms|), g_ambig and the T-replay error."""
+    """B1-B6.  Returns v2d [C,N,9] (v_mean2d 2, v_conic 3, v_rgb 3, v_opac_eff 1), and for the
+    parity tolerance (not part of the result): a2d, the sum over pixels of |per-pixel term|
+    with B4's v_alpha replaced by the magnitudes of its parts (fp32 cancellation floor),
+    s2d, the first-order change of each gradient for a 1-ulp shift of the fp32 projected
+    means the kernel works with, g_ambig and the T-replay error."""
     o = opts.c()
     bg = None if backgrounds is None else _f64(backgrounds)
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
     v_img = _f64(v_img)
     va = None if v_alpha is None else _f64(v_alpha)
-    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); amb = np.zeros((C, N), np.uint8)
+    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9))
+    amb = np.zeros((C, N), np.uint8)
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
-                        _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(amb), ct.byref(err))
-    return dict(v2d=v2d, a2d=a2d, g_ambig=amb, T_replay_err=err.value)
+                        _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err))
+    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value)
 
 
 def project_bwd(scene, proj, v2d, opts: Options):

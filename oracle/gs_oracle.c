@@ -581,9 +581,12 @@ typedef struct {
     int64_t li;      /* list index */
     double alpha, T, G, sigma, dx, dy;
     int clamped;     /* alpha saturated at alpha_max (decision path) */
+    double delta;    /* 1 ulp of the fp32 mu' the kernel works with (tolerance model only) */
+    double qd;       /* first-order relative change of alpha for a delta shift of mu' */
 } contrib_t;
 
 typedef struct {
+    double eT;       /* sum over composited splats of alpha qd / (1 - alpha) (tolerance model) */
     double rgb[3], T;
     int64_t last_li;  /* -1 if none */
     int64_t end_li;   /* exclusive end of the evaluated part of the list */
@@ -615,7 +618,7 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
                               const double *conic, const double *opac_eff, const double *rgb, contrib_t *rec,
                               int64_t rec_cap)
 {
-    pixres_t r = {{0, 0, 0}, 1.0, -1, L->count, 0, 0};
+    pixres_t r = {0.0, {0, 0, 0}, 1.0, -1, L->count, 0, 0};
     int tx = px / o->tile_size, ty = py / o->tile_size;
     double p[2] = {px + 0.5, py + 0.5};            /* R1: pixel centre */
     const double amax = (float)o->alpha_max, amin = (float)o->alpha_min, tmin = (float)o->t_min;
@@ -641,11 +644,16 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
         double sigma = 0.5 * (Y[0] * dx * dx + Y[2] * dy * dy) + Y[1] * dx * dy;   /* P:543 */
         double G = exp(-sigma);
         double alpha = clamped ? o->alpha_max : opac_eff[g] * G;
+        /* tolerance model only (not part of the result): 1 ulp of the fp32 mu' */
+        double mm = fabs(mean2d[2 * g]) > fabs(mean2d[2 * g + 1]) ? fabs(mean2d[2 * g]) : fabs(mean2d[2 * g + 1]);
+        double delta = ldexp(mm > 1.0 ? mm : 1.0, -23);
+        double qd = clamped ? 0.0 : (fabs(Y[0] * dx + Y[1] * dy) + fabs(Y[1] * dx + Y[2] * dy)) * delta;
         if (rec && r.ncontrib < rec_cap) {
             contrib_t *e = &rec[r.ncontrib];
             e->li = i; e->alpha = alpha; e->T = T; e->G = G; e->sigma = sigma; e->dx = dx; e->dy = dy;
-            e->clamped = clamped;
+            e->clamped = clamped; e->delta = delta; e->qd = qd;
         }
+        r.eT += alpha * qd / (1.0 - alpha);
         for (int ch = 0; ch < 3; ch++) r.rgb[ch] += rgb[3 * g + ch] * alpha * T;   /* P:536-538 */
         T = T * (1.0 - alpha);
         Tdec = nT_d;
@@ -712,18 +720,19 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
 /* g_ambig[g] = 1 if g was evaluated at an ambiguous pixel.                     */
 /* T_replay_err (optional) = max |T_replayed - T_forward| over all steps.      */
 /* ------------------------------------------------------------------------- */
-typedef struct { int32_t g; double v[9], va[9]; } term_t;
+typedef struct { int32_t g; double v[9], va[9], vs[9]; } term_t;
 
 int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
                   const float *mean2d_f, const float *depth_f, const float *dec, const double *mean2d,
                   const double *conic,
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
-                  const double *v_img, const double *v_alpha_img, double *v2d, double *a2d,
+                  const double *v_img, const double *v_alpha_img, double *v2d, double *a2d, double *s2d,
                   uint8_t *g_ambig, double *T_replay_err)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
     memset(v2d, 0, sizeof(double) * 9 * C * N);
     if (a2d) memset(a2d, 0, sizeof(double) * 9 * C * N);
+    if (s2d) memset(s2d, 0, sizeof(double) * 9 * C * N);
     if (g_ambig) memset(g_ambig, 0, (size_t)C * N);
     double max_err = 0;
     for (int64_t c = 0; c < C; c++) {
@@ -818,9 +827,22 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                         tm->va[4] = vsa * 0.5 * e->dy * e->dy;
                         tm->va[0] = vsa * (fabs(Y[0] * e->dx) + fabs(Y[1] * e->dy));
                         tm->va[1] = vsa * (fabs(Y[1] * e->dx) + fabs(Y[2] * e->dy));
+                        /* first-order effect of the fp32 rounding of mu' (delta, 1 ulp) on the
+                         * polynomial factors of B6 */
+                        tm->vs[2] = vsa * fabs(e->dx) * e->delta;
+                        tm->vs[3] = vsa * (fabs(e->dx) + fabs(e->dy)) * e->delta;
+                        tm->vs[4] = vsa * fabs(e->dy) * e->delta;
+                        tm->vs[0] = vsa * (fabs(Y[0]) + fabs(Y[1])) * e->delta;
+                        tm->vs[1] = vsa * (fabs(Y[1]) + fabs(Y[2])) * e->delta;
                     } else {
                         tm->v[8] = tm->v[0] = tm->v[1] = tm->v[2] = tm->v[3] = tm->v[4] = 0;
                         tm->va[8] = tm->va[0] = tm->va[1] = tm->va[2] = tm->va[3] = tm->va[4] = 0;
+                        tm->vs[0] = tm->vs[1] = tm->vs[2] = tm->vs[3] = tm->vs[4] = 0;
+                    }
+                    /* ... and through alpha (this splat's qd, all splats' via T and S) */
+                    for (int j = 0; j < 9; j++) {
+                        if (j >= 5 && j <= 7) tm->vs[j] = 0;
+                        tm->vs[j] += tm->va[j] * (e->qd + r.eT);
                     }
                 }
                 errs[pix] = err;
@@ -833,6 +855,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
             for (int j = 0; j < 9; j++) {
                 v2d[9 * (int64_t)g + j] += terms[i].v[j];
                 if (a2d) a2d[9 * (int64_t)g + j] += terms[i].va[j];
+                if (s2d) s2d[9 * (int64_t)g + j] += terms[i].vs[j];
             }
         }
         for (int64_t pix = 0; pix < P; pix++)

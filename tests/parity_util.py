@@ -70,10 +70,16 @@ def v2d_from_splats(v_splats):
     return np.concatenate([vs[..., 0:2], vs[..., 4:7], vs[..., 8:11], vs[..., 2:3]], axis=-1)
 
 
-def check_grad2d(g, r, a, comparable):
-    """|g - r| <= GRAD_RTOL |r| + GRAD2D_FLOOR * a on comparable (c,n) entries."""
+GRAD2D_ULP = 2.0          # ... plus this multiple of the 1-ulp(mu') sensitivity s2d
+
+
+def check_grad2d(g, r, a, comparable, s=None):
+    """|g - r| <= GRAD_RTOL |r| + GRAD2D_FLOOR * a + GRAD2D_ULP * s on comparable (c,n)."""
     m = comparable[..., None] & np.ones_like(r, bool)
-    bad = (np.abs(g - r) > GRAD_RTOL * np.abs(r) + GRAD2D_FLOOR * a + 1e-12) & m
+    tol = GRAD_RTOL * np.abs(r) + GRAD2D_FLOOR * a + 1e-12
+    if s is not None:
+        tol = tol + GRAD2D_ULP * s
+    bad = (np.abs(g - r) > tol) & m
     return bad
 
 

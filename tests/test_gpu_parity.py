@@ -163,7 +163,7 @@ def test_backward_parity(cache, name):
     b = ref["bwd"]
     vis = ref["proj"]["radii"][..., 0] > 0
     g2 = U.v2d_from_splats(gpu["v_splats"])
-    bad = U.check_grad2d(g2, b["v2d"], b["a2d"], vis)
+    bad = U.check_grad2d(g2, b["v2d"], b["a2d"], vis, b["s2d"])
     assert not bad.any(), f"2D grads: {bad.sum()} bad of {vis.sum() * 9}"
     comp_n = vis.any(axis=0)
     gr = ref["grads"]
@@ -180,7 +180,7 @@ def test_background_and_alpha_gradient(cache):
     assert np.abs(gpu["rgb"] - f["rgb"])[ok].max() <= U.IMG_ATOL
     b = ref["bwd"]
     vis = ref["proj"]["radii"][..., 0] > 0
-    bad = U.check_grad2d(U.v2d_from_splats(gpu["v_splats"]), b["v2d"], b["a2d"], vis)
+    bad = U.check_grad2d(U.v2d_from_splats(gpu["v_splats"]), b["v2d"], b["a2d"], vis, b["s2d"])
     assert not bad.any()
 
 
@@ -229,7 +229,8 @@ def test_rasterization_api_autograd():
     gpu = U.run_gpu(sc, v_img=v, v_alpha=va)
     assert np.array_equal(rgb.detach().cpu().numpy(), gpu["rgb"])
     for t, k in zip(ts[:5], ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]):
-        np.testing.assert_allclose(t.grad.cpu().numpy(), gpu[k], rtol=1e-4, atol=1e-6)
+        # same kernels, different fp32 atomic order only
+        np.testing.assert_allclose(t.grad.cpu().numpy(), gpu[k], rtol=1e-4, atol=1e-5 * np.abs(gpu[k]).max())
     assert meta["means2d"].shape == (2, 1500, 2) and meta["radii"].dtype == torch.int32
 
 
@@ -269,7 +270,7 @@ def test_config2_full_scale_sampled():
     assert np.abs(gpu["rgb"] - f["rgb"])[sel].max() <= U.IMG_ATOL
     assert np.abs(gpu["T"] - f["T"])[sel].max() <= U.IMG_ATOL
     b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64), tile_mask=mask)
-    bad = U.check_grad2d(U.v2d_from_splats(gpu["v_splats"]), b["v2d"], b["a2d"], vis)
+    bad = U.check_grad2d(U.v2d_from_splats(gpu["v_splats"]), b["v2d"], b["a2d"], vis, b["s2d"])
     assert bad.sum() == 0, bad.sum()
     g = oracle.project_bwd(sc, p, b["v2d"], o)
     touched = (np.abs(b["v2d"]).sum(-1) > 0)[0]
