@@ -209,9 +209,11 @@ def run_ours(args):
     peaks = _peaks()
     clk_mhz = peaks["sm_max_mhz"]
     alu_peak = SMS * FP32_LANES_PER_SM * clk_mhz * 1e6 / 1e12          # T FP32 instr/s
+    # useful (algorithmic) work: the composited pairs only -- evaluating a pair that ends up
+    # skipped (alpha < alpha_min) is overhead the kernel tries to avoid (K6/K7)
     alu = {
-        "raster_fwd": (OPS_EVAL * E_f + OPS_FWD_CONTRIB * E_c) / 1e12,
-        "raster_bwd": (OPS_EVAL * E_b + OPS_BWD_CONTRIB * E_c) / 1e12,
+        "raster_fwd": (OPS_EVAL + OPS_FWD_CONTRIB) * E_c / 1e12,
+        "raster_bwd": (OPS_EVAL + OPS_BWD_CONTRIB) * E_c / 1e12,
     }
     # algorithmic HBM bytes per launch (SURVEY 8d formulas)
     Kc = 16 if sc["sh_degree"] == 3 else (sc["sh_degree"] + 1) ** 2
@@ -227,7 +229,7 @@ def run_ours(args):
         roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2),
                 "unit": "T FP32 instr/s", "frac": round(ach / alu_peak, 4), "traffic": None,
                 "peak_src": f"{SMS} SMs x {FP32_LANES_PER_SM} FP32 lanes x {clk_mhz:.0f} MHz ({peaks['src']})",
-                "work": {"E_eval": E_f, "E_contrib": E_c, "E_bwd": E_b}}
+                "work": {"pairs_composited": E_c, "pairs_evaluated_fwd": E_f, "pairs_walked_bwd": E_b}}
     else:
         ach = hbm[dom] / (stage_ms[dom] / 1e3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",

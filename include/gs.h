@@ -85,9 +85,9 @@ typedef struct gs_options {
  *   k=2    opac_eff = opacity * comp (F15)
  *   k=3    depth = t_z (F4)
  *   k=4..6 conic (A, B, C) = (Sigma' + s I)^-1 = [[A,B],[B,C]] (F10)
- *   k=7    comp (1 in classic mode)
+ *   k=7    a = (Sigma' + s I)_xx  (blurred variance along x, F8; bounds the alpha support)
  *   k=8..10 rgb (F14)
- *   k=11   0
+ *   k=11   c = (Sigma' + s I)_yy
  * Culled records (radii == 0) are all zeros.  gs_rasterize_bwd writes gradients in the
  * SAME slot layout (v_mean2d in 0,1; v_opac_eff in 2; v_conic in 4..6; v_rgb in 8..10;
  * slot 3 = d/d depth (0 unless depth rendering), slots 7 and 11 = absgrad |v_mean2d|

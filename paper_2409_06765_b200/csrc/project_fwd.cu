@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
             }
             *rad = make_int2(rx, ry);
             rec[0] = make_float4(mx, my, op * comp, tz);
-            rec[1] = make_float4(cA, cB, cC, comp);
-            rec[2] = make_float4(r, g, bl, 0.f);
+            rec[1] = make_float4(cA, cB, cC, a);      // a = Sigma'_b,xx (support box of K6/K7)
+            rec[2] = make_float4(r, g, bl, c);        // c = Sigma'_b,yy
         }
     }
 }

@@ -2,23 +2,30 @@
 // B1..B6 of SURVEY Appendix A, restating App. B.2 and App. C.2 of
 // arXiv 2409.06765.
 //
-// Design (B200): one CTA per 16x16 tile, one thread per pixel.  The tile's
-// depth-sorted range is walked in batches of 256 splats; each batch is gathered from the
-// 48-byte projected records (L2-resident at 1-MP scale) into shared memory once and then
-// broadcast to all 256 pixels (TMA-free on purpose: the gather is an indirect load through
-// isect_ids, which cp.async.bulk cannot express).  The conic is pre-scaled by -log2(e) at
-// staging so the per-pair exponent is two FMAs and one MUFU.EX2.  Forward and backward
-// evaluate alpha with the SAME inline function built from _rn intrinsics, so the skip
-// decisions of the backward replay those of the forward bit for bit.  The backward reduces
-// each splat's 9 gradient values across the warp with shuffles and issues three 16-byte
-// vector reductions (red.global.add.v4.f32) per (splat, warp) that touched it.
-// These kernels are bound by FP32/MUFU issue, not HBM (DESIGN.md roofline K6/K7).
+// Design (B200).  One CTA per 16x16 tile, one thread per pixel, each warp owning an
+// 8x4 pixel block.  The tile's depth-sorted range is walked in batches of 256 splats: each
+// batch is gathered from the 48-byte projected records (L2-resident at 1-MP scale) into
+// shared memory once and broadcast to all pixels.  While staging, every splat also gets an
+// 8-bit mask of the warps whose pixels can see it with alpha >= alpha_min: the
+// axis-aligned box of the ellipse sigma <= ln(o/alpha_min), from the blurred variances a, c
+// of the record, inflated by a margin that covers fp32 rounding and the ex2/lg2
+// approximations.  Each warp then compacts the batch to its own list (ballot, order
+// preserving) and walks only that list.  Pixels outside the box would have computed
+// alpha < alpha_min and been skipped anyway (Q14), so the result is bit-identical to
+// walking every splat; only instruction issue is saved (these kernels are FP32/MUFU issue
+// bound, DESIGN.md roofline K6/K7).  The conic is pre-scaled by -log2(e) at staging so the
+// per-pair exponent is two FMAs and one MUFU.EX2.  Forward and backward evaluate alpha with
+// the same inline function built from _rn intrinsics, so the backward's skip decisions
+// replay the forward's bit for bit.  The backward reduces each splat's gradient values
+// across the warp with a transposed (reduce-scatter) shuffle tree -- 9 shuffles for 8
+// values instead of 40 -- and lanes holding distinct values issue one fp32 reduction each.
 #include "gs_internal.cuh"
 
 namespace gsb {
 namespace {
 
 constexpr int kBatch = GS_BLOCK_PIXELS;   // 256 splats per staged batch
+constexpr int kWarps = kBatch / 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -48,9 +55,35 @@ __device__ __forceinline__ bool eval_alpha(float mx, float my, float o, float4 c
     return alpha >= alpha_min;
 }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
+// 8-bit mask of the warps (8x4 pixel blocks, warp w at column w&1, row w>>1 of the tile)
+// whose pixel centres intersect the box |dx| <= hx, |dy| <= hy of the ellipse
+// sigma <= tau = ln(o / alpha_min): hx = sqrt(2 tau a), hy = sqrt(2 tau c) with
+// a, c the blurred variances.  Conservative margins: tau is inflated by 0.4% + 4e-3
+// (lg2.approx error, fp32 rounding of the exponent, ex2.approx error are all < 1e-5
+// relative) and the box by cond*1e-6 (cond = a*A = a c / det, which bounds the relative
+// error of the fp32 conic the kernel evaluates) plus 1e-2 px.
+__device__ __forceinline__ uint32_t support_mask(float mx, float my, float o, float A, float a, float c, float x0,
+                                                 float y0, float alpha_min) {
+    if (o < alpha_min * 0.9999f) return 0u;   // alpha = min(alpha_max, o G) <= o (G <= 1)
+    float tau = fmaxf(0.f, __logf(o / alpha_min));
+    tau = tau * 1.004f + 4e-3f;
+    const float grow = 1.f + 1e-6f * a * A;
+    const float hx = sqrtf(2.f * tau * a) * grow + 1e-2f;
+    const float hy = sqrtf(2.f * tau * c) * grow + 1e-2f;
+    if (!(hx < 1e30f) || !(hy < 1e30f)) return 0xffu;
+    uint32_t m = 0;
+#pragma unroll
+    for (int wy = 0; wy < 4; wy++) {
+        const float ylo = y0 + (float)(wy * 4) + 0.5f, yhi = ylo + 3.f;
+        if (my + hy >= ylo && my - hy <= yhi) {
+#pragma unroll
+            for (int wx = 0; wx < 2; wx++) {
+                const float xlo = x0 + (float)(wx * 8) + 0.5f, xhi = xlo + 7.f;
+                if (mx + hx >= xlo && mx - hx <= xhi) m |= 1u << (wy * 2 + wx);
+            }
+        }
+    }
+    return m;
 }
 
 struct RasterParams {
@@ -75,70 +108,116 @@ struct RasterParams {
     int32_t* n_contrib;
 };
 
+struct PixelCoord {
+    int px, py, warp, lane;
+    bool inside;
+    float fpx, fpy, x0, y0;
+};
+
+__device__ __forceinline__ PixelCoord pixel_coord(const RasterParams& p, int tile) {
+    PixelCoord c;
+    c.warp = threadIdx.x >> 5;
+    c.lane = threadIdx.x & 31;
+    const int tx = tile % p.TX, ty = tile / p.TX;
+    c.px = tx * GS_TILE + (c.warp & 1) * 8 + (c.lane & 7);
+    c.py = ty * GS_TILE + (c.warp >> 1) * 4 + (c.lane >> 3);
+    c.inside = c.px < p.W && c.py < p.H;
+    c.fpx = (float)c.px + 0.5f;   // pixel centre
+    c.fpy = (float)c.py + 0.5f;
+    c.x0 = (float)(tx * GS_TILE);
+    c.y0 = (float)(ty * GS_TILE);
+    return c;
+}
+
+struct Stage {
+    float4 xyo[kBatch];   // mean2d.x, mean2d.y, opac_eff, (unused)
+    float4 con[kBatch];   // pre-scaled conic
+    float4 rgb[kBatch];   // rgb, (unused)
+    int32_t id[kBatch];
+    uint8_t mask[kBatch];
+    uint8_t list[kWarps][kBatch];
+};
+
+__device__ __forceinline__ void stage_splat(const RasterParams& p, Stage& s, int slot, int idx, float x0, float y0) {
+    const int32_t g = p.ids[idx];
+    const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
+    const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
+    s.xyo[slot] = r0;
+    s.con[slot] = prescale_conic(r1.x, r1.y, r1.z);
+    s.rgb[slot] = r2;
+    s.id[slot] = g;
+    s.mask[slot] = (uint8_t)support_mask(r0.x, r0.y, r0.z, r1.x, r1.w, r2.w, x0, y0, p.alpha_min);
+}
+
+// Order-preserving compaction of the batch slots [0, n) whose mask has this warp's bit
+// (and, in the backward, slot index <= max_slot).  Returns the list length.
+__device__ __forceinline__ int build_warp_list(Stage& s, int n, int warp, int lane, int max_slot) {
+    int cnt = 0;
+    for (int c = 0; c < n; c += 32) {
+        const int j = c + lane;
+        const bool keep = j < n && j <= max_slot && ((s.mask[j] >> warp) & 1u);
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) s.list[warp][cnt + __popc(b & ((1u << lane) - 1u))] = (uint8_t)j;
+        cnt += __popc(b);
+    }
+    __syncwarp();
+    return cnt;
+}
+
 template <bool STATS>
 __global__ void __launch_bounds__(kBatch) k_raster_fwd(RasterParams p) {
-    __shared__ float4 s_xyo[kBatch];
-    __shared__ float4 s_con[kBatch];
-    __shared__ float4 s_rgb[kBatch];
+    __shared__ Stage s;
     const int tile = blockIdx.x, cam = blockIdx.y;
-    const int tx = tile % p.TX, ty = tile / p.TX;
-    const int px = tx * GS_TILE + (threadIdx.x & (GS_TILE - 1));
-    const int py = ty * GS_TILE + (threadIdx.x / GS_TILE);
-    const bool inside = px < p.W && py < p.H;
-    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;   // pixel centre
+    const PixelCoord q = pixel_coord(p, tile);
     const int bin = cam * p.TX * p.TY + tile;
     const int start = p.offs[bin], end = p.offs[bin + 1];
 
     float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
     int last = start - 1;
-    bool done = !inside;
+    bool done = !q.inside;
     int n_eval = 0, n_contrib = 0;
     for (int b0 = start; b0 < end; b0 += kBatch) {
         if (__syncthreads_count(done) == kBatch) break;
-        const int idx = b0 + threadIdx.x;
-        if (idx < end) {
-            const int64_t g = p.ids[idx];
-            const float4* rec = reinterpret_cast<const float4*>(p.splats + g * GS_SPLAT_FLOATS);
-            const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
-            s_xyo[threadIdx.x] = r0;
-            s_con[threadIdx.x] = prescale_conic(r1.x, r1.y, r1.z);
-            s_rgb[threadIdx.x] = r2;
-        }
+        const int n = min(kBatch, end - b0);
+        if ((int)threadIdx.x < n) stage_splat(p, s, threadIdx.x, b0 + threadIdx.x, q.x0, q.y0);
         __syncthreads();
-        if (!done) {
-            const int n = min(kBatch, end - b0);
-            for (int j = 0; j < n; j++) {
-                const float4 xyo = s_xyo[j];
+        if (__all_sync(0xffffffffu, done)) continue;
+        const int cnt = build_warp_list(s, n, q.warp, q.lane, kBatch);
+        for (int k = 0; k < cnt; k++) {
+            const int j = s.list[q.warp][k];
+            if (!done) {
+                const float4 xyo = s.xyo[j];
                 float dx, dy, G, alpha;
                 if (STATS) n_eval++;
-                if (!eval_alpha(xyo.x, xyo.y, xyo.z, s_con[j], fpx, fpy, p.alpha_max, p.alpha_min, dx, dy, G, alpha))
-                    continue;
-                const float nT = __fmul_rn(T, __fsub_rn(1.f, alpha));
-                if (nT <= p.t_min) {   // Q15: stop without compositing this splat
-                    done = true;
-                    break;
+                if (eval_alpha(xyo.x, xyo.y, xyo.z, s.con[j], q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, G,
+                               alpha)) {
+                    const float nT = __fmul_rn(T, __fsub_rn(1.f, alpha));
+                    if (nT <= p.t_min) {   // Q15: stop without compositing this splat
+                        done = true;
+                    } else {
+                        const float w = __fmul_rn(alpha, T);
+                        const float4 rgb = s.rgb[j];
+                        c0 = __fmaf_rn(rgb.x, w, c0);   // C += c alpha T
+                        c1 = __fmaf_rn(rgb.y, w, c1);
+                        c2 = __fmaf_rn(rgb.z, w, c2);
+                        T = nT;
+                        last = b0 + j;
+                        if (STATS) n_contrib++;
+                    }
                 }
-                const float w = __fmul_rn(alpha, T);
-                const float4 rgb = s_rgb[j];
-                c0 = __fmaf_rn(rgb.x, w, c0);   // C += c alpha T
-                c1 = __fmaf_rn(rgb.y, w, c1);
-                c2 = __fmaf_rn(rgb.z, w, c2);
-                T = nT;
-                last = b0 + j;
-                if (STATS) n_contrib++;
             }
+            if (__all_sync(0xffffffffu, done)) break;
         }
     }
+    const int64_t pix = ((int64_t)cam * p.H + q.py) * p.W + q.px;
     if (STATS) {
-        if (inside) {
-            const int64_t pix = ((int64_t)cam * p.H + py) * p.W + px;
+        if (q.inside) {
             p.n_eval[pix] = n_eval;
             p.n_contrib[pix] = n_contrib;
         }
         return;
     }
-    if (inside) {
-        const int64_t pix = ((int64_t)cam * p.H + py) * p.W + px;
+    if (q.inside) {
         float b0 = 0.f, b1 = 0.f, b2 = 0.f;
         if (p.bg) {
             b0 = p.bg[3 * cam];
@@ -154,33 +233,72 @@ __global__ void __launch_bounds__(kBatch) k_raster_fwd(RasterParams p) {
     }
 }
 
+// Transposed warp reduction of 8 values: after it, lane l holds the warp sum of value
+// (l >> 2) & 7.  9 shuffles + 9 adds instead of 40 + 40.
+__device__ __forceinline__ float reduce_scatter8(const float (&v)[8], int lane) {
+    const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+    float u[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const float send = h4 ? v[i] : v[i + 4];
+        const float keep = h4 ? v[i + 4] : v[i];
+        u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float w[2];
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const float send = h3 ? u[i] : u[i + 2];
+        const float keep = h3 ? u[i + 2] : u[i];
+        w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float x = (h2 ? w[1] : w[0]) + __shfl_xor_sync(0xffffffffu, h2 ? w[0] : w[1], 4);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+
+// Same for 4 values: lane l holds the warp sum of value (l >> 3) & 3.
+__device__ __forceinline__ float reduce_scatter4(const float (&v)[4], int lane) {
+    const bool h4 = lane & 16, h3 = lane & 8;
+    float u[2];
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const float send = h4 ? v[i] : v[i + 2];
+        const float keep = h4 ? v[i + 2] : v[i];
+        u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float x = (h3 ? u[1] : u[0]) + __shfl_xor_sync(0xffffffffu, h3 ? u[0] : u[1], 8);
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
+// v_splats slot of value i of the 8-value group: v_mean2d.x, .y, v_opac, v_conic A, B, C, v_r, v_g
+__device__ constexpr int kSlot8[8] = {0, 1, 2, 4, 5, 6, 8, 9};
+// 4-value group (absgrad): v_b, |v_mean2d.x|, |v_mean2d.y|, (none)
+__device__ constexpr int kSlot4[4] = {10, 7, 11, -1};
+
 template <bool ABSGRAD>
 __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
-    __shared__ float4 s_xyo[kBatch];
-    __shared__ float4 s_con[kBatch];
-    __shared__ float4 s_rgb[kBatch];
-    __shared__ int32_t s_id[kBatch];
+    __shared__ Stage s;
     __shared__ int s_maxlast;
     const int tile = blockIdx.x, cam = blockIdx.y;
-    const int tx = tile % p.TX, ty = tile / p.TX;
-    const int px = tx * GS_TILE + (threadIdx.x & (GS_TILE - 1));
-    const int py = ty * GS_TILE + (threadIdx.x / GS_TILE);
-    const bool inside = px < p.W && py < p.H;
-    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+    const PixelCoord q = pixel_coord(p, tile);
     const int bin = cam * p.TX * p.TY + tile;
     const int start = p.offs[bin];
-    const int lane = threadIdx.x & 31;
+    const int lane = q.lane;
 
     float Tfin = 1.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, vA = 0.f, bgdot = 0.f;
     int last = start - 1;
-    if (inside) {
-        const int64_t pix = ((int64_t)cam * p.H + py) * p.W + px;
+    if (q.inside) {
+        const int64_t pix = ((int64_t)cam * p.H + q.py) * p.W + q.px;
         Tfin = p.out_T[pix];
         last = p.last_ids[pix];
         v0 = p.v_rgb[3 * pix + 0];
@@ -191,10 +309,8 @@ __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
     }
     if (threadIdx.x == 0) s_maxlast = start - 1;
     __syncthreads();
-    {
-        int m = __reduce_max_sync(0xffffffffu, last);
-        if (lane == 0) atomicMax(&s_maxlast, m);
-    }
+    const int wlast = __reduce_max_sync(0xffffffffu, last);
+    if (lane == 0) atomicMax(&s_maxlast, wlast);
     __syncthreads();
     const int max_last = s_maxlast;
     // constant part of d C_total / d alpha_k: -T_final ra (bg . v_C) + T_final ra v_A (B4)
@@ -203,35 +319,30 @@ __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
     float T = Tfin, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     for (int bend = max_last + 1; bend > start; bend -= kBatch) {
         const int bstart = max(start, bend - kBatch);
+        const int n = bend - bstart;
         __syncthreads();
-        const int idx = bstart + threadIdx.x;
-        if (idx < bend) {
-            const int32_t g = p.ids[idx];
-            const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
-            const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
-            s_xyo[threadIdx.x] = r0;
-            s_con[threadIdx.x] = prescale_conic(r1.x, r1.y, r1.z);
-            s_rgb[threadIdx.x] = r2;
-            s_id[threadIdx.x] = g;
-        }
+        if ((int)threadIdx.x < n) stage_splat(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0);
         __syncthreads();
-        for (int j = bend - 1 - bstart; j >= 0; j--) {
-            const int k = bstart + j;
-            bool valid = inside && k <= last;
-            const float4 xyo = s_xyo[j];
-            const float4 con = s_con[j];
+        if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
+        const int cnt = build_warp_list(s, n, q.warp, lane, wlast - bstart);
+        for (int k = cnt - 1; k >= 0; k--) {
+            const int j = s.list[q.warp][k];
+            bool valid = q.inside && bstart + j <= last;
+            const float4 xyo = s.xyo[j];
+            const float4 con = s.con[j];
             float dx = 0.f, dy = 0.f, G = 0.f, alpha = 0.f;
             if (valid)
-                valid = eval_alpha(xyo.x, xyo.y, xyo.z, con, fpx, fpy, p.alpha_max, p.alpha_min, dx, dy, G, alpha);
+                valid = eval_alpha(xyo.x, xyo.y, xyo.z, con, q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, G, alpha);
             if (!__any_sync(0xffffffffu, valid)) continue;
-            float g_mx = 0.f, g_my = 0.f, g_o = 0.f, g_a = 0.f, g_b = 0.f, g_c = 0.f, g_r = 0.f, g_g = 0.f, g_bl = 0.f;
+            float g8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // mx, my, o, A, B, C, r, g
+            float g_bl = 0.f;
             if (valid) {
-                const float4 rgb = s_rgb[j];
+                const float4 rgb = s.rgb[j];
                 const float ra = 1.f / (1.f - alpha);
                 T = T * ra;                        // B2: T_{n-1} = T_n / (1 - alpha_{n-1})
                 const float fac = alpha * T;
-                g_r = fac * v0;                    // B3
-                g_g = fac * v1;
+                g8[6] = fac * v0;                  // B3
+                g8[7] = fac * v1;
                 g_bl = fac * v2;
                 // B4 + background / alpha-output terms (Q25, Q26)
                 const float v_alpha = (rgb.x * T - S0 * ra) * v0 + (rgb.y * T - S1 * ra) * v1 +
@@ -241,37 +352,28 @@ __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
                 S2 += rgb.z * fac;
                 const float raw = xyo.z * G;
                 if (raw < p.alpha_max) {           // B6 (Q24)
-                    g_o = G * v_alpha;
+                    g8[2] = G * v_alpha;
                     const float v_sigma = -raw * v_alpha;
-                    g_a = 0.5f * v_sigma * dx * dx;
-                    g_b = v_sigma * dx * dy;
-                    g_c = 0.5f * v_sigma * dy * dy;
+                    g8[3] = 0.5f * v_sigma * dx * dx;
+                    g8[4] = v_sigma * dx * dy;
+                    g8[5] = 0.5f * v_sigma * dy * dy;
                     // d sigma / d mu' = Sigma'^-1 Delta, with the conic recovered from
                     // the pre-scaled one: A = a' (-2 ln2), B = b' (-ln2), C = c' (-2 ln2)
                     const float k2 = -kLn2 * v_sigma;
-                    g_mx = k2 * (2.f * con.x * dx + con.y * dy);
-                    g_my = k2 * (con.y * dx + 2.f * con.z * dy);
+                    g8[0] = k2 * (2.f * con.x * dx + con.y * dy);
+                    g8[1] = k2 * (con.y * dx + 2.f * con.z * dy);
                 }
             }
-            float a_mx = 0.f, a_my = 0.f;
+            float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
+            const float r8 = reduce_scatter8(g8, lane);
+            if ((lane & 3) == 0) atomicAdd(dst + kSlot8[lane >> 2], r8);
             if (ABSGRAD) {
-                a_mx = warp_sum(fabsf(g_mx));
-                a_my = warp_sum(fabsf(g_my));
-            }
-            g_mx = warp_sum(g_mx);
-            g_my = warp_sum(g_my);
-            g_o = warp_sum(g_o);
-            g_a = warp_sum(g_a);
-            g_b = warp_sum(g_b);
-            g_c = warp_sum(g_c);
-            g_r = warp_sum(g_r);
-            g_g = warp_sum(g_g);
-            g_bl = warp_sum(g_bl);
-            if (lane == 0) {
-                float* dst = p.v_splats + (int64_t)s_id[j] * GS_SPLAT_FLOATS;
-                red_add_v4(dst, g_mx, g_my, g_o, 0.f);
-                red_add_v4(dst + 4, g_a, g_b, g_c, a_mx);
-                red_add_v4(dst + 8, g_r, g_g, g_bl, a_my);
+                const float g4[4] = {g_bl, fabsf(g8[0]), fabsf(g8[1]), 0.f};
+                const float r4 = reduce_scatter4(g4, lane);
+                if ((lane & 7) == 0 && (lane >> 3) < 3) atomicAdd(dst + kSlot4[lane >> 3], r4);
+            } else {
+                const float rb = warp_sum(g_bl);
+                if (lane == 0) atomicAdd(dst + 10, rb);
             }
         }
     }

@@ -119,7 +119,7 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
                                                               backgrounds)]
     out_rgb, out_alpha, radii, splats, ids, offs, out_T, last_ids, Mdev = _Rasterize.apply(*args, cfg, absgrad_out)
     meta = dict(radii=radii, means2d=splats[..., 0:2], depths=splats[..., 3], conics=splats[..., 4:7],
-                opacities=splats[..., 2], colors=splats[..., 8:11], compensations=splats[..., 7], splats=splats,
+                opacities=splats[..., 2], colors=splats[..., 8:11], splats=splats,
                 isect_ids=ids, flatten_ids=ids, tile_offsets=offs, n_isects=Mdev, T_final=out_T, last_ids=last_ids,
                 width=int(width), height=int(height), tile_size=tile_size, n_cameras=C, absgrad=absgrad_out,
                 cfg=cfg)

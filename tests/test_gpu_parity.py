@@ -79,7 +79,11 @@ def test_project_parity(cache, name):
     assert np.all(sp[~vis] == 0)
     np.testing.assert_allclose(sp[..., 4:7][vis], p["conic"][vis], rtol=1e-3, atol=1e-7)
     np.testing.assert_allclose(sp[..., 8:11][vis], p["rgb"][vis], rtol=1e-5, atol=1e-5)
-    np.testing.assert_allclose(sp[..., 7][vis], p["comp"][vis], rtol=1e-3, atol=1e-4)
+    # slots 7, 11: blurred variances a, c = diag((Sigma'+sI)) = diag(conic^-1)
+    A, B, Cc = p["conic"][..., 0][vis], p["conic"][..., 1][vis], p["conic"][..., 2][vis]
+    det = A * Cc - B * B
+    np.testing.assert_allclose(sp[..., 7][vis], Cc / det, rtol=1e-3)
+    np.testing.assert_allclose(sp[..., 11][vis], A / det, rtol=1e-3)
     np.testing.assert_allclose(sp[..., 2][vis], p["opac_eff"][vis], rtol=1e-3, atol=1e-4)
 
 
