@@ -280,10 +280,17 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// v_splats slot of value i of the 8-value group: v_mean2d.x, .y, v_opac, v_conic A, B, C, v_r, v_g
-__device__ constexpr int kSlot8[8] = {0, 1, 2, 4, 5, 6, 8, 9};
-// 4-value group (absgrad): v_b, |v_mean2d.x|, |v_mean2d.y|, (none)
-__device__ constexpr int kSlot4[4] = {10, 7, 11, -1};
+// v_splats slot of value i of the 8-value group (v_mean2d.x, .y, v_opac, v_conic A, B, C,
+// v_r, v_g) is i + i/3 = {0, 1, 2, 4, 5, 6, 8, 9}; of the 4-value absgrad group (v_b,
+// |v_mean2d.x|, |v_mean2d.y|) it is {10, 7, 11}.
+__device__ __forceinline__ int slot8(int i) { return i + i / 3; }
+__device__ __forceinline__ int slot4(int i) { return i == 0 ? 10 : (i == 1 ? 7 : 11); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 template <bool ABSGRAD>
 __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
             float g_bl = 0.f;
             if (valid) {
                 const float4 rgb = s.rgb[j];
-                const float ra = 1.f / (1.f - alpha);
+                const float ra = rcp_approx(1.f - alpha);
                 T = T * ra;                        // B2: T_{n-1} = T_n / (1 - alpha_{n-1})
                 const float fac = alpha * T;
                 g8[6] = fac * v0;                  // B3
@@ -366,11 +373,11 @@ __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
             }
             float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
             const float r8 = reduce_scatter8(g8, lane);
-            if ((lane & 3) == 0) atomicAdd(dst + kSlot8[lane >> 2], r8);
+            if ((lane & 3) == 0) atomicAdd(dst + slot8(lane >> 2), r8);
             if (ABSGRAD) {
                 const float g4[4] = {g_bl, fabsf(g8[0]), fabsf(g8[1]), 0.f};
                 const float r4 = reduce_scatter4(g4, lane);
-                if ((lane & 7) == 0 && (lane >> 3) < 3) atomicAdd(dst + kSlot4[lane >> 3], r4);
+                if ((lane & 7) == 0 && (lane >> 3) < 3) atomicAdd(dst + slot4(lane >> 3), r4);
             } else {
                 const float rb = warp_sum(g_bl);
                 if (lane == 0) atomicAdd(dst + 10, rb);

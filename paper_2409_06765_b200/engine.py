@@ -20,10 +20,7 @@ import math
 import torch
 
 from . import _lib as L
-
-
-def _align4(n):
-    return (n + 3) // 4 * 4
+from . import dist as D
 
 
 class Engine:
@@ -49,21 +46,13 @@ class Engine:
         self.out_alpha = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
         self.out_T = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
         self.last_ids = torch.zeros((C, H, W), dtype=torch.int32, device=dev)
-        # flat gradient buffer: [quats 4N | means 3N | scales 3N | opacities N | colors 3KN],
-        # each section 16-byte aligned (float4 stores in K8)
-        ncol = 3 * self.K * N if self.sh_degree >= 0 else 3 * N
-        sizes = [4 * N, 3 * N, 3 * N, N, ncol]
-        offs = [0]
-        for s in sizes[:-1]:
-            offs.append(offs[-1] + _align4(s))
-        self.flat_grad = torch.zeros(offs[-1] + _align4(sizes[-1]), dtype=torch.float32, device=dev)
-        fg = self.flat_grad
-        self.v_quats = fg[offs[0]:offs[0] + sizes[0]].view(N, 4)
-        self.v_means = fg[offs[1]:offs[1] + sizes[1]].view(N, 3)
-        self.v_scales = fg[offs[2]:offs[2] + sizes[2]].view(N, 3)
-        self.v_opacities = fg[offs[3]:offs[3] + sizes[3]].view(N)
-        colshape = (N, self.K, 3) if self.sh_degree >= 0 else (N, 3)
-        self.v_colors = fg[offs[4]:offs[4] + sizes[4]].view(*colshape)
+        # flat gradient buffer (the single all-reduce unit, dist.flat_layout)
+        sh = self.sh_degree >= 0
+        self.flat_layout, total = D.flat_layout(N, self.K, sh)
+        self.flat_grad = torch.zeros(total, dtype=torch.float32, device=dev)
+        v = D.views(self.flat_grad, N, self.K, sh)
+        self.v_quats, self.v_means, self.v_scales = v["quats"], v["means"], v["scales"]
+        self.v_opacities, self.v_colors = v["opacities"], v["colors"]
         self.cap = 0
         self.isect_ids = None
         self.isect_keys = None
