@@ -13,7 +13,7 @@
 namespace gsb {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 
 struct PBParams {
     int64_t N;
@@ -40,7 +40,7 @@ struct PBParams {
 template <int DEG>
 __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
     const int64_t n = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (n >= p.N) return;
+    if (n >= p.N) return;   // no block-level synchronisation below
     constexpr int NB = DEG < 0 ? 1 : (DEG + 1) * (DEG + 1);
 
     const float mu[3] = {p.means[3 * n], p.means[3 * n + 1], p.means[3 * n + 2]};
@@ -65,11 +65,17 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
 
     float g_mu[3] = {0.f, 0.f, 0.f}, g_S[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
     float g_op = 0.f;
-    float coef[NB * 3];
-    float g_coef[NB * 3];
+    // SH gradient accumulators live in shared memory (one column per thread, conflict-free)
+    // and the coefficients are streamed from L1/L2, keeping registers and occupancy for this
+    // HBM-bound kernel
+    __shared__ float s_gc[DEG < 0 ? 1 : NB * 3][kThreads];
+    float g_rgb[3] = {0.f, 0.f, 0.f};
+    if (DEG >= 0) {
 #pragma unroll
-    for (int i = 0; i < NB * 3; i++) g_coef[i] = 0.f;
-    bool coef_loaded = false;
+        for (int i = 0; i < NB * 3; i++) s_gc[i][threadIdx.x] = 0.f;
+    }
+    const float* src = p.colors + n * (int64_t)p.K * 3;
+    const bool vec = p.vec_colors && (NB * 3) % 4 == 0;
     bool seen = false;
 
     for (int c = 0; c < p.C; c++) {
@@ -201,16 +207,10 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
             for (int j = 0; j < 3; j++) g_S[i][j] += Wr[0][i] * T1[0][j] + Wr[1][i] * T1[1][j] + Wr[2][i] * T1[2][j];
         // ---- P7: colour
         if (DEG < 0) {
-            g_coef[0] += v2.x;
-            g_coef[1] += v2.y;
-            g_coef[2] += v2.z;
+            g_rgb[0] += v2.x;
+            g_rgb[1] += v2.y;
+            g_rgb[2] += v2.z;
         } else {
-            if (!coef_loaded) {
-                const float* src = p.colors + n * (int64_t)p.K * 3;
-#pragma unroll
-                for (int i = 0; i < NB * 3; i++) coef[i] = src[i];
-                coef_loaded = true;
-            }
             float campos[3];
 #pragma unroll
             for (int i = 0; i < 3; i++) campos[i] = -(Wr[0][i] * w[0] + Wr[1][i] * w[1] + Wr[2][i] * w[2]);
@@ -219,23 +219,40 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
             const float dx = ex / en, dy = ey / en, dz = ez / en;
             float Yb[NB];
             sh_eval_basis<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, Yb);
-            float raw0 = 0.5f, raw1 = 0.5f, raw2 = 0.5f;
+            float raw[3] = {0.5f, 0.5f, 0.5f};
+            if (vec) {
 #pragma unroll
-            for (int j = 0; j < NB; j++) {
-                raw0 += Yb[j] * coef[3 * j];
-                raw1 += Yb[j] * coef[3 * j + 1];
-                raw2 += Yb[j] * coef[3 * j + 2];
-            }
-            const float vr0 = raw0 > 0.f ? v2.x : 0.f, vr1 = raw1 > 0.f ? v2.y : 0.f, vr2 = raw2 > 0.f ? v2.z : 0.f;
-            float wj[NB];
+                for (int i = 0; i < NB * 3 / 4; i++) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
+                    raw[(4 * i + 0) % 3] += Yb[(4 * i + 0) / 3] * v.x;
+                    raw[(4 * i + 1) % 3] += Yb[(4 * i + 1) / 3] * v.y;
+                    raw[(4 * i + 2) % 3] += Yb[(4 * i + 2) / 3] * v.z;
+                    raw[(4 * i + 3) % 3] += Yb[(4 * i + 3) / 3] * v.w;
+                }
+            } else {
 #pragma unroll
-            for (int j = 0; j < NB; j++) {
-                g_coef[3 * j] += Yb[j] * vr0;
-                g_coef[3 * j + 1] += Yb[j] * vr1;
-                g_coef[3 * j + 2] += Yb[j] * vr2;
-                wj[j] = coef[3 * j] * vr0 + coef[3 * j + 1] * vr1 + coef[3 * j + 2] * vr2;
+                for (int i = 0; i < NB * 3; i++) raw[i % 3] += Yb[i / 3] * __ldg(src + i);
             }
+            const float vr[3] = {raw[0] > 0.f ? v2.x : 0.f, raw[1] > 0.f ? v2.y : 0.f, raw[2] > 0.f ? v2.z : 0.f};
+#pragma unroll
+            for (int i = 0; i < NB * 3; i++) s_gc[i][threadIdx.x] += Yb[i / 3] * vr[i % 3];
             if (DEG > 0) {
+                float wj[NB];
+#pragma unroll
+                for (int j = 0; j < NB; j++) wj[j] = 0.f;
+                if (vec) {
+#pragma unroll
+                    for (int i = 0; i < NB * 3 / 4; i++) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
+                        wj[(4 * i + 0) / 3] += v.x * vr[(4 * i + 0) % 3];
+                        wj[(4 * i + 1) / 3] += v.y * vr[(4 * i + 1) % 3];
+                        wj[(4 * i + 2) / 3] += v.z * vr[(4 * i + 2) % 3];
+                        wj[(4 * i + 3) / 3] += v.w * vr[(4 * i + 3) % 3];
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NB * 3; i++) wj[i / 3] += __ldg(src + i) * vr[i % 3];
+                }
                 float gx = 0.f, gy = 0.f, gz = 0.f;
                 sh_basis_vjp<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, wj, gx, gy, gz);
                 const float dd = dx * gx + dy * gy + dz * gz;
@@ -290,20 +307,19 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
     p.v_opac[n] = g_op;
     if (DEG < 0) {
 #pragma unroll
-        for (int i = 0; i < 3; i++) p.v_colors[3 * n + i] = g_coef[i];
+        for (int i = 0; i < 3; i++) p.v_colors[3 * n + i] = g_rgb[i];
     } else {
         float* dst = p.v_colors + n * (int64_t)p.K * 3;
-        if (p.vec_colors && (NB * 3) % 4 == 0) {
+        if (vec) {
 #pragma unroll
             for (int i = 0; i < NB * 3 / 4; i++)
-                reinterpret_cast<float4*>(dst)[i] =
-                    make_float4(g_coef[4 * i], g_coef[4 * i + 1], g_coef[4 * i + 2], g_coef[4 * i + 3]);
-            for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
+                reinterpret_cast<float4*>(dst)[i] = make_float4(s_gc[4 * i][threadIdx.x], s_gc[4 * i + 1][threadIdx.x],
+                                                                s_gc[4 * i + 2][threadIdx.x], s_gc[4 * i + 3][threadIdx.x]);
         } else {
 #pragma unroll
-            for (int i = 0; i < NB * 3; i++) dst[i] = g_coef[i];
-            for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
+            for (int i = 0; i < NB * 3; i++) dst[i] = s_gc[i][threadIdx.x];
         }
+        for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
     }
 }
 

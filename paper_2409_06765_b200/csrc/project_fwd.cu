@@ -107,8 +107,6 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
         S22 = (M20 * M20 + M21 * M21) + M22 * M22;
     }
     constexpr int NB = DEG < 0 ? 1 : (DEG + 1) * (DEG + 1);
-    float coef[NB * 3];
-    bool coef_loaded = false;
 
     for (int c0 = 0; c0 < p.C; c0 += kCamChunk) {
         const int nc = min(kCamChunk, p.C - c0);
@@ -215,34 +213,28 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
                 g = p.colors[3 * n + 1];
                 bl = p.colors[3 * n + 2];
             } else {
-                if (!coef_loaded) {
-                    const float* src = p.colors + n * (int64_t)p.K * 3;
-                    if (p.vec_colors && (NB * 3) % 4 == 0) {
-#pragma unroll
-                        for (int i = 0; i < NB * 3 / 4; i++) {
-                            float4 v = reinterpret_cast<const float4*>(src)[i];
-                            coef[4 * i + 0] = v.x;
-                            coef[4 * i + 1] = v.y;
-                            coef[4 * i + 2] = v.z;
-                            coef[4 * i + 3] = v.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < NB * 3; i++) coef[i] = src[i];
-                    }
-                    coef_loaded = true;
-                }
                 float ex = mu0 - cc.campos[0], ey = mu1 - cc.campos[1], ez = mu2 - cc.campos[2];
                 float en = sqrtf((ex * ex + ey * ey) + ez * ez);
                 float Y[NB];
                 sh_eval_basis<(DEG < 0 ? 0 : DEG)>(ex / en, ey / en, ez / en, Y);
-                float acc0 = 0.5f, acc1 = 0.5f, acc2 = 0.5f;
+                // coefficients streamed (16-byte loads; the row stays in L1/L2 for the next
+                // camera) instead of held in registers: keeps occupancy up in this HBM-bound kernel
+                float acc[3] = {0.5f, 0.5f, 0.5f};
+                const float* src = p.colors + n * (int64_t)p.K * 3;
+                if (p.vec_colors && (NB * 3) % 4 == 0) {
 #pragma unroll
-                for (int j = 0; j < NB; j++) {
-                    acc0 += Y[j] * coef[3 * j + 0];
-                    acc1 += Y[j] * coef[3 * j + 1];
-                    acc2 += Y[j] * coef[3 * j + 2];
+                    for (int i = 0; i < NB * 3 / 4; i++) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
+                        acc[(4 * i + 0) % 3] += Y[(4 * i + 0) / 3] * v.x;
+                        acc[(4 * i + 1) % 3] += Y[(4 * i + 1) / 3] * v.y;
+                        acc[(4 * i + 2) % 3] += Y[(4 * i + 2) / 3] * v.z;
+                        acc[(4 * i + 3) % 3] += Y[(4 * i + 3) / 3] * v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NB * 3; i++) acc[i % 3] += Y[i / 3] * __ldg(src + i);
                 }
+                const float acc0 = acc[0], acc1 = acc[1], acc2 = acc[2];
                 r = fmaxf(acc0, 0.f);
                 g = fmaxf(acc1, 0.f);
                 bl = fmaxf(acc2, 0.f);
