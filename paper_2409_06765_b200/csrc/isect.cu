@@ -33,6 +33,8 @@ constexpr int kT = 256;              // threads per block
 constexpr int kWarps = kT / 32;
 constexpr int kItems = 16;           // items per thread
 constexpr int kTile = kT * kItems;   // items per block (4096)
+constexpr int kSortItems = 4;                  // radix sort: items per thread ...
+constexpr int kSortTile = kT * kSortItems;     // ... and per block (1024: enough blocks to fill 148 SMs)
 constexpr int kScanThreads = 1024;
 constexpr int kEmit = 2048;          // output positions per emission block
 
@@ -151,81 +153,105 @@ __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ rad
 }
 
 // ---------------------------------------------------------------------------------------
-// K4: one pass of a stable LSD radix sort (8-bit digit at `shift`).
-// hist layout: hist[d * nb_max + b] = count of digit d in block b (digit-major rows).
-__global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
-                                                   int shift, int* hist, int nb_max) {
-    __shared__ int s_hist[256];
+// K4: stable LSD radix sort, one kernel per 8-bit pass (Onesweep-style decoupled look-back).
+// k_global_hist computes, in one read of the keys, the digit histogram of EVERY pass (the
+// global digit totals do not depend on the order).  Each pass kernel then takes a ticket
+// (blocks are numbered in scheduling order, so waiting on lower tickets cannot deadlock),
+// ranks its 4096 keys stably in shared memory, publishes its per-digit count, looks back
+// over the predecessors' published counts/prefixes to get its global offset per digit,
+// reorders the tile by digit in shared memory and writes every digit run coalesced.
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagPre = 2u << 30, kCountMask = (1u << 30) - 1u;
+
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Lanes of the warp holding the same 8-bit digit d (d >= 256 marks an invalid lane, which
+// only matches invalid lanes): 9 ballots instead of MATCH.ANY, whose issue cost made the
+// radix kernels latency-bound.
+__device__ __forceinline__ unsigned warp_peers(unsigned d) {
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; b++) {
+        const unsigned bit = (d >> b) & 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? m : ~m;
+    }
+    return peers;
+}
+
+// g_hist[p * 256 + d] += number of keys whose digit p is d, for p in [0, passes).
+__global__ void __launch_bounds__(kT) k_global_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
+                                                    int passes, int* g_hist) {
+    __shared__ int s_hist[4][256];
     const int n = (int)min((int64_t)*d_n, cap);
-    const int nb = div_up(n, kTile);
+    const int nb = div_up(n, kSortTile);
     if ((int)blockIdx.x >= nb) return;
-    s_hist[threadIdx.x] = 0;
+#pragma unroll
+    for (int p = 0; p < 4; p++) s_hist[p][threadIdx.x] = 0;
     __syncthreads();
-    const int base = blockIdx.x * kTile;
+    const int base = blockIdx.x * kSortTile;
     const int lane = threadIdx.x & 31;
-#pragma unroll 4
-    for (int k = 0; k < kItems; k++) {
+    for (int k = 0; k < kSortItems; k++) {
         const int i = base + k * kT + threadIdx.x;
-        const unsigned d = i < n ? (keys[i] >> shift) & 255u : 256u + lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (d < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[d], __popc(peers));
+        const bool valid = i < n;
+        const uint32_t key = valid ? keys[i] : 0u;
+        for (int p = 0; p < passes; p++) {
+            const unsigned d = valid ? (key >> (8 * p)) & 255u : 256u;
+            const unsigned peers = warp_peers(d);
+            if (d < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[p][d], __popc(peers));
+        }
     }
     __syncthreads();
-    hist[threadIdx.x * nb_max + blockIdx.x] = s_hist[threadIdx.x];
-}
-
-// One block per digit: exclusive scan of that digit's row over the live blocks; the
-// row total goes to rowtot[d].
-__global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, const int* d_n, int64_t cap,
-                                                        int* rowtot) {
-    __shared__ int s_warp[33];
-    const int n = (int)min((int64_t)*d_n, cap);
-    const int nb = div_up(n, kTile);
-    int* row = hist + (int64_t)blockIdx.x * nb_max;
-    int carry = 0;
-    for (int r = 0; r < nb; r += kT) {
-        const int i = r + threadIdx.x;
-        const int v = i < nb ? row[i] : 0;
-        int tot;
-        const int ex = block_exclusive_scan(v, s_warp, &tot);
-        if (i < nb) row[i] = carry + ex;
-        carry += tot;
+    for (int p = 0; p < passes; p++) {
+        const int c = s_hist[p][threadIdx.x];
+        if (c) atomicAdd(&g_hist[p * 256 + threadIdx.x], c);
     }
-    if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
 }
 
-__global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict__ keys_in,
-                                                      const int32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-                                                      int32_t* __restrict__ vals_out, const int* d_n, int64_t cap,
-                                                      int shift, const int* __restrict__ hist, int nb_max,
-                                                      const int* __restrict__ rowtot) {
+__global__ void __launch_bounds__(kT) k_onesweep(const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
+                                                 uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out,
+                                                 const int* d_n, int64_t cap, int shift, const int* __restrict__ g_hist,
+                                                 uint32_t* status, int* ticket) {
     __shared__ int s_cnt[kWarps][256];    // per-warp running digit counts, then per-warp offsets
     __shared__ int s_dstart[256];         // start of digit d inside this block's sorted tile
     __shared__ int s_goff[256];           // global start of digit d for this block
     __shared__ int s_warp[33];
-    __shared__ uint32_t s_k[kTile];
-    __shared__ int32_t s_v[kTile];
+    __shared__ int s_bid;
+    __shared__ uint32_t s_k[kSortTile];
+    __shared__ int32_t s_v[kSortTile];
     const int n = (int)min((int64_t)*d_n, cap);
-    const int nb = div_up(n, kTile);
-    if ((int)blockIdx.x >= nb) return;
+    const int nb = div_up(n, kSortTile);
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll
     for (int w = 0; w < kWarps; w++) s_cnt[w][threadIdx.x] = 0;
     __syncthreads();
+    const int bid = s_bid;
+    if (bid >= nb) return;
     // 1. per-warp stable ranks over the warp's contiguous slice of 512 items
-    const int base = blockIdx.x * kTile + warp * (kTile / kWarps);
-    uint32_t key[kItems];
-    int32_t val[kItems];
-    int rank[kItems];
+    const int base = bid * kSortTile + warp * (kSortTile / kWarps);
+    uint32_t key[kSortItems];
+    int32_t val[kSortItems];
+    int rank[kSortItems];
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
+    for (int k = 0; k < kSortItems; k++) {
         const int i = base + k * 32 + lane;
         const bool valid = i < n;
         key[k] = valid ? keys_in[i] : 0u;
         val[k] = valid ? vals_in[i] : 0;
-        const unsigned d = valid ? (key[k] >> shift) & 255u : 256u + lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+    }
+#pragma unroll
+    for (int k = 0; k < kSortItems; k++) {
+        const bool valid = base + k * 32 + lane < n;
+        const unsigned d = valid ? (key[k] >> shift) & 255u : 256u;
+        const unsigned peers = warp_peers(d);
         int b = 0;
         if (valid) b = s_cnt[warp][d];
         __syncwarp();
@@ -234,7 +260,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
         rank[k] = valid ? b + __popc(peers & lt_mask) : -1;
     }
     __syncthreads();
-    // 2. per digit: exclusive offsets across warps, block digit totals, digit starts
+    // 2. per digit: offsets across warps, block digit count, publish + look back
     {
         const int d = threadIdx.x;
         int run = 0;
@@ -244,19 +270,44 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
             s_cnt[w][d] = run;
             run += c;
         }
+        uint32_t* my = status + (int64_t)bid * 256 + d;
+        int excl = 0;
+        if (bid == 0) {
+            st_relaxed(my, kFlagPre | (uint32_t)run);
+        } else {
+            st_relaxed(my, kFlagAgg | (uint32_t)run);
+            // windowed look-back: kWin predecessors per round trip
+            constexpr int kWin = 16;
+            int k = bid - 1;
+            bool found = false;
+            while (!found) {
+                uint32_t v[kWin];
+#pragma unroll
+                for (int i = 0; i < kWin; i++)
+                    v[i] = (k - i >= 0) ? ld_relaxed(status + (int64_t)(k - i) * 256 + d) : kFlagPre;
+                int i = 0;
+                for (; i < kWin; i++) {
+                    const uint32_t f = v[i] & ~kCountMask;
+                    if (f == 0u) break;   // not published yet: re-poll from here
+                    excl += (int)(v[i] & kCountMask);
+                    if (f == kFlagPre) {
+                        found = true;
+                        break;
+                    }
+                }
+                k -= i;
+            }
+            st_relaxed(my, kFlagPre | (uint32_t)(excl + run));
+        }
         int tot;
-        const int start = block_exclusive_scan(run, s_warp, &tot);   // digits in ascending order
-        s_dstart[d] = start;
-        // global start: rows scanned per digit + digit base (exclusive scan of row totals)
-        int dbase;
+        s_dstart[d] = block_exclusive_scan(run, s_warp, &tot);          // digits in ascending order
         int dummy;
-        dbase = block_exclusive_scan(rowtot[d], s_warp, &dummy);
-        s_goff[d] = dbase + hist[d * nb_max + blockIdx.x];
+        s_goff[d] = block_exclusive_scan(g_hist[d], s_warp, &dummy) + excl;
     }
     __syncthreads();
     // 3. reorder the tile by digit in shared memory
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
+    for (int k = 0; k < kSortItems; k++) {
         if (rank[k] >= 0) {
             const unsigned d = (key[k] >> shift) & 255u;
             const int p = s_dstart[d] + s_cnt[warp][d] + rank[k];
@@ -266,9 +317,9 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
     }
     __syncthreads();
     // 4. coalesced write-out of the digit runs
-    const int nloc = min(kTile, n - blockIdx.x * kTile);
+    const int nloc = min(kSortTile, n - bid * kSortTile);
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
+    for (int k = 0; k < kSortItems; k++) {
         const int j = k * kT + threadIdx.x;
         if (j < nloc) {
             const uint32_t kk = s_k[j];
@@ -418,10 +469,13 @@ __global__ void k_keys64(const uint32_t* __restrict__ keys32, const int32_t* __r
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+constexpr int kMaxPasses = 8;   // 4 (depth) + up to 4 ((camera, tile) key)
+
 struct WsLayout {
-    size_t off_scalars, off_blocksum, off_rowtot, off_hist, off_vk, off_vv, off_ak, off_av, off_rect, off_cnt,
-        off_eoff, off_ka, off_va, off_kb, off_vb, total;
-    int nb_max;
+    size_t off_scalars, off_blocksum, off_sweep, off_vk, off_vv, off_ak, off_av, off_rect, off_cnt, off_eoff, off_ka,
+        off_va, off_kb, off_vb, total, sweep_bytes;
+    int nb_max;        // blocks of kTile items (compaction, tile counts)
+    int nb_sort_max;   // blocks of kSortTile items (radix passes)
 };
 
 WsLayout ws_layout(int C, int64_t N, int64_t cap) {
@@ -429,11 +483,14 @@ WsLayout ws_layout(int C, int64_t N, int64_t cap) {
     const int64_t n_items = (int64_t)C * N;
     const int64_t big = n_items > cap ? n_items : cap;
     L.nb_max = div_up(big > 0 ? big : 1, kTile);
+    L.nb_sort_max = div_up(big > 0 ? big : 1, kSortTile);
     size_t o = 0;
     L.off_scalars = o; o = align256(o + 64);
     L.off_blocksum = o; o = align256(o + sizeof(int) * (size_t)(L.nb_max + 1));
-    L.off_rowtot = o; o = align256(o + sizeof(int) * 256);
-    L.off_hist = o; o = align256(o + sizeof(int) * 256 * (size_t)L.nb_max);
+    // onesweep state, zeroed once per call: per pass a ticket, 256 digit totals and the
+    // [nb_max][256] look-back status words
+    L.sweep_bytes = (size_t)kMaxPasses * (sizeof(int) * (1 + 256) + sizeof(uint32_t) * 256 * (size_t)L.nb_sort_max);
+    L.off_sweep = o; o = align256(o + L.sweep_bytes);
     L.off_vk = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_vv = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_ak = o; o = align256(o + 4 * (size_t)(n_items + 1));
@@ -454,18 +511,36 @@ struct KV {
     int32_t* v;
 };
 
-// Runs ceil(bits/8) stable 8-bit LSD passes over `a` (live count *d_n <= cap), ping-ponging
-// with `b`.  The last pass writes its values to `final_vals` when given.  Returns the
-// buffers holding the sorted result.
-KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
-              int nb_max, cudaStream_t s) {
+struct Sweep {
+    int* tickets;      // [kMaxPasses]
+    int* g_hist;       // [kMaxPasses][256]
+    uint32_t* status;  // [kMaxPasses][nb_max][256]
+    int nb_max;
+};
+
+Sweep sweep_state(char* base, int nb_max) {
+    Sweep w;
+    w.tickets = reinterpret_cast<int*>(base);
+    w.g_hist = w.tickets + kMaxPasses;
+    w.status = reinterpret_cast<uint32_t*>(w.g_hist + kMaxPasses * 256);
+    w.nb_max = nb_max;
+    return w;
+}
+
+// ceil(bits/8) stable 8-bit LSD passes over `a` (live count *d_n <= cap), ping-ponging with
+// `b`, using sweep slots [pass0, pass0 + passes).  The last pass writes its values to
+// `final_vals` when given.  Returns the buffers holding the sorted result.
+KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, const Sweep& w, int pass0,
+              cudaStream_t s) {
     const int passes = bits <= 0 ? 0 : div_up(bits, 8);
+    if (passes == 0) return a;
+    k_global_hist<<<w.nb_max, kT, 0, s>>>(a.k, d_n, cap, passes, w.g_hist + pass0 * 256);
     KV in = a, out = b;
     for (int p = 0; p < passes; p++) {
         int32_t* vdst = (p == passes - 1 && final_vals) ? final_vals : out.v;
-        k_radix_hist<<<nb_max, kT, 0, s>>>(in.k, d_n, cap, 8 * p, hist, nb_max);
-        k_radix_scan_rows<<<256, kT, 0, s>>>(hist, nb_max, d_n, cap, rowtot);
-        k_radix_scatter<<<nb_max, kT, 0, s>>>(in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max, rowtot);
+        const int slot = pass0 + p;
+        k_onesweep<<<w.nb_max, kT, 0, s>>>(in.k, in.v, out.k, vdst, d_n, cap, 8 * p, w.g_hist + slot * 256 + 0 * 0,
+                                           w.status + (size_t)slot * 256 * w.nb_max, w.tickets + slot);
         KV next_in{out.k, vdst};
         out = in;
         in = next_in;
@@ -491,8 +566,7 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     int* d_V = scal + 0;
     int* d_nsort = scal + 1;
     int* blocksum = reinterpret_cast<int*>(w + L.off_blocksum);
-    int* rowtot = reinterpret_cast<int*>(w + L.off_rowtot);
-    int* hist = reinterpret_cast<int*>(w + L.off_hist);
+    const Sweep sw = sweep_state(w + L.off_sweep, L.nb_sort_max);
     KV vis{reinterpret_cast<uint32_t*>(w + L.off_vk), reinterpret_cast<int32_t*>(w + L.off_vv)};
     KV alt{reinterpret_cast<uint32_t*>(w + L.off_ak), reinterpret_cast<int32_t*>(w + L.off_av)};
     int4* ent_rect = reinterpret_cast<int4*>(w + L.off_rect);
@@ -509,6 +583,10 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     const int2* r2 = reinterpret_cast<const int2*>(radii);
     const int nb_items = div_up(n_items > 0 ? n_items : 1, kTile);
 
+    if (cudaMemsetAsync(w + L.off_sweep, 0, L.sweep_bytes, s) != cudaSuccess) {
+        GS_LAUNCH_CHECK("isect/memset");
+        return GS_ERR_CUDA;
+    }
     // 1. stable compaction of the visible (c,n) items (K2a, K2b)
     k_vis_count<<<nb_items, kT, 0, s>>>(r2, n_items, blocksum);
     k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, nullptr, n_items, INT64_MAX, d_V, nullptr, nullptr, 0,
@@ -516,7 +594,7 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     k_vis_compact<<<nb_items, kT, 0, s>>>(r2, splats, n_items, blocksum, vis.k, vis.v);
     GS_LAUNCH_CHECK("isect/compact");
     // 2. stable sort by fp32 depth bits (K4, 4 passes)
-    KV dsorted = radix_sort(vis, alt, nullptr, d_V, n_items, 32, hist, rowtot, L.nb_max, s);
+    KV dsorted = radix_sort(vis, alt, nullptr, d_V, n_items, 32, sw, 0, s);
     GS_LAUNCH_CHECK("isect/depth-sort");
     // 3. tile rectangles, counts, offsets, M, overflow, clamped count (K2c, K2d)
     k_tiles_count<<<nb_items, kT, 0, s>>>(r2, splats, dsorted.v, d_V, g, ent_rect, ent_cnt, blocksum);
@@ -527,7 +605,7 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     GS_LAUNCH_CHECK("isect/emit");
     // 5. stable sort by (camera, tile) (K4); values land in the caller's isect_ids
     const int kbits = tile_bits(nbins) > 0 ? tile_bits(nbins) : 1;
-    KV sorted = radix_sort(ia, ib, ids, d_nsort, cap, kbits, hist, rowtot, L.nb_max, s);
+    KV sorted = radix_sort(ia, ib, ids, d_nsort, cap, kbits, sw, 4, s);
     GS_LAUNCH_CHECK("isect/tile-sort");
     // 6. tile ranges (K5)
     k_ranges_fill<<<div_up(nbins + 1, 256), 256, 0, s>>>(tile_offsets, nbins, d_nsort);
