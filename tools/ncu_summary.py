@@ -1,0 +1,93 @@
+"""Summarise ncu captures for profiles/ (run here, on the CPU box, on files gpurun
+brought back in gpurun_out/).
+
+  python tools/ncu_summary.py launches <launches.csv> > profiles/rN_launches.txt
+  python tools/ncu_summary.py full <report.ncu-rep> [--traffic profiles/traffic.json] > profiles/rN_full.txt
+"""
+import csv
+import json
+import re
+import subprocess
+import sys
+
+STAGE_OF = {"k_project_fwd": "project", "k_raster_fwd": "raster_fwd", "k_raster_bwd": "raster_bwd",
+            "k_project_bwd": "project_bwd"}
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "smsp__thread_inst_executed_per_inst_executed.ratio", "launch__registers_per_thread",
+        "launch__occupancy_limit_registers", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lts__t_sectors.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio"]
+
+
+def short(n):
+    m = re.search(r"(k_\w+)", n)
+    return m.group(1) if m else n[:40]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    ks = [(int(r[ii]), r[ki], float(r[vi].replace(",", ""))) for r in rows[hi + 1:]
+          if len(r) > vi and r[mi] == "gpu__time_duration.sum"]
+    starts = [j for j, k in enumerate(ks) if "k_project_fwd" in k[1]]
+    st = starts[-1]
+    end = next(j for j in range(st, len(ks)) if "k_project_bwd" in ks[j][1])
+    step = ks[st:end + 1]
+    tot = sum(v for _, _, v in step)
+    print("# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialised launches)")
+    print(f"# last full step: {len(step)} launches of libgsplat_b200, sum {tot / 1e3:.1f} us")
+    for i, n, v in step:
+        print(f"{i:5d}  {short(n):24s} {v / 1e3:9.1f} us  {100 * v / tot:5.1f} %")
+    agg = {}
+    for _, n, v in step:
+        agg[short(n)] = agg.get(short(n), 0) + v
+    print("# by kernel")
+    for k, v in sorted(agg.items(), key=lambda x: -x[1]):
+        print(f"   {k:24s} {v / 1e3:9.1f} us  {100 * v / tot:5.1f} %")
+
+
+def full(path, traffic_out=None):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, u = rows[0], rows[1]
+    traffic = {}
+    print(f"# ncu --set full --clock-control none summary of {path.split('/')[-1]}")
+    for r in rows[2:]:
+        name = short(r[h.index("Kernel Name")])
+        print(f"== {name}")
+        for k in KEYS:
+            if k in h and r[h.index(k)]:
+                print(f"   {k:78s} {r[h.index(k)]} {u[h.index(k)]}")
+        if name in STAGE_OF:
+            rd = float(r[h.index("dram__bytes_read.sum")].replace(",", ""))
+            wr = float(r[h.index("dram__bytes_write.sum")].replace(",", ""))
+            mult = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}
+            traffic[STAGE_OF[name]] = {"kernel": name, "dram_bytes_per_launch": rd * mult[u[h.index("dram__bytes_read.sum")]] +
+                                       wr * mult[u[h.index("dram__bytes_write.sum")]],
+                                       "source": path.split("/")[-1]}
+    if traffic_out:
+        old = {}
+        try:
+            old = json.load(open(traffic_out))
+        except Exception:
+            pass
+        old.update(traffic)
+        json.dump(old, open(traffic_out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2])
+    else:
+        tr = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
+        full(sys.argv[2], tr)
