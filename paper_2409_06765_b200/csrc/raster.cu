@@ -19,13 +19,17 @@
 // replay the forward's bit for bit.  The backward reduces each splat's gradient values
 // across the warp with a transposed (reduce-scatter) shuffle tree -- 9 shuffles for 8
 // values instead of 40 -- and lanes holding distinct values issue one fp32 reduction each.
+#include <type_traits>
+
 #include "gs_internal.cuh"
 
 namespace gsb {
 namespace {
 
-constexpr int kBatch = GS_BLOCK_PIXELS;   // 256 splats per staged batch
-constexpr int kWarps = kBatch / 32;
+constexpr int kThreads = GS_BLOCK_PIXELS; // one thread per pixel of the 16x16 tile
+constexpr int kWarps = kThreads / 32;
+constexpr int kBatchFwd = 512;            // splats per staged batch: forward (2 per thread) ...
+constexpr int kBatchBwd = 256;            // ... backward (1 per thread; keeps its registers at 48)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -129,16 +133,19 @@ __device__ __forceinline__ PixelCoord pixel_coord(const RasterParams& p, int til
     return c;
 }
 
+template <int kBatch>
 struct Stage {
     float4 xyo[kBatch];   // mean2d.x, mean2d.y, opac_eff, (unused)
     float4 con[kBatch];   // pre-scaled conic
     float4 rgb[kBatch];   // rgb, (unused)
     int32_t id[kBatch];
     uint8_t mask[kBatch];
-    uint8_t list[kWarps][kBatch];
+    // per-warp compacted slot lists (8-bit slots when they fit: fewer registers in K7)
+    typename std::conditional<(kBatch <= 256), uint8_t, uint16_t>::type list[kWarps][kBatch];
 };
 
-__device__ __forceinline__ void stage_splat(const RasterParams& p, Stage& s, int slot, int idx, float x0, float y0) {
+template <class StageT>
+__device__ __forceinline__ void stage_splat(const RasterParams& p, StageT& s, int slot, int idx, float x0, float y0) {
     const int32_t g = p.ids[idx];
     const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
     const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
@@ -151,13 +158,14 @@ __device__ __forceinline__ void stage_splat(const RasterParams& p, Stage& s, int
 
 // Order-preserving compaction of the batch slots [0, n) whose mask has this warp's bit
 // (and, in the backward, slot index <= max_slot).  Returns the list length.
-__device__ __forceinline__ int build_warp_list(Stage& s, int n, int warp, int lane, int max_slot) {
+template <class StageT>
+__device__ __forceinline__ int build_warp_list(StageT& s, int n, int warp, int lane, int max_slot) {
     int cnt = 0;
     for (int c = 0; c < n; c += 32) {
         const int j = c + lane;
         const bool keep = j < n && j <= max_slot && ((s.mask[j] >> warp) & 1u);
         const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (keep) s.list[warp][cnt + __popc(b & ((1u << lane) - 1u))] = (uint8_t)j;
+        if (keep) s.list[warp][cnt + __popc(b & ((1u << lane) - 1u))] = j;
         cnt += __popc(b);
     }
     __syncwarp();
@@ -165,8 +173,8 @@ __device__ __forceinline__ int build_warp_list(Stage& s, int n, int warp, int la
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(kBatch) k_raster_fwd(RasterParams p) {
-    __shared__ Stage s;
+__global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
+    __shared__ Stage<kBatchFwd> s;
     const int tile = blockIdx.x, cam = blockIdx.y;
     const PixelCoord q = pixel_coord(p, tile);
     const int bin = cam * p.TX * p.TY + tile;
@@ -176,13 +184,13 @@ __global__ void __launch_bounds__(kBatch) k_raster_fwd(RasterParams p) {
     int last = start - 1;
     bool done = !q.inside;
     int n_eval = 0, n_contrib = 0;
-    for (int b0 = start; b0 < end; b0 += kBatch) {
-        if (__syncthreads_count(done) == kBatch) break;
-        const int n = min(kBatch, end - b0);
-        if ((int)threadIdx.x < n) stage_splat(p, s, threadIdx.x, b0 + threadIdx.x, q.x0, q.y0);
+    for (int b0 = start; b0 < end; b0 += kBatchFwd) {
+        if (__syncthreads_count(done) == kThreads) break;
+        const int n = min(kBatchFwd, end - b0);
+        for (int t = threadIdx.x; t < n; t += kThreads) stage_splat(p, s, t, b0 + t, q.x0, q.y0);
         __syncthreads();
         if (__all_sync(0xffffffffu, done)) continue;
-        const int cnt = build_warp_list(s, n, q.warp, q.lane, kBatch);
+        const int cnt = build_warp_list(s, n, q.warp, q.lane, kBatchFwd);
         for (int k = 0; k < cnt; k++) {
             const int j = s.list[q.warp][k];
             if (!done) {
@@ -293,8 +301,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 template <bool ABSGRAD>
-__global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
-    __shared__ Stage s;
+__global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
+    __shared__ Stage<kBatchBwd> s;
     __shared__ int s_maxlast;
     const int tile = blockIdx.x, cam = blockIdx.y;
     const PixelCoord q = pixel_coord(p, tile);
@@ -324,10 +332,11 @@ __global__ void __launch_bounds__(kBatch) k_raster_bwd(RasterParams p) {
     const float kbg = Tfin * (vA - bgdot);
 
     float T = Tfin, S0 = 0.f, S1 = 0.f, S2 = 0.f;
-    for (int bend = max_last + 1; bend > start; bend -= kBatch) {
-        const int bstart = max(start, bend - kBatch);
+    for (int bend = max_last + 1; bend > start; bend -= kBatchBwd) {
+        const int bstart = max(start, bend - kBatchBwd);
         const int n = bend - bstart;
         __syncthreads();
+        static_assert(kBatchBwd == kThreads, "one staged splat per thread");
         if ((int)threadIdx.x < n) stage_splat(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0);
         __syncthreads();
         if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
@@ -404,7 +413,7 @@ gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H,
     RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
     p.out_rgb = out_rgb; p.out_alpha = out_alpha; p.out_T = out_T; p.last_ids = last_ids;
     dim3 grid(p.TX * p.TY, C);
-    k_raster_fwd<false><<<grid, kBatch, 0, s>>>(p);
+    k_raster_fwd<false><<<grid, kThreads, 0, s>>>(p);
     GS_LAUNCH_CHECK("k_raster_fwd");
     return GS_OK;
 }
@@ -415,7 +424,7 @@ gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int 
     RasterParams p = make_params(o, C, N, W, H, splats, nullptr, ids, offs);
     p.n_eval = n_eval; p.n_contrib = n_contrib;
     dim3 grid(p.TX * p.TY, C);
-    k_raster_fwd<true><<<grid, kBatch, 0, s>>>(p);
+    k_raster_fwd<true><<<grid, kThreads, 0, s>>>(p);
     GS_LAUNCH_CHECK("k_raster_fwd<stats>");
     return GS_OK;
 }
@@ -432,9 +441,9 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
     }
     dim3 grid(p.TX * p.TY, C);
     if (absgrad)
-        k_raster_bwd<true><<<grid, kBatch, 0, s>>>(p);
+        k_raster_bwd<true><<<grid, kThreads, 0, s>>>(p);
     else
-        k_raster_bwd<false><<<grid, kBatch, 0, s>>>(p);
+        k_raster_bwd<false><<<grid, kThreads, 0, s>>>(p);
     GS_LAUNCH_CHECK("k_raster_bwd");
     return GS_OK;
 }
