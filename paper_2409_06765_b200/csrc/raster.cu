@@ -39,6 +39,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// 16-byte shared-memory load from a 32-bit shared-window address (hoisted base: keeps the
+// shared-window base computation out of the inner loops).
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
 // Pre-scaled conic: p = a' dx^2 + c' dy^2 + b' dx dy = -sigma * log2(e)
 __device__ __forceinline__ float4 prescale_conic(float A, float B, float C) {
     return make_float4(__fmul_rn(-0.5f * kLog2e, A), __fmul_rn(-kLog2e, B), __fmul_rn(-0.5f * kLog2e, C), 0.f);
@@ -184,6 +192,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     int last = start - 1;
     bool done = !q.inside;
     int n_eval = 0, n_contrib = 0;
+    // keep the pixel centre in registers (stops ptxas re-deriving it in the inner loop)
+    float fpx = q.fpx, fpy = q.fpy;
+    asm volatile("" : "+f"(fpx), "+f"(fpy));
+    const float amax = p.alpha_max, amin = p.alpha_min, tmin = p.t_min;
     for (int b0 = start; b0 < end; b0 += kBatchFwd) {
         if (__syncthreads_count(done) == kThreads) break;
         const int n = min(kBatchFwd, end - b0);
@@ -191,30 +203,31 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         __syncthreads();
         if (__all_sync(0xffffffffu, done)) continue;
         const int cnt = build_warp_list(s, n, q.warp, q.lane, kBatchFwd);
+        if (done) continue;
+        const auto* list = s.list[q.warp];
+        const uint32_t a_xyo = (uint32_t)__cvta_generic_to_shared(s.xyo);
+        const uint32_t a_con = (uint32_t)__cvta_generic_to_shared(s.con);
+        const uint32_t a_rgb = (uint32_t)__cvta_generic_to_shared(s.rgb);
+        // each lane leaves the walk on its own at termination; the warp leaves when all have
         for (int k = 0; k < cnt; k++) {
-            const int j = s.list[q.warp][k];
-            if (!done) {
-                const float4 xyo = s.xyo[j];
-                float dx, dy, G, alpha;
-                if (STATS) n_eval++;
-                if (eval_alpha(xyo.x, xyo.y, xyo.z, s.con[j], q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, G,
-                               alpha)) {
-                    const float nT = __fmul_rn(T, __fsub_rn(1.f, alpha));
-                    if (nT <= p.t_min) {   // Q15: stop without compositing this splat
-                        done = true;
-                    } else {
-                        const float w = __fmul_rn(alpha, T);
-                        const float4 rgb = s.rgb[j];
-                        c0 = __fmaf_rn(rgb.x, w, c0);   // C += c alpha T
-                        c1 = __fmaf_rn(rgb.y, w, c1);
-                        c2 = __fmaf_rn(rgb.z, w, c2);
-                        T = nT;
-                        last = b0 + j;
-                        if (STATS) n_contrib++;
-                    }
-                }
+            const uint32_t j16 = (uint32_t)list[k] << 4;
+            const float4 xyo = lds4(a_xyo + j16);
+            float dx, dy, G, alpha;
+            if (STATS) n_eval++;
+            if (!eval_alpha(xyo.x, xyo.y, xyo.z, lds4(a_con + j16), fpx, fpy, amax, amin, dx, dy, G, alpha)) continue;
+            const float nT = __fmul_rn(T, __fsub_rn(1.f, alpha));
+            if (nT <= tmin) {   // Q15: stop without compositing this splat
+                done = true;
+                break;
             }
-            if (__all_sync(0xffffffffu, done)) break;
+            const float w = __fmul_rn(alpha, T);
+            const float4 rgb = lds4(a_rgb + j16);
+            c0 = __fmaf_rn(rgb.x, w, c0);   // C += c alpha T
+            c1 = __fmaf_rn(rgb.y, w, c1);
+            c2 = __fmaf_rn(rgb.z, w, c2);
+            T = nT;
+            last = b0 + (int)(j16 >> 4);
+            if (STATS) n_contrib++;
         }
     }
     const int64_t pix = ((int64_t)cam * p.H + q.py) * p.W + q.px;
