@@ -16,11 +16,12 @@
 // device memory, so the stage never synchronises the host; grids are sized for the
 // capacities and blocks past the live count exit at once.
 //
-// Radix pass (K4) = three kernels: per-block digit histogram (warp-aggregated shared
-// atomics), one block per digit scanning that digit's row across blocks (coalesced), and
-// a scatter that ranks the block's 4096 keys stably in shared memory (per-warp running
-// digit counters + match.any), reorders them by digit there, and writes each digit run
-// with consecutive threads (coalesced 32-byte sectors instead of 256 scattered streams).
+// Radix pass (K4) = three fully parallel kernels (no serial look-back chain, which at
+// these sizes -- 0.6 M and 2.9 M keys -- made a single-pass Onesweep latency-bound):
+// per-block digit histogram, one block per digit scanning that digit's row across blocks
+// (coalesced), and a scatter that ranks the block's 1024 keys stably in shared memory,
+// reorders them by digit there and writes each digit run with consecutive threads.
+// Warp-level multi-split uses 9 ballots per key instead of MATCH.ANY.
 //
 // Compiled with -fmad=false: the tile rectangle (Q20) is evaluated in fp32 with the
 // same op order as the oracle so keys match bit for bit.
@@ -31,10 +32,10 @@ namespace {
 
 constexpr int kT = 256;              // threads per block
 constexpr int kWarps = kT / 32;
-constexpr int kItems = 16;           // items per thread
-constexpr int kTile = kT * kItems;   // items per block (4096)
-constexpr int kSortItems = 4;                  // radix sort: items per thread ...
-constexpr int kSortTile = kT * kSortItems;     // ... and per block (1024: enough blocks to fill 148 SMs)
+constexpr int kItems = 16;           // compaction: items per thread
+constexpr int kTile = kT * kItems;   // compaction: items per block (4096)
+constexpr int kSortItems = 4;        // radix passes and per-item tile counts: items per thread ...
+constexpr int kSortTile = kT * kSortItems;   // ... and per block (1024: enough blocks to fill 148 SMs)
 constexpr int kScanThreads = 1024;
 constexpr int kEmit = 2048;          // output positions per emission block
 
@@ -80,14 +81,14 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* tot
     return res;
 }
 
-// Single-block in-place exclusive scan of nb = ceil(n / kTile) block sums (n = *d_n or
+// Single-block in-place exclusive scan of nb = ceil(n / tile) block sums (n = *d_n or
 // n_host, clamped to cap).  Coalesced rounds of 1024.  Writes totals / overflow.
-__global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, const int* d_n, int64_t n_host,
+__global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, int tile, const int* d_n, int64_t n_host,
                                                                int64_t cap, int* total_i32, int64_t* total_i64,
                                                                int32_t* overflow, int64_t ovf_cap, int* clamped_n) {
     __shared__ int s_warp[33];
     const int n = (int)min(d_n ? (int64_t)*d_n : n_host, cap);
-    const int nb = div_up(n, kTile);
+    const int nb = div_up(n, tile);
     int carry = 0;
     for (int r = 0; r < nb; r += kScanThreads) {
         const int i = r + threadIdx.x;
@@ -106,15 +107,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, cons
 }
 
 // ---------------------------------------------------------------------------------------
-// K2a / K2b: stable compaction of the visible (c,n) items.  Thread t owns kItems
-// consecutive items of its block's tile.
+// K2a / K2b: stable compaction of the visible (c,n) items.  Warp w of a block owns the
+// contiguous slice [base + 512 w, base + 512 (w+1)) and walks it in 16 coalesced rounds of
+// 32; its ballots give every visible item its rank inside the slice without block syncs.
 __global__ void __launch_bounds__(kT) k_vis_count(const int2* __restrict__ radii, int64_t n_items, int* blocksum) {
     __shared__ int s_warp[33];
-    const int64_t i0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    const int64_t base = (int64_t)blockIdx.x * kTile;
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < kItems; k++) {
-        const int64_t i = i0 + k;
+        const int64_t i = base + k * kT + threadIdx.x;
         if (i < n_items) {
             const int2 r = radii[i];
             cnt += (r.x > 0 && r.y > 0) ? 1 : 0;
@@ -128,52 +130,45 @@ __global__ void __launch_bounds__(kT) k_vis_count(const int2* __restrict__ radii
 __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ radii, const float* __restrict__ splats,
                                                    int64_t n_items, const int* __restrict__ blockoff,
                                                    uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
-    __shared__ int s_warp[33];
-    const int64_t i0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
-    unsigned vis = 0;
+    __shared__ int s_wtot[kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * kTile + warp * (kTile / kWarps);
+    unsigned ball[kItems];
+    int run = 0;
 #pragma unroll
     for (int k = 0; k < kItems; k++) {
-        const int64_t i = i0 + k;
+        const int64_t i = base + k * 32 + lane;
+        bool vis = false;
         if (i < n_items) {
             const int2 r = radii[i];
-            if (r.x > 0 && r.y > 0) vis |= 1u << k;
+            vis = r.x > 0 && r.y > 0;
         }
+        ball[k] = __ballot_sync(0xffffffffu, vis);
+        run += __popc(ball[k]);
     }
-    int tot;
-    int pos = blockoff[blockIdx.x] + block_exclusive_scan(__popc(vis), s_warp, &tot);
+    if (lane == 0) s_wtot[warp] = run;
+    __syncthreads();
+    int pos = blockoff[blockIdx.x];
+    for (int w = 0; w < warp; w++) pos += s_wtot[w];
+    const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int k = 0; k < kItems; k++) {
-        if (vis & (1u << k)) {
-            const int64_t i = i0 + k;
-            out_key[pos] = __float_as_uint(splats[i * GS_SPLAT_FLOATS + 3]);   // depth >= near > 0 (Q17)
-            out_val[pos] = (int32_t)i;
-            pos++;
+        if (ball[k] & (1u << lane)) {
+            const int64_t i = base + k * 32 + lane;
+            const int p = pos + __popc(ball[k] & lt);
+            out_key[p] = __float_as_uint(splats[i * GS_SPLAT_FLOATS + 3]);   // depth >= near > 0 (Q17)
+            out_val[p] = (int32_t)i;
         }
+        pos += __popc(ball[k]);
     }
 }
 
 // ---------------------------------------------------------------------------------------
-// K4: stable LSD radix sort, one kernel per 8-bit pass (Onesweep-style decoupled look-back).
-// k_global_hist computes, in one read of the keys, the digit histogram of EVERY pass (the
-// global digit totals do not depend on the order).  Each pass kernel then takes a ticket
-// (blocks are numbered in scheduling order, so waiting on lower tickets cannot deadlock),
-// ranks its 4096 keys stably in shared memory, publishes its per-digit count, looks back
-// over the predecessors' published counts/prefixes to get its global offset per digit,
-// reorders the tile by digit in shared memory and writes every digit run coalesced.
-constexpr uint32_t kFlagAgg = 1u << 30, kFlagPre = 2u << 30, kCountMask = (1u << 30) - 1u;
+// K4: one stable LSD radix pass (8-bit digit at `shift`), reduce-then-scan.
+// hist layout: hist[d * nb_max + b] = count of digit d in block b (digit-major rows).
 
-__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Lanes of the warp holding the same 8-bit digit d (d >= 256 marks an invalid lane, which
-// only matches invalid lanes): 9 ballots instead of MATCH.ANY, whose issue cost made the
-// radix kernels latency-bound.
+// Lanes of the warp holding the same 8-bit digit d (d = 256 marks an invalid lane, which
+// only matches invalid lanes): 9 ballots.
 __device__ __forceinline__ unsigned warp_peers(unsigned d) {
     unsigned peers = 0xffffffffu;
 #pragma unroll
@@ -185,58 +180,74 @@ __device__ __forceinline__ unsigned warp_peers(unsigned d) {
     return peers;
 }
 
-// g_hist[p * 256 + d] += number of keys whose digit p is d, for p in [0, passes).
-__global__ void __launch_bounds__(kT) k_global_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
-                                                    int passes, int* g_hist) {
-    __shared__ int s_hist[4][256];
+__global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
+                                                   int shift, int* hist, int nb_max) {
+    __shared__ int s_hist[256];
     const int n = (int)min((int64_t)*d_n, cap);
     const int nb = div_up(n, kSortTile);
     if ((int)blockIdx.x >= nb) return;
-#pragma unroll
-    for (int p = 0; p < 4; p++) s_hist[p][threadIdx.x] = 0;
+    s_hist[threadIdx.x] = 0;
     __syncthreads();
     const int base = blockIdx.x * kSortTile;
     const int lane = threadIdx.x & 31;
+    uint32_t key[kSortItems];
+#pragma unroll
     for (int k = 0; k < kSortItems; k++) {
         const int i = base + k * kT + threadIdx.x;
-        const bool valid = i < n;
-        const uint32_t key = valid ? keys[i] : 0u;
-        for (int p = 0; p < passes; p++) {
-            const unsigned d = valid ? (key >> (8 * p)) & 255u : 256u;
-            const unsigned peers = warp_peers(d);
-            if (d < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[p][d], __popc(peers));
-        }
+        key[k] = i < n ? keys[i] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kSortItems; k++) {
+        const int i = base + k * kT + threadIdx.x;
+        const unsigned d = i < n ? (key[k] >> shift) & 255u : 256u;
+        const unsigned peers = warp_peers(d);
+        if (d < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[d], __popc(peers));
     }
     __syncthreads();
-    for (int p = 0; p < passes; p++) {
-        const int c = s_hist[p][threadIdx.x];
-        if (c) atomicAdd(&g_hist[p * 256 + threadIdx.x], c);
-    }
+    hist[threadIdx.x * nb_max + blockIdx.x] = s_hist[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(kT) k_onesweep(const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
-                                                 uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out,
-                                                 const int* d_n, int64_t cap, int shift, const int* __restrict__ g_hist,
-                                                 uint32_t* status, int* ticket) {
+// One block per digit: exclusive scan of that digit's row over the live blocks; the
+// row total goes to rowtot[d].
+__global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, const int* d_n, int64_t cap,
+                                                        int* rowtot) {
+    __shared__ int s_warp[33];
+    const int n = (int)min((int64_t)*d_n, cap);
+    const int nb = div_up(n, kSortTile);
+    int* row = hist + (int64_t)blockIdx.x * nb_max;
+    int carry = 0;
+    for (int r = 0; r < nb; r += kT) {
+        const int i = r + threadIdx.x;
+        const int v = i < nb ? row[i] : 0;
+        int tot;
+        const int ex = block_exclusive_scan(v, s_warp, &tot);
+        if (i < nb) row[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict__ keys_in,
+                                                      const int32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+                                                      int32_t* __restrict__ vals_out, const int* d_n, int64_t cap,
+                                                      int shift, const int* __restrict__ hist, int nb_max,
+                                                      const int* __restrict__ rowtot) {
     __shared__ int s_cnt[kWarps][256];    // per-warp running digit counts, then per-warp offsets
     __shared__ int s_dstart[256];         // start of digit d inside this block's sorted tile
     __shared__ int s_goff[256];           // global start of digit d for this block
     __shared__ int s_warp[33];
-    __shared__ int s_bid;
     __shared__ uint32_t s_k[kSortTile];
     __shared__ int32_t s_v[kSortTile];
     const int n = (int)min((int64_t)*d_n, cap);
     const int nb = div_up(n, kSortTile);
-    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1);
+    if ((int)blockIdx.x >= nb) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll
     for (int w = 0; w < kWarps; w++) s_cnt[w][threadIdx.x] = 0;
     __syncthreads();
-    const int bid = s_bid;
-    if (bid >= nb) return;
-    // 1. per-warp stable ranks over the warp's contiguous slice of 512 items
-    const int base = bid * kSortTile + warp * (kSortTile / kWarps);
+    // 1. per-warp stable ranks over the warp's contiguous slice of 128 items
+    const int base = blockIdx.x * kSortTile + warp * (kSortTile / kWarps);
     uint32_t key[kSortItems];
     int32_t val[kSortItems];
     int rank[kSortItems];
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(kT) k_onesweep(const uint32_t* __restrict__ ke
         rank[k] = valid ? b + __popc(peers & lt_mask) : -1;
     }
     __syncthreads();
-    // 2. per digit: offsets across warps, block digit count, publish + look back
+    // 2. per digit: exclusive offsets across warps, block digit totals, digit starts
     {
         const int d = threadIdx.x;
         int run = 0;
@@ -270,39 +281,10 @@ __global__ void __launch_bounds__(kT) k_onesweep(const uint32_t* __restrict__ ke
             s_cnt[w][d] = run;
             run += c;
         }
-        uint32_t* my = status + (int64_t)bid * 256 + d;
-        int excl = 0;
-        if (bid == 0) {
-            st_relaxed(my, kFlagPre | (uint32_t)run);
-        } else {
-            st_relaxed(my, kFlagAgg | (uint32_t)run);
-            // windowed look-back: kWin predecessors per round trip
-            constexpr int kWin = 16;
-            int k = bid - 1;
-            bool found = false;
-            while (!found) {
-                uint32_t v[kWin];
-#pragma unroll
-                for (int i = 0; i < kWin; i++)
-                    v[i] = (k - i >= 0) ? ld_relaxed(status + (int64_t)(k - i) * 256 + d) : kFlagPre;
-                int i = 0;
-                for (; i < kWin; i++) {
-                    const uint32_t f = v[i] & ~kCountMask;
-                    if (f == 0u) break;   // not published yet: re-poll from here
-                    excl += (int)(v[i] & kCountMask);
-                    if (f == kFlagPre) {
-                        found = true;
-                        break;
-                    }
-                }
-                k -= i;
-            }
-            st_relaxed(my, kFlagPre | (uint32_t)(excl + run));
-        }
         int tot;
-        s_dstart[d] = block_exclusive_scan(run, s_warp, &tot);          // digits in ascending order
+        s_dstart[d] = block_exclusive_scan(run, s_warp, &tot);   // digits in ascending order
         int dummy;
-        s_goff[d] = block_exclusive_scan(g_hist[d], s_warp, &dummy) + excl;
+        s_goff[d] = block_exclusive_scan(rowtot[d], s_warp, &dummy) + hist[d * nb_max + blockIdx.x];
     }
     __syncthreads();
     // 3. reorder the tile by digit in shared memory
@@ -317,7 +299,7 @@ __global__ void __launch_bounds__(kT) k_onesweep(const uint32_t* __restrict__ ke
     }
     __syncthreads();
     // 4. coalesced write-out of the digit runs
-    const int nloc = min(kSortTile, n - bid * kSortTile);
+    const int nloc = min(kSortTile, n - blockIdx.x * kSortTile);
 #pragma unroll
     for (int k = 0; k < kSortItems; k++) {
         const int j = k * kT + threadIdx.x;
@@ -333,7 +315,7 @@ __global__ void __launch_bounds__(kT) k_onesweep(const uint32_t* __restrict__ ke
 
 // ---------------------------------------------------------------------------------------
 // K2c: tile rectangle and tile count of every depth-sorted visible item (stored for the
-// emission), plus per-block sums.
+// emission), plus per-block (kSortTile items) sums.
 struct TileGeom {
     int TX, TY, TT;
     int64_t N;
@@ -345,18 +327,31 @@ __global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ rad
                                                     int* blocksum) {
     __shared__ int s_warp[33];
     const int V = *d_V;
-    const int nb = div_up(V, kTile);
+    const int nb = div_up(V, kSortTile);
     if ((int)blockIdx.x >= nb) return;
-    const int base = blockIdx.x * kTile;
-    int cnt = 0;
-    for (int k = 0; k < kItems; k++) {
+    const int base = blockIdx.x * kSortTile;
+    int32_t id[kSortItems];
+#pragma unroll
+    for (int k = 0; k < kSortItems; k++) {
         const int j = base + k * kT + threadIdx.x;
-        if (j < V) {
-            const int32_t id = vis_val[j];
-            const int2 r = radii[id];
-            const float2 m = *reinterpret_cast<const float2*>(splats + (int64_t)id * GS_SPLAT_FLOATS);
-            const int4 rc = tile_rect(m.x, m.y, r.x, r.y, g.TX, g.TY);
+        id[k] = j < V ? vis_val[j] : -1;
+    }
+    int2 r[kSortItems];
+    float2 m[kSortItems];
+#pragma unroll
+    for (int k = 0; k < kSortItems; k++) {
+        if (id[k] >= 0) {
+            r[k] = radii[id[k]];
+            m[k] = *reinterpret_cast<const float2*>(splats + (int64_t)id[k] * GS_SPLAT_FLOATS);
+        }
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kSortItems; k++) {
+        if (id[k] >= 0) {
+            const int4 rc = tile_rect(m[k].x, m[k].y, r[k].x, r[k].y, g.TX, g.TY);
             const int c = (rc.y - rc.x) * (rc.w - rc.z);
+            const int j = base + k * kT + threadIdx.x;
             ent_rect[j] = rc;
             ent_cnt[j] = c;
             cnt += c;
@@ -367,58 +362,57 @@ __global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ rad
     if (threadIdx.x == 0) blocksum[blockIdx.x] = tot;
 }
 
-// K2d: exclusive offsets of the per-item counts (ent_off[V] = M), in item order.
+// K2d: exclusive offsets of the per-item counts (ent_off[V] = M), in item order, and the
+// first item of every emission block (the item owning position b * kEmit).
 __global__ void __launch_bounds__(kT) k_tiles_offsets(const int* __restrict__ ent_cnt, const int* d_V,
-                                                      const int* __restrict__ blockoff, int* __restrict__ ent_off) {
+                                                      const int* __restrict__ blockoff, int* __restrict__ ent_off,
+                                                      int* __restrict__ first_item, int n_emit_blocks) {
     __shared__ int s_warp[33];
     const int V = *d_V;
-    const int nb = div_up(V, kTile);
+    const int nb = div_up(V, kSortTile);
     if ((int)blockIdx.x >= nb) return;
-    const int j0 = blockIdx.x * kTile + threadIdx.x * kItems;
-    int c[kItems];
+    const int j0 = blockIdx.x * kSortTile + threadIdx.x * kSortItems;
+    int c[kSortItems];
     int sum = 0;
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
+    for (int k = 0; k < kSortItems; k++) {
         c[k] = (j0 + k < V) ? ent_cnt[j0 + k] : 0;
         sum += c[k];
     }
     int tot;
     int run = blockoff[blockIdx.x] + block_exclusive_scan(sum, s_warp, &tot);
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
-        if (j0 + k < V) ent_off[j0 + k] = run;
+    for (int k = 0; k < kSortItems; k++) {
+        const int j = j0 + k;
+        if (j < V) {
+            ent_off[j] = run;
+            // emission blocks whose first position falls in [run, run + c)
+            for (int b = div_up(run, kEmit); b * kEmit < run + c[k] && b < n_emit_blocks; b++) first_item[b] = j;
+        }
         run += c[k];
     }
-    if (j0 <= V - 1 && V - 1 < j0 + kItems) ent_off[V] = run;   // owner of the last item: run = M
+    if (j0 <= V - 1 && V - 1 < j0 + kSortItems) ent_off[V] = run;   // owner of the last item: run = M
 }
 
 // K3: load-balanced emission.  Block b writes output positions [b*kEmit, (b+1)*kEmit):
-// each position finds its item by binary search over the item offsets staged in shared
-// memory, so writes are perfectly coalesced whatever the per-splat tile counts.
+// the owning items [first_item[b], first_item[b+1]] are staged in shared memory and every
+// position finds its item by binary search there, so writes are fully coalesced whatever
+// the per-splat tile counts.
 __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_rect, const int* __restrict__ ent_off,
                                                    const int32_t* __restrict__ vis_val, const int* d_V,
-                                                   const int* d_nsort, TileGeom g, uint32_t* __restrict__ out_key,
-                                                   int32_t* __restrict__ out_val) {
+                                                   const int* d_nsort, const int* __restrict__ first_item, TileGeom g,
+                                                   uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
     __shared__ int s_off[kEmit + 1];
-    __shared__ int s_lo, s_hi;
     const int n = *d_nsort;
     const int V = *d_V;
     const int o0 = blockIdx.x * kEmit;
     if (o0 >= n) return;
     const int o1 = min(n, o0 + kEmit);
-    if (threadIdx.x < 2) {
-        // item owning position o (largest j with ent_off[j] <= o)
-        const int o = threadIdx.x == 0 ? o0 : o1 - 1;
-        int lo = 0, hi = V - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (ent_off[mid] <= o) lo = mid; else hi = mid - 1;
-        }
-        if (threadIdx.x == 0) s_lo = lo; else s_hi = lo;
-    }
-    __syncthreads();
+    const int nblocks = div_up(n, kEmit);
+    const int e0 = first_item[blockIdx.x];
+    const int e1 = (int)blockIdx.x + 1 < nblocks ? first_item[blockIdx.x + 1] : V - 1;
     // ne <= kEmit unless zero-count items (empty rectangles) interleave; then search globally
-    const int e0 = s_lo, ne = s_hi - s_lo + 1;
+    const int ne = e1 - e0 + 1;
     const bool staged = ne <= kEmit;
     if (staged)
         for (int k = threadIdx.x; k <= ne; k += kT) s_off[k] = ent_off[e0 + k];
@@ -469,28 +463,24 @@ __global__ void k_keys64(const uint32_t* __restrict__ keys32, const int32_t* __r
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-constexpr int kMaxPasses = 8;   // 4 (depth) + up to 4 ((camera, tile) key)
-
 struct WsLayout {
-    size_t off_scalars, off_blocksum, off_sweep, off_vk, off_vv, off_ak, off_av, off_rect, off_cnt, off_eoff, off_ka,
-        off_va, off_kb, off_vb, total, sweep_bytes;
-    int nb_max;        // blocks of kTile items (compaction, tile counts)
-    int nb_sort_max;   // blocks of kSortTile items (radix passes)
+    size_t off_scalars, off_blocksum, off_rowtot, off_hist, off_first, off_vk, off_vv, off_ak, off_av, off_rect,
+        off_cnt, off_eoff, off_ka, off_va, off_kb, off_vb, total;
+    int nb_sort_max;   // blocks of kSortTile items (radix passes, tile counts)
 };
 
 WsLayout ws_layout(int C, int64_t N, int64_t cap) {
     WsLayout L;
     const int64_t n_items = (int64_t)C * N;
     const int64_t big = n_items > cap ? n_items : cap;
-    L.nb_max = div_up(big > 0 ? big : 1, kTile);
     L.nb_sort_max = div_up(big > 0 ? big : 1, kSortTile);
+    const int64_t nb_emit = div_up(cap > 0 ? cap : 1, kEmit) + 1;
     size_t o = 0;
     L.off_scalars = o; o = align256(o + 64);
-    L.off_blocksum = o; o = align256(o + sizeof(int) * (size_t)(L.nb_max + 1));
-    // onesweep state, zeroed once per call: per pass a ticket, 256 digit totals and the
-    // [nb_max][256] look-back status words
-    L.sweep_bytes = (size_t)kMaxPasses * (sizeof(int) * (1 + 256) + sizeof(uint32_t) * 256 * (size_t)L.nb_sort_max);
-    L.off_sweep = o; o = align256(o + L.sweep_bytes);
+    L.off_blocksum = o; o = align256(o + sizeof(int) * (size_t)(L.nb_sort_max + 1));
+    L.off_rowtot = o; o = align256(o + sizeof(int) * 256);
+    L.off_hist = o; o = align256(o + sizeof(int) * 256 * (size_t)L.nb_sort_max);
+    L.off_first = o; o = align256(o + sizeof(int) * (size_t)nb_emit);
     L.off_vk = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_vv = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_ak = o; o = align256(o + 4 * (size_t)(n_items + 1));
@@ -511,36 +501,18 @@ struct KV {
     int32_t* v;
 };
 
-struct Sweep {
-    int* tickets;      // [kMaxPasses]
-    int* g_hist;       // [kMaxPasses][256]
-    uint32_t* status;  // [kMaxPasses][nb_max][256]
-    int nb_max;
-};
-
-Sweep sweep_state(char* base, int nb_max) {
-    Sweep w;
-    w.tickets = reinterpret_cast<int*>(base);
-    w.g_hist = w.tickets + kMaxPasses;
-    w.status = reinterpret_cast<uint32_t*>(w.g_hist + kMaxPasses * 256);
-    w.nb_max = nb_max;
-    return w;
-}
-
 // ceil(bits/8) stable 8-bit LSD passes over `a` (live count *d_n <= cap), ping-ponging with
-// `b`, using sweep slots [pass0, pass0 + passes).  The last pass writes its values to
-// `final_vals` when given.  Returns the buffers holding the sorted result.
-KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, const Sweep& w, int pass0,
-              cudaStream_t s) {
+// `b`.  The last pass writes its values to `final_vals` when given.  Returns the buffers
+// holding the sorted result.
+KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
+              int nb_max, cudaStream_t s) {
     const int passes = bits <= 0 ? 0 : div_up(bits, 8);
-    if (passes == 0) return a;
-    k_global_hist<<<w.nb_max, kT, 0, s>>>(a.k, d_n, cap, passes, w.g_hist + pass0 * 256);
     KV in = a, out = b;
     for (int p = 0; p < passes; p++) {
         int32_t* vdst = (p == passes - 1 && final_vals) ? final_vals : out.v;
-        const int slot = pass0 + p;
-        k_onesweep<<<w.nb_max, kT, 0, s>>>(in.k, in.v, out.k, vdst, d_n, cap, 8 * p, w.g_hist + slot * 256 + 0 * 0,
-                                           w.status + (size_t)slot * 256 * w.nb_max, w.tickets + slot);
+        k_radix_hist<<<nb_max, kT, 0, s>>>(in.k, d_n, cap, 8 * p, hist, nb_max);
+        k_radix_scan_rows<<<256, kT, 0, s>>>(hist, nb_max, d_n, cap, rowtot);
+        k_radix_scatter<<<nb_max, kT, 0, s>>>(in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max, rowtot);
         KV next_in{out.k, vdst};
         out = in;
         in = next_in;
@@ -566,7 +538,9 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     int* d_V = scal + 0;
     int* d_nsort = scal + 1;
     int* blocksum = reinterpret_cast<int*>(w + L.off_blocksum);
-    const Sweep sw = sweep_state(w + L.off_sweep, L.nb_sort_max);
+    int* rowtot = reinterpret_cast<int*>(w + L.off_rowtot);
+    int* hist = reinterpret_cast<int*>(w + L.off_hist);
+    int* first_item = reinterpret_cast<int*>(w + L.off_first);
     KV vis{reinterpret_cast<uint32_t*>(w + L.off_vk), reinterpret_cast<int32_t*>(w + L.off_vv)};
     KV alt{reinterpret_cast<uint32_t*>(w + L.off_ak), reinterpret_cast<int32_t*>(w + L.off_av)};
     int4* ent_rect = reinterpret_cast<int4*>(w + L.off_rect);
@@ -583,29 +557,29 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     const int2* r2 = reinterpret_cast<const int2*>(radii);
     const int nb_items = div_up(n_items > 0 ? n_items : 1, kTile);
 
-    if (cudaMemsetAsync(w + L.off_sweep, 0, L.sweep_bytes, s) != cudaSuccess) {
-        GS_LAUNCH_CHECK("isect/memset");
-        return GS_ERR_CUDA;
-    }
     // 1. stable compaction of the visible (c,n) items (K2a, K2b)
     k_vis_count<<<nb_items, kT, 0, s>>>(r2, n_items, blocksum);
-    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, nullptr, n_items, INT64_MAX, d_V, nullptr, nullptr, 0,
-                                                 nullptr);
+    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, kTile, nullptr, n_items, INT64_MAX, d_V, nullptr, nullptr,
+                                                 0, nullptr);
     k_vis_compact<<<nb_items, kT, 0, s>>>(r2, splats, n_items, blocksum, vis.k, vis.v);
     GS_LAUNCH_CHECK("isect/compact");
     // 2. stable sort by fp32 depth bits (K4, 4 passes)
-    KV dsorted = radix_sort(vis, alt, nullptr, d_V, n_items, 32, sw, 0, s);
+    KV dsorted = radix_sort(vis, alt, nullptr, d_V, n_items, 32, hist, rowtot, L.nb_sort_max, s);
     GS_LAUNCH_CHECK("isect/depth-sort");
     // 3. tile rectangles, counts, offsets, M, overflow, clamped count (K2c, K2d)
-    k_tiles_count<<<nb_items, kT, 0, s>>>(r2, splats, dsorted.v, d_V, g, ent_rect, ent_cnt, blocksum);
-    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, d_V, 0, INT64_MAX, nullptr, M, overflow, cap, d_nsort);
-    k_tiles_offsets<<<nb_items, kT, 0, s>>>(ent_cnt, d_V, blocksum, ent_off);
+    const int nb_v = div_up(n_items > 0 ? n_items : 1, kSortTile);
+    k_tiles_count<<<nb_v, kT, 0, s>>>(r2, splats, dsorted.v, d_V, g, ent_rect, ent_cnt, blocksum);
+    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, kSortTile, d_V, 0, INT64_MAX, nullptr, M, overflow, cap,
+                                                 d_nsort);
+    k_tiles_offsets<<<nb_v, kT, 0, s>>>(ent_cnt, d_V, blocksum, ent_off, first_item, div_up(cap, kEmit));
     // 4. load-balanced emission in depth order (K3)
-    if (cap > 0) k_tiles_emit<<<div_up(cap, kEmit), kT, 0, s>>>(ent_rect, ent_off, dsorted.v, d_V, d_nsort, g, ia.k, ia.v);
+    if (cap > 0)
+        k_tiles_emit<<<div_up(cap, kEmit), kT, 0, s>>>(ent_rect, ent_off, dsorted.v, d_V, d_nsort, first_item, g,
+                                                       ia.k, ia.v);
     GS_LAUNCH_CHECK("isect/emit");
     // 5. stable sort by (camera, tile) (K4); values land in the caller's isect_ids
     const int kbits = tile_bits(nbins) > 0 ? tile_bits(nbins) : 1;
-    KV sorted = radix_sort(ia, ib, ids, d_nsort, cap, kbits, sw, 4, s);
+    KV sorted = radix_sort(ia, ib, ids, d_nsort, cap, kbits, hist, rowtot, L.nb_sort_max, s);
     GS_LAUNCH_CHECK("isect/tile-sort");
     // 6. tile ranges (K5)
     k_ranges_fill<<<div_up(nbins + 1, 256), 256, 0, s>>>(tile_offsets, nbins, d_nsort);

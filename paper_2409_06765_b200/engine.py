@@ -82,13 +82,13 @@ class Engine:
         return True
 
     def launches_per_step(self) -> int:
-        """Kernels of the library launched by one step() (the memsets are not kernels):
-        project 1; isect 3 (compaction) + 1+4 (depth sort) + 4 (tile counts, scan, offsets,
-        emission) + 1+P (tile sort, P = ceil(bits/8)) + 2 (ranges); raster fwd 1, bwd 1;
-        project bwd 1."""
+        """Kernels of the library launched by one step() (the memset is not a kernel):
+        project 1; isect 3 (compaction) + 3x4 (depth sort) + 3 (tile counts, scan,
+        offsets) + 1 (emission) + 3P (tile sort, P = ceil(bits/8)) + 2 (ranges);
+        raster fwd 1, bwd 1; project bwd 1."""
         bits = max(1, (self.C * self.TX * self.TY - 1).bit_length())
         P = (bits + 7) // 8
-        return 1 + (3 + 5 + 4 + 1 + P + 2) + 1 + 1 + 1
+        return 1 + (3 + 12 + 3 + 1 + 3 * P + 2) + 1 + 1 + 1
 
     @property
     def n_isect(self) -> int:
