@@ -67,6 +67,22 @@ __device__ __forceinline__ bool eval_alpha(float mx, float my, float o, float4 c
     return alpha >= alpha_min;
 }
 
+// Same decision, also returning the products dx^2, dy^2, dx dy it formed (reused by B6).
+__device__ __forceinline__ bool eval_alpha_q(float mx, float my, float o, float4 con, float fpx, float fpy,
+                                             float alpha_max, float alpha_min, float& dx, float& dy, float& xx,
+                                             float& yy, float& xy, float& G, float& alpha) {
+    dx = __fsub_rn(mx, fpx);
+    dy = __fsub_rn(my, fpy);
+    xx = __fmul_rn(dx, dx);
+    yy = __fmul_rn(dy, dy);
+    xy = __fmul_rn(dx, dy);
+    const float p = __fmaf_rn(con.y, xy, __fmaf_rn(con.x, xx, __fmul_rn(con.z, yy)));
+    if (p > 0.f) return false;
+    G = ex2_approx(p);
+    alpha = fminf(alpha_max, __fmul_rn(o, G));
+    return alpha >= alpha_min;
+}
+
 // 8-bit mask of the warps (8x4 pixel blocks, warp w at column w&1, row w>>1 of the tile)
 // whose pixel centres intersect the box |dx| <= hx, |dy| <= hy of the ellipse
 // sigma <= tau = ln(o / alpha_min): hx = sqrt(2 tau a), hy = sqrt(2 tau c) with
@@ -344,7 +360,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     // constant part of d C_total / d alpha_k: -T_final ra (bg . v_C) + T_final ra v_A (B4)
     const float kbg = Tfin * (vA - bgdot);
 
-    float T = Tfin, S0 = 0.f, S1 = 0.f, S2 = 0.f;
+    // S only ever enters B4 contracted with this pixel's v_C, so the three channel
+    // recurrences are carried as the single scalar Sv = S . v_C (same recurrence, dotted)
+    float T = Tfin, Sv = 0.f;
     for (int bend = max_last + 1; bend > start; bend -= kBatchBwd) {
         const int bstart = max(start, bend - kBatchBwd);
         const int n = bend - bstart;
@@ -359,9 +377,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             bool valid = q.inside && bstart + j <= last;
             const float4 xyo = s.xyo[j];
             const float4 con = s.con[j];
-            float dx = 0.f, dy = 0.f, G = 0.f, alpha = 0.f;
+            float dx = 0.f, dy = 0.f, xx = 0.f, yy = 0.f, xy = 0.f, G = 0.f, alpha = 0.f;
             if (valid)
-                valid = eval_alpha(xyo.x, xyo.y, xyo.z, con, q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, G, alpha);
+                valid = eval_alpha_q(xyo.x, xyo.y, xyo.z, con, q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, xx, yy,
+                                     xy, G, alpha);
             if (!__any_sync(0xffffffffu, valid)) continue;
             float g8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // mx, my, o, A, B, C, r, g
             float g_bl = 0.f;
@@ -373,19 +392,19 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 g8[6] = fac * v0;                  // B3
                 g8[7] = fac * v1;
                 g_bl = fac * v2;
-                // B4 + background / alpha-output terms (Q25, Q26)
-                const float v_alpha = (rgb.x * T - S0 * ra) * v0 + (rgb.y * T - S1 * ra) * v1 +
-                                      (rgb.z * T - S2 * ra) * v2 + kbg * ra;
-                S0 += rgb.x * fac;                 // B5
-                S1 += rgb.y * fac;
-                S2 += rgb.z * fac;
+                // B4 + background / alpha-output terms (Q25, Q26):
+                // v_alpha = sum_ch (c T - S ra) v_C + kbg ra = T (c . v_C) + ra (kbg - Sv)
+                const float cv = rgb.x * v0 + rgb.y * v1 + rgb.z * v2;
+                const float v_alpha = T * cv + ra * (kbg - Sv);
+                Sv += cv * fac;                    // B5, dotted with v_C
                 const float raw = xyo.z * G;
                 if (raw < p.alpha_max) {           // B6 (Q24)
                     g8[2] = G * v_alpha;
                     const float v_sigma = -raw * v_alpha;
-                    g8[3] = 0.5f * v_sigma * dx * dx;
-                    g8[4] = v_sigma * dx * dy;
-                    g8[5] = 0.5f * v_sigma * dy * dy;
+                    const float hv = 0.5f * v_sigma;
+                    g8[3] = hv * xx;
+                    g8[4] = v_sigma * xy;
+                    g8[5] = hv * yy;
                     // d sigma / d mu' = Sigma'^-1 Delta, with the conic recovered from
                     // the pre-scaled one: A = a' (-2 ln2), B = b' (-ln2), C = c' (-2 ln2)
                     const float k2 = -kLn2 * v_sigma;
