@@ -37,6 +37,15 @@ struct PBParams {
     float* v_colors;
 };
 
+// R(q / |q|)
+__device__ __forceinline__ void quat_rot(float4 q4, float (&R)[3][3]) {
+    const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+    const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
+    R[0][0] = 1.f - 2.f * (qy * qy + qz * qz); R[0][1] = 2.f * (qx * qy - qw * qz); R[0][2] = 2.f * (qx * qz + qw * qy);
+    R[1][0] = 2.f * (qx * qy + qw * qz); R[1][1] = 1.f - 2.f * (qx * qx + qz * qz); R[1][2] = 2.f * (qy * qz - qw * qx);
+    R[2][0] = 2.f * (qx * qz - qw * qy); R[2][1] = 2.f * (qy * qz + qw * qx); R[2][2] = 1.f - 2.f * (qx * qx + qy * qy);
+}
+
 template <int DEG>
 __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
     const int64_t n = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -47,28 +56,28 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
     const float4 q4 = reinterpret_cast<const float4*>(p.quats)[n];
     const float s[3] = {p.scales[3 * n], p.scales[3 * n + 1], p.scales[3 * n + 2]};
     const float op = p.opac[n];
-    const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
-    const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
-    float R[3][3];
-    R[0][0] = 1.f - 2.f * (qy * qy + qz * qz); R[0][1] = 2.f * (qx * qy - qw * qz); R[0][2] = 2.f * (qx * qz + qw * qy);
-    R[1][0] = 2.f * (qx * qy + qw * qz); R[1][1] = 1.f - 2.f * (qx * qx + qz * qz); R[1][2] = 2.f * (qy * qz - qw * qx);
-    R[2][0] = 2.f * (qx * qz - qw * qy); R[2][1] = 2.f * (qy * qz + qw * qx); R[2][2] = 1.f - 2.f * (qx * qx + qy * qy);
-    float M[3][3], Sig[3][3];
+    // Sigma = M M^T with M = R(q_hat) S (only Sigma stays live through the camera loop; R and M
+    // are recomputed after it -- fewer registers, more warps in flight for this HBM-bound kernel)
+    float Sig[3][3];
+    {
+        float R[3][3], M[3][3];
+        quat_rot(q4, R);
 #pragma unroll
-    for (int i = 0; i < 3; i++)
+        for (int i = 0; i < 3; i++)
 #pragma unroll
-        for (int j = 0; j < 3; j++) M[i][j] = R[i][j] * s[j];
+            for (int j = 0; j < 3; j++) M[i][j] = R[i][j] * s[j];
 #pragma unroll
-    for (int i = 0; i < 3; i++)
+        for (int i = 0; i < 3; i++)
 #pragma unroll
-        for (int j = 0; j < 3; j++) Sig[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
+            for (int j = 0; j < 3; j++) Sig[i][j] = M[i][0] * M[j][0] + M[i][1] * M[j][1] + M[i][2] * M[j][2];
+    }
 
     float g_mu[3] = {0.f, 0.f, 0.f}, g_S[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
     float g_op = 0.f;
     // SH gradient accumulators live in shared memory (one column per thread, conflict-free)
     // and the coefficients are streamed from L1/L2, keeping registers and occupancy for this
     // HBM-bound kernel
-    __shared__ float s_gc[DEG < 0 ? 1 : NB * 3][kThreads];
+    __shared__ float s_gc[DEG < 0 ? 1 : NB * 3][kThreads + 1];   // +1: conflict-free transposed reads
     float g_rgb[3] = {0.f, 0.f, 0.f};
     if (DEG >= 0) {
 #pragma unroll
@@ -267,6 +276,14 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
     }
 
     // ---- P8: v_M = (vS + vS^T) M; v_s_j = (R^T v_M)_jj; v_R = v_M S
+    const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+    const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
+    float R[3][3], M[3][3];
+    quat_rot(q4, R);
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) M[i][j] = R[i][j] * s[j];
     float vM[3][3];
 #pragma unroll
     for (int i = 0; i < 3; i++)
@@ -309,17 +326,30 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
 #pragma unroll
         for (int i = 0; i < 3; i++) p.v_colors[3 * n + i] = g_rgb[i];
     } else {
-        float* dst = p.v_colors + n * (int64_t)p.K * 3;
-        if (vec) {
+        const int lane = threadIdx.x & 31, wslot = threadIdx.x & ~31;
+        const int64_t wbase = n - lane;
+        constexpr int F = NB * 3;   // floats per Gaussian
+        if (vec && p.K == NB && wbase + 32 <= p.N) {
+            // the warp's 32 consecutive rows are one contiguous block: transpose through shared
+            // memory and write it with coalesced 16-byte stores
+            __syncwarp();
+            float4* dstw = reinterpret_cast<float4*>(p.v_colors + wbase * F);
+#pragma unroll 4
+            for (int c = lane; c < 32 * F / 4; c += 32) {
+                float v[4];
 #pragma unroll
-            for (int i = 0; i < NB * 3 / 4; i++)
-                reinterpret_cast<float4*>(dst)[i] = make_float4(s_gc[4 * i][threadIdx.x], s_gc[4 * i + 1][threadIdx.x],
-                                                                s_gc[4 * i + 2][threadIdx.x], s_gc[4 * i + 3][threadIdx.x]);
+                for (int e = 0; e < 4; e++) {
+                    const int f = 4 * c + e;
+                    v[e] = s_gc[f % F][wslot + f / F];
+                }
+                dstw[c] = make_float4(v[0], v[1], v[2], v[3]);
+            }
         } else {
+            float* dst = p.v_colors + n * (int64_t)p.K * 3;
 #pragma unroll
             for (int i = 0; i < NB * 3; i++) dst[i] = s_gc[i][threadIdx.x];
+            for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
         }
-        for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
     }
 }
 
