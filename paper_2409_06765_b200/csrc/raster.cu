@@ -323,6 +323,13 @@ __device__ __forceinline__ float warp_sum(float v) {
 __device__ __forceinline__ int slot8(int i) { return i + i / 3; }
 __device__ __forceinline__ int slot4(int i) { return i == 0 ? 10 : (i == 1 ? 7 : 11); }
 
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
+constexpr int kFewLanes = 16;  // <= this many contributing lanes: per-lane vector reductions (measured optimum)
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -381,7 +388,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             if (valid)
                 valid = eval_alpha_q(xyo.x, xyo.y, xyo.z, con, q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, xx, yy,
                                      xy, G, alpha);
-            if (!__any_sync(0xffffffffu, valid)) continue;
+            const unsigned vb = __ballot_sync(0xffffffffu, valid);
+            if (!vb) continue;
             float g8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // mx, my, o, A, B, C, r, g
             float g_bl = 0.f;
             if (valid) {
@@ -413,6 +421,16 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 }
             }
             float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
+            if (__popc(vb) <= kFewLanes) {
+                // few contributing lanes: each issues its own three 16-byte reductions -- 3 warp
+                // instructions instead of the ~45 of the shuffle tree
+                if (valid) {
+                    red_add_v4(dst, g8[0], g8[1], g8[2], 0.f);
+                    red_add_v4(dst + 4, g8[3], g8[4], g8[5], ABSGRAD ? fabsf(g8[0]) : 0.f);
+                    red_add_v4(dst + 8, g8[6], g8[7], g_bl, ABSGRAD ? fabsf(g8[1]) : 0.f);
+                }
+                continue;
+            }
             const float r8 = reduce_scatter8(g8, lane);
             if ((lane & 3) == 0) atomicAdd(dst + slot8(lane >> 2), r8);
             if (ABSGRAD) {
