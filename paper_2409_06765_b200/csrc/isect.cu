@@ -207,8 +207,11 @@ __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ 
     hist[threadIdx.x * nb_max + blockIdx.x] = s_hist[threadIdx.x];
 }
 
-// One block per digit: exclusive scan of that digit's row over the live blocks; the
-// row total goes to rowtot[d].
+// One block per digit: exclusive scan of that digit's row over the live blocks (each thread
+// owns up to kRowItems consecutive entries: one block-wide scan per row); the row total
+// goes to rowtot[d].
+constexpr int kRowItems = 16;   // rows up to 4096 blocks (4 M keys) in one pass, more in rounds
+
 __global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, const int* d_n, int64_t cap,
                                                         int* rowtot) {
     __shared__ int s_warp[33];
@@ -216,12 +219,22 @@ __global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, c
     const int nb = div_up(n, kSortTile);
     int* row = hist + (int64_t)blockIdx.x * nb_max;
     int carry = 0;
-    for (int r = 0; r < nb; r += kT) {
-        const int i = r + threadIdx.x;
-        const int v = i < nb ? row[i] : 0;
+    for (int r = 0; r < nb; r += kT * kRowItems) {
+        const int i0 = r + threadIdx.x * kRowItems;
+        int v[kRowItems];
+        int sum = 0;
+#pragma unroll
+        for (int k = 0; k < kRowItems; k++) {
+            v[k] = i0 + k < nb ? row[i0 + k] : 0;
+            sum += v[k];
+        }
         int tot;
-        const int ex = block_exclusive_scan(v, s_warp, &tot);
-        if (i < nb) row[i] = carry + ex;
+        int run = carry + block_exclusive_scan(sum, s_warp, &tot);
+#pragma unroll
+        for (int k = 0; k < kRowItems; k++) {
+            if (i0 + k < nb) row[i0 + k] = run;
+            run += v[k];
+        }
         carry += tot;
     }
     if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
