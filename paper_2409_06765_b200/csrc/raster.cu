@@ -114,6 +114,31 @@ __device__ __forceinline__ uint32_t support_mask(float mx, float my, float o, fl
     return m;
 }
 
+// 16-bit mask of the 4x4 pixel blocks of the tile (bit 4 r + c for the block at column c,
+// row r) whose pixel centres intersect the same conservative support box as support_mask.
+__device__ __forceinline__ uint32_t support_mask16(float mx, float my, float o, float A, float a, float c, float x0,
+                                                   float y0, float alpha_min) {
+    if (o < alpha_min * 0.9999f) return 0u;
+    float tau = fmaxf(0.f, __logf(o / alpha_min));
+    tau = tau * 1.004f + 4e-3f;
+    const float grow = 1.f + 1e-6f * a * A;
+    const float hx = sqrtf(2.f * tau * a) * grow + 1e-2f;
+    const float hy = sqrtf(2.f * tau * c) * grow + 1e-2f;
+    if (!(hx < 1e30f) || !(hy < 1e30f)) return 0xffffu;
+    uint32_t cm = 0, rm = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const float lo = (float)(k * 4) + 0.5f, hi = lo + 3.f;
+        if (mx - x0 + hx >= lo && mx - x0 - hx <= hi) cm |= 1u << k;
+        if (my - y0 + hy >= lo && my - y0 - hy <= hi) rm |= 1u << k;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+        if (rm & (1u << r)) m |= cm << (4 * r);
+    return m;
+}
+
 struct RasterParams {
     int C, W, H, TX, TY;
     int64_t N;
@@ -196,35 +221,74 @@ __device__ __forceinline__ int build_warp_list(StageT& s, int n, int warp, int l
     return cnt;
 }
 
+// Forward staging: per splat a 16-bit half-warp mask; per half-warp an ordered slot list.
+struct StageFwd {
+    float4 xyo[kBatchFwd];
+    float4 con[kBatchFwd];
+    float4 rgb[kBatchFwd];
+    uint16_t mask[kBatchFwd];
+    uint16_t list[2 * kWarps][kBatchFwd];
+};
+
 template <bool STATS>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
-    __shared__ Stage<kBatchFwd> s;
+    __shared__ StageFwd s;
     const int tile = blockIdx.x, cam = blockIdx.y;
-    const PixelCoord q = pixel_coord(p, tile);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp w: 8x4 block at (8 (w&1), 4 (w>>1)); half h = lane>>4: its left/right 4x4 block
+    const int half = lane >> 4, l4 = lane & 15;
+    const int hw = 2 * warp + half;   // = 4 * row + column of the 4x4 block
+    const int tx = tile % p.TX, ty = tile / p.TX;
+    const int px = tx * GS_TILE + (hw & 3) * 4 + (l4 & 3);
+    const int py = ty * GS_TILE + (hw >> 2) * 4 + (l4 >> 2);
+    const bool inside = px < p.W && py < p.H;
+    const float x0 = (float)(tx * GS_TILE), y0 = (float)(ty * GS_TILE);
     const int bin = cam * p.TX * p.TY + tile;
     const int start = p.offs[bin], end = p.offs[bin + 1];
 
     float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
     int last = start - 1;
-    bool done = !q.inside;
+    bool done = !inside;
     int n_eval = 0, n_contrib = 0;
-    // keep the pixel centre in registers (stops ptxas re-deriving it in the inner loop)
-    float fpx = q.fpx, fpy = q.fpy;
+    float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;   // pixel centre
     asm volatile("" : "+f"(fpx), "+f"(fpy));
     const float amax = p.alpha_max, amin = p.alpha_min, tmin = p.t_min;
+    const unsigned lt = (1u << lane) - 1u;
     for (int b0 = start; b0 < end; b0 += kBatchFwd) {
         if (__syncthreads_count(done) == kThreads) break;
         const int n = min(kBatchFwd, end - b0);
-        for (int t = threadIdx.x; t < n; t += kThreads) stage_splat(p, s, t, b0 + t, q.x0, q.y0);
+        for (int t = threadIdx.x; t < n; t += kThreads) {
+            const int32_t g = p.ids[b0 + t];
+            const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
+            const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
+            s.xyo[t] = r0;
+            s.con[t] = prescale_conic(r1.x, r1.y, r1.z);
+            s.rgb[t] = r2;
+            s.mask[t] = (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.w, r2.w, x0, y0, amin);
+        }
         __syncthreads();
         if (__all_sync(0xffffffffu, done)) continue;
-        const int cnt = build_warp_list(s, n, q.warp, q.lane, kBatchFwd);
+        // both half-warp lists of this warp, order preserving
+        int cnt0 = 0, cnt1 = 0;
+        for (int c = 0; c < n; c += 32) {
+            const int j = c + lane;
+            const uint32_t m = j < n ? s.mask[j] : 0u;
+            const bool k0 = (m >> (2 * warp)) & 1u, k1 = (m >> (2 * warp + 1)) & 1u;
+            const unsigned bb0 = __ballot_sync(0xffffffffu, k0), bb1 = __ballot_sync(0xffffffffu, k1);
+            if (k0) s.list[2 * warp][cnt0 + __popc(bb0 & lt)] = (uint16_t)j;
+            if (k1) s.list[2 * warp + 1][cnt1 + __popc(bb1 & lt)] = (uint16_t)j;
+            cnt0 += __popc(bb0);
+            cnt1 += __popc(bb1);
+        }
+        __syncwarp();
         if (done) continue;
-        const auto* list = s.list[q.warp];
+        const int cnt = half ? cnt1 : cnt0;
+        const uint16_t* list = s.list[hw];
         const uint32_t a_xyo = (uint32_t)__cvta_generic_to_shared(s.xyo);
         const uint32_t a_con = (uint32_t)__cvta_generic_to_shared(s.con);
         const uint32_t a_rgb = (uint32_t)__cvta_generic_to_shared(s.rgb);
-        // each lane leaves the walk on its own at termination; the warp leaves when all have
+        // the two halves of the warp walk their own lists in lockstep; each lane leaves on its
+        // own at termination or at the end of its half's list
         for (int k = 0; k < cnt; k++) {
             const uint32_t j16 = (uint32_t)list[k] << 4;
             const float4 xyo = lds4(a_xyo + j16);
@@ -246,24 +310,24 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             if (STATS) n_contrib++;
         }
     }
-    const int64_t pix = ((int64_t)cam * p.H + q.py) * p.W + q.px;
+    const int64_t pix = ((int64_t)cam * p.H + py) * p.W + px;
     if (STATS) {
-        if (q.inside) {
+        if (inside) {
             p.n_eval[pix] = n_eval;
             p.n_contrib[pix] = n_contrib;
         }
         return;
     }
-    if (q.inside) {
-        float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+    if (inside) {
+        float g0 = 0.f, g1 = 0.f, g2 = 0.f;
         if (p.bg) {
-            b0 = p.bg[3 * cam];
-            b1 = p.bg[3 * cam + 1];
-            b2 = p.bg[3 * cam + 2];
+            g0 = p.bg[3 * cam];
+            g1 = p.bg[3 * cam + 1];
+            g2 = p.bg[3 * cam + 2];
         }
-        p.out_rgb[3 * pix + 0] = c0 + T * b0;   // R3, Q25
-        p.out_rgb[3 * pix + 1] = c1 + T * b1;
-        p.out_rgb[3 * pix + 2] = c2 + T * b2;
+        p.out_rgb[3 * pix + 0] = c0 + T * g0;   // R3, Q25
+        p.out_rgb[3 * pix + 1] = c1 + T * g1;
+        p.out_rgb[3 * pix + 2] = c2 + T * g2;
         p.out_alpha[pix] = 1.f - T;
         p.out_T[pix] = T;
         p.last_ids[pix] = last;
