@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _mtime(o) < max(_mtime(s), hdr_t, _mtime(__file__)):
-            cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *COMMON, *extra, *os.environ.get("GS_NVCC_EXTRA", "").split(), "-c", s, "-o", o]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
                 print(" ".join(cmd), flush=True)

@@ -83,59 +83,76 @@ __device__ __forceinline__ bool eval_alpha_q(float mx, float my, float o, float4
     return alpha >= alpha_min;
 }
 
-// 8-bit mask of the warps (8x4 pixel blocks, warp w at column w&1, row w>>1 of the tile)
-// whose pixel centres intersect the box |dx| <= hx, |dy| <= hy of the ellipse
-// sigma <= tau = ln(o / alpha_min): hx = sqrt(2 tau a), hy = sqrt(2 tau c) with
-// a, c the blurred variances.  Conservative margins: tau is inflated by 0.4% + 4e-3
-// (lg2.approx error, fp32 rounding of the exponent, ex2.approx error are all < 1e-5
-// relative) and the box by cond*1e-6 (cond = a*A = a c / det, which bounds the relative
-// error of the fp32 conic the kernel evaluates) plus 1e-2 px.
-__device__ __forceinline__ uint32_t support_mask(float mx, float my, float o, float A, float a, float c, float x0,
-                                                 float y0, float alpha_min) {
+// Conservative support of a splat inside its tile.  The set a pixel can take the splat
+// from is the ellipse E: sigma(d) = 1/2 (A dx^2 + C dy^2) + B dx dy <= tau, tau =
+// ln(o / alpha_min) (alpha = min(alpha_max, o G) < alpha_min outside it, Q14), with
+// (A, B, C) the fp32 conic of the record and a, c its blurred variances.  Margins make the
+// test conservative with respect to the kernel's fp32 arithmetic: tau is inflated by 0.4 %
+// + 4e-3 (lg2.approx, ex2.approx and the rounding of the exponent are all < 1e-5
+// relative), every extent by eps = 1e-6 cond (cond = a A = a c / det bounds the relative
+// error of the fp32 conic and of the fp32 determinant below) plus 1e-2 px.
+//
+// Per row r of 4-pixel-high blocks (pixel centres y0 + 4r + 0.5 ... + 3.5) the x-extent of
+// E over that slab is [L_r, R_r]: with the exact x-bounds of E at height dy
+//   x_+-(dy) = (-B dy +- sqrt(2 A tau - det dy^2)) / A,     det = A C - B^2,
+// x_+ is concave and peaks at the rightmost point dy_R = -B hx / C (hx = sqrt(2 tau a)),
+// x_- is convex with its minimum at -dy_R, so R_r = x_+(clamp(dy_R, slab)) and
+// L_r = x_-(clamp(-dy_R, slab)).  The result is a 4-bit mask of 4-pixel-wide columns per
+// row: bit 4 r + k of the returned 16-bit mask is the 4x4 block at column k, row r.
+// Ill-conditioned conics (eps >= 1e-2) fall back to the axis-aligned box of E.
+__device__ __forceinline__ uint32_t support_mask16(float mx, float my, float o, float A, float B, float Cc, float a,
+                                                   float c, float x0, float y0, float alpha_min) {
     if (o < alpha_min * 0.9999f) return 0u;   // alpha = min(alpha_max, o G) <= o (G <= 1)
     float tau = fmaxf(0.f, __logf(o / alpha_min));
     tau = tau * 1.004f + 4e-3f;
-    const float grow = 1.f + 1e-6f * a * A;
-    const float hx = sqrtf(2.f * tau * a) * grow + 1e-2f;
-    const float hy = sqrtf(2.f * tau * c) * grow + 1e-2f;
-    if (!(hx < 1e30f) || !(hy < 1e30f)) return 0xffu;
+    const float eps = 1e-6f * a * A;
+    const float grow = 1.f + eps;
+    const float hx0 = sqrtf(2.f * tau * a), hy0 = sqrtf(2.f * tau * c);
+    const float hx = hx0 * grow + 1e-2f;
+    const float hy = hy0 * grow + 1e-2f;
+    if (!(hx < 1e30f) || !(hy < 1e30f)) return 0xffffu;
+    const float u = mx - x0, v = my - y0;
+    const bool ell = eps < 1e-2f;
+    const float mfrac = 2.f * sqrtf(eps) + eps;
+    const float mxm = hx0 * mfrac + 1e-2f, mym = hy0 * mfrac + 1e-2f;
+    const float det = A * Cc - B * B;
+    const float s2 = 2.f * A * tau;
+    const float iA = 1.f / A;
+    const float dyR = -B * hx0 / Cc;
     uint32_t m = 0;
 #pragma unroll
-    for (int wy = 0; wy < 4; wy++) {
-        const float ylo = y0 + (float)(wy * 4) + 0.5f, yhi = ylo + 3.f;
-        if (my + hy >= ylo && my - hy <= yhi) {
+    for (int r = 0; r < 4; r++) {
+        const float lo = (float)(r * 4) + 0.5f - v, hi = lo + 3.f;   // slab in dy = y - my
+        if (!(hi >= -hy && lo <= hy)) continue;
+        float L = -hx, R = hx;
+        if (ell) {
+            const float ylo = lo - mym, yhi = hi + mym;
+            const float d1 = fminf(fmaxf(dyR, ylo), yhi);
+            const float d2 = fminf(fmaxf(-dyR, ylo), yhi);
+            const float R1 = (-B * d1 + sqrtf(fmaxf(0.f, s2 - det * d1 * d1))) * iA + mxm;
+            const float L1 = (-B * d2 - sqrtf(fmaxf(0.f, s2 - det * d2 * d2))) * iA - mxm;
+            R = fminf(R, R1);
+            L = fmaxf(L, L1);
+        }
 #pragma unroll
-            for (int wx = 0; wx < 2; wx++) {
-                const float xlo = x0 + (float)(wx * 8) + 0.5f, xhi = xlo + 7.f;
-                if (mx + hx >= xlo && mx - hx <= xhi) m |= 1u << (wy * 2 + wx);
-            }
+        for (int k = 0; k < 4; k++) {
+            const float xlo = (float)(k * 4) + 0.5f, xhi = xlo + 3.f;
+            if (u + R >= xlo && u + L <= xhi) m |= 1u << (4 * r + k);
         }
     }
     return m;
 }
 
-// 16-bit mask of the 4x4 pixel blocks of the tile (bit 4 r + c for the block at column c,
-// row r) whose pixel centres intersect the same conservative support box as support_mask.
-__device__ __forceinline__ uint32_t support_mask16(float mx, float my, float o, float A, float a, float c, float x0,
-                                                   float y0, float alpha_min) {
-    if (o < alpha_min * 0.9999f) return 0u;
-    float tau = fmaxf(0.f, __logf(o / alpha_min));
-    tau = tau * 1.004f + 4e-3f;
-    const float grow = 1.f + 1e-6f * a * A;
-    const float hx = sqrtf(2.f * tau * a) * grow + 1e-2f;
-    const float hy = sqrtf(2.f * tau * c) * grow + 1e-2f;
-    if (!(hx < 1e30f) || !(hy < 1e30f)) return 0xffffu;
-    uint32_t cm = 0, rm = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const float lo = (float)(k * 4) + 0.5f, hi = lo + 3.f;
-        if (mx - x0 + hx >= lo && mx - x0 - hx <= hi) cm |= 1u << k;
-        if (my - y0 + hy >= lo && my - y0 - hy <= hi) rm |= 1u << k;
-    }
+// 8-bit mask of the 8x4 warp blocks (bit 2 r + w for the block at column w, row r): the
+// union of the two 4x4 blocks it covers.
+__device__ __forceinline__ uint32_t support_mask8(uint32_t m16) {
     uint32_t m = 0;
 #pragma unroll
-    for (int r = 0; r < 4; r++)
-        if (rm & (1u << r)) m |= cm << (4 * r);
+    for (int r = 0; r < 4; r++) {
+        const uint32_t row = (m16 >> (4 * r)) & 0xfu;
+        m |= ((row & 3u) ? 1u : 0u) << (2 * r);
+        m |= ((row & 12u) ? 1u : 0u) << (2 * r + 1);
+    }
     return m;
 }
 
@@ -202,7 +219,7 @@ __device__ __forceinline__ void stage_splat(const RasterParams& p, StageT& s, in
     s.con[slot] = prescale_conic(r1.x, r1.y, r1.z);
     s.rgb[slot] = r2;
     s.id[slot] = g;
-    s.mask[slot] = (uint8_t)support_mask(r0.x, r0.y, r0.z, r1.x, r1.w, r2.w, x0, y0, p.alpha_min);
+    s.mask[slot] = (uint8_t)support_mask8(support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, p.alpha_min));
 }
 
 // Order-preserving compaction of the batch slots [0, n) whose mask has this warp's bit
@@ -264,7 +281,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             s.xyo[t] = r0;
             s.con[t] = prescale_conic(r1.x, r1.y, r1.z);
             s.rgb[t] = r2;
-            s.mask[t] = (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.w, r2.w, x0, y0, amin);
+            s.mask[t] = (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, amin);
         }
         __syncthreads();
         if (__all_sync(0xffffffffu, done)) continue;
