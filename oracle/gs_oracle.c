@@ -841,7 +841,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     }
                     /* ... and through alpha (this splat's qd, all splats' via T and S) */
                     for (int j = 0; j < 9; j++) {
-                        if (j >= 5 && j <= 7) tm->vs[j] = 0;
+                        if (j >= 5) tm->vs[j] = 0;   /* rgb and opacity: only the alpha path */
                         tm->vs[j] += tm->va[j] * (e->qd + r.eT);
                     }
                 }
