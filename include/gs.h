@@ -75,7 +75,9 @@ typedef struct gs_options {
     int32_t sh_degree;  /* -1: colors are RGB [N,3]; 0..3: colors are SH [N,K,3]   */
     int32_t bbox_mode;  /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3 sqrt(lambda_max)     */
     int32_t fov_clamp;  /* 1 clamp t_x/t_z, t_y/t_z to the widened frustum for J only (Q27)*/
-    int32_t reserved;   /* must be 0                                                      */
+    int32_t packed;     /* 0 dense [C,N] records | 1 packed [nnz] records (Q29; the *_packed
+                           entry points require 1, the dense ones 0; gs_rasterize_* read
+                           N as the total record count when 1)                            */
 } gs_options;
 
 /* ---- Projected splat record ------------------------------------------------------
@@ -98,7 +100,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -162,7 +164,7 @@ GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N,
  * recurrence; per-(c,n) sums over pixels are accumulated with fp32 atomics.
  * In : as gs_rasterize_fwd plus out_T, last_ids, v_out_rgb [C,H,W,3],
  *      v_out_alpha [C,H,W] or NULL.
- * Out: v_splats [C,N,GS_SPLAT_FLOATS] (zero-filled here, then accumulated; slot layout
+ * Out: v_splats [C,N,GS_SPLAT_FLOATS] ([N,...] when opt->packed; zero-filled here, then accumulated; slot layout
  *      above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 7, 11. */
 GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
@@ -181,6 +183,58 @@ GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int
                          const float* viewmats, const float* Ks, const int32_t* radii,
                          const float* v_splats, float* v_means, float* v_quats, float* v_scales,
                          float* v_opacities, float* v_colors, void* stream);
+
+/* ==== Packed mode (Q29; BASELINE configs[4]) ==========================================
+ * Only the visible (c,n) pairs are stored: item i of a packed call is the pair
+ * (camera_ids[i], gaussian_ids[i]), items ordered camera-major then by Gaussian index,
+ * i.e. the order of the visible entries of the dense [C,N] layout.  Every per-item array
+ * (radii [nnz,2], splats / v_splats [nnz, GS_SPLAT_FLOATS]) is the dense one with the
+ * culled rows removed, so stage 3 / 4a are the SAME calls (gs_rasterize_fwd/bwd with
+ * opt->packed = 1 and N = the packed capacity) and their images are bit-identical to the
+ * dense path's.  Tile keys are identical; isect_ids hold packed indices instead of c*N+n.
+ * The live count nnz stays on the device: the caller sizes nnz_capacity once (e.g. from
+ * one read of *nnz, or C*N) and checks *overflow lazily, as for M in stage 2.
+ * All three calls require opt->packed == 1. */
+
+/* Projection into the packed layout.  Two passes over the Gaussians (visibility count per
+ * (camera, block of 256 Gaussians); scan; full projection writing each visible record at
+ * its packed position).  Out: *nnz (device int64), *overflow (device int32: 1 iff *nnz >
+ * nnz_capacity; rows past the capacity are dropped), camera_ids / gaussian_ids [cap]
+ * int32, radii [cap,2] int32, splats [cap, GS_SPLAT_FLOATS].  Rows >= *nnz are undefined.
+ * workspace >= gs_project_packed_workspace_size(N, C) bytes, 256-byte aligned. */
+GS_API size_t gs_project_packed_workspace_size(int64_t N, int32_t C);
+GS_API gs_status gs_project_packed(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
+                                   const float* means, const float* quats, const float* scales,
+                                   const float* opacities, const float* colors, int32_t K,
+                                   const float* viewmats, const float* Ks, int64_t nnz_capacity, int64_t* nnz,
+                                   int32_t* overflow, int32_t* camera_ids, int32_t* gaussian_ids, int32_t* radii,
+                                   float* splats, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Stage 2 over packed items (nnz read on the device, clamped to nnz_capacity).  Outputs as
+ * gs_isect_tiles; isect_ids are packed indices.  workspace >=
+ * gs_isect_packed_workspace_size(C, nnz_capacity, width, height, M_capacity). */
+GS_API size_t gs_isect_packed_workspace_size(int32_t C, int64_t nnz_capacity, int32_t width, int32_t height,
+                                             int64_t M_capacity);
+GS_API gs_status gs_isect_tiles_packed(const gs_options* opt, int32_t C, int64_t nnz_capacity, const int64_t* nnz,
+                                       int32_t width, int32_t height, const int32_t* camera_ids,
+                                       const int32_t* radii, const float* splats, int64_t M_capacity, int64_t* M,
+                                       int32_t* overflow, int32_t* isect_ids, uint64_t* isect_keys,
+                                       int32_t* tile_offsets, void* workspace, size_t workspace_bytes,
+                                       void* stream);
+
+/* Stage 4b from packed per-item gradients v_splats [cap, GS_SPLAT_FLOATS].  Builds the
+ * (c,n) -> item map in the workspace (C*N int32), then runs the dense kernel through it:
+ * same per-Gaussian camera sum, same outputs as gs_project_bwd.  workspace >=
+ * gs_project_bwd_packed_workspace_size(N, C). */
+GS_API size_t gs_project_bwd_packed_workspace_size(int64_t N, int32_t C);
+GS_API gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
+                                       const float* means, const float* quats, const float* scales,
+                                       const float* opacities, const float* colors, int32_t K,
+                                       const float* viewmats, const float* Ks, int64_t nnz_capacity,
+                                       const int64_t* nnz, const int32_t* camera_ids, const int32_t* gaussian_ids,
+                                       const int32_t* radii, const float* v_splats, float* v_means, float* v_quats,
+                                       float* v_scales, float* v_opacities, float* v_colors, void* workspace,
+                                       size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

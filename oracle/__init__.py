@@ -218,6 +218,19 @@ def project_bwd(scene, proj, v2d, opts: Options):
     return out
 
 
+def pack(proj):
+    """Packed mode (BASELINE configs[4]): the visible (c,n) pairs of the
+    dense [C,N] layout in camera-major, then Gaussian order -- the definition written out
+    (row-major nonzero of the visibility mask).  Returns (camera_ids, gaussian_ids) and the
+    dense->packed index map (-1 where culled)."""
+    r = proj["radii"]
+    vis = (r[..., 0] > 0) & (r[..., 1] > 0)
+    cam, gid = np.nonzero(vis)              # C order: camera-major, then n
+    index = np.full(vis.shape, -1, np.int64)
+    index[cam, gid] = np.arange(cam.size)
+    return cam.astype(np.int32), gid.astype(np.int32), index
+
+
 def forward_backward(scene, opts: Options, v_img, v_alpha=None, backgrounds=None, tile_mask=None,
                      with_isect=True):
     """The whole path: project -> isect -> render fwd -> render bwd -> project bwd."""

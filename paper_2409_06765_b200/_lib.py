@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 
@@ -25,7 +25,7 @@ class GsOptions(ct.Structure):
         ("near_plane", ct.c_float), ("far_plane", ct.c_float), ("eps2d", ct.c_float),
         ("alpha_max", ct.c_float), ("alpha_min", ct.c_float), ("t_min", ct.c_float),
         ("tile_size", ct.c_int32), ("antialiased", ct.c_int32), ("sh_degree", ct.c_int32),
-        ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("reserved", ct.c_int32),
+        ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("packed", ct.c_int32),
     ]
 
 
@@ -50,6 +50,15 @@ SIGNATURES = {
     "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
     "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                               _P, _P, _P]),
+    "gs_project_packed_workspace_size": (_SZ, [_I64, _I32]),
+    "gs_project_packed": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P,
+                                 _P, _P, _P, _SZ, _P]),
+    "gs_isect_packed_workspace_size": (_SZ, [_I32, _I64, _I32, _I32, _I64]),
+    "gs_isect_tiles_packed": (_I32, [_P, _I32, _I64, _P, _I32, _I32, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _SZ,
+                                     _P]),
+    "gs_project_bwd_packed_workspace_size": (_SZ, [_I64, _I32]),
+    "gs_project_bwd_packed": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P,
+                                     _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 
 
@@ -78,13 +87,15 @@ def check(status: int, what: str) -> None:
 
 
 def options(sh_degree=3, antialiased=False, near_plane=0.01, far_plane=1e10, eps2d=0.3, alpha_max=0.99,
-            alpha_min=1.0 / 255.0, t_min=1e-4, tile_size=16, bbox_mode=0, fov_clamp=True) -> GsOptions:
+            alpha_min=1.0 / 255.0, t_min=1e-4, tile_size=16, bbox_mode=0, fov_clamp=True,
+            packed=False) -> GsOptions:
     o = GsOptions()
     lib().gs_default_options(ct.byref(o))
     o.near_plane, o.far_plane, o.eps2d = near_plane, far_plane, eps2d
     o.alpha_max, o.alpha_min, o.t_min = alpha_max, alpha_min, t_min
     o.tile_size, o.antialiased, o.sh_degree = tile_size, int(bool(antialiased)), int(sh_degree)
     o.bbox_mode, o.fov_clamp = int(bbox_mode), int(bool(fov_clamp))
+    o.packed = int(bool(packed))
     return o
 
 
@@ -178,3 +189,62 @@ def gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, 
                                ptr(v_scales, name="v_scales"), ptr(v_opacities, name="v_opacities"),
                                ptr(v_colors, name="v_colors"), stream_ptr(stream)),
           "gs_project_bwd")
+
+
+# ---- packed mode (Q29) ------------------------------------------------------------------
+def gs_project_packed_workspace_size(N, C):
+    return int(lib().gs_project_packed_workspace_size(N, C))
+
+
+def gs_project_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, width, height, cap, nnz,
+                      overflow, camera_ids, gaussian_ids, radii, splats, workspace, stream=None):
+    N, C = means.shape[0], viewmats.shape[0]
+    check(lib().gs_project_packed(ct.byref(o), N, C, width, height, ptr(means, name="means"),
+                                  ptr(quats, name="quats"), ptr(scales, name="scales"),
+                                  ptr(opacities, name="opacities"), ptr(colors, name="colors"), K,
+                                  ptr(viewmats, name="viewmats"), ptr(Ks, name="Ks"), cap,
+                                  ptr(nnz, torch.int64, "nnz"), ptr(overflow, torch.int32, "overflow"),
+                                  ptr(camera_ids, torch.int32, "camera_ids"),
+                                  ptr(gaussian_ids, torch.int32, "gaussian_ids"), ptr(radii, torch.int32, "radii"),
+                                  ptr(splats, name="splats"), ptr(workspace, torch.uint8, "ws"), workspace.numel(),
+                                  stream_ptr(stream)),
+          "gs_project_packed")
+
+
+def gs_isect_packed_workspace_size(C, cap_nnz, width, height, cap):
+    return int(lib().gs_isect_packed_workspace_size(C, cap_nnz, width, height, cap))
+
+
+def gs_isect_tiles_packed(o, C, cap_nnz, nnz, width, height, camera_ids, radii, splats, cap, M, overflow, isect_ids,
+                          isect_keys, tile_offsets, workspace, stream=None):
+    check(lib().gs_isect_tiles_packed(ct.byref(o), C, cap_nnz, ptr(nnz, torch.int64, "nnz"), width, height,
+                                      ptr(camera_ids, torch.int32, "camera_ids"), ptr(radii, torch.int32, "radii"),
+                                      ptr(splats, name="splats"), cap, ptr(M, torch.int64, "M"),
+                                      ptr(overflow, torch.int32, "overflow"),
+                                      ptr(isect_ids, torch.int32, "isect_ids"),
+                                      ptr(isect_keys, torch.int64, "isect_keys"),
+                                      ptr(tile_offsets, torch.int32, "tile_offsets"),
+                                      ptr(workspace, torch.uint8, "ws"), workspace.numel(), stream_ptr(stream)),
+          "gs_isect_tiles_packed")
+
+
+def gs_project_bwd_packed_workspace_size(N, C):
+    return int(lib().gs_project_bwd_packed_workspace_size(N, C))
+
+
+def gs_project_bwd_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, width, height, cap_nnz, nnz,
+                          camera_ids, gaussian_ids, radii, v_splats, v_means, v_quats, v_scales, v_opacities,
+                          v_colors, workspace, stream=None):
+    N, C = means.shape[0], viewmats.shape[0]
+    check(lib().gs_project_bwd_packed(ct.byref(o), N, C, width, height, ptr(means, name="means"),
+                                      ptr(quats, name="quats"), ptr(scales, name="scales"),
+                                      ptr(opacities, name="opacities"), ptr(colors, name="colors"), K,
+                                      ptr(viewmats, name="viewmats"), ptr(Ks, name="Ks"), cap_nnz,
+                                      ptr(nnz, torch.int64, "nnz"), ptr(camera_ids, torch.int32, "camera_ids"),
+                                      ptr(gaussian_ids, torch.int32, "gaussian_ids"),
+                                      ptr(radii, torch.int32, "radii"), ptr(v_splats, name="v_splats"),
+                                      ptr(v_means, name="v_means"), ptr(v_quats, name="v_quats"),
+                                      ptr(v_scales, name="v_scales"), ptr(v_opacities, name="v_opacities"),
+                                      ptr(v_colors, name="v_colors"), ptr(workspace, torch.uint8, "ws"),
+                                      workspace.numel(), stream_ptr(stream)),
+          "gs_project_bwd_packed")

@@ -26,7 +26,7 @@ gs_status check_opts(const gs_options* o) {
     if (!(o->eps2d >= 0.f) || !(o->alpha_max > 0.f) || !(o->alpha_max < 1.f) || !(o->alpha_min >= 0.f) ||
         !(o->t_min >= 0.f) || !(o->near_plane > 0.f))
         return GS_ERR_INVALID_ARGUMENT;
-    if (o->bbox_mode < 0 || o->bbox_mode > 1 || o->reserved != 0) return GS_ERR_INVALID_ARGUMENT;
+    if (o->bbox_mode < 0 || o->bbox_mode > 1 || o->packed < 0 || o->packed > 1) return GS_ERR_INVALID_ARGUMENT;
     return GS_OK;
 }
 
@@ -65,7 +65,7 @@ void gs_default_options(gs_options* o) {
     o->sh_degree = 3;
     o->bbox_mode = 0;
     o->fov_clamp = 1;
-    o->reserved = 0;
+    o->packed = 0;
 }
 
 const char* gs_status_string(int32_t s) {
@@ -86,6 +86,7 @@ gs_status gs_project(const gs_options* opt, int64_t N, int32_t C, int32_t width,
                      const float* quats, const float* scales, const float* opacities, const float* colors, int32_t K,
                      const float* viewmats, const float* Ks, int32_t* radii, float* splats, void* stream) {
     GS_TRY(check_opts(opt));
+    GS_REQ(opt->packed == 0);
     GS_TRY(check_dims(N, C, width, height));
     if (N == 0) return GS_OK;
     GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && splats);
@@ -99,7 +100,7 @@ gs_status gs_project(const gs_options* opt, int64_t N, int32_t C, int32_t width,
 
 size_t gs_isect_workspace_size(int32_t C, int64_t N, int32_t width, int32_t height, int64_t M_capacity) {
     if (C < 1 || N < 0 || width < 1 || height < 1 || M_capacity < 0) return 0;
-    return gsb::isect_workspace_bytes(C, N, width, height, M_capacity);
+    return gsb::isect_workspace_bytes((int64_t)C * N, M_capacity);
 }
 
 gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
@@ -107,6 +108,7 @@ gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int32_t wi
                          int32_t* isect_ids, uint64_t* isect_keys, int32_t* tile_offsets, void* workspace,
                          size_t workspace_bytes, void* stream) {
     GS_TRY(check_opts(opt));
+    GS_REQ(opt->packed == 0);
     GS_TRY(check_dims(N, C, width, height));
     GS_REQ(M_capacity >= 0 && M_capacity < ((int64_t)1 << 31) - 1);
     GS_REQ(M && overflow && tile_offsets && workspace);
@@ -115,9 +117,10 @@ gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int32_t wi
     GS_REQ(aligned8(M) && aligned4(overflow) && aligned4(tile_offsets) && aligned4(isect_ids) &&
            aligned8(isect_keys) && (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
     GS_REQ(N == 0 || (aligned8(radii) && aligned16(splats)));
-    GS_REQ(workspace_bytes >= gsb::isect_workspace_bytes(C, N, width, height, M_capacity));
-    return gsb::launch_isect(*opt, C, N, width, height, radii, splats, M_capacity, M, overflow, isect_ids, isect_keys,
-                             tile_offsets, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+    GS_REQ(workspace_bytes >= gsb::isect_workspace_bytes((int64_t)C * N, M_capacity));
+    return gsb::launch_isect(*opt, C, N, width, height, radii, splats, (int64_t)C * N, nullptr, nullptr, M_capacity, M,
+                             overflow, isect_ids, isect_keys, tile_offsets, workspace, workspace_bytes,
+                             static_cast<cudaStream_t>(stream));
 }
 
 gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
@@ -165,6 +168,7 @@ gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t wi
                          const float* v_splats, float* v_means, float* v_quats, float* v_scales, float* v_opacities,
                          float* v_colors, void* stream) {
     GS_TRY(check_opts(opt));
+    GS_REQ(opt->packed == 0);
     GS_TRY(check_dims(N, C, width, height));
     if (N == 0) return GS_OK;
     GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && v_splats && v_means &&
@@ -175,6 +179,97 @@ gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t wi
     return gsb::launch_project_bwd(*opt, N, C, width, height, means, quats, scales, opacities, colors,
                                    opt->sh_degree >= 0 ? K : 1, viewmats, Ks, radii, v_splats, v_means, v_quats,
                                    v_scales, v_opacities, v_colors, static_cast<cudaStream_t>(stream));
+}
+
+// ---- packed mode (Q29) ----------------------------------------------------------------
+
+size_t gs_project_packed_workspace_size(int64_t N, int32_t C) {
+    if (N < 0 || C < 1) return 0;
+    return gsb::project_packed_workspace_bytes(N, C);
+}
+
+gs_status gs_project_packed(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
+                            const float* means, const float* quats, const float* scales, const float* opacities,
+                            const float* colors, int32_t K, const float* viewmats, const float* Ks,
+                            int64_t nnz_capacity, int64_t* nnz, int32_t* overflow, int32_t* camera_ids,
+                            int32_t* gaussian_ids, int32_t* radii, float* splats, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_REQ(opt->packed == 1);
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(nnz_capacity >= 0 && nnz_capacity < ((int64_t)1 << 31) - 1);
+    GS_REQ(nnz && overflow && workspace && aligned8(nnz) && aligned4(overflow));
+    GS_REQ((reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
+    GS_REQ(workspace_bytes >= gsb::project_packed_workspace_bytes(N, C));
+    GS_REQ(N == 0 || (means && quats && scales && opacities && colors && viewmats && Ks));
+    GS_REQ(nnz_capacity == 0 || (camera_ids && gaussian_ids && radii && splats));
+    GS_REQ(aligned16(quats) && aligned16(splats) && aligned8(radii) && aligned4(camera_ids) &&
+           aligned4(gaussian_ids) && aligned4(means) && aligned4(scales) && aligned4(opacities) &&
+           aligned4(colors) && aligned4(viewmats) && aligned4(Ks));
+    if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
+    return gsb::launch_project_packed(*opt, N, C, width, height, means, quats, scales, opacities, colors,
+                                      opt->sh_degree >= 0 ? K : 1, viewmats, Ks, nnz_capacity, nnz, overflow,
+                                      camera_ids, gaussian_ids, radii, splats, workspace,
+                                      static_cast<cudaStream_t>(stream));
+}
+
+size_t gs_isect_packed_workspace_size(int32_t C, int64_t nnz_capacity, int32_t width, int32_t height,
+                                      int64_t M_capacity) {
+    if (C < 1 || nnz_capacity < 0 || width < 1 || height < 1 || M_capacity < 0) return 0;
+    return gsb::isect_workspace_bytes(nnz_capacity, M_capacity);
+}
+
+gs_status gs_isect_tiles_packed(const gs_options* opt, int32_t C, int64_t nnz_capacity, const int64_t* nnz,
+                                int32_t width, int32_t height, const int32_t* camera_ids, const int32_t* radii,
+                                const float* splats, int64_t M_capacity, int64_t* M, int32_t* overflow,
+                                int32_t* isect_ids, uint64_t* isect_keys, int32_t* tile_offsets, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_REQ(opt->packed == 1);
+    GS_TRY(check_dims(nnz_capacity, 1, width, height));
+    GS_TRY(check_dims(0, C, width, height));
+    GS_REQ(M_capacity >= 0 && M_capacity < ((int64_t)1 << 31) - 1);
+    GS_REQ(nnz && M && overflow && tile_offsets && workspace);
+    GS_REQ(nnz_capacity == 0 || (camera_ids && radii && splats));
+    GS_REQ(M_capacity == 0 || isect_ids);
+    GS_REQ(aligned8(nnz) && aligned8(M) && aligned4(overflow) && aligned4(tile_offsets) && aligned4(isect_ids) &&
+           aligned8(isect_keys) && aligned4(camera_ids) && aligned8(radii) && aligned16(splats) &&
+           (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
+    GS_REQ(workspace_bytes >= gsb::isect_workspace_bytes(nnz_capacity, M_capacity));
+    return gsb::launch_isect(*opt, C, 0, width, height, radii, splats, nnz_capacity, nnz, camera_ids, M_capacity, M,
+                             overflow, isect_ids, isect_keys, tile_offsets, workspace, workspace_bytes,
+                             static_cast<cudaStream_t>(stream));
+}
+
+size_t gs_project_bwd_packed_workspace_size(int64_t N, int32_t C) {
+    if (N < 0 || C < 1) return 0;
+    return gsb::project_bwd_packed_workspace_bytes(N, C);
+}
+
+gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
+                                const float* means, const float* quats, const float* scales, const float* opacities,
+                                const float* colors, int32_t K, const float* viewmats, const float* Ks,
+                                int64_t nnz_capacity, const int64_t* nnz, const int32_t* camera_ids,
+                                const int32_t* gaussian_ids, const int32_t* radii, const float* v_splats,
+                                float* v_means, float* v_quats, float* v_scales, float* v_opacities, float* v_colors,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_REQ(opt->packed == 1);
+    GS_TRY(check_dims(N, C, width, height));
+    if (N == 0) return GS_OK;
+    GS_REQ(nnz_capacity >= 0 && nnz && workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
+    GS_REQ(workspace_bytes >= gsb::project_bwd_packed_workspace_bytes(N, C));
+    GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && v_means && v_quats && v_scales &&
+           v_opacities && v_colors);
+    GS_REQ(nnz_capacity == 0 || (camera_ids && gaussian_ids && radii && v_splats));
+    GS_REQ(aligned8(nnz) && aligned16(quats) && aligned16(v_quats) && aligned16(v_splats) && aligned8(radii) &&
+           aligned4(camera_ids) && aligned4(gaussian_ids) && aligned4(means) && aligned4(v_means) &&
+           aligned4(colors) && aligned4(v_colors) && aligned4(scales) && aligned4(v_scales));
+    if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
+    return gsb::launch_project_bwd_packed(*opt, N, C, width, height, means, quats, scales, opacities, colors,
+                                          opt->sh_degree >= 0 ? K : 1, viewmats, Ks, nnz_capacity, nnz, camera_ids,
+                                          gaussian_ids, radii, v_splats, v_means, v_quats, v_scales, v_opacities,
+                                          v_colors, workspace, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

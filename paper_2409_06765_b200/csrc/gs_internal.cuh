@@ -43,10 +43,27 @@ gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H
                              const int32_t* radii, const float* v_splats, float* v_means,
                              float* v_quats, float* v_scales, float* v_opac, float* v_colors,
                              cudaStream_t s);
-size_t isect_workspace_bytes(int C, int64_t N, int W, int H, int64_t cap);
+size_t project_packed_workspace_bytes(int64_t N, int C);
+gs_status launch_project_packed(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                                const float* quats, const float* scales, const float* opac, const float* colors,
+                                int K, const float* viewmats, const float* Ks, int64_t cap, int64_t* nnz,
+                                int32_t* overflow, int32_t* camera_ids, int32_t* gaussian_ids, int32_t* radii,
+                                float* splats, void* ws, cudaStream_t s);
+size_t project_bwd_packed_workspace_bytes(int64_t N, int C);
+gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                                    const float* quats, const float* scales, const float* opac,
+                                    const float* colors, int K, const float* viewmats, const float* Ks,
+                                    int64_t cap, const int64_t* nnz, const int32_t* camera_ids,
+                                    const int32_t* gaussian_ids, const int32_t* radii, const float* v_splats,
+                                    float* v_means, float* v_quats, float* v_scales, float* v_opac,
+                                    float* v_colors, void* ws, cudaStream_t s);
+// n_items = C*N dense items (camera = id / N), or the packed capacity with the live count
+// *d_nnz and camera_ids (both NULL in dense mode).
+size_t isect_workspace_bytes(int64_t n_items, int64_t cap);
 gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, const int32_t* radii,
-                       const float* splats, int64_t cap, int64_t* M, int32_t* overflow, int32_t* ids,
-                       uint64_t* keys, int32_t* tile_offsets, void* ws, size_t ws_bytes, cudaStream_t s);
+                       const float* splats, int64_t n_items, const int64_t* d_nnz, const int32_t* camera_ids,
+                       int64_t cap, int64_t* M, int32_t* overflow, int32_t* ids, uint64_t* keys,
+                       int32_t* tile_offsets, void* ws, size_t ws_bytes, cudaStream_t s);
 gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                             const float* bg, const int32_t* ids, const int32_t* offs, float* out_rgb,
                             float* out_alpha, float* out_T, int32_t* last_ids, cudaStream_t s);

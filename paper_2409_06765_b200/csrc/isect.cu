@@ -163,6 +163,18 @@ __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ rad
     }
 }
 
+// Packed mode: every item is visible, so the "compaction" is the identity on the live
+// count V = min(*nnz, cap) (Q29).
+__global__ void k_packed_items(const float* __restrict__ splats, const int64_t* d_nnz, int64_t cap, int* d_V,
+                               uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+    const int V = (int)min(*d_nnz, cap);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *d_V = V;
+    if (i >= V) return;
+    out_key[i] = __float_as_uint(splats[i * GS_SPLAT_FLOATS + 3]);
+    out_val[i] = (int32_t)i;
+}
+
 // ---------------------------------------------------------------------------------------
 // K4: one stable LSD radix pass (8-bit digit at `shift`), reduce-then-scan.
 // hist layout: hist[d * nb_max + b] = count of digit d in block b (digit-major rows).
@@ -332,6 +344,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
 struct TileGeom {
     int TX, TY, TT;
     int64_t N;
+    const int32_t* cam_ids;   // packed mode: camera of each item (else camera = id / N)
 };
 
 __global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ radii, const float* __restrict__ splats,
@@ -443,7 +456,8 @@ __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_
         const int w = rc.y - rc.x;
         const int ty = rc.z + kk / w, tx = rc.x + kk % w;
         const int32_t id = vis_val[j];
-        out_key[o] = (uint32_t)(id / g.N) * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
+        const uint32_t cam = g.cam_ids ? (uint32_t)g.cam_ids[id] : (uint32_t)(id / g.N);
+        out_key[o] = cam * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
         out_val[o] = id;
     }
 }
@@ -482,9 +496,8 @@ struct WsLayout {
     int nb_sort_max;   // blocks of kSortTile items (radix passes, tile counts)
 };
 
-WsLayout ws_layout(int C, int64_t N, int64_t cap) {
+WsLayout ws_layout(int64_t n_items, int64_t cap) {
     WsLayout L;
-    const int64_t n_items = (int64_t)C * N;
     const int64_t big = n_items > cap ? n_items : cap;
     L.nb_sort_max = div_up(big > 0 ? big : 1, kSortTile);
     const int64_t nb_emit = div_up(cap > 0 ? cap : 1, kEmit) + 1;
@@ -535,16 +548,14 @@ KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int 
 
 }  // namespace
 
-size_t isect_workspace_bytes(int C, int64_t N, int W, int H, int64_t cap) {
-    (void)W; (void)H;
-    return ws_layout(C, N, cap).total;
-}
+size_t isect_workspace_bytes(int64_t n_items, int64_t cap) { return ws_layout(n_items, cap).total; }
 
 gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, const int32_t* radii, const float* splats,
-                       int64_t cap, int64_t* M, int32_t* overflow, int32_t* ids, uint64_t* keys, int32_t* tile_offsets,
-                       void* ws, size_t ws_bytes, cudaStream_t s) {
+                       int64_t n_items, const int64_t* d_nnz, const int32_t* camera_ids, int64_t cap, int64_t* M,
+                       int32_t* overflow, int32_t* ids, uint64_t* keys, int32_t* tile_offsets, void* ws,
+                       size_t ws_bytes, cudaStream_t s) {
     (void)o;
-    const WsLayout L = ws_layout(C, N, cap);
+    const WsLayout L = ws_layout(n_items, cap);
     if (ws_bytes < L.total) return GS_ERR_INVALID_ARGUMENT;
     char* w = static_cast<char*>(ws);
     int* scal = reinterpret_cast<int*>(w + L.off_scalars);
@@ -562,19 +573,23 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     KV ia{reinterpret_cast<uint32_t*>(w + L.off_ka), reinterpret_cast<int32_t*>(w + L.off_va)};
     KV ib{reinterpret_cast<uint32_t*>(w + L.off_kb), reinterpret_cast<int32_t*>(w + L.off_vb)};
 
-    const int64_t n_items = (int64_t)C * N;
     const int TX = div_up(W, GS_TILE), TY = div_up(H, GS_TILE), TT = TX * TY;
     const int nbins = C * TT;
     const int B = tile_bits(TT);
-    TileGeom g{TX, TY, TT, N};
+    TileGeom g{TX, TY, TT, N > 0 ? N : 1, camera_ids};
     const int2* r2 = reinterpret_cast<const int2*>(radii);
     const int nb_items = div_up(n_items > 0 ? n_items : 1, kTile);
 
-    // 1. stable compaction of the visible (c,n) items (K2a, K2b)
-    k_vis_count<<<nb_items, kT, 0, s>>>(r2, n_items, blocksum);
-    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, kTile, nullptr, n_items, INT64_MAX, d_V, nullptr, nullptr,
-                                                 0, nullptr);
-    k_vis_compact<<<nb_items, kT, 0, s>>>(r2, splats, n_items, blocksum, vis.k, vis.v);
+    // 1. stable compaction of the visible (c,n) items (K2a, K2b); identity when packed
+    if (d_nnz) {
+        k_packed_items<<<div_up(n_items > 0 ? n_items : 1, 256), 256, 0, s>>>(splats, d_nnz, n_items, d_V, vis.k,
+                                                                             vis.v);
+    } else {
+        k_vis_count<<<nb_items, kT, 0, s>>>(r2, n_items, blocksum);
+        k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, kTile, nullptr, n_items, INT64_MAX, d_V, nullptr,
+                                                     nullptr, 0, nullptr);
+        k_vis_compact<<<nb_items, kT, 0, s>>>(r2, splats, n_items, blocksum, vis.k, vis.v);
+    }
     GS_LAUNCH_CHECK("isect/compact");
     // 2. stable sort by fp32 depth bits (K4, 4 passes)
     KV dsorted = radix_sort(vis, alt, nullptr, d_V, n_items, 32, hist, rowtot, L.nb_sort_max, s);

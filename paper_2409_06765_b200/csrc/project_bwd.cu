@@ -30,6 +30,7 @@ struct PBParams {
     const float* Ks;
     const int32_t* radii;
     const float* v_splats;
+    const int32_t* map;   // packed mode: (c,n) -> packed item or -1 (else NULL: item = c*N+n)
     float* v_means;
     float* v_quats;
     float* v_scales;
@@ -88,7 +89,12 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
     bool seen = false;
 
     for (int c = 0; c < p.C; c++) {
-        const int64_t idx = (int64_t)c * p.N + n;
+        int64_t idx = (int64_t)c * p.N + n;
+        if (p.map) {
+            const int m = p.map[idx];
+            if (m < 0) continue;
+            idx = m;
+        }
         const int2 rad = reinterpret_cast<const int2*>(p.radii)[idx];
         if (rad.x <= 0 || rad.y <= 0) continue;
         seen = true;
@@ -355,6 +361,43 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
 
 }  // namespace
 
+namespace {
+
+PBParams make_pb_params(const gs_options& o, int64_t N, int C, int W, int H, const float* means, const float* quats,
+                        const float* scales, const float* opac, const float* colors, int K, const float* viewmats,
+                        const float* Ks, const int32_t* radii, const float* v_splats, float* v_means,
+                        float* v_quats, float* v_scales, float* v_opac, float* v_colors) {
+    PBParams p{};
+    p.N = N; p.C = C; p.W = W; p.H = H; p.K = K;
+    p.eps2d = o.eps2d; p.antialiased = o.antialiased; p.fov_clamp = o.fov_clamp;
+    p.means = means; p.quats = quats; p.scales = scales; p.opac = opac; p.colors = colors;
+    p.viewmats = viewmats; p.Ks = Ks; p.radii = radii; p.v_splats = v_splats; p.map = nullptr;
+    p.vec_colors = ((reinterpret_cast<uintptr_t>(v_colors) & 15u) == 0) && ((K * 3) % 4 == 0);
+    p.v_means = v_means; p.v_quats = v_quats; p.v_scales = v_scales; p.v_opac = v_opac; p.v_colors = v_colors;
+    return p;
+}
+
+void launch_pb(int deg, const PBParams& p, cudaStream_t s) {
+    const int grid = div_up(p.N, kThreads);
+    switch (deg) {
+        case -1: k_project_bwd<-1><<<grid, kThreads, 0, s>>>(p); break;
+        case 0: k_project_bwd<0><<<grid, kThreads, 0, s>>>(p); break;
+        case 1: k_project_bwd<1><<<grid, kThreads, 0, s>>>(p); break;
+        case 2: k_project_bwd<2><<<grid, kThreads, 0, s>>>(p); break;
+        default: k_project_bwd<3><<<grid, kThreads, 0, s>>>(p); break;
+    }
+}
+
+// map[camera_ids[i] * N + gaussian_ids[i]] = i for the live packed items (map pre-set to -1)
+__global__ void k_pack_map(const int32_t* __restrict__ cam, const int32_t* __restrict__ gid, const int64_t* d_nnz,
+                           int64_t cap, int64_t N, int32_t* __restrict__ map) {
+    const int64_t n = min(*d_nnz, cap);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) map[(int64_t)cam[i] * N + gid[i]] = (int32_t)i;
+}
+
+}  // namespace
+
 gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
                              const float* quats, const float* scales, const float* opac,
                              const float* colors, int K, const float* viewmats, const float* Ks,
@@ -362,22 +405,36 @@ gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H
                              float* v_quats, float* v_scales, float* v_opac, float* v_colors,
                              cudaStream_t s) {
     if (N == 0) return GS_OK;
-    PBParams p;
-    p.N = N; p.C = C; p.W = W; p.H = H; p.K = K;
-    p.eps2d = o.eps2d; p.antialiased = o.antialiased; p.fov_clamp = o.fov_clamp;
-    p.means = means; p.quats = quats; p.scales = scales; p.opac = opac; p.colors = colors;
-    p.viewmats = viewmats; p.Ks = Ks; p.radii = radii; p.v_splats = v_splats;
-    p.vec_colors = ((reinterpret_cast<uintptr_t>(v_colors) & 15u) == 0) && ((K * 3) % 4 == 0);
-    p.v_means = v_means; p.v_quats = v_quats; p.v_scales = v_scales; p.v_opac = v_opac; p.v_colors = v_colors;
-    const int grid = div_up(N, kThreads);
-    switch (o.sh_degree) {
-        case -1: k_project_bwd<-1><<<grid, kThreads, 0, s>>>(p); break;
-        case 0: k_project_bwd<0><<<grid, kThreads, 0, s>>>(p); break;
-        case 1: k_project_bwd<1><<<grid, kThreads, 0, s>>>(p); break;
-        case 2: k_project_bwd<2><<<grid, kThreads, 0, s>>>(p); break;
-        default: k_project_bwd<3><<<grid, kThreads, 0, s>>>(p); break;
-    }
+    const PBParams p = make_pb_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii,
+                                      v_splats, v_means, v_quats, v_scales, v_opac, v_colors);
+    launch_pb(o.sh_degree, p, s);
     GS_LAUNCH_CHECK("k_project_bwd");
+    return GS_OK;
+}
+
+size_t project_bwd_packed_workspace_bytes(int64_t N, int C) {
+    return ((size_t)C * (size_t)N * sizeof(int32_t) + 255) & ~(size_t)255;
+}
+
+gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                                    const float* quats, const float* scales, const float* opac,
+                                    const float* colors, int K, const float* viewmats, const float* Ks,
+                                    int64_t cap, const int64_t* nnz, const int32_t* camera_ids,
+                                    const int32_t* gaussian_ids, const int32_t* radii, const float* v_splats,
+                                    float* v_means, float* v_quats, float* v_scales, float* v_opac,
+                                    float* v_colors, void* ws, cudaStream_t s) {
+    if (N == 0) return GS_OK;
+    int32_t* map = static_cast<int32_t*>(ws);
+    if (cudaMemsetAsync(map, 0xff, sizeof(int32_t) * (size_t)C * (size_t)N, s) != cudaSuccess) {
+        GS_LAUNCH_CHECK("packed map memset");
+        return GS_ERR_CUDA;
+    }
+    if (cap > 0) k_pack_map<<<div_up(cap, 256), 256, 0, s>>>(camera_ids, gaussian_ids, nnz, cap, N, map);
+    PBParams p = make_pb_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii, v_splats,
+                                v_means, v_quats, v_scales, v_opac, v_colors);
+    p.map = map;
+    launch_pb(o.sh_degree, p, s);
+    GS_LAUNCH_CHECK("k_project_bwd<packed>");
     return GS_OK;
 }
 

@@ -43,7 +43,16 @@ struct ProjParams {
     const float* Ks;
     int32_t* radii;
     float* splats;
+    // packed mode (Q29)
+    int* blockcnt;            // [C][gridDim.x] visible items per (camera, block); then offsets
+    int64_t cap;              // packed capacity
+    int32_t* camera_ids;
+    int32_t* gaussian_ids;
 };
+
+// Kernel modes: dense [C,N] records; packed pass 1 (visibility count per (camera, block));
+// packed pass 2 (write each visible record at its packed position).
+enum { kDense = 0, kCount = 1, kPacked = 2 };
 
 __device__ __forceinline__ void setup_cam(const ProjParams& p, int c, CamConst& cc) {
     const float* vm = p.viewmats + 16 * (int64_t)c;
@@ -66,9 +75,10 @@ __device__ __forceinline__ void setup_cam(const ProjParams& p, int c, CamConst& 
     cc.pad = 0.f;
 }
 
-template <int DEG>
+template <int DEG, int MODE>
 __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
     __shared__ CamConst s_cam[kCamChunk];
+    __shared__ int s_wcnt[kThreads / 32];
     const int64_t n = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const bool active = n < p.N;
 
@@ -113,12 +123,9 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
         __syncthreads();
         if (threadIdx.x < nc) setup_cam(p, c0 + threadIdx.x, s_cam[threadIdx.x]);
         __syncthreads();
-        if (!active) continue;
+        if (MODE == kDense && !active) continue;   // the packed modes keep every thread (block scans)
         for (int ci = 0; ci < nc; ci++) {
             const CamConst& cc = s_cam[ci];
-            const int64_t idx = (int64_t)(c0 + ci) * p.N + n;
-            float4* rec = reinterpret_cast<float4*>(p.splats + idx * GS_SPLAT_FLOATS);
-            int2* rad = reinterpret_cast<int2*>(p.radii) + idx;
             // KP1 (F3): t = W mu + w
             const float tx = ((cc.vm[0] * mu0 + cc.vm[1] * mu1) + cc.vm[2] * mu2) + cc.vm[3];
             const float ty = ((cc.vm[4] * mu0 + cc.vm[5] * mu1) + cc.vm[6] * mu2) + cc.vm[7];
@@ -191,6 +198,31 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
                         vis = false;
                 }
             }
+            // ---- where this (c,n) goes ----
+            int64_t idx = (int64_t)(c0 + ci) * p.N + n;
+            if (MODE == kCount) {
+                const int cnt = __syncthreads_count(vis);
+                if (threadIdx.x == 0) p.blockcnt[(int64_t)(c0 + ci) * gridDim.x + blockIdx.x] = cnt;
+                continue;
+            }
+            if (MODE == kPacked) {
+                // packed position = block offset of camera c + rank of this thread's visible
+                // item inside the block (camera-major, then n: Q29)
+                const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                const unsigned bal = __ballot_sync(0xffffffffu, vis);
+                __syncthreads();   // s_wcnt reuse across cameras
+                if (lane == 0) s_wcnt[warp] = __popc(bal);
+                __syncthreads();
+                int before = 0;
+                for (int w = 0; w < warp; w++) before += s_wcnt[w];
+                idx = (int64_t)p.blockcnt[(int64_t)(c0 + ci) * gridDim.x + blockIdx.x] + before +
+                      __popc(bal & ((1u << lane) - 1u));
+                if (!vis || idx >= p.cap) continue;
+                p.camera_ids[idx] = c0 + ci;
+                p.gaussian_ids[idx] = (int32_t)n;
+            }
+            float4* rec = reinterpret_cast<float4*>(p.splats + idx * GS_SPLAT_FLOATS);
+            int2* rad = reinterpret_cast<int2*>(p.radii) + idx;
             if (!vis) {
                 *rad = make_int2(0, 0);
                 const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -249,27 +281,119 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
 
 }  // namespace
 
-gs_status launch_project_fwd(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
-                             const float* quats, const float* scales, const float* opac,
-                             const float* colors, int K, const float* viewmats, const float* Ks,
-                             int32_t* radii, float* splats, cudaStream_t s) {
-    if (N == 0) return GS_OK;
-    ProjParams p;
+namespace {
+
+// Exclusive scan (in place) of the C * nblk per-(camera, block) counts, camera-major;
+// *nnz = total, *overflow = total > cap.  One block, 16 consecutive entries per thread per
+// round of 16384.
+constexpr int kScanT = 1024, kScanItems = 16;
+__global__ void __launch_bounds__(kScanT) k_pack_scan(int* cnt, int64_t n, int64_t cap, int64_t* nnz,
+                                                      int32_t* overflow) {
+    __shared__ int s_w[kScanT / 32 + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t carry = 0;
+    for (int64_t r = 0; r < n; r += (int64_t)kScanT * kScanItems) {
+        const int64_t i0 = r + (int64_t)threadIdx.x * kScanItems;
+        int v[kScanItems];
+        int sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; k++) {
+            v[k] = i0 + k < n ? cnt[i0 + k] : 0;
+            sum += v[k];
+        }
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            const int w = s_w[lane];
+            int wx = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, wx, o);
+                if (lane >= o) wx += y;
+            }
+            s_w[lane] = wx - w;
+            if (lane == 31) s_w[32] = wx;
+        }
+        __syncthreads();
+        int64_t run = carry + (x - sum) + s_w[warp];
+#pragma unroll
+        for (int k = 0; k < kScanItems; k++) {
+            if (i0 + k < n) cnt[i0 + k] = (int)run;
+            run += v[k];
+        }
+        carry += s_w[32];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *nnz = carry;
+        *overflow = carry > cap ? 1 : 0;
+    }
+}
+
+ProjParams make_proj_params(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                            const float* quats, const float* scales, const float* opac, const float* colors, int K,
+                            const float* viewmats, const float* Ks, int32_t* radii, float* splats) {
+    ProjParams p{};
     p.N = N; p.C = C; p.W = W; p.H = H; p.K = K;
     p.near_plane = o.near_plane; p.far_plane = o.far_plane; p.eps2d = o.eps2d;
     p.antialiased = o.antialiased; p.bbox_mode = o.bbox_mode; p.fov_clamp = o.fov_clamp;
     p.means = means; p.quats = quats; p.scales = scales; p.opac = opac; p.colors = colors;
     p.viewmats = viewmats; p.Ks = Ks; p.radii = radii; p.splats = splats;
     p.vec_colors = ((reinterpret_cast<uintptr_t>(colors) & 15u) == 0) && ((K * 3) % 4 == 0);
-    const int grid = div_up(N, kThreads);
-    switch (o.sh_degree) {
-        case -1: k_project_fwd<-1><<<grid, kThreads, 0, s>>>(p); break;
-        case 0: k_project_fwd<0><<<grid, kThreads, 0, s>>>(p); break;
-        case 1: k_project_fwd<1><<<grid, kThreads, 0, s>>>(p); break;
-        case 2: k_project_fwd<2><<<grid, kThreads, 0, s>>>(p); break;
-        default: k_project_fwd<3><<<grid, kThreads, 0, s>>>(p); break;
+    return p;
+}
+
+template <int MODE>
+void launch_mode(int deg, int grid, const ProjParams& p, cudaStream_t s) {
+    switch (deg) {
+        case -1: k_project_fwd<-1, MODE><<<grid, kThreads, 0, s>>>(p); break;
+        case 0: k_project_fwd<0, MODE><<<grid, kThreads, 0, s>>>(p); break;
+        case 1: k_project_fwd<1, MODE><<<grid, kThreads, 0, s>>>(p); break;
+        case 2: k_project_fwd<2, MODE><<<grid, kThreads, 0, s>>>(p); break;
+        default: k_project_fwd<3, MODE><<<grid, kThreads, 0, s>>>(p); break;
     }
+}
+
+}  // namespace
+
+gs_status launch_project_fwd(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                             const float* quats, const float* scales, const float* opac,
+                             const float* colors, int K, const float* viewmats, const float* Ks,
+                             int32_t* radii, float* splats, cudaStream_t s) {
+    if (N == 0) return GS_OK;
+    const ProjParams p = make_proj_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii,
+                                          splats);
+    launch_mode<kDense>(o.sh_degree, div_up(N, kThreads), p, s);
     GS_LAUNCH_CHECK("k_project_fwd");
+    return GS_OK;
+}
+
+size_t project_packed_workspace_bytes(int64_t N, int C) {
+    return ((size_t)C * (size_t)div_up(N > 0 ? N : 1, kThreads) * sizeof(int) + 255) & ~(size_t)255;
+}
+
+gs_status launch_project_packed(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
+                                const float* quats, const float* scales, const float* opac, const float* colors,
+                                int K, const float* viewmats, const float* Ks, int64_t cap, int64_t* nnz,
+                                int32_t* overflow, int32_t* camera_ids, int32_t* gaussian_ids, int32_t* radii,
+                                float* splats, void* ws, cudaStream_t s) {
+    ProjParams p = make_proj_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii,
+                                    splats);
+    const int grid = div_up(N > 0 ? N : 1, kThreads);
+    p.blockcnt = static_cast<int*>(ws);
+    p.cap = cap;
+    p.camera_ids = camera_ids;
+    p.gaussian_ids = gaussian_ids;
+    if (N > 0) launch_mode<kCount>(o.sh_degree, grid, p, s);
+    k_pack_scan<<<1, kScanT, 0, s>>>(p.blockcnt, N > 0 ? (int64_t)C * grid : 0, cap, nnz, overflow);
+    if (N > 0) launch_mode<kPacked>(o.sh_degree, grid, p, s);
+    GS_LAUNCH_CHECK("k_project_fwd<packed>");
     return GS_OK;
 }
 

@@ -471,6 +471,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                                      xy, G, alpha);
             const unsigned vb = __ballot_sync(0xffffffffu, valid);
             if (!vb) continue;
+#ifdef GS_EXP_EVALONLY
+            if (valid && alpha * T == 1234.5f) p.v_splats[s.id[j]] = 1.f;
+            continue;
+#endif
             float g8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // mx, my, o, A, B, C, r, g
             float g_bl = 0.f;
             if (valid) {
@@ -502,6 +506,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 }
             }
             float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
+#ifdef GS_EXP_NORED
+            if (valid && g8[0] + g8[1] + g8[2] + g8[3] + g8[4] + g8[5] + g8[6] + g8[7] + g_bl == 1234.5f) dst[0] = 1.f;
+            continue;
+#endif
             if (__popc(vb) <= kFewLanes) {
                 // few contributing lanes: each issues its own three 16-byte reductions -- 3 warp
                 // instructions instead of the ~45 of the shuffle tree
@@ -566,7 +574,8 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
     RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
     p.out_T = const_cast<float*>(out_T); p.last_ids = const_cast<int32_t*>(last_ids);
     p.v_rgb = v_rgb; p.v_alpha = v_alpha; p.v_splats = v_splats; p.absgrad = absgrad;
-    if (N > 0 && cudaMemsetAsync(v_splats, 0, sizeof(float) * GS_SPLAT_FLOATS * (size_t)C * (size_t)N, s) != cudaSuccess) {
+    const size_t nrec = o.packed ? (size_t)N : (size_t)C * (size_t)N;   // packed: N records in total (Q29)
+    if (N > 0 && cudaMemsetAsync(v_splats, 0, sizeof(float) * GS_SPLAT_FLOATS * nrec, s) != cudaSuccess) {
         GS_LAUNCH_CHECK("v_splats memset");
         return GS_ERR_CUDA;
     }

@@ -10,7 +10,9 @@ The intersection count M is data dependent.  The engine keeps an M capacity; the
 isect stage writes M and an overflow flag on the device, and `ensure_capacity()` (one
 small device->host read) grows the capacity and tells the caller to re-run when the
 flag is set.  In steady state (bench.py, CUDA-graph replay) the flag is checked after
-the timed region only.  Parameter gradients land in ONE flat fp32 buffer (`flat_grad`)
+the timed region only.  With packed=True (Q29) only the visible (camera, Gaussian) pairs
+are stored: the projection writes nnz device-side and the per-item buffers are sized by
+an nnz capacity handled the same way as M.  Parameter gradients land in ONE flat fp32 buffer (`flat_grad`)
 so the data-parallel gradient sum is a single collective.
 """
 from __future__ import annotations
@@ -25,20 +27,31 @@ from . import dist as D
 
 class Engine:
     def __init__(self, N, C, width, height, sh_degree=3, K=None, antialiased=False, M_capacity=None,
-                 device="cuda", absgrad=False, with_keys=False, **opt_kwargs):
+                 device="cuda", absgrad=False, with_keys=False, packed=False, nnz_capacity=None, **opt_kwargs):
         self.N, self.C, self.W, self.H = int(N), int(C), int(width), int(height)
         self.sh_degree = int(sh_degree)
         self.K = (K if K is not None else (self.sh_degree + 1) ** 2) if self.sh_degree >= 0 else 1
         self.absgrad = bool(absgrad)
         self.with_keys = bool(with_keys)
         self.device = torch.device(device)
-        self.opts = L.options(sh_degree=self.sh_degree, antialiased=antialiased, **opt_kwargs)
+        self.packed = bool(packed)
+        self.opts = L.options(sh_degree=self.sh_degree, antialiased=antialiased, packed=self.packed, **opt_kwargs)
         self.TX, self.TY = L.tiles(self.W, self.H)
         dev = self.device
         C, N, W, H = self.C, self.N, self.W, self.H
-        self.radii = torch.zeros((C, N, 2), dtype=torch.int32, device=dev)
-        self.splats = torch.zeros((C, N, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
-        self.v_splats = torch.zeros_like(self.splats)
+        self.nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.nnz_overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.nnz_cap = 0
+        if self.packed:
+            self._alloc_items(nnz_capacity if nnz_capacity is not None else C * N)
+            pw = L.gs_project_packed_workspace_size(N, C)
+            bw = L.gs_project_bwd_packed_workspace_size(N, C)
+            self._proj_ws = self._aligned(pw)
+            self._pbwd_ws = self._aligned(bw)
+        else:
+            self.radii = torch.zeros((C, N, 2), dtype=torch.int32, device=dev)
+            self.splats = torch.zeros((C, N, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
+            self.v_splats = torch.zeros_like(self.splats)
         self.M = torch.zeros(1, dtype=torch.int64, device=dev)
         self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
         self.tile_offsets = torch.zeros(C * self.TX * self.TY + 1, dtype=torch.int32, device=dev)
@@ -60,6 +73,30 @@ class Engine:
         self._alloc_isect(M_capacity if M_capacity is not None else max(1 << 16, 4 * C * N))
 
     # ------------------------------------------------------------------------------
+    def _aligned(self, nbytes):
+        """A 256-byte aligned uint8 view of nbytes (the C-ABI workspace contract)."""
+        raw = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        off = (-raw.data_ptr()) % 256
+        return raw[off:off + nbytes]
+
+    def _alloc_items(self, cap):
+        """Packed mode: per-item buffers for `cap` visible (camera, Gaussian) pairs."""
+        cap = max(int(cap), 1)
+        dev = self.device
+        self.nnz_cap = cap
+        self.radii = torch.zeros((cap, 2), dtype=torch.int32, device=dev)
+        self.splats = torch.zeros((cap, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
+        self.v_splats = torch.zeros_like(self.splats)
+        self.camera_ids = torch.zeros(cap, dtype=torch.int32, device=dev)
+        self.gaussian_ids = torch.zeros(cap, dtype=torch.int32, device=dev)
+        self.isect_ids = None   # the isect workspace depends on the item capacity
+        self.cap = 0
+
+    @property
+    def n_items(self) -> int:
+        """Records per call: C*N dense, the packed capacity otherwise (the N of gs_rasterize_*)."""
+        return self.nnz_cap if self.packed else self.N
+
     def _alloc_isect(self, cap):
         cap = int(cap)
         if cap <= self.cap and self.isect_ids is not None:
@@ -67,15 +104,20 @@ class Engine:
         self.cap = cap
         self.isect_ids = torch.zeros(max(cap, 1), dtype=torch.int32, device=self.device)
         self.isect_keys = torch.zeros(max(cap, 1), dtype=torch.int64, device=self.device) if self.with_keys else None
-        ws = L.gs_isect_workspace_size(self.C, self.N, self.W, self.H, cap)
-        self.workspace = torch.empty(ws + 256, dtype=torch.uint8, device=self.device)
-        # the C-ABI wants a 256-byte aligned workspace
-        off = (-self.workspace.data_ptr()) % 256
-        self.workspace_view = self.workspace[off:off + ws]
+        if self.packed:
+            ws = L.gs_isect_packed_workspace_size(self.C, self.nnz_cap, self.W, self.H, cap)
+        else:
+            ws = L.gs_isect_workspace_size(self.C, self.N, self.W, self.H, cap)
+        self.workspace_view = self._aligned(ws)
 
     def ensure_capacity(self, headroom=1.25) -> bool:
         """Reads M and the overflow flag (one D->H sync).  Returns True when the last
         isect overflowed; the capacity is then grown and the caller must re-run."""
+        if self.packed and int(self.nnz_overflow.item()) != 0:
+            M_cap = self.cap
+            self._alloc_items(math.ceil(int(self.nnz.item()) * headroom) + 1024)
+            self._alloc_isect(M_cap)
+            return True
         if int(self.overflow.item()) == 0:
             return False
         self._alloc_isect(math.ceil(int(self.M.item()) * headroom) + 1024)
@@ -88,6 +130,8 @@ class Engine:
         raster fwd 1, bwd 1; project bwd 1."""
         bits = max(1, (self.C * self.TX * self.TY - 1).bit_length())
         P = (bits + 7) // 8
+        if self.packed:   # project: count, scan, write; isect: identity items; project bwd: map + kernel
+            return 3 + (1 + 12 + 3 + 1 + 3 * P + 2) + 1 + 1 + 2
         return 1 + (3 + 12 + 3 + 1 + 3 * P + 2) + 1 + 1 + 1
 
     @property
@@ -96,27 +140,44 @@ class Engine:
 
     # ------------------------------------------------------------------------------
     def project(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
-        L.gs_project(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W, self.H,
-                     self.radii, self.splats, stream)
+        if self.packed:
+            L.gs_project_packed(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W,
+                                self.H, self.nnz_cap, self.nnz, self.nnz_overflow, self.camera_ids,
+                                self.gaussian_ids, self.radii, self.splats, self._proj_ws, stream)
+        else:
+            L.gs_project(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W, self.H,
+                         self.radii, self.splats, stream)
 
     def isect(self, stream=None):
-        L.gs_isect_tiles(self.opts, self.C, self.N, self.W, self.H, self.radii, self.splats, self.cap, self.M,
-                         self.overflow, self.isect_ids, self.isect_keys, self.tile_offsets, self.workspace_view,
-                         stream)
+        if self.packed:
+            L.gs_isect_tiles_packed(self.opts, self.C, self.nnz_cap, self.nnz, self.W, self.H, self.camera_ids,
+                                    self.radii, self.splats, self.cap, self.M, self.overflow, self.isect_ids,
+                                    self.isect_keys, self.tile_offsets, self.workspace_view, stream)
+        else:
+            L.gs_isect_tiles(self.opts, self.C, self.N, self.W, self.H, self.radii, self.splats, self.cap, self.M,
+                             self.overflow, self.isect_ids, self.isect_keys, self.tile_offsets, self.workspace_view,
+                             stream)
 
     def rasterize_fwd(self, backgrounds=None, stream=None):
-        L.gs_rasterize_fwd(self.opts, self.C, self.N, self.W, self.H, self.splats, backgrounds, self.isect_ids,
-                           self.tile_offsets, self.out_rgb, self.out_alpha, self.out_T, self.last_ids, stream)
+        L.gs_rasterize_fwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
+                           self.isect_ids, self.tile_offsets, self.out_rgb, self.out_alpha, self.out_T,
+                           self.last_ids, stream)
 
     def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, stream=None):
-        L.gs_rasterize_bwd(self.opts, self.C, self.N, self.W, self.H, self.splats, backgrounds, self.isect_ids,
-                           self.tile_offsets, self.out_T, self.last_ids, v_rgb, v_alpha, self.absgrad,
-                           self.v_splats, stream)
+        L.gs_rasterize_bwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
+                           self.isect_ids, self.tile_offsets, self.out_T, self.last_ids, v_rgb, v_alpha,
+                           self.absgrad, self.v_splats, stream)
 
     def project_bwd(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
-        L.gs_project_bwd(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W, self.H,
-                         self.radii, self.v_splats, self.v_means, self.v_quats, self.v_scales, self.v_opacities,
-                         self.v_colors, stream)
+        if self.packed:
+            L.gs_project_bwd_packed(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks,
+                                    self.W, self.H, self.nnz_cap, self.nnz, self.camera_ids, self.gaussian_ids,
+                                    self.radii, self.v_splats, self.v_means, self.v_quats, self.v_scales,
+                                    self.v_opacities, self.v_colors, self._pbwd_ws, stream)
+        else:
+            L.gs_project_bwd(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W,
+                             self.H, self.radii, self.v_splats, self.v_means, self.v_quats, self.v_scales,
+                             self.v_opacities, self.v_colors, stream)
 
     def forward(self, means, quats, scales, opacities, colors, viewmats, Ks, backgrounds=None, stream=None):
         self.project(means, quats, scales, opacities, colors, viewmats, Ks, stream)

@@ -18,6 +18,14 @@ from . import _lib as L
 
 # last intersection count per problem shape: the next call's capacity estimate
 _M_CACHE: dict = {}
+# last packed item count per problem shape (packed mode, Q29)
+_NNZ_CACHE: dict = {}
+
+
+def _aligned_ws(nbytes, dev):
+    raw = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+    a = (-raw.data_ptr()) % 256
+    return raw[a:a + nbytes]
 
 
 def _sh_degree_of(colors, sh_degree):
@@ -36,9 +44,32 @@ class _Rasterize(torch.autograd.Function):
         N, C = means.shape[0], viewmats.shape[0]
         K = cfg["K"]
         dev = means.device
-        radii = torch.empty((C, N, 2), dtype=torch.int32, device=dev)
-        splats = torch.empty((C, N, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
-        L.gs_project(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, radii, splats)
+        packed = bool(cfg["packed"])
+        cam_ids = gid = nnz_dev = None
+        if packed:
+            # packed projection (Q29): one D->H read of nnz per call, like M below
+            nnz_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+            novf = torch.zeros(1, dtype=torch.int32, device=dev)
+            ws = _aligned_ws(L.gs_project_packed_workspace_size(N, C), dev)
+            n_rec = _NNZ_CACHE.get((N, C, W, H), C * N)
+            while True:
+                n_rec = max(int(n_rec), 1)
+                radii = torch.empty((n_rec, 2), dtype=torch.int32, device=dev)
+                splats = torch.empty((n_rec, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
+                cam_ids = torch.empty(n_rec, dtype=torch.int32, device=dev)
+                gid = torch.empty(n_rec, dtype=torch.int32, device=dev)
+                L.gs_project_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, n_rec,
+                                    nnz_dev, novf, cam_ids, gid, radii, splats, ws)
+                nnz = int(nnz_dev.item())
+                _NNZ_CACHE[(N, C, W, H)] = math.ceil(nnz * 1.25) + 1024
+                if int(novf.item()) == 0:
+                    break
+                n_rec = nnz + 1024
+        else:
+            n_rec = N
+            radii = torch.empty((C, N, 2), dtype=torch.int32, device=dev)
+            splats = torch.empty((C, N, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
+            L.gs_project(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, radii, splats)
         TX, TY = L.tiles(W, H)
         offs = torch.empty(C * TX * TY + 1, dtype=torch.int32, device=dev)
         Mdev = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -47,10 +78,13 @@ class _Rasterize(torch.autograd.Function):
         cap = _M_CACHE.get(key, max(1024, 4 * C * N))
         while True:
             ids = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-            wsz = L.gs_isect_workspace_size(C, N, W, H, cap)
-            ws_raw = torch.empty(wsz + 256, dtype=torch.uint8, device=dev)
-            a = (-ws_raw.data_ptr()) % 256
-            L.gs_isect_tiles(o, C, N, W, H, radii, splats, cap, Mdev, ovf, ids, None, offs, ws_raw[a:a + wsz])
+            if packed:
+                wsv = _aligned_ws(L.gs_isect_packed_workspace_size(C, n_rec, W, H, cap), dev)
+                L.gs_isect_tiles_packed(o, C, n_rec, nnz_dev, W, H, cam_ids, radii, splats, cap, Mdev, ovf, ids,
+                                        None, offs, wsv)
+            else:
+                wsv = _aligned_ws(L.gs_isect_workspace_size(C, N, W, H, cap), dev)
+                L.gs_isect_tiles(o, C, N, W, H, radii, splats, cap, Mdev, ovf, ids, None, offs, wsv)
             M = int(Mdev.item())                      # one D->H read per call (as gsplat's .item())
             _M_CACHE[key] = math.ceil(M * 1.25) + 1024
             if int(ovf.item()) == 0:
@@ -60,18 +94,24 @@ class _Rasterize(torch.autograd.Function):
         out_alpha = torch.empty((C, H, W), dtype=torch.float32, device=dev)
         out_T = torch.empty((C, H, W), dtype=torch.float32, device=dev)
         last_ids = torch.empty((C, H, W), dtype=torch.int32, device=dev)
-        L.gs_rasterize_fwd(o, C, N, W, H, splats, backgrounds, ids, offs, out_rgb, out_alpha, out_T, last_ids)
+        L.gs_rasterize_fwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_rgb, out_alpha, out_T, last_ids)
+        if not packed:
+            cam_ids = gid = torch.empty(0, dtype=torch.int32, device=dev)
+            nnz_dev = torch.full((1,), C * N, dtype=torch.int64, device=dev)
         ctx.save_for_backward(means, quats, scales, opacities, colors, viewmats, Ks, backgrounds, radii, splats,
-                              ids, offs, out_T, last_ids)
+                              ids, offs, out_T, last_ids, cam_ids, gid, nnz_dev)
         ctx.cfg = cfg
+        ctx.n_rec = n_rec
         ctx.absgrad_out = absgrad_out
-        ctx.mark_non_differentiable(radii, splats, ids, offs, out_T, last_ids)
-        return out_rgb, out_alpha, radii, splats, ids, offs, out_T, last_ids, Mdev
+        ctx.mark_non_differentiable(radii, splats, ids, offs, out_T, last_ids, cam_ids, gid, nnz_dev)
+        return out_rgb, out_alpha, radii, splats, ids, offs, out_T, last_ids, Mdev, cam_ids, gid, nnz_dev
 
     @staticmethod
     def backward(ctx, v_rgb, v_alpha, *unused):
         (means, quats, scales, opacities, colors, viewmats, Ks, backgrounds, radii, splats, ids, offs, out_T,
-         last_ids) = ctx.saved_tensors
+         last_ids, cam_ids, gid, nnz_dev) = ctx.saved_tensors
+        packed = bool(ctx.cfg["packed"])
+        n_rec = ctx.n_rec
         cfg = ctx.cfg
         o = cfg["opts"]
         W, H, K = cfg["width"], cfg["height"], cfg["K"]
@@ -80,29 +120,42 @@ class _Rasterize(torch.autograd.Function):
         v_alpha = v_alpha.contiguous() if v_alpha is not None else None
         v_splats = torch.empty_like(splats)
         absgrad = ctx.absgrad_out is not None
-        L.gs_rasterize_bwd(o, C, N, W, H, splats, backgrounds, ids, offs, out_T, last_ids, v_rgb, v_alpha, absgrad,
-                           v_splats)
+        L.gs_rasterize_bwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_T, last_ids, v_rgb, v_alpha,
+                           absgrad, v_splats)
         if absgrad:
-            ctx.absgrad_out.copy_(torch.stack([v_splats[..., 7], v_splats[..., 11]], dim=-1))
+            ag = torch.stack([v_splats[..., 7], v_splats[..., 11]], dim=-1)
+            if packed:
+                nnz = int(nnz_dev.item())
+                ctx.absgrad_out.zero_()
+                ctx.absgrad_out[cam_ids[:nnz].long(), gid[:nnz].long()] = ag[:nnz]
+            else:
+                ctx.absgrad_out.copy_(ag)
         v_means = torch.empty_like(means)
         v_quats = torch.empty_like(quats)
         v_scales = torch.empty_like(scales)
         v_opac = torch.empty_like(opacities)
         v_colors = torch.empty_like(colors)
-        L.gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, radii, v_splats, v_means,
-                         v_quats, v_scales, v_opac, v_colors)
+        if packed:
+            ws = _aligned_ws(L.gs_project_bwd_packed_workspace_size(N, C), means.device)
+            L.gs_project_bwd_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, n_rec, nnz_dev,
+                                    cam_ids, gid, radii, v_splats, v_means, v_quats, v_scales, v_opac, v_colors, ws)
+        else:
+            L.gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, radii, v_splats,
+                             v_means, v_quats, v_scales, v_opac, v_colors)
         cfg["v_splats"] = v_splats
         return v_means, v_quats, v_scales, v_opac, v_colors, None, None, None, None, None
 
 
 def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, height, *, sh_degree=None,
                   near_plane=0.01, far_plane=1e10, eps2d=0.3, rasterize_mode="classic", tile_size=16,
-                  backgrounds=None, alpha_max=0.99, absgrad=False, fov_clamp=True, bbox_mode=0):
+                  backgrounds=None, alpha_max=0.99, absgrad=False, fov_clamp=True, bbox_mode=0, packed=False):
     """Render C views of N Gaussians.
 
     means [N,3], quats [N,4] (w,x,y,z), scales [N,3] (activated), opacities [N] (activated),
     colors [N,3] (RGB, sh_degree None/-1) or [N,K,3] (SH), viewmats [C,4,4] (world->camera),
     Ks [C,3,3], backgrounds [C,3] or None.  rasterize_mode "classic" | "antialiased" (A.4).
+    packed=True stores only the visible (camera, Gaussian) pairs (Q29): the per-item meta
+    entries are then [nnz, ...] rows with meta["camera_ids"], meta["gaussian_ids"].
     Returns render_colors [C,H,W,3], render_alphas [C,H,W,1] and a meta dict.
     """
     if rasterize_mode not in ("classic", "antialiased"):
@@ -111,16 +164,21 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
     K = colors.shape[1] if deg >= 0 else 1
     o = L.options(sh_degree=deg, antialiased=rasterize_mode == "antialiased", near_plane=near_plane,
                   far_plane=far_plane, eps2d=eps2d, alpha_max=alpha_max, tile_size=tile_size, bbox_mode=bbox_mode,
-                  fov_clamp=fov_clamp)
-    cfg = dict(opts=o, width=int(width), height=int(height), K=K)
+                  fov_clamp=fov_clamp, packed=packed)
+    cfg = dict(opts=o, width=int(width), height=int(height), K=K, packed=bool(packed))
     C, N = viewmats.shape[0], means.shape[0]
     absgrad_out = torch.zeros((C, N, 2), device=means.device) if absgrad else None
     args = [t.contiguous() if t is not None else None for t in (means, quats, scales, opacities, colors, viewmats, Ks,
                                                               backgrounds)]
-    out_rgb, out_alpha, radii, splats, ids, offs, out_T, last_ids, Mdev = _Rasterize.apply(*args, cfg, absgrad_out)
+    (out_rgb, out_alpha, radii, splats, ids, offs, out_T, last_ids, Mdev, cam_ids, gid,
+     nnz_dev) = _Rasterize.apply(*args, cfg, absgrad_out)
+    if packed:
+        nnz = int(nnz_dev.item())
+        radii, splats, cam_ids, gid = radii[:nnz], splats[:nnz], cam_ids[:nnz], gid[:nnz]
     meta = dict(radii=radii, means2d=splats[..., 0:2], depths=splats[..., 3], conics=splats[..., 4:7],
                 opacities=splats[..., 2], colors=splats[..., 8:11], splats=splats,
                 isect_ids=ids, flatten_ids=ids, tile_offsets=offs, n_isects=Mdev, T_final=out_T, last_ids=last_ids,
                 width=int(width), height=int(height), tile_size=tile_size, n_cameras=C, absgrad=absgrad_out,
+                packed=bool(packed), camera_ids=cam_ids if packed else None, gaussian_ids=gid if packed else None,
                 cfg=cfg)
     return out_rgb, out_alpha.unsqueeze(-1), meta

@@ -20,7 +20,7 @@ def to_torch(scene, device):
 
 
 def run_gpu(scene, *, antialiased=False, v_img=None, v_alpha=None, backgrounds=None, absgrad=False, device="cuda",
-            cap=None, **opt):
+            cap=None, packed=False, nnz_capacity=None, **opt):
     import torch
     from paper_2409_06765_b200 import Engine
     C, N = scene["viewmats"].shape[0], scene["means"].shape[0]
@@ -28,7 +28,7 @@ def run_gpu(scene, *, antialiased=False, v_img=None, v_alpha=None, backgrounds=N
     deg = int(scene["sh_degree"])
     K = scene["colors"].shape[1] if deg >= 0 else None
     eng = Engine(N, C, W, H, sh_degree=deg, K=K, antialiased=antialiased, device=device, absgrad=absgrad,
-                 with_keys=True, M_capacity=cap, **opt)
+                 with_keys=True, M_capacity=cap, packed=packed, nnz_capacity=nnz_capacity, **opt)
     params = to_torch(scene, device)
     if v_img is None:
         v_img = np.zeros((C, H, W, 3), np.float32)
@@ -45,7 +45,20 @@ def run_gpu(scene, *, antialiased=False, v_img=None, v_alpha=None, backgrounds=N
         T=eng.out_T.cpu().numpy(), last_ids=eng.last_ids.cpu().numpy(), v_splats=eng.v_splats.cpu().numpy(),
         v_means=eng.v_means.cpu().numpy(), v_quats=eng.v_quats.cpu().numpy(), v_scales=eng.v_scales.cpu().numpy(),
         v_opacities=eng.v_opacities.cpu().numpy(), v_colors=eng.v_colors.cpu().numpy(), engine=eng)
+    if packed:
+        nnz = int(eng.nnz.item())
+        out.update(nnz=nnz, camera_ids=eng.camera_ids[:nnz].cpu().numpy(),
+                   gaussian_ids=eng.gaussian_ids[:nnz].cpu().numpy())
+        for k in ("radii", "splats", "v_splats"):
+            out[k] = out[k][:nnz]
     return out
+
+
+def unpack(packed_rows, cam, gid, C, N):
+    """Scatter packed per-item rows back into the dense [C, N, ...] layout (zeros elsewhere)."""
+    dense = np.zeros((C, N) + packed_rows.shape[1:], packed_rows.dtype)
+    dense[cam, gid] = packed_rows
+    return dense
 
 
 def last_gid(gpu, N):

@@ -236,6 +236,17 @@ def test_rasterization_api_autograd():
         # same kernels, different fp32 atomic order only
         np.testing.assert_allclose(t.grad.cpu().numpy(), gpu[k], rtol=1e-4, atol=1e-5 * np.abs(gpu[k]).max())
     assert meta["means2d"].shape == (2, 1500, 2) and meta["radii"].dtype == torch.int32
+    # packed mode through the same API: bit-identical images (Q29), same gradients up to atomic order
+    tp = [t.detach().clone().requires_grad_(i < 5) for i, t in enumerate(ts)]
+    rgb_p, alpha_p, meta_p = rasterization(*tp, 200, 150, sh_degree=3, packed=True)
+    assert torch.equal(rgb_p, rgb) and torch.equal(alpha_p, alpha)
+    nnz = meta_p["camera_ids"].numel()
+    assert meta_p["means2d"].shape == (nnz, 2) and nnz == int((meta["radii"][..., 0] > 0).sum())
+    loss_p = (rgb_p * torch.from_numpy(v).to(dev)).sum() + (alpha_p[..., 0] * torch.from_numpy(va).to(dev)).sum()
+    loss_p.backward()
+    for t, q in zip(ts[:5], tp[:5]):
+        np.testing.assert_allclose(q.grad.cpu().numpy(), t.grad.cpu().numpy(), rtol=1e-4,
+                                   atol=1e-5 * np.abs(t.grad.cpu().numpy()).max())
 
 
 def test_absgrad():
@@ -278,6 +289,94 @@ def test_config2_full_scale_sampled():
     assert bad.sum() == 0, bad.sum()
     g = oracle.project_bwd(sc, p, b["v2d"], o)
     touched = (np.abs(b["v2d"]).sum(-1) > 0)[0]
+    for k in ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]:
+        badk, rel = U.check_grad3d(gpu[k], g[k], touched)
+        assert rel <= U.GRAD_RTOL, (k, rel)
+
+
+# ---- packed mode (Q29, BASELINE configs[4]) -------------------------------------------
+@pytest.mark.parametrize("name", ["tiny_sh3_ragged", "mip_small_aa", "rgb_direct"])
+def test_packed_parity(name):
+    """Packed items = the oracle's pack() of the visible set; records bit-identical to the
+    dense path's rows; keys bit-exact with packed values; images bit-identical to the dense
+    path (Q29); gradients against the oracle."""
+    sc, kw = _scene(name)
+    aa = kw.get("antialiased", 0)
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    v_img, _ = S.image_grads(4, C, H, W, l1_scale=False)
+    o = oracle.Options(sh_degree=sc["sh_degree"], antialiased=aa)
+    p = oracle.project(sc, o)
+    f = oracle.render_fwd(p, C, N, W, H, o)
+    v_img[f["ambig"].astype(bool)] = 0
+    dense = U.run_gpu(sc, antialiased=aa, v_img=v_img)
+    pk = U.run_gpu(sc, antialiased=aa, v_img=v_img, packed=True)
+    cam, gid, index = oracle.pack(p)
+    assert pk["nnz"] == cam.size
+    assert np.array_equal(pk["camera_ids"], cam) and np.array_equal(pk["gaussian_ids"], gid)
+    assert np.array_equal(pk["radii"], dense["radii"][cam, gid])
+    assert np.array_equal(pk["splats"], dense["splats"][cam, gid])
+    keys, ids, offs = oracle.isect(p, C, N, W, H, o)
+    assert np.array_equal(pk["keys"], keys), "tile keys must be bit-exact"
+    assert np.array_equal(pk["ids"], index.reshape(-1)[ids]), "sorted order (packed values) must be bit-exact"
+    assert np.array_equal(pk["offsets"], offs)
+    for k in ("rgb", "alpha", "T", "last_ids"):
+        assert np.array_equal(pk[k], dense[k]), f"packed {k} must be bit-identical to dense (Q29)"
+    b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64))
+    vs = U.unpack(pk["v_splats"], cam, gid, C, N)
+    vis = (p["radii"][..., 0] > 0)
+    bad = U.check_grad2d(U.v2d_from_splats(vs), b["v2d"], b["a2d"], vis, b["s2d"])
+    assert bad.sum() == 0, bad.sum()
+    g = oracle.project_bwd(sc, p, b["v2d"], o)
+    for k in ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]:
+        badk, rel = U.check_grad3d(pk[k], g[k], vis.any(axis=0))
+        assert rel <= U.GRAD_RTOL, (k, rel)
+        assert badk.sum() <= max(1, 1e-3 * badk.size), (k, badk.sum())
+
+
+def test_packed_capacity_growth():
+    """A too-small nnz capacity sets the device overflow flag; run_checked grows it and
+    re-runs to the same result."""
+    sc, _ = _scene("tiny_sh3_ragged")
+    a = U.run_gpu(sc, packed=True)
+    b = U.run_gpu(sc, packed=True, nnz_capacity=7, cap=16)
+    assert a["nnz"] == b["nnz"] > 7
+    assert np.array_equal(a["rgb"], b["rgb"]) and np.array_equal(a["ids"], b["ids"])
+
+
+@pytest.mark.slow
+def test_config5_aa_packed_full_scale_sampled():
+    """BASELINE configs[4] at full size (1M Gaussians, antialiased, packed, 4 views):
+    packed items, keys / order / ranges bit-exact over every view; images and masked-loss
+    gradients on 32 seeded tiles per view."""
+    sc = S.scene_from_config("aa_packed1m")
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    mask = S.tile_subset_mask(5, C, W, H, 32)
+    pm = np.repeat(np.repeat(mask, 16, 1), 16, 2)[:, :H, :W]
+    v_img, _ = S.image_grads(5, C, H, W, l1_scale=False)
+    v_img *= pm[..., None]
+    o = oracle.Options(sh_degree=3, antialiased=1)
+    p = oracle.project(sc, o)
+    f = oracle.render_fwd(p, C, N, W, H, o, tile_mask=mask)
+    v_img[f["ambig"].astype(bool)] = 0
+    gpu = U.run_gpu(sc, antialiased=True, v_img=v_img, packed=True)
+    cam, gid, index = oracle.pack(p)
+    assert np.array_equal(gpu["camera_ids"], cam) and np.array_equal(gpu["gaussian_ids"], gid)
+    assert np.array_equal(gpu["radii"], p["radii"][cam, gid])
+    assert np.array_equal(gpu["splats"][:, 0:2], p["mean2d_f"][cam, gid])
+    assert np.array_equal(gpu["splats"][:, 3], p["depth_f"][cam, gid])
+    keys, ids, offs = oracle.isect(p, C, N, W, H, o)
+    assert np.array_equal(gpu["keys"], keys) and np.array_equal(gpu["ids"], index.reshape(-1)[ids])
+    assert np.array_equal(gpu["offsets"], offs)
+    sel = pm.astype(bool) & ~f["ambig"].astype(bool)
+    assert np.abs(gpu["rgb"] - f["rgb"])[sel].max() <= U.IMG_ATOL
+    assert np.abs(gpu["T"] - f["T"])[sel].max() <= U.IMG_ATOL
+    b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64), tile_mask=mask)
+    vs = U.unpack(gpu["v_splats"], cam, gid, C, N)
+    vis = p["radii"][..., 0] > 0
+    bad = U.check_grad2d(U.v2d_from_splats(vs), b["v2d"], b["a2d"], vis, b["s2d"])
+    assert bad.sum() == 0, bad.sum()
+    g = oracle.project_bwd(sc, p, b["v2d"], o)
+    touched = (np.abs(b["v2d"]).sum(-1) > 0).any(0)
     for k in ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]:
         badk, rel = U.check_grad3d(gpu[k], g[k], touched)
         assert rel <= U.GRAD_RTOL, (k, rel)

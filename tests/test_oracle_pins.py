@@ -540,3 +540,31 @@ class TestBackward:
             tot = r1 if tot is None else {k: tot[k] + r1[k] for k in tot}
         for k in tot:
             assert np.allclose(tot[k], res["grads"][k], rtol=1e-12, atol=1e-15)
+
+
+class TestPacked:
+    """Q29: packed items are the visible (c,n) pairs, camera-major then by n."""
+
+    def test_pack_order_bruteforce(self, oracle_lib):
+        rng = np.random.default_rng(5)
+        C, N = 3, 50
+        radii = rng.integers(0, 3, size=(C, N, 2)).astype(np.int32)
+        cam, gid, index = oracle.pack(dict(radii=radii))
+        exp = [(c, n) for c in range(C) for n in range(N) if radii[c, n, 0] > 0 and radii[c, n, 1] > 0]
+        assert list(zip(cam.tolist(), gid.tolist())) == exp
+        for i, (c, n) in enumerate(exp):
+            assert index[c, n] == i
+        assert (index >= 0).sum() == len(exp)
+
+    def test_packed_keys_are_dense_keys(self, oracle_lib):
+        """Tile keys do not depend on the storage layout; the values re-index through
+        pack()'s map (SURVEY 8c 'Dense vs packed')."""
+        sc = S.tiny_scene(3, N=300, width=96, height=80, sh_degree=0, views=2)
+        o = oracle.Options(sh_degree=0)
+        p = oracle.project(sc, o)
+        C, N = 2, 300
+        keys, ids, offs = oracle.isect(p, C, N, 96, 80, o)
+        cam, gid, index = oracle.pack(p)
+        assert np.all(index.reshape(-1)[ids] >= 0)          # every intersected item is packed
+        packed_ids = index.reshape(-1)[ids]
+        assert np.array_equal(cam[packed_ids] * N + gid[packed_ids], ids)
