@@ -258,40 +258,72 @@ def test_absgrad():
     assert np.all(vs[..., 11] >= np.abs(vs[..., 1]) * (1 - 1e-5) - 1e-7)
 
 
-@pytest.mark.slow
-def test_config2_full_scale_sampled():
-    """BASELINE configs[1] at full size, in the launch configuration bench.py times:
-    key path and tile keys / order / ranges bit-exact over the whole frame; image and
-    masked-loss gradients on 32 seeded tiles (exact for that loss)."""
-    sc = S.scene_from_config("garden1m")
-    C, N, W, H = 1, sc["means"].shape[0], sc["width"], sc["height"]
-    mask = S.tile_subset_mask(0, C, W, H, 32)
+def _full_scale_sampled(cfg_name, views=None, n_tiles=32, seed=0, packed=False, antialiased=False):
+    """A BASELINE config at full size, in the launch configuration bench.py times (one GPU,
+    all of that GPU's views in one call): key path, tile keys / order / ranges bit-exact over
+    every view; images and the gradients of a masked loss on n_tiles seeded tiles per view
+    (exact for that loss, SURVEY 8c 'cheap parity for large configs')."""
+    sc = S.scene_from_config(cfg_name, views=views)
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    mask = S.tile_subset_mask(seed, C, W, H, n_tiles)
     pm = np.repeat(np.repeat(mask, 16, 1), 16, 2)[:, :H, :W]
-    v_img, _ = S.image_grads(0, C, H, W, l1_scale=False)
+    v_img, _ = S.image_grads(seed, C, H, W, l1_scale=False)
     v_img *= pm[..., None]
-    o = oracle.Options(sh_degree=3)
+    o = oracle.Options(sh_degree=sc["sh_degree"], antialiased=int(antialiased))
     p = oracle.project(sc, o)
     f = oracle.render_fwd(p, C, N, W, H, o, tile_mask=mask)
     v_img[f["ambig"].astype(bool)] = 0
-    gpu = U.run_gpu(sc, v_img=v_img)
-    assert np.array_equal(gpu["radii"], p["radii"])
-    vis = p["radii"][..., 0] > 0
-    assert np.array_equal(gpu["splats"][..., 0:2][vis], p["mean2d_f"][vis])
-    assert np.array_equal(gpu["splats"][..., 3][vis], p["depth_f"][vis])
+    gpu = U.run_gpu(sc, antialiased=antialiased, v_img=v_img, packed=packed)
+    vis = (p["radii"][..., 0] > 0) & (p["radii"][..., 1] > 0)
     keys, ids, offs = oracle.isect(p, C, N, W, H, o)
-    assert np.array_equal(gpu["keys"], keys) and np.array_equal(gpu["ids"], ids)
+    if packed:
+        cam, gid, index = oracle.pack(p)
+        assert np.array_equal(gpu["camera_ids"], cam) and np.array_equal(gpu["gaussian_ids"], gid)
+        assert np.array_equal(gpu["radii"], p["radii"][cam, gid])
+        assert np.array_equal(gpu["splats"][:, 0:2], p["mean2d_f"][cam, gid])
+        assert np.array_equal(gpu["splats"][:, 3], p["depth_f"][cam, gid])
+        assert np.array_equal(gpu["ids"], index.reshape(-1)[ids])
+        vs = U.unpack(gpu["v_splats"], cam, gid, C, N)
+    else:
+        assert np.array_equal(gpu["radii"], p["radii"])
+        assert np.array_equal(gpu["splats"][..., 0:2][vis], p["mean2d_f"][vis])
+        assert np.array_equal(gpu["splats"][..., 3][vis], p["depth_f"][vis])
+        assert np.array_equal(gpu["ids"], ids)
+        vs = gpu["v_splats"]
+    assert np.array_equal(gpu["keys"], keys)
     assert np.array_equal(gpu["offsets"], offs)
     sel = pm.astype(bool) & ~f["ambig"].astype(bool)
     assert np.abs(gpu["rgb"] - f["rgb"])[sel].max() <= U.IMG_ATOL
     assert np.abs(gpu["T"] - f["T"])[sel].max() <= U.IMG_ATOL
     b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64), tile_mask=mask)
-    bad = U.check_grad2d(U.v2d_from_splats(gpu["v_splats"]), b["v2d"], b["a2d"], vis, b["s2d"])
+    bad = U.check_grad2d(U.v2d_from_splats(vs), b["v2d"], b["a2d"], vis, b["s2d"])
     assert bad.sum() == 0, bad.sum()
     g = oracle.project_bwd(sc, p, b["v2d"], o)
-    touched = (np.abs(b["v2d"]).sum(-1) > 0)[0]
+    touched = (np.abs(b["v2d"]).sum(-1) > 0).any(0)
     for k in ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]:
         badk, rel = U.check_grad3d(gpu[k], g[k], touched)
         assert rel <= U.GRAD_RTOL, (k, rel)
+    return len(keys)
+
+
+@pytest.mark.slow
+def test_config2_full_scale_sampled():
+    """BASELINE configs[1]: 1M Gaussians, SH3, one 1297x840 view (the bench workload)."""
+    _full_scale_sampled("garden1m")
+
+
+@pytest.mark.slow
+def test_config3_batch_full_scale_sampled():
+    """BASELINE configs[2]: 3M Gaussians, 8 views of 1297x840 in one call (the N=1 shard of
+    the 1/2/4/8-GPU view-parallel run)."""
+    _full_scale_sampled("batch3m", n_tiles=16, seed=3)
+
+
+@pytest.mark.slow
+def test_config4_large_shard_full_scale_sampled():
+    """BASELINE configs[3]: 6M Gaussians, SH3, 1920x1080 -- one GPU's shard of the 32-view,
+    8-GPU step (4 views in one call)."""
+    _full_scale_sampled("large6m", views=4, n_tiles=16, seed=4)
 
 
 # ---- packed mode (Q29, BASELINE configs[4]) -------------------------------------------
@@ -345,38 +377,5 @@ def test_packed_capacity_growth():
 
 @pytest.mark.slow
 def test_config5_aa_packed_full_scale_sampled():
-    """BASELINE configs[4] at full size (1M Gaussians, antialiased, packed, 4 views):
-    packed items, keys / order / ranges bit-exact over every view; images and masked-loss
-    gradients on 32 seeded tiles per view."""
-    sc = S.scene_from_config("aa_packed1m")
-    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
-    mask = S.tile_subset_mask(5, C, W, H, 32)
-    pm = np.repeat(np.repeat(mask, 16, 1), 16, 2)[:, :H, :W]
-    v_img, _ = S.image_grads(5, C, H, W, l1_scale=False)
-    v_img *= pm[..., None]
-    o = oracle.Options(sh_degree=3, antialiased=1)
-    p = oracle.project(sc, o)
-    f = oracle.render_fwd(p, C, N, W, H, o, tile_mask=mask)
-    v_img[f["ambig"].astype(bool)] = 0
-    gpu = U.run_gpu(sc, antialiased=True, v_img=v_img, packed=True)
-    cam, gid, index = oracle.pack(p)
-    assert np.array_equal(gpu["camera_ids"], cam) and np.array_equal(gpu["gaussian_ids"], gid)
-    assert np.array_equal(gpu["radii"], p["radii"][cam, gid])
-    assert np.array_equal(gpu["splats"][:, 0:2], p["mean2d_f"][cam, gid])
-    assert np.array_equal(gpu["splats"][:, 3], p["depth_f"][cam, gid])
-    keys, ids, offs = oracle.isect(p, C, N, W, H, o)
-    assert np.array_equal(gpu["keys"], keys) and np.array_equal(gpu["ids"], index.reshape(-1)[ids])
-    assert np.array_equal(gpu["offsets"], offs)
-    sel = pm.astype(bool) & ~f["ambig"].astype(bool)
-    assert np.abs(gpu["rgb"] - f["rgb"])[sel].max() <= U.IMG_ATOL
-    assert np.abs(gpu["T"] - f["T"])[sel].max() <= U.IMG_ATOL
-    b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64), tile_mask=mask)
-    vs = U.unpack(gpu["v_splats"], cam, gid, C, N)
-    vis = p["radii"][..., 0] > 0
-    bad = U.check_grad2d(U.v2d_from_splats(vs), b["v2d"], b["a2d"], vis, b["s2d"])
-    assert bad.sum() == 0, bad.sum()
-    g = oracle.project_bwd(sc, p, b["v2d"], o)
-    touched = (np.abs(b["v2d"]).sum(-1) > 0).any(0)
-    for k in ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]:
-        badk, rel = U.check_grad3d(gpu[k], g[k], touched)
-        assert rel <= U.GRAD_RTOL, (k, rel)
+    """BASELINE configs[4]: 1M Gaussians, antialiased, packed, 4 views of 1297x840."""
+    _full_scale_sampled("aa_packed1m", seed=5, packed=True, antialiased=True)
