@@ -78,9 +78,9 @@ def lib():
         _lib.or_project.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32, P, P] + [P] * 10
         _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
         _lib.or_isect.restype = i64
-        _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6
-        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7
-        _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6
+        _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6 + [P] * 2
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 5
+        _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6 + [P] * 2
         _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_quat_to_rotmat.argtypes = [P, P]
@@ -169,42 +169,71 @@ def isect(proj, C, N, W, H, opts: Options):
     return keys[:M], ids[:M], offs
 
 
+def _depth64(proj):
+    """fp64 depth t_z of every (c,n) (hand-built projections may give only the fp32 one)."""
+    return _f64(proj["depth"] if "depth" in proj else proj["depth_f"])
+
+
 def render_fwd(proj, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None):
+    """R1-R3 per pixel.  Also returns the accumulated depth sum z alpha T ("depth")
+    and the expected depth ("depth_exp" = that sum / sum alpha T, with
+    sum alpha T = 1 - T_final; 0 where nothing composited)."""
     o = opts.c()
     bg = None if backgrounds is None else _f64(backgrounds)
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
     out = dict(rgb=np.zeros((C, H, W, 3)), alpha=np.zeros((C, H, W)), T=np.zeros((C, H, W)),
                last_gid=np.zeros((C, H, W), np.int64), ambig=np.zeros((C, H, W), np.uint8),
-               ncontrib=np.zeros((C, H, W), np.int32))
+               ncontrib=np.zeros((C, H, W), np.int32), depth=np.zeros((C, H, W)))
     lib().or_render_fwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(out["rgb"]), _p(out["alpha"]), _p(out["T"]), _p(out["last_gid"]),
-                        _p(out["ambig"]), _p(out["ncontrib"]))
+                        _p(out["ambig"]), _p(out["ncontrib"]), _p(_depth64(proj)), _p(out["depth"]))
+    A = 1.0 - out["T"]
+    out["depth_exp"] = np.where(A > 0, out["depth"] / np.where(A > 0, A, 1.0), 0.0)
     return out
 
 
-def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds=None, tile_mask=None):
+def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds=None, tile_mask=None,
+               v_depth=None, v_depth_exp=None):
     """B1-B6.  Returns v2d [C,N,9] (v_mean2d 2, v_conic 3, v_rgb 3, v_opac_eff 1), and for the
     parity tolerance (not part of the result): a2d, the sum over pixels of |per-pixel term|
     with B4's v_alpha replaced by the magnitudes of its parts (fp32 cancellation floor),
     s2d, the first-order change of each gradient for a 1-ulp shift of the fp32 projected
-    means the kernel works with, g_ambig and the T-replay error."""
+    means the kernel works with, g_ambig and the T-replay error.
+    Depth rendering: v_depth = dL/d(accumulated depth) [C,H,W] and/or
+    v_depth_exp = dL/d(expected depth); the expected depth D/A (A = 1 - T_final = sum alpha T)
+    enters by the quotient rule, dL/dD += v_exp / A and dL/dA += -v_exp D / A^2 (the alpha
+    output's gradient, Q26).  vz [C,N] = dL/d(depth of each (c,n)) (+ az, sz floors)."""
     o = opts.c()
     bg = None if backgrounds is None else _f64(backgrounds)
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
     v_img = _f64(v_img)
     va = None if v_alpha is None else _f64(v_alpha)
+    vD = None if v_depth is None else _f64(v_depth).copy()
+    if v_depth_exp is not None:
+        f = render_fwd(proj, C, N, W, H, opts, backgrounds, tile_mask)
+        A = 1.0 - f["T"]
+        ok = A > 0
+        Ar = np.where(ok, A, 1.0)
+        ve = _f64(v_depth_exp)
+        vD = (np.zeros((C, H, W)) if vD is None else vD) + np.where(ok, ve / Ar, 0.0)
+        va = (np.zeros((C, H, W)) if va is None else va.copy()) + np.where(ok, -ve * f["depth"] / (Ar * Ar), 0.0)
     v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9))
+    vz = np.zeros((C, N)); az = np.zeros((C, N)); sz = np.zeros((C, N))
     amb = np.zeros((C, N), np.uint8)
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
-                        _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err))
-    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value)
+                        _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
+                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz))
+    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vz=vz, az=az, sz=sz)
 
 
-def project_bwd(scene, proj, v2d, opts: Options):
-    """P1-P9, summed over cameras.  Returns v_means, v_quats, v_scales, v_opacities, v_colors (f64)."""
+def project_bwd(scene, proj, v2d, opts: Options, vz=None, pose=False):
+    """P1-P9, summed over cameras.  Returns v_means, v_quats, v_scales, v_opacities, v_colors
+    (f64); vz [C,N] = dL/d depth (depth rendering) enters through t_z; pose=True also
+    returns v_viewmats [C,4,4] (App. pose optimisation: the t, the
+    Sigma_c = W Sigma W^T and the SH view-direction campos = -W^T w paths)."""
     means, quats, scales, opac, colors, viewmats, Ks = _scene_arrays(scene)
     N, C = means.shape[0], viewmats.shape[0]
     W, H = int(scene["width"]), int(scene["height"])
@@ -212,9 +241,12 @@ def project_bwd(scene, proj, v2d, opts: Options):
     o = opts.c()
     out = dict(v_means=np.zeros((N, 3)), v_quats=np.zeros((N, 4)), v_scales=np.zeros((N, 3)),
                v_opacities=np.zeros(N), v_colors=np.zeros(colors.shape))
+    if pose:
+        out["v_viewmats"] = np.zeros((C, 4, 4))
     lib().or_project_bwd(ct.byref(o), N, C, W, H, _p(means), _p(quats), _p(scales), _p(opac), _p(colors), K,
                          _p(viewmats), _p(Ks), _p(proj["radii"]), _p(_f64(v2d)), _p(out["v_means"]),
-                         _p(out["v_quats"]), _p(out["v_scales"]), _p(out["v_opacities"]), _p(out["v_colors"]))
+                         _p(out["v_quats"]), _p(out["v_scales"]), _p(out["v_opacities"]), _p(out["v_colors"]),
+                         _p(None if vz is None else _f64(vz)), _p(out.get("v_viewmats")))
     return out
 
 

@@ -588,6 +588,7 @@ typedef struct {
 typedef struct {
     double eT;       /* sum over composited splats of alpha qd / (1 - alpha) (tolerance model) */
     double rgb[3], T;
+    double dacc;      /* accumulated depth sum z alpha T (App. depth rendering) */
     int64_t last_li;  /* -1 if none */
     int64_t end_li;   /* exclusive end of the evaluated part of the list */
     int ambig;
@@ -615,10 +616,10 @@ static double decision_raw(const float *dec4, const float *m2f, int px, int py)
 
 static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, int64_t N, int px, int py,
                               const float *mean2d_f, const float *dec, const double *mean2d,
-                              const double *conic, const double *opac_eff, const double *rgb, contrib_t *rec,
-                              int64_t rec_cap)
+                              const double *conic, const double *opac_eff, const double *rgb,
+                              const double *depth, contrib_t *rec, int64_t rec_cap)
 {
-    pixres_t r = {0.0, {0, 0, 0}, 1.0, -1, L->count, 0, 0};
+    pixres_t r = {0.0, {0, 0, 0}, 1.0, 0.0, -1, L->count, 0, 0};
     int tx = px / o->tile_size, ty = py / o->tile_size;
     double p[2] = {px + 0.5, py + 0.5};            /* R1: pixel centre */
     const double amax = (float)o->alpha_max, amin = (float)o->alpha_min, tmin = (float)o->t_min;
@@ -655,6 +656,7 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
         }
         r.eT += alpha * qd / (1.0 - alpha);
         for (int ch = 0; ch < 3; ch++) r.rgb[ch] += rgb[3 * g + ch] * alpha * T;   /* P:536-538 */
+        if (depth) r.dacc += depth[g] * alpha * T;                                 /* P:250 */
         T = T * (1.0 - alpha);
         Tdec = nT_d;
         r.last_li = i;
@@ -677,7 +679,7 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                   const double *conic,
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   double *out_rgb, double *out_alpha, double *out_T, int64_t *out_last_gid,
-                  uint8_t *out_ambig, int32_t *out_ncontrib)
+                  uint8_t *out_ambig, int32_t *out_ncontrib, const double *depth, double *out_depth)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
     for (int64_t c = 0; c < C; c++) {
@@ -691,12 +693,15 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
             if (!tile_selected(tile_mask, c, TX, TY, px, py, T)) {
                 for (int ch = 0; ch < 3; ch++) out_rgb[3 * oi + ch] = b ? b[ch] : 0.0;
                 out_alpha[oi] = 0; out_T[oi] = 1; out_last_gid[oi] = -1;
+                if (out_depth) out_depth[oi] = 0;
                 if (out_ambig) out_ambig[oi] = 0;
                 if (out_ncontrib) out_ncontrib[oi] = 0;
                 continue;
             }
-            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL, 0);
+            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, depth,
+                                       NULL, 0);
             for (int ch = 0; ch < 3; ch++) out_rgb[3 * oi + ch] = r.rgb[ch] + r.T * (b ? b[ch] : 0.0);  /* R3, Q25 */
+            if (out_depth) out_depth[oi] = r.dacc;                                 /* no background term */
             out_alpha[oi] = 1.0 - r.T;
             out_T[oi] = r.T;
             out_last_gid[oi] = r.last_li >= 0 ? c * N + L.n[r.last_li] : -1;
@@ -720,20 +725,25 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
 /* g_ambig[g] = 1 if g was evaluated at an ambiguous pixel.                     */
 /* T_replay_err (optional) = max |T_replayed - T_forward| over all steps.      */
 /* ------------------------------------------------------------------------- */
-typedef struct { int32_t g; double v[9], va[9], vs[9]; } term_t;
+typedef struct { int32_t g; double v[10], va[10], vs[10]; } term_t;   /* [9]: v_depth */
 
 int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
                   const float *mean2d_f, const float *depth_f, const float *dec, const double *mean2d,
                   const double *conic,
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   const double *v_img, const double *v_alpha_img, double *v2d, double *a2d, double *s2d,
-                  uint8_t *g_ambig, double *T_replay_err)
+                  uint8_t *g_ambig, double *T_replay_err, const double *depth, const double *v_depth_img,
+                  double *vz, double *az, double *sz)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
     memset(v2d, 0, sizeof(double) * 9 * C * N);
     if (a2d) memset(a2d, 0, sizeof(double) * 9 * C * N);
     if (s2d) memset(s2d, 0, sizeof(double) * 9 * C * N);
     if (g_ambig) memset(g_ambig, 0, (size_t)C * N);
+    if (vz) memset(vz, 0, sizeof(double) * C * N);
+    if (az) memset(az, 0, sizeof(double) * C * N);
+    if (sz) memset(sz, 0, sizeof(double) * C * N);
+    const int with_depth = depth && v_depth_img;
     double max_err = 0;
     for (int64_t c = 0; c < C; c++) {
         camlist_t L;
@@ -745,7 +755,8 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
         for (int64_t pix = 0; pix < P; pix++) {
             int px = (int)(pix % W), py = (int)(pix / W);
             if (!tile_selected(tile_mask, c, TX, TY, px, py, T)) continue;
-            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL, 0);
+            pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL,
+                                       NULL, 0);
             cnt[pix] = (int32_t)r.ncontrib;
             if (r.ambig && g_ambig) {
                 /* mark every splat this pixel evaluated (in-tile, up to termination) */
@@ -778,15 +789,17 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     cap = cnt[pix];
                     rec = (contrib_t *)realloc(rec, sizeof(contrib_t) * cap);
                 }
-                pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, rec, cap);
+                pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL,
+                                           rec, cap);
                 int64_t oi = c * P + pix;
                 const double *vC = &v_img[3 * oi];
                 double vA = v_alpha_img ? v_alpha_img[oi] : 0.0;
                 const double *b = bg ? bg + 3 * c : NULL;
                 double bgdot = b ? (b[0] * vC[0] + b[1] * vC[1] + b[2] * vC[2]) : 0.0;
                 double Tfin = r.T;
+                double vD = with_depth ? v_depth_img[oi] : 0.0;   /* d L / d (accumulated depth) */
                 double Tn = Tfin;                /* B1 */
-                double S[3] = {0, 0, 0};
+                double S[3] = {0, 0, 0}, Sd = 0;  /* Sd: the depth channel's S */
                 double err = 0;
                 for (int64_t k = r.ncontrib - 1; k >= 0; k--) {
                     const contrib_t *e = &rec[k];
@@ -801,16 +814,22 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     tm->g = (int32_t)g;
                     for (int ch = 0; ch < 3; ch++) tm->v[5 + ch] = fac * vC[ch];   /* B3 */
                     for (int ch = 0; ch < 3; ch++) tm->va[5 + ch] = fabs(tm->v[5 + ch]);
+                    double z = with_depth ? depth[g] : 0.0;
+                    tm->v[9] = fac * vD;                                           /* depth as a channel: B3 */
+                    tm->va[9] = fabs(tm->v[9]);
                     double v_alpha = 0;                                            /* B4 */
                     for (int ch = 0; ch < 3; ch++) v_alpha += (rgb[3 * g + ch] * Tn - S[ch] * ra) * vC[ch];
+                    v_alpha += (z * Tn - Sd * ra) * vD;                            /* depth channel */
                     v_alpha += -Tfin * ra * bgdot + Tfin * ra * vA;
                     /* magnitude of B4 before its internal cancellation (c T vs S/(1-alpha)):
                      * the condition floor a2d of the v_alpha-dependent gradients uses it */
                     double v_alpha_abs = fabs(Tfin * ra * bgdot) + fabs(Tfin * ra * vA);
                     for (int ch = 0; ch < 3; ch++)
                         v_alpha_abs += fabs(rgb[3 * g + ch] * Tn * vC[ch]) + fabs(S[ch] * ra * vC[ch]);
+                    v_alpha_abs += fabs(z * Tn * vD) + fabs(Sd * ra * vD);
 
                     for (int ch = 0; ch < 3; ch++) S[ch] += rgb[3 * g + ch] * fac;  /* B5 */
+                    Sd += z * fac;
                     if (!e->clamped) {                                           /* B6 (Q24) */
                         tm->v[8] = e->G * v_alpha;
                         double v_sigma = -opac_eff[g] * e->G * v_alpha;
@@ -840,8 +859,8 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                         tm->vs[0] = tm->vs[1] = tm->vs[2] = tm->vs[3] = tm->vs[4] = 0;
                     }
                     /* ... and through alpha (this splat's qd, all splats' via T and S) */
-                    for (int j = 0; j < 9; j++) {
-                        if (j >= 5) tm->vs[j] = 0;   /* rgb and opacity: only the alpha path */
+                    for (int j = 0; j < 10; j++) {
+                        if (j >= 5) tm->vs[j] = 0;   /* rgb, opacity, depth: only the alpha path */
                         tm->vs[j] += tm->va[j] * (e->qd + r.eT);
                     }
                 }
@@ -857,6 +876,9 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 if (a2d) a2d[9 * (int64_t)g + j] += terms[i].va[j];
                 if (s2d) s2d[9 * (int64_t)g + j] += terms[i].vs[j];
             }
+            if (vz) vz[g] += terms[i].v[9];
+            if (az) az[g] += terms[i].va[9];
+            if (sz) sz[g] += terms[i].vs[9];
         }
         for (int64_t pix = 0; pix < P; pix++)
             if (errs[pix] > max_err) max_err = errs[pix];
@@ -876,11 +898,23 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
 int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H, const float *means,
                    const float *quats, const float *scales, const float *opacities, const float *colors,
                    int32_t K, const float *viewmats, const float *Ks, const int32_t *radii, const double *v2d,
-                   double *v_means, double *v_quats, double *v_scales, double *v_opac, double *v_colors)
+                   double *v_means, double *v_quats, double *v_scales, double *v_opac, double *v_colors,
+                   const double *vz, double *v_viewmats)
 {
     int64_t stride = o->sh_degree >= 0 ? (int64_t)K * 3 : 3;
+    /* pose gradients (App. pose optimisation): per-thread partial sums
+     * over Gaussians, summed in thread order after the loop */
+    int nthr = 1;
+#ifdef _OPENMP
+    nthr = omp_get_max_threads();
+#endif
+    double *vpart = v_viewmats ? (double *)calloc((size_t)nthr * C * 16, sizeof(double)) : NULL;
 #pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < N; n++) {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
         double gm[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gs[3] = {0, 0, 0}, go = 0;
         double *gc = &v_colors[stride * n];
         for (int64_t j = 0; j < stride; j++) gc[j] = 0;
@@ -947,6 +981,23 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
             vt[0] += fx / tz * vg[0];
             vt[1] += fy / tz * vg[1];
             vt[2] += -(fx * tx / tz2) * vg[0] - (fy * ty / tz2) * vg[1];
+            if (vz) vt[2] += vz[idx];                  /* depth = t_z (F4; depth rendering P:250) */
+            double *vW = vpart ? vpart + ((size_t)tid * C + c) * 16 : NULL;
+            if (vW) {
+                /* t = W mu + w: dL/dW += v_t mu^T, dL/dw += v_t */
+                for (int i = 0; i < 3; i++) {
+                    for (int j = 0; j < 3; j++) vW[4 * i + j] += vt[i] * P.mu[j];
+                    vW[4 * i + 3] += vt[i];
+                }
+                /* Sigma_c = W Sigma W^T (Fig. P:423): dL/dW += (vSc + vSc^T) W Sigma */
+                for (int i = 0; i < 3; i++)
+                    for (int j = 0; j < 3; j++) {
+                        double acc = 0;
+                        for (int k = 0; k < 3; k++)
+                            for (int l = 0; l < 3; l++) acc += (vSc[i][k] + vSc[k][i]) * P.Wr[k][l] * P.Sig[l][j];
+                        vW[4 * i + j] += acc;
+                    }
+            }
             /* P6: v_mu += W^T v_t, v_Sigma = W^T v_Sc W */
             for (int i = 0; i < 3; i++)
                 for (int k = 0; k < 3; k++) gm[i] += P.Wr[k][i] * vt[k];
@@ -978,7 +1029,17 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
                 }
                 /* dir = e/|e|, d dir/d mu = (I - dir dir^T)/|e| */
                 double dd = P.dir[0] * vdir[0] + P.dir[1] * vdir[1] + P.dir[2] * vdir[2];
-                for (int i = 0; i < 3; i++) gm[i] += (vdir[i] - P.dir[i] * dd) / P.enorm;
+                double ve[3];
+                for (int i = 0; i < 3; i++) ve[i] = (vdir[i] - P.dir[i] * dd) / P.enorm;
+                for (int i = 0; i < 3; i++) gm[i] += ve[i];
+                /* e = mu - campos, campos = -W^T w: dL/dW_ki += ve_i w_k, dL/dw_k += (W ve)_k */
+                double *vW = vpart ? vpart + ((size_t)tid * C + c) * 16 : NULL;
+                if (vW)
+                    for (int k = 0; k < 3; k++)
+                        for (int i = 0; i < 3; i++) {
+                            vW[4 * k + i] += ve[i] * P.w[k];
+                            vW[4 * k + 3] += P.Wr[k][i] * ve[i];
+                        }
             } else {
                 for (int ch = 0; ch < 3; ch++) gc[ch] += vrgb[ch];
             }
@@ -1018,6 +1079,12 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
         for (int i = 0; i < 3; i++) v_means[3 * n + i] = gm[i], v_scales[3 * n + i] = gs[i];
         for (int i = 0; i < 4; i++) v_quats[4 * n + i] = gq[i];
         v_opac[n] = go;
+    }
+    if (v_viewmats) {
+        memset(v_viewmats, 0, sizeof(double) * 16 * C);
+        for (int t = 0; t < nthr; t++)
+            for (int64_t k = 0; k < 16 * (int64_t)C; k++) v_viewmats[k] += vpart[(size_t)t * C * 16 + k];
+        free(vpart);
     }
     return 0;
 }

@@ -414,12 +414,17 @@ def _clean_scene(seed, N=24, W=32, H=32, sh_degree=1, views=1, antialiased=0, ma
     raise RuntimeError("no clean scene")
 
 
-def _loss(sc, o, v_img, v_a, bg=None):
+def _loss(sc, o, v_img, v_a, bg=None, v_d=None, v_e=None):
     C, N = sc["viewmats"].shape[0], sc["means"].shape[0]
     p = oracle.project(sc, o)
     r = oracle.render_fwd(p, C, N, sc["width"], sc["height"], o, backgrounds=bg)
     _, ids, offs = oracle.isect(p, C, N, sc["width"], sc["height"], o)
-    return float((r["rgb"] * v_img).sum() + (r["alpha"] * v_a).sum()), (ids, offs)
+    l = float((r["rgb"] * v_img).sum() + (r["alpha"] * v_a).sum())
+    if v_d is not None:
+        l += float((r["depth"] * v_d).sum())
+    if v_e is not None:
+        l += float((r["depth_exp"] * v_e).sum())
+    return l, (ids, offs)
 
 
 class TestBackward:
@@ -568,3 +573,120 @@ class TestPacked:
         assert np.all(index.reshape(-1)[ids] >= 0)          # every intersected item is packed
         packed_ids = index.reshape(-1)[ids]
         assert np.array_equal(cam[packed_ids] * N + gid[packed_ids], ids)
+
+
+
+# --------------------------------------------------------------------------- depth rendering, pose gradients
+class TestDepthAndPose:
+    """NEXT-2 (accumulated / expected depth) and NEXT-3 (camera pose gradients,
+    P:233-239) in the oracle: closed forms and central finite differences."""
+
+    def test_depth_closed_forms(self, oracle_lib):
+        o = oracle.Options()
+        # one splat: alpha at the centre = o_eff; expected depth = its depth for any alpha
+        p = _splat2d([[5.5, 5.5]], [[1, 0, 1]], [0.3], [[0.3, 0.4, 0.5]], [2.5], [[3, 3]])
+        r = oracle.render_fwd(p, 1, 1, 16, 16, o)
+        assert r["depth"][0, 5, 5] == pytest.approx(0.3 * 2.5, rel=1e-7)
+        assert r["depth_exp"][0, 5, 5] == pytest.approx(2.5, rel=1e-6)
+        assert r["depth"][0, 0, 0] == 0 and r["depth_exp"][0, 0, 0] == 0   # nothing composited
+        # two splats, alpha 0.5 each, depths 1 then 2: acc = 0.5*1 + 0.25*2, exp = acc / 0.75
+        p = _splat2d([[5.5, 5.5], [5.5, 5.5]], [[1, 0, 1], [1, 0, 1]], [0.5, 0.5], [[1, 0, 0], [0, 1, 0]],
+                     [1.0, 2.0], [[3, 3], [3, 3]])
+        r = oracle.render_fwd(p, 1, 2, 16, 16, o)
+        assert r["depth"][0, 5, 5] == pytest.approx(1.0, rel=1e-7)
+        assert r["depth_exp"][0, 5, 5] == pytest.approx(1.0 / 0.75, rel=1e-7)
+
+    @pytest.mark.parametrize("seed", [0, 1])
+    def test_depth_render_bwd_matches_fd(self, oracle_lib, seed):
+        """dL/d(mean2d, conic, opac_eff, depth) for L = <v_C, C> + <v_D, D_acc> + <v_E, D_exp>
+        equals central FD of the f64 render."""
+        sc, o = _clean_scene(seed + 40, sh_degree=0)
+        C, N, W, H = 1, sc["means"].shape[0], sc["width"], sc["height"]
+        p = oracle.project(sc, o)
+        rng = np.random.default_rng(seed)
+        v_img = rng.normal(size=(C, H, W, 3)); v_d = rng.normal(size=(C, H, W)); v_e = rng.normal(size=(C, H, W))
+        b = oracle.render_bwd(p, C, N, W, H, o, v_img, v_depth=v_d, v_depth_exp=v_e)
+
+        def L(pp):
+            r = oracle.render_fwd(pp, C, N, W, H, o)
+            return (r["rgb"] * v_img).sum() + (r["depth"] * v_d).sum() + (r["depth_exp"] * v_e).sum()
+        fields = [("mean2d", 0, 2), ("conic", 2, 3), ("opac_eff", 8, 1), ("depth", None, 1)]
+        checked = 0
+        for n in np.nonzero(p["radii"][0, :, 0] > 0)[0]:
+            for name, off, k in fields:
+                for j in range(k):
+                    h = 1e-6
+                    pp = {kk: vv.copy() for kk, vv in p.items()}
+                    arr = pp[name].reshape(C, N, -1)
+                    arr[0, n, j] += h; lp = L(pp)
+                    arr[0, n, j] -= 2 * h; lm = L(pp)
+                    fd = (lp - lm) / (2 * h)
+                    an = b["vz"][0, n] if off is None else b["v2d"][0, n, off + j]
+                    assert abs(an - fd) <= 1e-5 * abs(fd) + 1e-6, (name, n, j, an, fd)
+                    checked += 1
+        assert checked > 40
+
+    @pytest.mark.parametrize("seed,sh", [(0, 0), (1, 3)])
+    def test_depth_full_chain_and_pose_match_fd(self, oracle_lib, seed, sh):
+        """Through the projection: dL/d means (incl. the depth = t_z path) and dL/d viewmats
+        (t, Sigma_c and SH view-direction paths) equal central FD over the f32 inputs."""
+        sc, o = _clean_scene(seed + 60, sh_degree=sh, views=2)
+        C, N, W, H = 2, sc["means"].shape[0], sc["width"], sc["height"]
+        rng = np.random.default_rng(seed)
+        v_img = rng.normal(size=(C, H, W, 3)); v_a = rng.normal(size=(C, H, W))
+        v_d = rng.normal(size=(C, H, W)); v_e = rng.normal(size=(C, H, W))
+        p = oracle.project(sc, o)
+        _, ids0, offs0 = oracle.isect(p, C, N, W, H, o)
+        b = oracle.render_bwd(p, C, N, W, H, o, v_img, v_a, v_depth=v_d, v_depth_exp=v_e)
+        g = oracle.project_bwd(sc, p, b["v2d"], o, vz=b["vz"], pose=True)
+
+        def fd_of(name, idx):
+            x0 = sc[name].reshape(-1)[idx]
+            h = np.float32(1e-6 * max(1.0, abs(float(x0))))
+            vals, steps = [], []
+            for sgn in (+1, -1):
+                sc2 = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in sc.items()}
+                arr = sc2[name].reshape(-1)
+                arr[idx] = np.float32(x0 + sgn * h)
+                steps.append(float(arr[idx]) - float(x0))
+                l, (ids1, offs1) = _loss(sc2, o, v_img, v_a, v_d=v_d, v_e=v_e)
+                if not (np.array_equal(ids1, ids0) and np.array_equal(offs1, offs0)):
+                    return None
+                vals.append(l)
+            return (vals[0] - vals[1]) / (steps[0] - steps[1])
+        checked = 0
+        vis = np.nonzero((p["radii"][..., 0] > 0).any(axis=0))[0][:8]
+        for n in vis:
+            for j in range(3):
+                fd = fd_of("means", 3 * n + j)
+                if fd is None:
+                    continue
+                an = g["v_means"][n, j]
+                assert abs(an - fd) <= 2e-4 * abs(fd) + 1e-6, ("means", n, j, an, fd)
+                checked += 1
+        for c in range(C):
+            for i in range(3):
+                for j in range(4):
+                    fd = fd_of("viewmats", 16 * c + 4 * i + j)
+                    if fd is None:
+                        continue
+                    an = g["v_viewmats"][c, i, j]
+                    assert abs(an - fd) <= 2e-4 * abs(fd) + 1e-5 * (1 + abs(an)), ("viewmat", c, i, j, an, fd)
+                    checked += 1
+            assert np.all(g["v_viewmats"][c, 3] == 0)
+        assert checked > 30, checked
+
+    def test_pose_translation_identity(self, oracle_lib):
+        """A.2: dL/dt (camera translation) = sum_n dL/d(camera-space mean) when the
+        view direction does not enter (direct colours) and Sigma_c does not depend on w."""
+        sc, o = _clean_scene(77, sh_degree=0, views=1)
+        C, N, W, H = 1, sc["means"].shape[0], sc["width"], sc["height"]
+        rng = np.random.default_rng(1)
+        v_img = rng.normal(size=(C, H, W, 3))
+        p = oracle.project(sc, o)
+        b = oracle.render_bwd(p, C, N, W, H, o, v_img)
+        g = oracle.project_bwd(sc, p, b["v2d"], o, pose=True)
+        # with W = the view rotation, dL/dw = sum_n v_t(n) and dL/dmu_n = W^T v_t(n) (SH0: no
+        # direction dependence), so dL/dw = W (sum_n dL/dmu_n)
+        Wr = sc["viewmats"][0, :3, :3].astype(np.float64)
+        np.testing.assert_allclose(g["v_viewmats"][0, :3, 3], Wr @ g["v_means"].sum(0), rtol=1e-9, atol=1e-12)
