@@ -100,7 +100,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 2
+#define GS_ABI_VERSION 3
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -145,11 +145,15 @@ GS_API gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int
  * In : splats, isect_ids, tile_offsets; backgrounds [C,3] or NULL (black).
  * Out: out_rgb [C,H,W,3], out_alpha [C,H,W] (= 1 - T), out_T [C,H,W] (final
  *      transmittance, saved for the backward: P:605), last_ids [C,H,W] int32 (index into
- *      isect_ids of the last composited splat; tile_offsets[tile]-1 if none). */
+ *      isect_ids of the last composited splat; tile_offsets[tile]-1 if none).
+ * Depth rendering (App. "Depth rendering"; NULL out_depth = off): out_depth
+ *      [C,H,W] = the accumulated depth sum z alpha T (depth_mode 1) or the expected
+ *      depth = that sum / sum alpha T, with sum alpha T = 1 - T_final, 0 where nothing was
+ *      composited (depth_mode 2); z = record slot 3.  No background term. */
 GS_API gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, float* out_rgb, float* out_alpha, float* out_T,
-                           int32_t* last_ids, void* stream);
+                           int32_t* last_ids, float* out_depth, int32_t depth_mode, void* stream);
 
 /* ---- Diagnostics (not on the hot path): per-pixel work counts of stage 3 ---------
  * Runs the forward walk of gs_rasterize_fwd and writes, per pixel, n_eval [C,H,W] (pairs
@@ -165,24 +169,38 @@ GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N,
  * In : as gs_rasterize_fwd plus out_T, last_ids, v_out_rgb [C,H,W,3],
  *      v_out_alpha [C,H,W] or NULL.
  * Out: v_splats [C,N,GS_SPLAT_FLOATS] ([N,...] when opt->packed; zero-filled here, then accumulated; slot layout
- *      above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 7, 11. */
+ *      above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 7, 11.
+ * Depth (NULL v_out_depth = off): v_out_depth [C,H,W] = dL/d out_depth of the forward
+ *      with the same depth_mode; depth is composited as a fourth channel, its per-splat
+ *      gradient accumulates into slot 3; mode 2 (expected depth D/A) also needs the
+ *      forward's out_depth and adds -v E / A to the alpha gradient (quotient rule, Q26). */
 GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
-                           const float* v_out_rgb, const float* v_out_alpha, int32_t absgrad,
+                           const float* v_out_rgb, const float* v_out_alpha, const float* out_depth,
+                           const float* v_out_depth, int32_t depth_mode, int32_t absgrad,
                            float* v_splats, void* stream);
 
 /* ---- Stage 4b: projection backward (P1-P9) -------------------------------
  * In : the gs_project inputs, its radii output, v_splats from gs_rasterize_bwd.
  * Out: v_means [N,3], v_quats [N,4], v_scales [N,3], v_opacities [N],
  *      v_colors (same shape as colors).  Summed over the C cameras inside one thread per
- *      Gaussian (deterministic; Q30); Gaussians culled in every camera get zeros. */
+ *      Gaussian (deterministic; Q30); Gaussians culled in every camera get zeros.
+ *      Slot 3 of v_splats (dL/d depth, depth rendering) enters through t_z (F4).
+ * Pose (NEXT-3; NULL v_viewmats = off): v_viewmats [C,4,4] = dL/d viewmats (App. pose
+ *      optimisation): the t = W mu + w, Sigma_c = W Sigma W^T and SH
+ *      view-direction (campos = -W^T w) paths; row 3 is 0.  Reduced per (block, camera)
+ *      into the workspace (>= gs_project_bwd_workspace_size(N, C) bytes, 256-byte aligned;
+ *      unused and may be NULL when v_viewmats is NULL), then summed in block order
+ *      (deterministic). */
+GS_API size_t gs_project_bwd_workspace_size(int64_t N, int32_t C);
 GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
                          const float* means, const float* quats, const float* scales,
                          const float* opacities, const float* colors, int32_t K,
                          const float* viewmats, const float* Ks, const int32_t* radii,
                          const float* v_splats, float* v_means, float* v_quats, float* v_scales,
-                         float* v_opacities, float* v_colors, void* stream);
+                         float* v_opacities, float* v_colors, float* v_viewmats, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* ==== Packed mode (Q29; BASELINE configs[4]) ==========================================
  * Only the visible (c,n) pairs are stored: item i of a packed call is the pair
@@ -233,8 +251,8 @@ GS_API gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t
                                        const float* viewmats, const float* Ks, int64_t nnz_capacity,
                                        const int64_t* nnz, const int32_t* camera_ids, const int32_t* gaussian_ids,
                                        const int32_t* radii, const float* v_splats, float* v_means, float* v_quats,
-                                       float* v_scales, float* v_opacities, float* v_colors, void* workspace,
-                                       size_t workspace_bytes, void* stream);
+                                       float* v_scales, float* v_opacities, float* v_colors, float* v_viewmats,
+                                       void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 
@@ -45,11 +45,13 @@ SIGNATURES = {
     "gs_project": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "gs_isect_workspace_size": (_SZ, [_I32, _I64, _I32, _I32, _I64]),
     "gs_isect_tiles": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
-    "gs_rasterize_fwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "gs_rasterize_fwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "gs_rasterize_stats": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P]),
-    "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
+    "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P,
+                                _P]),
+    "gs_project_bwd_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
-                              _P, _P, _P]),
+                              _P, _P, _P, _P, _SZ, _P]),
     "gs_project_packed_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_packed": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P,
                                  _P, _P, _P, _SZ, _P]),
@@ -58,7 +60,7 @@ SIGNATURES = {
                                      _P]),
     "gs_project_bwd_packed_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd_packed": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P,
-                                     _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+                                     _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 
 
@@ -150,12 +152,13 @@ def gs_isect_tiles(o, C, N, width, height, radii, splats, cap, M, overflow, isec
 
 
 def gs_rasterize_fwd(o, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_rgb, out_alpha,
-                     out_T, last_ids, stream=None):
+                     out_T, last_ids, out_depth=None, depth_mode=0, stream=None):
     check(lib().gs_rasterize_fwd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
                                  ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
                                  ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_rgb, name="out_rgb"),
                                  ptr(out_alpha, name="out_alpha"), ptr(out_T, name="out_T"),
-                                 ptr(last_ids, torch.int32, "last_ids"), stream_ptr(stream)),
+                                 ptr(last_ids, torch.int32, "last_ids"), ptr(out_depth, name="out_depth"),
+                                 int(depth_mode), stream_ptr(stream)),
           "gs_rasterize_fwd")
 
 
@@ -168,18 +171,24 @@ def gs_rasterize_stats(o, C, N, width, height, splats, isect_ids, tile_offsets, 
 
 
 def gs_rasterize_bwd(o, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T, last_ids,
-                     v_out_rgb, v_out_alpha, absgrad, v_splats, stream=None):
+                     v_out_rgb, v_out_alpha, absgrad, v_splats, out_depth=None, v_out_depth=None, depth_mode=0,
+                     stream=None):
     check(lib().gs_rasterize_bwd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
                                  ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
                                  ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_T, name="out_T"),
                                  ptr(last_ids, torch.int32, "last_ids"), ptr(v_out_rgb, name="v_out_rgb"),
-                                 ptr(v_out_alpha, name="v_out_alpha"), int(bool(absgrad)),
+                                 ptr(v_out_alpha, name="v_out_alpha"), ptr(out_depth, name="out_depth"),
+                                 ptr(v_out_depth, name="v_out_depth"), int(depth_mode), int(bool(absgrad)),
                                  ptr(v_splats, name="v_splats"), stream_ptr(stream)),
           "gs_rasterize_bwd")
 
 
+def gs_project_bwd_workspace_size(N, C):
+    return int(lib().gs_project_bwd_workspace_size(N, C))
+
+
 def gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, width, height, radii, v_splats,
-                   v_means, v_quats, v_scales, v_opacities, v_colors, stream=None):
+                   v_means, v_quats, v_scales, v_opacities, v_colors, v_viewmats=None, workspace=None, stream=None):
     N, C = means.shape[0], viewmats.shape[0]
     check(lib().gs_project_bwd(ct.byref(o), N, C, width, height, ptr(means, name="means"), ptr(quats, name="quats"),
                                ptr(scales, name="scales"), ptr(opacities, name="opacities"),
@@ -187,7 +196,9 @@ def gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, 
                                ptr(radii, torch.int32, "radii"), ptr(v_splats, name="v_splats"),
                                ptr(v_means, name="v_means"), ptr(v_quats, name="v_quats"),
                                ptr(v_scales, name="v_scales"), ptr(v_opacities, name="v_opacities"),
-                               ptr(v_colors, name="v_colors"), stream_ptr(stream)),
+                               ptr(v_colors, name="v_colors"), ptr(v_viewmats, name="v_viewmats"),
+                               ptr(workspace, torch.uint8, "ws"), 0 if workspace is None else workspace.numel(),
+                               stream_ptr(stream)),
           "gs_project_bwd")
 
 
@@ -234,7 +245,7 @@ def gs_project_bwd_packed_workspace_size(N, C):
 
 def gs_project_bwd_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, width, height, cap_nnz, nnz,
                           camera_ids, gaussian_ids, radii, v_splats, v_means, v_quats, v_scales, v_opacities,
-                          v_colors, workspace, stream=None):
+                          v_colors, workspace, v_viewmats=None, stream=None):
     N, C = means.shape[0], viewmats.shape[0]
     check(lib().gs_project_bwd_packed(ct.byref(o), N, C, width, height, ptr(means, name="means"),
                                       ptr(quats, name="quats"), ptr(scales, name="scales"),
@@ -245,6 +256,6 @@ def gs_project_bwd_packed(o, means, quats, scales, opacities, colors, K, viewmat
                                       ptr(radii, torch.int32, "radii"), ptr(v_splats, name="v_splats"),
                                       ptr(v_means, name="v_means"), ptr(v_quats, name="v_quats"),
                                       ptr(v_scales, name="v_scales"), ptr(v_opacities, name="v_opacities"),
-                                      ptr(v_colors, name="v_colors"), ptr(workspace, torch.uint8, "ws"),
-                                      workspace.numel(), stream_ptr(stream)),
+                                      ptr(v_colors, name="v_colors"), ptr(v_viewmats, name="v_viewmats"),
+                                      ptr(workspace, torch.uint8, "ws"), workspace.numel(), stream_ptr(stream)),
           "gs_project_bwd_packed")

@@ -126,14 +126,16 @@ gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int32_t wi
 gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, float* out_rgb, float* out_alpha, float* out_T,
-                           int32_t* last_ids, void* stream) {
+                           int32_t* last_ids, float* out_depth, int32_t depth_mode, void* stream) {
     GS_TRY(check_opts(opt));
     GS_TRY(check_dims(N, C, width, height));
     GS_REQ(tile_offsets && out_rgb && out_alpha && out_T && last_ids);
+    GS_REQ(!out_depth || depth_mode == 1 || depth_mode == 2);
     GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(backgrounds) && aligned4(out_rgb) &&
-           aligned4(out_alpha) && aligned4(out_T) && aligned4(last_ids));
+           aligned4(out_alpha) && aligned4(out_T) && aligned4(last_ids) && aligned4(out_depth));
     return gsb::launch_raster_fwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_rgb,
-                                  out_alpha, out_T, last_ids, static_cast<cudaStream_t>(stream));
+                                  out_alpha, out_T, last_ids, out_depth, depth_mode,
+                                  static_cast<cudaStream_t>(stream));
 }
 
 gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
@@ -150,35 +152,49 @@ gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N, int32_
 gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
-                           const float* v_out_rgb, const float* v_out_alpha, int32_t absgrad, float* v_splats,
+                           const float* v_out_rgb, const float* v_out_alpha, const float* out_depth,
+                           const float* v_out_depth, int32_t depth_mode, int32_t absgrad, float* v_splats,
                            void* stream) {
     GS_TRY(check_opts(opt));
     GS_TRY(check_dims(N, C, width, height));
     GS_REQ(tile_offsets && out_T && last_ids && v_out_rgb && (v_splats || N == 0));
+    GS_REQ(!v_out_depth || depth_mode == 1 || (depth_mode == 2 && out_depth));
     GS_REQ(aligned16(splats) && aligned16(v_splats) && aligned4(isect_ids) && aligned4(backgrounds) &&
-           aligned4(out_T) && aligned4(last_ids) && aligned4(v_out_rgb) && aligned4(v_out_alpha));
+           aligned4(out_T) && aligned4(last_ids) && aligned4(v_out_rgb) && aligned4(v_out_alpha) &&
+           aligned4(out_depth) && aligned4(v_out_depth));
     return gsb::launch_raster_bwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T,
-                                  last_ids, v_out_rgb, v_out_alpha, absgrad, v_splats,
-                                  static_cast<cudaStream_t>(stream));
+                                  last_ids, v_out_rgb, v_out_alpha, out_depth, v_out_depth, depth_mode, absgrad,
+                                  v_splats, static_cast<cudaStream_t>(stream));
+}
+
+size_t gs_project_bwd_workspace_size(int64_t N, int32_t C) {
+    if (N < 0 || C < 1) return 0;
+    return gsb::project_bwd_workspace_bytes(N, C);
 }
 
 gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
                          const float* means, const float* quats, const float* scales, const float* opacities,
                          const float* colors, int32_t K, const float* viewmats, const float* Ks, const int32_t* radii,
                          const float* v_splats, float* v_means, float* v_quats, float* v_scales, float* v_opacities,
-                         float* v_colors, void* stream) {
+                         float* v_colors, float* v_viewmats, void* workspace, size_t workspace_bytes, void* stream) {
     GS_TRY(check_opts(opt));
     GS_REQ(opt->packed == 0);
     GS_TRY(check_dims(N, C, width, height));
-    if (N == 0) return GS_OK;
-    GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && v_splats && v_means &&
-           v_quats && v_scales && v_opacities && v_colors);
-    GS_REQ(aligned16(quats) && aligned16(v_quats) && aligned16(v_splats) && aligned8(radii) && aligned4(means) &&
-           aligned4(v_means) && aligned4(colors) && aligned4(v_colors) && aligned4(scales) && aligned4(v_scales));
-    if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
+    GS_REQ(aligned4(v_viewmats));
+    if (v_viewmats)
+        GS_REQ(workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0 &&
+               workspace_bytes >= gsb::project_bwd_workspace_bytes(N, C));
+    if (N > 0) {
+        GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && v_splats && v_means &&
+               v_quats && v_scales && v_opacities && v_colors);
+        GS_REQ(aligned16(quats) && aligned16(v_quats) && aligned16(v_splats) && aligned8(radii) && aligned4(means) &&
+               aligned4(v_means) && aligned4(colors) && aligned4(v_colors) && aligned4(scales) && aligned4(v_scales));
+        if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
+    }
     return gsb::launch_project_bwd(*opt, N, C, width, height, means, quats, scales, opacities, colors,
                                    opt->sh_degree >= 0 ? K : 1, viewmats, Ks, radii, v_splats, v_means, v_quats,
-                                   v_scales, v_opacities, v_colors, static_cast<cudaStream_t>(stream));
+                                   v_scales, v_opacities, v_colors, v_viewmats, workspace,
+                                   static_cast<cudaStream_t>(stream));
 }
 
 // ---- packed mode (Q29) ----------------------------------------------------------------
@@ -252,11 +268,16 @@ gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t C, int
                                 int64_t nnz_capacity, const int64_t* nnz, const int32_t* camera_ids,
                                 const int32_t* gaussian_ids, const int32_t* radii, const float* v_splats,
                                 float* v_means, float* v_quats, float* v_scales, float* v_opacities, float* v_colors,
-                                void* workspace, size_t workspace_bytes, void* stream) {
+                                float* v_viewmats, void* workspace, size_t workspace_bytes, void* stream) {
     GS_TRY(check_opts(opt));
     GS_REQ(opt->packed == 1);
     GS_TRY(check_dims(N, C, width, height));
-    if (N == 0) return GS_OK;
+    GS_REQ(aligned4(v_viewmats));
+    if (N == 0)
+        return gsb::launch_project_bwd_packed(*opt, 0, C, width, height, nullptr, nullptr, nullptr, nullptr, nullptr, 1,
+                                              nullptr, nullptr, 0, nnz, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                              nullptr, nullptr, nullptr, nullptr, v_viewmats, nullptr,
+                                              static_cast<cudaStream_t>(stream));
     GS_REQ(nnz_capacity >= 0 && nnz && workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
     GS_REQ(workspace_bytes >= gsb::project_bwd_packed_workspace_bytes(N, C));
     GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && v_means && v_quats && v_scales &&
@@ -269,7 +290,7 @@ gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t C, int
     return gsb::launch_project_bwd_packed(*opt, N, C, width, height, means, quats, scales, opacities, colors,
                                           opt->sh_degree >= 0 ? K : 1, viewmats, Ks, nnz_capacity, nnz, camera_ids,
                                           gaussian_ids, radii, v_splats, v_means, v_quats, v_scales, v_opacities,
-                                          v_colors, workspace, static_cast<cudaStream_t>(stream));
+                                          v_colors, v_viewmats, workspace, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

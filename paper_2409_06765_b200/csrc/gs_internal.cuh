@@ -42,7 +42,8 @@ gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H
                              const float* colors, int K, const float* viewmats, const float* Ks,
                              const int32_t* radii, const float* v_splats, float* v_means,
                              float* v_quats, float* v_scales, float* v_opac, float* v_colors,
-                             cudaStream_t s);
+                             float* v_viewmats, void* ws, cudaStream_t s);
+size_t project_bwd_workspace_bytes(int64_t N, int C);
 size_t project_packed_workspace_bytes(int64_t N, int C);
 gs_status launch_project_packed(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
                                 const float* quats, const float* scales, const float* opac, const float* colors,
@@ -56,7 +57,7 @@ gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W
                                     int64_t cap, const int64_t* nnz, const int32_t* camera_ids,
                                     const int32_t* gaussian_ids, const int32_t* radii, const float* v_splats,
                                     float* v_means, float* v_quats, float* v_scales, float* v_opac,
-                                    float* v_colors, void* ws, cudaStream_t s);
+                                    float* v_colors, float* v_viewmats, void* ws, cudaStream_t s);
 // n_items = C*N dense items (camera = id / N), or the packed capacity with the live count
 // *d_nnz and camera_ids (both NULL in dense mode).
 size_t isect_workspace_bytes(int64_t n_items, int64_t cap);
@@ -66,13 +67,15 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
                        int32_t* tile_offsets, void* ws, size_t ws_bytes, cudaStream_t s);
 gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                             const float* bg, const int32_t* ids, const int32_t* offs, float* out_rgb,
-                            float* out_alpha, float* out_T, int32_t* last_ids, cudaStream_t s);
+                            float* out_alpha, float* out_T, int32_t* last_ids, float* out_depth, int depth_mode,
+                            cudaStream_t s);
 gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                               const int32_t* ids, const int32_t* offs, int32_t* n_eval, int32_t* n_contrib,
                               cudaStream_t s);
 gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                             const float* bg, const int32_t* ids, const int32_t* offs, const float* out_T,
                             const int32_t* last_ids, const float* v_rgb, const float* v_alpha,
-                            int absgrad, float* v_splats, cudaStream_t s);
+                            const float* out_depth, const float* v_depth, int depth_mode, int absgrad,
+                            float* v_splats, cudaStream_t s);
 
 }  // namespace gsb

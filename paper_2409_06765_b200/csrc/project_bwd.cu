@@ -31,6 +31,7 @@ struct PBParams {
     const int32_t* radii;
     const float* v_splats;
     const int32_t* map;   // packed mode: (c,n) -> packed item or -1 (else NULL: item = c*N+n)
+    float* pose_part;     // pose gradients: per-(block, camera) partial dL/dviewmat rows 0..2 [nblk][C][12]
     float* v_means;
     float* v_quats;
     float* v_scales;
@@ -47,11 +48,43 @@ __device__ __forceinline__ void quat_rot(float4 q4, float (&R)[3][3]) {
     R[2][0] = 2.f * (qx * qz - qw * qy); R[2][1] = 2.f * (qy * qz + qw * qx); R[2][2] = 1.f - 2.f * (qx * qx + qy * qy);
 }
 
-template <int DEG>
+// Transposed warp reduction of 16 values: lane l ends with the warp sum of value (l >> 1) & 15.
+__device__ __forceinline__ float reduce_scatter16(const float (&v)[16], int lane) {
+    float u[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const bool h = lane & 16;
+        u[i] = (h ? v[i + 8] : v[i]) + __shfl_xor_sync(0xffffffffu, h ? v[i] : v[i + 8], 16);
+    }
+    float w[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const bool h = lane & 8;
+        w[i] = (h ? u[i + 4] : u[i]) + __shfl_xor_sync(0xffffffffu, h ? u[i] : u[i + 4], 8);
+    }
+    float x[2];
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const bool h = lane & 4;
+        x[i] = (h ? w[i + 2] : w[i]) + __shfl_xor_sync(0xffffffffu, h ? w[i] : w[i + 2], 4);
+    }
+    const bool h = lane & 2;
+    float y = (h ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, h ? x[0] : x[1], 2);
+    y += __shfl_xor_sync(0xffffffffu, y, 1);
+    return y;
+}
+
+// POSE: also the camera pose gradients dL/dviewmat (App. pose optimisation, P:233-239,
+// P:713-726): per camera, every thread's contribution is reduced over the block and written
+// as one per-(block, camera) partial; k_pose_reduce sums the partials in a fixed order.
+template <int DEG, bool POSE>
 __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
-    const int64_t n = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (n >= p.N) return;   // no block-level synchronisation below
+    const int64_t n0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const bool active = n0 < p.N;
+    if (!POSE && !active) return;   // without POSE there is no block-level synchronisation below
+    const int64_t n = active ? n0 : p.N - 1;   // POSE: idle threads read a valid row, contribute nothing
     constexpr int NB = DEG < 0 ? 1 : (DEG + 1) * (DEG + 1);
+    __shared__ float s_pose[POSE ? kThreads / 32 : 1][12];
 
     const float mu[3] = {p.means[3 * n], p.means[3 * n + 1], p.means[3 * n + 2]};
     const float4 q4 = reinterpret_cast<const float4*>(p.quats)[n];
@@ -90,196 +123,251 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
 
     for (int c = 0; c < p.C; c++) {
         int64_t idx = (int64_t)c * p.N + n;
-        if (p.map) {
+        bool vis = active;
+        if (vis && p.map) {
             const int m = p.map[idx];
-            if (m < 0) continue;
-            idx = m;
+            vis = m >= 0;
+            idx = vis ? m : 0;
         }
-        const int2 rad = reinterpret_cast<const int2*>(p.radii)[idx];
-        if (rad.x <= 0 || rad.y <= 0) continue;
+        if (vis) {
+            const int2 rad = reinterpret_cast<const int2*>(p.radii)[idx];
+            vis = rad.x > 0 && rad.y > 0;
+        }
+        float pw[12];   // this thread's dL/dviewmat rows 0..2 for camera c
+#pragma unroll
+        for (int i = 0; i < 12; i++) pw[i] = 0.f;
+        if (vis) {
         seen = true;
-        const float4* vr = reinterpret_cast<const float4*>(p.v_splats + idx * GS_SPLAT_FLOATS);
-        const float4 v0 = vr[0], v1 = vr[1], v2 = vr[2];
-        const float* vm = p.viewmats + 16 * (int64_t)c;
-        const float* Kc = p.Ks + 9 * (int64_t)c;
-        float Wr[3][3], w[3];
-#pragma unroll
-        for (int i = 0; i < 3; i++) {
-#pragma unroll
-            for (int j = 0; j < 3; j++) Wr[i][j] = vm[4 * i + j];
-            w[i] = vm[4 * i + 3];
-        }
-        const float fx = Kc[0], fy = Kc[4], cx = Kc[2], cy = Kc[5];
-        float t[3];
-#pragma unroll
-        for (int i = 0; i < 3; i++) t[i] = Wr[i][0] * mu[0] + Wr[i][1] * mu[1] + Wr[i][2] * mu[2] + w[i];
-        const float tz = t[2];
-        // Sigma_c = Wr Sigma Wr^T
-        float A[3][3], Sc[3][3];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) A[i][j] = Wr[i][0] * Sig[0][j] + Wr[i][1] * Sig[1][j] + Wr[i][2] * Sig[2][j];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) Sc[i][j] = A[i][0] * Wr[j][0] + A[i][1] * Wr[j][1] + A[i][2] * Wr[j][2];
-        // J with clamp (Q27)
-        float txc = t[0], tyc = t[1];
-        bool clx = false, cly = false;
-        if (p.fov_clamp) {
-            const float Wf = (float)p.W, Hf = (float)p.H;
-            const float tanx = 0.5f * Wf / fx, tany = 0.5f * Hf / fy;
-            const float lxp = (Wf - cx) / fx + 0.3f * tanx, lxn = cx / fx + 0.3f * tanx;
-            const float lyp = (Hf - cy) / fy + 0.3f * tany, lyn = cy / fy + 0.3f * tany;
-            const float u = t[0] / tz, v = t[1] / tz;
-            clx = (u > lxp) || (u < -lxn);
-            cly = (v > lyp) || (v < -lyn);
-            txc = tz * fminf(lxp, fmaxf(-lxn, u));
-            tyc = tz * fminf(lyp, fmaxf(-lyn, v));
-        }
-        const float J[2][3] = {{fx / tz, 0.f, -fx * txc / (tz * tz)}, {0.f, fy / tz, -fy * tyc / (tz * tz)}};
-        float B[2][3], Sp[2][2];
-#pragma unroll
-        for (int i = 0; i < 2; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) B[i][j] = J[i][0] * Sc[0][j] + J[i][1] * Sc[1][j] + J[i][2] * Sc[2][j];
-#pragma unroll
-        for (int i = 0; i < 2; i++)
-#pragma unroll
-            for (int j = 0; j < 2; j++) Sp[i][j] = B[i][0] * J[j][0] + B[i][1] * J[j][1] + B[i][2] * J[j][2];
-        const float a = Sp[0][0] + p.eps2d, b = Sp[0][1], cc = Sp[1][1] + p.eps2d;
-        const float detb = a * cc - b * b;
-        const float Y00 = cc / detb, Y01 = -b / detb, Y11 = a / detb;
-        float comp = 1.f, det_raw = 0.f;
-        if (p.antialiased) {
-            det_raw = Sp[0][0] * Sp[1][1] - Sp[0][1] * Sp[0][1];
-            comp = sqrtf(fmaxf(0.f, det_raw / detb));
-        }
-        // ---- P1: o_eff = o * comp
-        const float v_oeff = v0.z;
-        g_op += v_oeff * comp;
-        const float v_comp = v_oeff * op;
-        // ---- P2: v_Spb = -Y G_Y Y, G_Y = [[vA, vB/2],[vB/2, vC]]
-        const float gA = v1.x, gB = 0.5f * v1.y, gC = v1.z;
-        const float YG00 = Y00 * gA + Y01 * gB, YG01 = Y00 * gB + Y01 * gC;
-        const float YG10 = Y01 * gA + Y11 * gB, YG11 = Y01 * gB + Y11 * gC;
-        float vS00 = -(YG00 * Y00 + YG01 * Y01);
-        float vS01 = -(YG00 * Y01 + YG01 * Y11);
-        float vS11 = -(YG10 * Y01 + YG11 * Y11);
-        // ---- P3 (AA): + v_comp * comp/2 * (Sigma'^-1 - Spb^-1)
-        if (p.antialiased && det_raw > 0.f) {
-            const float k = v_comp * 0.5f * comp;
-            vS00 += k * (Sp[1][1] / det_raw - Y00);
-            vS01 += k * (-Sp[0][1] / det_raw - Y01);
-            vS11 += k * (Sp[0][0] / det_raw - Y11);
-        }
-        const float vSp[2][2] = {{vS00, vS01}, {vS01, vS11}};
-        // ---- P4: v_Sc = J^T vSp J; v_J = 2 vSp J Sc (Q11)
-        float vSc[3][3], vJ[2][3];
-        float PJ[2][3];
-#pragma unroll
-        for (int i = 0; i < 2; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) PJ[i][j] = vSp[i][0] * J[0][j] + vSp[i][1] * J[1][j];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) vSc[i][j] = J[0][i] * PJ[0][j] + J[1][i] * PJ[1][j];
-#pragma unroll
-        for (int i = 0; i < 2; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) vJ[i][j] = 2.f * (PJ[i][0] * Sc[0][j] + PJ[i][1] * Sc[1][j] + PJ[i][2] * Sc[2][j]);
-        // ---- P5: v_t through J (exact with clamp Q27) and mu' (Q10)
-        const float rz = 1.f / tz, rz2 = rz * rz, rz3 = rz2 * rz;
-        float vt0 = 0.f, vt1 = 0.f, vt2 = -fx * rz2 * vJ[0][0] - fy * rz2 * vJ[1][1];
-        if (!clx) {
-            vt0 += -fx * rz2 * vJ[0][2];
-            vt2 += 2.f * fx * t[0] * rz3 * vJ[0][2];
-        } else {
-            vt2 += fx * txc * rz3 * vJ[0][2];
-        }
-        if (!cly) {
-            vt1 += -fy * rz2 * vJ[1][2];
-            vt2 += 2.f * fy * t[1] * rz3 * vJ[1][2];
-        } else {
-            vt2 += fy * tyc * rz3 * vJ[1][2];
-        }
-        vt0 += fx * rz * v0.x;
-        vt1 += fy * rz * v0.y;
-        vt2 -= fx * t[0] * rz2 * v0.x + fy * t[1] * rz2 * v0.y;
-        // ---- P6: v_mu += W^T v_t; v_Sigma += W^T v_Sc W
-#pragma unroll
-        for (int i = 0; i < 3; i++) g_mu[i] += Wr[0][i] * vt0 + Wr[1][i] * vt1 + Wr[2][i] * vt2;
-        float T1[3][3];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) T1[i][j] = vSc[i][0] * Wr[0][j] + vSc[i][1] * Wr[1][j] + vSc[i][2] * Wr[2][j];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-#pragma unroll
-            for (int j = 0; j < 3; j++) g_S[i][j] += Wr[0][i] * T1[0][j] + Wr[1][i] * T1[1][j] + Wr[2][i] * T1[2][j];
-        // ---- P7: colour
-        if (DEG < 0) {
-            g_rgb[0] += v2.x;
-            g_rgb[1] += v2.y;
-            g_rgb[2] += v2.z;
-        } else {
-            float campos[3];
-#pragma unroll
-            for (int i = 0; i < 3; i++) campos[i] = -(Wr[0][i] * w[0] + Wr[1][i] * w[1] + Wr[2][i] * w[2]);
-            const float ex = mu[0] - campos[0], ey = mu[1] - campos[1], ez = mu[2] - campos[2];
-            const float en = sqrtf(ex * ex + ey * ey + ez * ez);
-            const float dx = ex / en, dy = ey / en, dz = ez / en;
-            float Yb[NB];
-            sh_eval_basis<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, Yb);
-            float raw[3] = {0.5f, 0.5f, 0.5f};
-            if (vec) {
-#pragma unroll
-                for (int i = 0; i < NB * 3 / 4; i++) {
-                    const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
-                    raw[(4 * i + 0) % 3] += Yb[(4 * i + 0) / 3] * v.x;
-                    raw[(4 * i + 1) % 3] += Yb[(4 * i + 1) / 3] * v.y;
-                    raw[(4 * i + 2) % 3] += Yb[(4 * i + 2) / 3] * v.z;
-                    raw[(4 * i + 3) % 3] += Yb[(4 * i + 3) / 3] * v.w;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < NB * 3; i++) raw[i % 3] += Yb[i / 3] * __ldg(src + i);
+            const float4* vr = reinterpret_cast<const float4*>(p.v_splats + idx * GS_SPLAT_FLOATS);
+            const float4 v0 = vr[0], v1 = vr[1], v2 = vr[2];
+            const float* vm = p.viewmats + 16 * (int64_t)c;
+            const float* Kc = p.Ks + 9 * (int64_t)c;
+            float Wr[3][3], w[3];
+    #pragma unroll
+            for (int i = 0; i < 3; i++) {
+    #pragma unroll
+                for (int j = 0; j < 3; j++) Wr[i][j] = vm[4 * i + j];
+                w[i] = vm[4 * i + 3];
             }
-            const float vr[3] = {raw[0] > 0.f ? v2.x : 0.f, raw[1] > 0.f ? v2.y : 0.f, raw[2] > 0.f ? v2.z : 0.f};
+            const float fx = Kc[0], fy = Kc[4], cx = Kc[2], cy = Kc[5];
+            float t[3];
+    #pragma unroll
+            for (int i = 0; i < 3; i++) t[i] = Wr[i][0] * mu[0] + Wr[i][1] * mu[1] + Wr[i][2] * mu[2] + w[i];
+            const float tz = t[2];
+            // Sigma_c = Wr Sigma Wr^T
+            float A[3][3], Sc[3][3];
+    #pragma unroll
+            for (int i = 0; i < 3; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) A[i][j] = Wr[i][0] * Sig[0][j] + Wr[i][1] * Sig[1][j] + Wr[i][2] * Sig[2][j];
+    #pragma unroll
+            for (int i = 0; i < 3; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) Sc[i][j] = A[i][0] * Wr[j][0] + A[i][1] * Wr[j][1] + A[i][2] * Wr[j][2];
+            // J with clamp (Q27)
+            float txc = t[0], tyc = t[1];
+            bool clx = false, cly = false;
+            if (p.fov_clamp) {
+                const float Wf = (float)p.W, Hf = (float)p.H;
+                const float tanx = 0.5f * Wf / fx, tany = 0.5f * Hf / fy;
+                const float lxp = (Wf - cx) / fx + 0.3f * tanx, lxn = cx / fx + 0.3f * tanx;
+                const float lyp = (Hf - cy) / fy + 0.3f * tany, lyn = cy / fy + 0.3f * tany;
+                const float u = t[0] / tz, v = t[1] / tz;
+                clx = (u > lxp) || (u < -lxn);
+                cly = (v > lyp) || (v < -lyn);
+                txc = tz * fminf(lxp, fmaxf(-lxn, u));
+                tyc = tz * fminf(lyp, fmaxf(-lyn, v));
+            }
+            const float J[2][3] = {{fx / tz, 0.f, -fx * txc / (tz * tz)}, {0.f, fy / tz, -fy * tyc / (tz * tz)}};
+            float B[2][3], Sp[2][2];
+    #pragma unroll
+            for (int i = 0; i < 2; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) B[i][j] = J[i][0] * Sc[0][j] + J[i][1] * Sc[1][j] + J[i][2] * Sc[2][j];
+    #pragma unroll
+            for (int i = 0; i < 2; i++)
+    #pragma unroll
+                for (int j = 0; j < 2; j++) Sp[i][j] = B[i][0] * J[j][0] + B[i][1] * J[j][1] + B[i][2] * J[j][2];
+            const float a = Sp[0][0] + p.eps2d, b = Sp[0][1], cc = Sp[1][1] + p.eps2d;
+            const float detb = a * cc - b * b;
+            const float Y00 = cc / detb, Y01 = -b / detb, Y11 = a / detb;
+            float comp = 1.f, det_raw = 0.f;
+            if (p.antialiased) {
+                det_raw = Sp[0][0] * Sp[1][1] - Sp[0][1] * Sp[0][1];
+                comp = sqrtf(fmaxf(0.f, det_raw / detb));
+            }
+            // ---- P1: o_eff = o * comp
+            const float v_oeff = v0.z;
+            g_op += v_oeff * comp;
+            const float v_comp = v_oeff * op;
+            // ---- P2: v_Spb = -Y G_Y Y, G_Y = [[vA, vB/2],[vB/2, vC]]
+            const float gA = v1.x, gB = 0.5f * v1.y, gC = v1.z;
+            const float YG00 = Y00 * gA + Y01 * gB, YG01 = Y00 * gB + Y01 * gC;
+            const float YG10 = Y01 * gA + Y11 * gB, YG11 = Y01 * gB + Y11 * gC;
+            float vS00 = -(YG00 * Y00 + YG01 * Y01);
+            float vS01 = -(YG00 * Y01 + YG01 * Y11);
+            float vS11 = -(YG10 * Y01 + YG11 * Y11);
+            // ---- P3 (AA): + v_comp * comp/2 * (Sigma'^-1 - Spb^-1)
+            if (p.antialiased && det_raw > 0.f) {
+                const float k = v_comp * 0.5f * comp;
+                vS00 += k * (Sp[1][1] / det_raw - Y00);
+                vS01 += k * (-Sp[0][1] / det_raw - Y01);
+                vS11 += k * (Sp[0][0] / det_raw - Y11);
+            }
+            const float vSp[2][2] = {{vS00, vS01}, {vS01, vS11}};
+            // ---- P4: v_Sc = J^T vSp J; v_J = 2 vSp J Sc (Q11)
+            float vSc[3][3], vJ[2][3];
+            float PJ[2][3];
+    #pragma unroll
+            for (int i = 0; i < 2; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) PJ[i][j] = vSp[i][0] * J[0][j] + vSp[i][1] * J[1][j];
+    #pragma unroll
+            for (int i = 0; i < 3; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) vSc[i][j] = J[0][i] * PJ[0][j] + J[1][i] * PJ[1][j];
+    #pragma unroll
+            for (int i = 0; i < 2; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) vJ[i][j] = 2.f * (PJ[i][0] * Sc[0][j] + PJ[i][1] * Sc[1][j] + PJ[i][2] * Sc[2][j]);
+            // ---- P5: v_t through J (exact with clamp Q27) and mu' (Q10)
+            const float rz = 1.f / tz, rz2 = rz * rz, rz3 = rz2 * rz;
+            float vt0 = 0.f, vt1 = 0.f, vt2 = -fx * rz2 * vJ[0][0] - fy * rz2 * vJ[1][1];
+            if (!clx) {
+                vt0 += -fx * rz2 * vJ[0][2];
+                vt2 += 2.f * fx * t[0] * rz3 * vJ[0][2];
+            } else {
+                vt2 += fx * txc * rz3 * vJ[0][2];
+            }
+            if (!cly) {
+                vt1 += -fy * rz2 * vJ[1][2];
+                vt2 += 2.f * fy * t[1] * rz3 * vJ[1][2];
+            } else {
+                vt2 += fy * tyc * rz3 * vJ[1][2];
+            }
+            vt0 += fx * rz * v0.x;
+            vt1 += fy * rz * v0.y;
+            vt2 -= fx * t[0] * rz2 * v0.x + fy * t[1] * rz2 * v0.y;
+            vt2 += v0.w;   // depth = t_z (F4), the depth-rendering gradient (slot 3)
+            if constexpr (POSE) {
+                // t = W mu + w: dL/dW += v_t mu^T, dL/dw += v_t
+                const float vt[3] = {vt0, vt1, vt2};
 #pragma unroll
-            for (int i = 0; i < NB * 3; i++) s_gc[i][threadIdx.x] += Yb[i / 3] * vr[i % 3];
-            if (DEG > 0) {
-                float wj[NB];
+                for (int i = 0; i < 3; i++) {
 #pragma unroll
-                for (int j = 0; j < NB; j++) wj[j] = 0.f;
+                    for (int j = 0; j < 3; j++) pw[4 * i + j] += vt[i] * mu[j];
+                    pw[4 * i + 3] += vt[i];
+                }
+            }
+            if constexpr (POSE) {
+                // Sigma_c = W Sigma W^T (Fig. P:423): dL/dW += (vSc + vSc^T) W Sigma, W Sigma = A
+#pragma unroll
+                for (int i = 0; i < 3; i++)
+#pragma unroll
+                    for (int j = 0; j < 3; j++)
+                        pw[4 * i + j] += (vSc[i][0] + vSc[0][i]) * A[0][j] + (vSc[i][1] + vSc[1][i]) * A[1][j] +
+                                         (vSc[i][2] + vSc[2][i]) * A[2][j];
+            }
+            // ---- P6: v_mu += W^T v_t; v_Sigma += W^T v_Sc W
+    #pragma unroll
+            for (int i = 0; i < 3; i++) g_mu[i] += Wr[0][i] * vt0 + Wr[1][i] * vt1 + Wr[2][i] * vt2;
+            float T1[3][3];
+    #pragma unroll
+            for (int i = 0; i < 3; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) T1[i][j] = vSc[i][0] * Wr[0][j] + vSc[i][1] * Wr[1][j] + vSc[i][2] * Wr[2][j];
+    #pragma unroll
+            for (int i = 0; i < 3; i++)
+    #pragma unroll
+                for (int j = 0; j < 3; j++) g_S[i][j] += Wr[0][i] * T1[0][j] + Wr[1][i] * T1[1][j] + Wr[2][i] * T1[2][j];
+            // ---- P7: colour
+            if (DEG < 0) {
+                g_rgb[0] += v2.x;
+                g_rgb[1] += v2.y;
+                g_rgb[2] += v2.z;
+            } else {
+                float campos[3];
+    #pragma unroll
+                for (int i = 0; i < 3; i++) campos[i] = -(Wr[0][i] * w[0] + Wr[1][i] * w[1] + Wr[2][i] * w[2]);
+                const float ex = mu[0] - campos[0], ey = mu[1] - campos[1], ez = mu[2] - campos[2];
+                const float en = sqrtf(ex * ex + ey * ey + ez * ez);
+                const float dx = ex / en, dy = ey / en, dz = ez / en;
+                float Yb[NB];
+                sh_eval_basis<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, Yb);
+                float raw[3] = {0.5f, 0.5f, 0.5f};
                 if (vec) {
-#pragma unroll
+    #pragma unroll
                     for (int i = 0; i < NB * 3 / 4; i++) {
                         const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
-                        wj[(4 * i + 0) / 3] += v.x * vr[(4 * i + 0) % 3];
-                        wj[(4 * i + 1) / 3] += v.y * vr[(4 * i + 1) % 3];
-                        wj[(4 * i + 2) / 3] += v.z * vr[(4 * i + 2) % 3];
-                        wj[(4 * i + 3) / 3] += v.w * vr[(4 * i + 3) % 3];
+                        raw[(4 * i + 0) % 3] += Yb[(4 * i + 0) / 3] * v.x;
+                        raw[(4 * i + 1) % 3] += Yb[(4 * i + 1) / 3] * v.y;
+                        raw[(4 * i + 2) % 3] += Yb[(4 * i + 2) / 3] * v.z;
+                        raw[(4 * i + 3) % 3] += Yb[(4 * i + 3) / 3] * v.w;
                     }
                 } else {
-#pragma unroll
-                    for (int i = 0; i < NB * 3; i++) wj[i / 3] += __ldg(src + i) * vr[i % 3];
+    #pragma unroll
+                    for (int i = 0; i < NB * 3; i++) raw[i % 3] += Yb[i / 3] * __ldg(src + i);
                 }
-                float gx = 0.f, gy = 0.f, gz = 0.f;
-                sh_basis_vjp<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, wj, gx, gy, gz);
-                const float dd = dx * gx + dy * gy + dz * gz;
-                const float ren = 1.f / en;
-                g_mu[0] += (gx - dx * dd) * ren;
-                g_mu[1] += (gy - dy * dd) * ren;
-                g_mu[2] += (gz - dz * dd) * ren;
+                const float vr[3] = {raw[0] > 0.f ? v2.x : 0.f, raw[1] > 0.f ? v2.y : 0.f, raw[2] > 0.f ? v2.z : 0.f};
+    #pragma unroll
+                for (int i = 0; i < NB * 3; i++) s_gc[i][threadIdx.x] += Yb[i / 3] * vr[i % 3];
+                if (DEG > 0) {
+                    float wj[NB];
+    #pragma unroll
+                    for (int j = 0; j < NB; j++) wj[j] = 0.f;
+                    if (vec) {
+    #pragma unroll
+                        for (int i = 0; i < NB * 3 / 4; i++) {
+                            const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
+                            wj[(4 * i + 0) / 3] += v.x * vr[(4 * i + 0) % 3];
+                            wj[(4 * i + 1) / 3] += v.y * vr[(4 * i + 1) % 3];
+                            wj[(4 * i + 2) / 3] += v.z * vr[(4 * i + 2) % 3];
+                            wj[(4 * i + 3) / 3] += v.w * vr[(4 * i + 3) % 3];
+                        }
+                    } else {
+    #pragma unroll
+                        for (int i = 0; i < NB * 3; i++) wj[i / 3] += __ldg(src + i) * vr[i % 3];
+                    }
+                    float gx = 0.f, gy = 0.f, gz = 0.f;
+                    sh_basis_vjp<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, wj, gx, gy, gz);
+                    const float dd = dx * gx + dy * gy + dz * gz;
+                    const float ren = 1.f / en;
+                    const float ve[3] = {(gx - dx * dd) * ren, (gy - dy * dd) * ren, (gz - dz * dd) * ren};
+                    g_mu[0] += ve[0];
+                    g_mu[1] += ve[1];
+                    g_mu[2] += ve[2];
+                    if constexpr (POSE) {
+                        // e = mu - campos, campos = -W^T w: dL/dW_ki += ve_i w_k, dL/dw_k += (W ve)_k
+#pragma unroll
+                        for (int k = 0; k < 3; k++) {
+#pragma unroll
+                            for (int i = 0; i < 3; i++) pw[4 * k + i] += ve[i] * w[k];
+                            pw[4 * k + 3] += Wr[k][0] * ve[0] + Wr[k][1] * ve[1] + Wr[k][2] * ve[2];
+                        }
+                    }
+                }
             }
+            (void)cy;
+            (void)cx;
+        }  // vis
+        if constexpr (POSE) {
+            float v16[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) v16[i] = i < 12 ? pw[i] : 0.f;
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            const float r = reduce_scatter16(v16, lane);
+            if ((lane & 1) == 0 && (lane >> 1) < 12) s_pose[warp][lane >> 1] = r;
+            __syncthreads();
+            if (threadIdx.x < 12) {
+                float t = 0.f;
+#pragma unroll
+                for (int w2 = 0; w2 < kThreads / 32; w2++) t += s_pose[w2][threadIdx.x];
+                p.pose_part[((int64_t)blockIdx.x * p.C + c) * 12 + threadIdx.x] = t;
+            }
+            __syncthreads();
         }
-        (void)cy;
-        (void)cx;
     }
+    if (!active) return;
 
     // ---- P8: v_M = (vS + vS^T) M; v_s_j = (R^T v_M)_jj; v_R = v_M S
     const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
@@ -377,15 +465,46 @@ PBParams make_pb_params(const gs_options& o, int64_t N, int C, int W, int H, con
     return p;
 }
 
-void launch_pb(int deg, const PBParams& p, cudaStream_t s) {
+template <bool POSE>
+void launch_pb_t(int deg, const PBParams& p, cudaStream_t s) {
     const int grid = div_up(p.N, kThreads);
     switch (deg) {
-        case -1: k_project_bwd<-1><<<grid, kThreads, 0, s>>>(p); break;
-        case 0: k_project_bwd<0><<<grid, kThreads, 0, s>>>(p); break;
-        case 1: k_project_bwd<1><<<grid, kThreads, 0, s>>>(p); break;
-        case 2: k_project_bwd<2><<<grid, kThreads, 0, s>>>(p); break;
-        default: k_project_bwd<3><<<grid, kThreads, 0, s>>>(p); break;
+        case -1: k_project_bwd<-1, POSE><<<grid, kThreads, 0, s>>>(p); break;
+        case 0: k_project_bwd<0, POSE><<<grid, kThreads, 0, s>>>(p); break;
+        case 1: k_project_bwd<1, POSE><<<grid, kThreads, 0, s>>>(p); break;
+        case 2: k_project_bwd<2, POSE><<<grid, kThreads, 0, s>>>(p); break;
+        default: k_project_bwd<3, POSE><<<grid, kThreads, 0, s>>>(p); break;
     }
+}
+
+// dL/dviewmat[c] = sum over blocks of the per-(block, camera) partials, in block order
+// (deterministic); row 3 of the 4x4 is not a parameter of the projection: 0.
+constexpr int kPoseT = 120;   // 12 values x 10 lanes each
+__global__ void __launch_bounds__(kPoseT) k_pose_reduce(const float* __restrict__ part, int nblk, int C,
+                                                      float* __restrict__ v_viewmats) {
+    __shared__ float s_acc[kPoseT];
+    const int c = blockIdx.x, v = threadIdx.x / 10, r = threadIdx.x % 10;
+    float t = 0.f;
+    for (int b = r; b < nblk; b += 10) t += part[((int64_t)b * C + c) * 12 + v];
+    s_acc[threadIdx.x] = t;
+    __syncthreads();
+    if (r == 0) {
+        float u = 0.f;
+        for (int k = 0; k < 10; k++) u += s_acc[threadIdx.x + k];
+        v_viewmats[16 * (int64_t)c + v] = u;
+    }
+    if (threadIdx.x < 4) v_viewmats[16 * (int64_t)c + 12 + threadIdx.x] = 0.f;
+}
+
+gs_status launch_pb(int deg, PBParams p, float* v_viewmats, void* pose_ws, cudaStream_t s) {
+    if (!v_viewmats) {
+        launch_pb_t<false>(deg, p, s);
+        return GS_OK;
+    }
+    p.pose_part = static_cast<float*>(pose_ws);
+    launch_pb_t<true>(deg, p, s);
+    k_pose_reduce<<<p.C, kPoseT, 0, s>>>(p.pose_part, div_up(p.N, kThreads), p.C, v_viewmats);
+    return GS_OK;
 }
 
 // map[camera_ids[i] * N + gaussian_ids[i]] = i for the live packed items (map pre-set to -1)
@@ -403,17 +522,27 @@ gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H
                              const float* colors, int K, const float* viewmats, const float* Ks,
                              const int32_t* radii, const float* v_splats, float* v_means,
                              float* v_quats, float* v_scales, float* v_opac, float* v_colors,
-                             cudaStream_t s) {
-    if (N == 0) return GS_OK;
+                             float* v_viewmats, void* ws, cudaStream_t s) {
+    if (N == 0) {
+        if (v_viewmats && cudaMemsetAsync(v_viewmats, 0, sizeof(float) * 16 * (size_t)C, s) != cudaSuccess)
+            return GS_ERR_CUDA;
+        return GS_OK;
+    }
     const PBParams p = make_pb_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii,
                                       v_splats, v_means, v_quats, v_scales, v_opac, v_colors);
-    launch_pb(o.sh_degree, p, s);
+    launch_pb(o.sh_degree, p, v_viewmats, ws, s);
     GS_LAUNCH_CHECK("k_project_bwd");
     return GS_OK;
 }
 
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t project_bwd_workspace_bytes(int64_t N, int C) {
+    return align256((size_t)div_up(N > 0 ? N : 1, kThreads) * (size_t)C * 12 * sizeof(float));
+}
+
 size_t project_bwd_packed_workspace_bytes(int64_t N, int C) {
-    return ((size_t)C * (size_t)N * sizeof(int32_t) + 255) & ~(size_t)255;
+    return align256((size_t)C * (size_t)N * sizeof(int32_t)) + project_bwd_workspace_bytes(N, C);
 }
 
 gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
@@ -422,9 +551,14 @@ gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W
                                     int64_t cap, const int64_t* nnz, const int32_t* camera_ids,
                                     const int32_t* gaussian_ids, const int32_t* radii, const float* v_splats,
                                     float* v_means, float* v_quats, float* v_scales, float* v_opac,
-                                    float* v_colors, void* ws, cudaStream_t s) {
-    if (N == 0) return GS_OK;
+                                    float* v_colors, float* v_viewmats, void* ws, cudaStream_t s) {
+    if (N == 0) {
+        if (v_viewmats && cudaMemsetAsync(v_viewmats, 0, sizeof(float) * 16 * (size_t)C, s) != cudaSuccess)
+            return GS_ERR_CUDA;
+        return GS_OK;
+    }
     int32_t* map = static_cast<int32_t*>(ws);
+    void* pose_ws = static_cast<char*>(ws) + align256((size_t)C * (size_t)N * sizeof(int32_t));
     if (cudaMemsetAsync(map, 0xff, sizeof(int32_t) * (size_t)C * (size_t)N, s) != cudaSuccess) {
         GS_LAUNCH_CHECK("packed map memset");
         return GS_ERR_CUDA;
@@ -433,7 +567,7 @@ gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W
     PBParams p = make_pb_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii, v_splats,
                                 v_means, v_quats, v_scales, v_opac, v_colors);
     p.map = map;
-    launch_pb(o.sh_degree, p, s);
+    launch_pb(o.sh_degree, p, v_viewmats, pose_ws, s);
     GS_LAUNCH_CHECK("k_project_bwd<packed>");
     return GS_OK;
 }

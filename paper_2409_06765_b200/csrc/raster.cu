@@ -173,6 +173,10 @@ struct RasterParams {
     const float* v_alpha;
     float* v_splats;
     int absgrad;
+    // depth rendering (App. depth rendering): 0 off, 1 accumulated, 2 expected
+    int depth_mode;
+    float* out_depth;            // fwd output; bwd reads it (expected depth, mode 2)
+    const float* v_depth;        // bwd: dL/d out_depth
     // diagnostics (gs_rasterize_stats)
     int32_t* n_eval;
     int32_t* n_contrib;
@@ -247,7 +251,7 @@ struct StageFwd {
     uint16_t list[2 * kWarps][kBatchFwd];
 };
 
-template <bool STATS>
+template <bool STATS, bool DEPTH>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     __shared__ StageFwd s;
     const int tile = blockIdx.x, cam = blockIdx.y;
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     const int bin = cam * p.TX * p.TY + tile;
     const int start = p.offs[bin], end = p.offs[bin + 1];
 
-    float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dacc = 0.f;
     int last = start - 1;
     bool done = !inside;
     int n_eval = 0, n_contrib = 0;
@@ -322,6 +326,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             c0 = __fmaf_rn(rgb.x, w, c0);   // C += c alpha T
             c1 = __fmaf_rn(rgb.y, w, c1);
             c2 = __fmaf_rn(rgb.z, w, c2);
+            if (DEPTH) dacc = __fmaf_rn(xyo.w, w, dacc);   // sum z alpha T
             T = nT;
             last = b0 + (int)(j16 >> 4);
             if (STATS) n_contrib++;
@@ -348,6 +353,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         p.out_alpha[pix] = 1.f - T;
         p.out_T[pix] = T;
         p.last_ids[pix] = last;
+        if (DEPTH) {
+            // expected depth: the accumulated depth over sum alpha T = 1 - T_final
+            const float A = 1.f - T;
+            p.out_depth[pix] = p.depth_mode == 2 ? (A > 0.f ? dacc / A : 0.f) : dacc;
+        }
     }
 }
 
@@ -402,7 +412,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // v_r, v_g) is i + i/3 = {0, 1, 2, 4, 5, 6, 8, 9}; of the 4-value absgrad group (v_b,
 // |v_mean2d.x|, |v_mean2d.y|) it is {10, 7, 11}.
 __device__ __forceinline__ int slot8(int i) { return i + i / 3; }
-__device__ __forceinline__ int slot4(int i) { return i == 0 ? 10 : (i == 1 ? 7 : 11); }
+__device__ __forceinline__ int slot4(int i) { return i == 0 ? 10 : (i == 1 ? 7 : (i == 2 ? 11 : 3)); }
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -417,7 +427,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-template <bool ABSGRAD>
+template <bool ABSGRAD, bool DEPTH>
 __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     __shared__ Stage<kBatchBwd> s;
     __shared__ int s_maxlast;
@@ -427,7 +437,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     const int start = p.offs[bin];
     const int lane = q.lane;
 
-    float Tfin = 1.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, vA = 0.f, bgdot = 0.f;
+    float Tfin = 1.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, vA = 0.f, bgdot = 0.f, vD = 0.f;
     int last = start - 1;
     if (q.inside) {
         const int64_t pix = ((int64_t)cam * p.H + q.py) * p.W + q.px;
@@ -438,6 +448,17 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
         v2 = p.v_rgb[3 * pix + 2];
         if (p.v_alpha) vA = p.v_alpha[pix];
         if (p.bg) bgdot = p.bg[3 * cam] * v0 + p.bg[3 * cam + 1] * v1 + p.bg[3 * cam + 2] * v2;
+        if (DEPTH) {
+            vD = p.v_depth[pix];
+            if (p.depth_mode == 2) {
+                // expected depth E = D / A, A = 1 - T_final: dL/dD = v_E / A and, through the
+                // alpha output (Q26), dL/dA += -v_E E / A
+                const float A = 1.f - Tfin;
+                const float vE = vD;
+                vD = A > 0.f ? vE / A : 0.f;
+                if (A > 0.f) vA -= vE * p.out_depth[pix] / A;
+            }
+        }
     }
     if (threadIdx.x == 0) s_maxlast = start - 1;
     __syncthreads();
@@ -471,12 +492,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                                      xy, G, alpha);
             const unsigned vb = __ballot_sync(0xffffffffu, valid);
             if (!vb) continue;
-#ifdef GS_EXP_EVALONLY
-            if (valid && alpha * T == 1234.5f) p.v_splats[s.id[j]] = 1.f;
-            continue;
-#endif
             float g8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // mx, my, o, A, B, C, r, g
-            float g_bl = 0.f;
+            float g_bl = 0.f, g_z = 0.f;
             if (valid) {
                 const float4 rgb = s.rgb[j];
                 const float ra = rcp_approx(1.f - alpha);
@@ -487,7 +504,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 g_bl = fac * v2;
                 // B4 + background / alpha-output terms (Q25, Q26):
                 // v_alpha = sum_ch (c T - S ra) v_C + kbg ra = T (c . v_C) + ra (kbg - Sv)
-                const float cv = rgb.x * v0 + rgb.y * v1 + rgb.z * v2;
+                float cv = rgb.x * v0 + rgb.y * v1 + rgb.z * v2;
+                if (DEPTH) {                       // depth as a fourth channel
+                    g_z = fac * vD;
+                    cv += xyo.w * vD;
+                }
                 const float v_alpha = T * cv + ra * (kbg - Sv);
                 Sv += cv * fac;                    // B5, dotted with v_C
                 const float raw = xyo.z * G;
@@ -506,15 +527,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 }
             }
             float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
-#ifdef GS_EXP_NORED
-            if (valid && g8[0] + g8[1] + g8[2] + g8[3] + g8[4] + g8[5] + g8[6] + g8[7] + g_bl == 1234.5f) dst[0] = 1.f;
-            continue;
-#endif
             if (__popc(vb) <= kFewLanes) {
                 // few contributing lanes: each issues its own three 16-byte reductions -- 3 warp
                 // instructions instead of the ~45 of the shuffle tree
                 if (valid) {
-                    red_add_v4(dst, g8[0], g8[1], g8[2], 0.f);
+                    red_add_v4(dst, g8[0], g8[1], g8[2], g_z);
                     red_add_v4(dst + 4, g8[3], g8[4], g8[5], ABSGRAD ? fabsf(g8[0]) : 0.f);
                     red_add_v4(dst + 8, g8[6], g8[7], g_bl, ABSGRAD ? fabsf(g8[1]) : 0.f);
                 }
@@ -523,12 +540,16 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             const float r8 = reduce_scatter8(g8, lane);
             if ((lane & 3) == 0) atomicAdd(dst + slot8(lane >> 2), r8);
             if (ABSGRAD) {
-                const float g4[4] = {g_bl, fabsf(g8[0]), fabsf(g8[1]), 0.f};
+                const float g4[4] = {g_bl, fabsf(g8[0]), fabsf(g8[1]), g_z};
                 const float r4 = reduce_scatter4(g4, lane);
-                if ((lane & 7) == 0 && (lane >> 3) < 3) atomicAdd(dst + slot4(lane >> 3), r4);
+                if ((lane & 7) == 0 && (DEPTH || (lane >> 3) < 3)) atomicAdd(dst + slot4(lane >> 3), r4);
             } else {
                 const float rb = warp_sum(g_bl);
                 if (lane == 0) atomicAdd(dst + 10, rb);
+                if (DEPTH) {
+                    const float rz = warp_sum(g_z);
+                    if (lane == 0) atomicAdd(dst + 3, rz);
+                }
             }
         }
     }
@@ -548,11 +569,15 @@ RasterParams make_params(const gs_options& o, int C, int64_t N, int W, int H, co
 
 gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats, const float* bg,
                             const int32_t* ids, const int32_t* offs, float* out_rgb, float* out_alpha, float* out_T,
-                            int32_t* last_ids, cudaStream_t s) {
+                            int32_t* last_ids, float* out_depth, int depth_mode, cudaStream_t s) {
     RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
     p.out_rgb = out_rgb; p.out_alpha = out_alpha; p.out_T = out_T; p.last_ids = last_ids;
+    p.out_depth = out_depth; p.depth_mode = out_depth ? depth_mode : 0;
     dim3 grid(p.TX * p.TY, C);
-    k_raster_fwd<false><<<grid, kThreads, 0, s>>>(p);
+    if (p.depth_mode)
+        k_raster_fwd<false, true><<<grid, kThreads, 0, s>>>(p);
+    else
+        k_raster_fwd<false, false><<<grid, kThreads, 0, s>>>(p);
     GS_LAUNCH_CHECK("k_raster_fwd");
     return GS_OK;
 }
@@ -563,27 +588,33 @@ gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int 
     RasterParams p = make_params(o, C, N, W, H, splats, nullptr, ids, offs);
     p.n_eval = n_eval; p.n_contrib = n_contrib;
     dim3 grid(p.TX * p.TY, C);
-    k_raster_fwd<true><<<grid, kThreads, 0, s>>>(p);
+    k_raster_fwd<true, false><<<grid, kThreads, 0, s>>>(p);
     GS_LAUNCH_CHECK("k_raster_fwd<stats>");
     return GS_OK;
 }
 
 gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats, const float* bg,
                             const int32_t* ids, const int32_t* offs, const float* out_T, const int32_t* last_ids,
-                            const float* v_rgb, const float* v_alpha, int absgrad, float* v_splats, cudaStream_t s) {
+                            const float* v_rgb, const float* v_alpha, const float* out_depth, const float* v_depth,
+                            int depth_mode, int absgrad, float* v_splats, cudaStream_t s) {
     RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
     p.out_T = const_cast<float*>(out_T); p.last_ids = const_cast<int32_t*>(last_ids);
     p.v_rgb = v_rgb; p.v_alpha = v_alpha; p.v_splats = v_splats; p.absgrad = absgrad;
+    p.out_depth = const_cast<float*>(out_depth); p.v_depth = v_depth;
+    p.depth_mode = v_depth ? depth_mode : 0;
     const size_t nrec = o.packed ? (size_t)N : (size_t)C * (size_t)N;   // packed: N records in total (Q29)
     if (N > 0 && cudaMemsetAsync(v_splats, 0, sizeof(float) * GS_SPLAT_FLOATS * nrec, s) != cudaSuccess) {
         GS_LAUNCH_CHECK("v_splats memset");
         return GS_ERR_CUDA;
     }
     dim3 grid(p.TX * p.TY, C);
-    if (absgrad)
-        k_raster_bwd<true><<<grid, kThreads, 0, s>>>(p);
-    else
-        k_raster_bwd<false><<<grid, kThreads, 0, s>>>(p);
+    if (absgrad) {
+        if (p.depth_mode) k_raster_bwd<true, true><<<grid, kThreads, 0, s>>>(p);
+        else k_raster_bwd<true, false><<<grid, kThreads, 0, s>>>(p);
+    } else {
+        if (p.depth_mode) k_raster_bwd<false, true><<<grid, kThreads, 0, s>>>(p);
+        else k_raster_bwd<false, false><<<grid, kThreads, 0, s>>>(p);
+    }
     GS_LAUNCH_CHECK("k_raster_bwd");
     return GS_OK;
 }

@@ -27,7 +27,8 @@ from . import dist as D
 
 class Engine:
     def __init__(self, N, C, width, height, sh_degree=3, K=None, antialiased=False, M_capacity=None,
-                 device="cuda", absgrad=False, with_keys=False, packed=False, nnz_capacity=None, **opt_kwargs):
+                 device="cuda", absgrad=False, with_keys=False, packed=False, nnz_capacity=None, depth_mode=0,
+                 pose=False, **opt_kwargs):
         self.N, self.C, self.W, self.H = int(N), int(C), int(width), int(height)
         self.sh_degree = int(sh_degree)
         self.K = (K if K is not None else (self.sh_degree + 1) ** 2) if self.sh_degree >= 0 else 1
@@ -35,6 +36,8 @@ class Engine:
         self.with_keys = bool(with_keys)
         self.device = torch.device(device)
         self.packed = bool(packed)
+        self.depth_mode = int(depth_mode)   # 0 off | 1 accumulated | 2 expected depth
+        self.pose = bool(pose)              # camera pose gradients
         self.opts = L.options(sh_degree=self.sh_degree, antialiased=antialiased, packed=self.packed, **opt_kwargs)
         self.TX, self.TY = L.tiles(self.W, self.H)
         dev = self.device
@@ -59,6 +62,12 @@ class Engine:
         self.out_alpha = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
         self.out_T = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
         self.last_ids = torch.zeros((C, H, W), dtype=torch.int32, device=dev)
+        self.out_depth = torch.zeros((C, H, W), dtype=torch.float32, device=dev) if self.depth_mode else None
+        self.v_viewmats = torch.zeros((C, 4, 4), dtype=torch.float32, device=dev) if self.pose else None
+        if self.pose and not self.packed:
+            self._pbwd_ws = self._aligned(L.gs_project_bwd_workspace_size(N, C))
+        elif not self.packed:
+            self._pbwd_ws = None
         # flat gradient buffer (the single all-reduce unit, dist.flat_layout)
         sh = self.sh_degree >= 0
         self.flat_layout, total = D.flat_layout(N, self.K, sh)
@@ -130,9 +139,10 @@ class Engine:
         raster fwd 1, bwd 1; project bwd 1."""
         bits = max(1, (self.C * self.TX * self.TY - 1).bit_length())
         P = (bits + 7) // 8
+        pose = 1 if self.pose else 0      # k_pose_reduce
         if self.packed:   # project: count, scan, write; isect: identity items; project bwd: map + kernel
-            return 3 + (1 + 12 + 3 + 1 + 3 * P + 2) + 1 + 1 + 2
-        return 1 + (3 + 12 + 3 + 1 + 3 * P + 2) + 1 + 1 + 1
+            return 3 + (1 + 12 + 3 + 1 + 3 * P + 2) + 1 + 1 + 2 + pose
+        return 1 + (3 + 12 + 3 + 1 + 3 * P + 2) + 1 + 1 + 1 + pose
 
     @property
     def n_isect(self) -> int:
@@ -161,23 +171,27 @@ class Engine:
     def rasterize_fwd(self, backgrounds=None, stream=None):
         L.gs_rasterize_fwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
                            self.isect_ids, self.tile_offsets, self.out_rgb, self.out_alpha, self.out_T,
-                           self.last_ids, stream)
+                           self.last_ids, self.out_depth, self.depth_mode, stream=stream)
 
-    def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, stream=None):
+    def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None):
         L.gs_rasterize_bwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
                            self.isect_ids, self.tile_offsets, self.out_T, self.last_ids, v_rgb, v_alpha,
-                           self.absgrad, self.v_splats, stream)
+                           self.absgrad, self.v_splats, out_depth=self.out_depth,
+                           v_out_depth=v_depth if self.depth_mode else None, depth_mode=self.depth_mode,
+                           stream=stream)
 
     def project_bwd(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
         if self.packed:
             L.gs_project_bwd_packed(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks,
                                     self.W, self.H, self.nnz_cap, self.nnz, self.camera_ids, self.gaussian_ids,
                                     self.radii, self.v_splats, self.v_means, self.v_quats, self.v_scales,
-                                    self.v_opacities, self.v_colors, self._pbwd_ws, stream)
+                                    self.v_opacities, self.v_colors, self._pbwd_ws, v_viewmats=self.v_viewmats,
+                                    stream=stream)
         else:
             L.gs_project_bwd(self.opts, means, quats, scales, opacities, colors, self.K, viewmats, Ks, self.W,
                              self.H, self.radii, self.v_splats, self.v_means, self.v_quats, self.v_scales,
-                             self.v_opacities, self.v_colors, stream)
+                             self.v_opacities, self.v_colors, v_viewmats=self.v_viewmats, workspace=self._pbwd_ws,
+                             stream=stream)
 
     def forward(self, means, quats, scales, opacities, colors, viewmats, Ks, backgrounds=None, stream=None):
         self.project(means, quats, scales, opacities, colors, viewmats, Ks, stream)
@@ -185,19 +199,19 @@ class Engine:
         self.rasterize_fwd(backgrounds, stream)
 
     def backward(self, means, quats, scales, opacities, colors, viewmats, Ks, v_rgb, v_alpha=None,
-                 backgrounds=None, stream=None):
-        self.rasterize_bwd(v_rgb, v_alpha, backgrounds, stream)
+                 backgrounds=None, v_depth=None, stream=None):
+        self.rasterize_bwd(v_rgb, v_alpha, backgrounds, v_depth, stream)
         self.project_bwd(means, quats, scales, opacities, colors, viewmats, Ks, stream)
 
-    def step(self, params, v_rgb, v_alpha=None, backgrounds=None, stream=None):
+    def step(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None):
         """One pass of the whole hot path (forward + backward) over one batch of views.
         params = (means, quats, scales, opacities, colors, viewmats, Ks)."""
         self.forward(*params, backgrounds=backgrounds, stream=stream)
-        self.backward(*params, v_rgb, v_alpha, backgrounds, stream)
+        self.backward(*params, v_rgb, v_alpha, backgrounds, v_depth, stream)
 
-    def run_checked(self, params, v_rgb, v_alpha=None, backgrounds=None):
+    def run_checked(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None):
         """step() with capacity growth (syncs once to read the overflow flag)."""
         while True:
-            self.step(params, v_rgb, v_alpha, backgrounds)
+            self.step(params, v_rgb, v_alpha, backgrounds, v_depth)
             if not self.ensure_capacity():
                 return

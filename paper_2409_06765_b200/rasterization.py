@@ -94,22 +94,31 @@ class _Rasterize(torch.autograd.Function):
         out_alpha = torch.empty((C, H, W), dtype=torch.float32, device=dev)
         out_T = torch.empty((C, H, W), dtype=torch.float32, device=dev)
         last_ids = torch.empty((C, H, W), dtype=torch.int32, device=dev)
-        L.gs_rasterize_fwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_rgb, out_alpha, out_T, last_ids)
+        depth_mode = cfg["depth_mode"]
+        out_depth = torch.empty((C, H, W) if depth_mode else (0,), dtype=torch.float32, device=dev)
+        L.gs_rasterize_fwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_rgb, out_alpha, out_T, last_ids,
+                           out_depth if depth_mode else None, depth_mode)
         if not packed:
             cam_ids = gid = torch.empty(0, dtype=torch.int32, device=dev)
             nnz_dev = torch.full((1,), C * N, dtype=torch.int64, device=dev)
         ctx.save_for_backward(means, quats, scales, opacities, colors, viewmats, Ks, backgrounds, radii, splats,
-                              ids, offs, out_T, last_ids, cam_ids, gid, nnz_dev)
+                              ids, offs, out_T, last_ids, cam_ids, gid, nnz_dev, out_depth)
         ctx.cfg = cfg
         ctx.n_rec = n_rec
         ctx.absgrad_out = absgrad_out
         ctx.mark_non_differentiable(radii, splats, ids, offs, out_T, last_ids, cam_ids, gid, nnz_dev)
-        return out_rgb, out_alpha, radii, splats, ids, offs, out_T, last_ids, Mdev, cam_ids, gid, nnz_dev
+        return out_rgb, out_alpha, out_depth, radii, splats, ids, offs, out_T, last_ids, Mdev, cam_ids, gid, nnz_dev
 
     @staticmethod
-    def backward(ctx, v_rgb, v_alpha, *unused):
+    def backward(ctx, v_rgb, v_alpha, v_depth, *unused):
         (means, quats, scales, opacities, colors, viewmats, Ks, backgrounds, radii, splats, ids, offs, out_T,
-         last_ids, cam_ids, gid, nnz_dev) = ctx.saved_tensors
+         last_ids, cam_ids, gid, nnz_dev, out_depth) = ctx.saved_tensors
+        depth_mode = ctx.cfg["depth_mode"]
+        if depth_mode and v_depth is not None:
+            v_depth = v_depth.contiguous()
+        else:
+            v_depth = None
+        pose = ctx.needs_input_grad[5]
         packed = bool(ctx.cfg["packed"])
         n_rec = ctx.n_rec
         cfg = ctx.cfg
@@ -121,7 +130,8 @@ class _Rasterize(torch.autograd.Function):
         v_splats = torch.empty_like(splats)
         absgrad = ctx.absgrad_out is not None
         L.gs_rasterize_bwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_T, last_ids, v_rgb, v_alpha,
-                           absgrad, v_splats)
+                           absgrad, v_splats, out_depth=out_depth if depth_mode else None, v_out_depth=v_depth,
+                           depth_mode=depth_mode)
         if absgrad:
             ag = torch.stack([v_splats[..., 7], v_splats[..., 11]], dim=-1)
             if packed:
@@ -135,20 +145,24 @@ class _Rasterize(torch.autograd.Function):
         v_scales = torch.empty_like(scales)
         v_opac = torch.empty_like(opacities)
         v_colors = torch.empty_like(colors)
+        v_view = torch.empty_like(viewmats) if pose else None
         if packed:
             ws = _aligned_ws(L.gs_project_bwd_packed_workspace_size(N, C), means.device)
             L.gs_project_bwd_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, n_rec, nnz_dev,
-                                    cam_ids, gid, radii, v_splats, v_means, v_quats, v_scales, v_opac, v_colors, ws)
+                                    cam_ids, gid, radii, v_splats, v_means, v_quats, v_scales, v_opac, v_colors, ws,
+                                    v_viewmats=v_view)
         else:
+            ws = _aligned_ws(L.gs_project_bwd_workspace_size(N, C), means.device) if pose else None
             L.gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, radii, v_splats,
-                             v_means, v_quats, v_scales, v_opac, v_colors)
+                             v_means, v_quats, v_scales, v_opac, v_colors, v_viewmats=v_view, workspace=ws)
         cfg["v_splats"] = v_splats
-        return v_means, v_quats, v_scales, v_opac, v_colors, None, None, None, None, None
+        return v_means, v_quats, v_scales, v_opac, v_colors, v_view, None, None, None, None
 
 
 def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, height, *, sh_degree=None,
                   near_plane=0.01, far_plane=1e10, eps2d=0.3, rasterize_mode="classic", tile_size=16,
-                  backgrounds=None, alpha_max=0.99, absgrad=False, fov_clamp=True, bbox_mode=0, packed=False):
+                  backgrounds=None, alpha_max=0.99, absgrad=False, fov_clamp=True, bbox_mode=0, packed=False,
+                  render_mode="RGB"):
     """Render C views of N Gaussians.
 
     means [N,3], quats [N,4] (w,x,y,z), scales [N,3] (activated), opacities [N] (activated),
@@ -156,21 +170,29 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
     Ks [C,3,3], backgrounds [C,3] or None.  rasterize_mode "classic" | "antialiased" (A.4).
     packed=True stores only the visible (camera, Gaussian) pairs (Q29): the per-item meta
     entries are then [nnz, ...] rows with meta["camera_ids"], meta["gaussian_ids"].
+    render_mode (App. "Depth rendering"): "RGB" | "D" (accumulated depth) | "ED"
+    (expected depth) | "RGB+D" | "RGB+ED"; depth is rendered in the same kernels as colour and
+    is the last channel of render_colors.  Gradients w.r.t. viewmats (camera pose)
+    are computed when viewmats.requires_grad.
     Returns render_colors [C,H,W,3], render_alphas [C,H,W,1] and a meta dict.
     """
     if rasterize_mode not in ("classic", "antialiased"):
         raise ValueError("rasterize_mode must be 'classic' or 'antialiased'")
+    modes = {"RGB": 0, "D": 1, "ED": 2, "RGB+D": 1, "RGB+ED": 2}
+    if render_mode not in modes:
+        raise ValueError(f"render_mode must be one of {sorted(modes)}")
+    depth_mode = modes[render_mode]
     deg = _sh_degree_of(colors, sh_degree)
     K = colors.shape[1] if deg >= 0 else 1
     o = L.options(sh_degree=deg, antialiased=rasterize_mode == "antialiased", near_plane=near_plane,
                   far_plane=far_plane, eps2d=eps2d, alpha_max=alpha_max, tile_size=tile_size, bbox_mode=bbox_mode,
                   fov_clamp=fov_clamp, packed=packed)
-    cfg = dict(opts=o, width=int(width), height=int(height), K=K, packed=bool(packed))
+    cfg = dict(opts=o, width=int(width), height=int(height), K=K, packed=bool(packed), depth_mode=depth_mode)
     C, N = viewmats.shape[0], means.shape[0]
     absgrad_out = torch.zeros((C, N, 2), device=means.device) if absgrad else None
     args = [t.contiguous() if t is not None else None for t in (means, quats, scales, opacities, colors, viewmats, Ks,
                                                               backgrounds)]
-    (out_rgb, out_alpha, radii, splats, ids, offs, out_T, last_ids, Mdev, cam_ids, gid,
+    (out_rgb, out_alpha, out_depth, radii, splats, ids, offs, out_T, last_ids, Mdev, cam_ids, gid,
      nnz_dev) = _Rasterize.apply(*args, cfg, absgrad_out)
     if packed:
         nnz = int(nnz_dev.item())
@@ -181,4 +203,10 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
                 width=int(width), height=int(height), tile_size=tile_size, n_cameras=C, absgrad=absgrad_out,
                 packed=bool(packed), camera_ids=cam_ids if packed else None, gaussian_ids=gid if packed else None,
                 cfg=cfg)
-    return out_rgb, out_alpha.unsqueeze(-1), meta
+    if render_mode in ("D", "ED"):
+        colors_out = out_depth.unsqueeze(-1)
+    elif render_mode in ("RGB+D", "RGB+ED"):
+        colors_out = torch.cat([out_rgb, out_depth.unsqueeze(-1)], dim=-1)
+    else:
+        colors_out = out_rgb
+    return colors_out, out_alpha.unsqueeze(-1), meta

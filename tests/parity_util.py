@@ -20,7 +20,7 @@ def to_torch(scene, device):
 
 
 def run_gpu(scene, *, antialiased=False, v_img=None, v_alpha=None, backgrounds=None, absgrad=False, device="cuda",
-            cap=None, packed=False, nnz_capacity=None, **opt):
+            cap=None, packed=False, nnz_capacity=None, depth_mode=0, v_depth=None, pose=False, **opt):
     import torch
     from paper_2409_06765_b200 import Engine
     C, N = scene["viewmats"].shape[0], scene["means"].shape[0]
@@ -28,14 +28,16 @@ def run_gpu(scene, *, antialiased=False, v_img=None, v_alpha=None, backgrounds=N
     deg = int(scene["sh_degree"])
     K = scene["colors"].shape[1] if deg >= 0 else None
     eng = Engine(N, C, W, H, sh_degree=deg, K=K, antialiased=antialiased, device=device, absgrad=absgrad,
-                 with_keys=True, M_capacity=cap, packed=packed, nnz_capacity=nnz_capacity, **opt)
+                 with_keys=True, M_capacity=cap, packed=packed, nnz_capacity=nnz_capacity, depth_mode=depth_mode,
+                 pose=pose, **opt)
     params = to_torch(scene, device)
     if v_img is None:
         v_img = np.zeros((C, H, W, 3), np.float32)
     v = torch.from_numpy(np.ascontiguousarray(v_img, dtype=np.float32)).to(device)
     va = None if v_alpha is None else torch.from_numpy(np.ascontiguousarray(v_alpha, np.float32)).to(device)
     bg = None if backgrounds is None else torch.from_numpy(np.ascontiguousarray(backgrounds, np.float32)).to(device)
-    eng.run_checked(params, v, va, bg)
+    vd = None if v_depth is None else torch.from_numpy(np.ascontiguousarray(v_depth, np.float32)).to(device)
+    eng.run_checked(params, v, va, bg, vd)
     torch.cuda.synchronize()
     M = eng.n_isect
     out = dict(
@@ -45,6 +47,10 @@ def run_gpu(scene, *, antialiased=False, v_img=None, v_alpha=None, backgrounds=N
         T=eng.out_T.cpu().numpy(), last_ids=eng.last_ids.cpu().numpy(), v_splats=eng.v_splats.cpu().numpy(),
         v_means=eng.v_means.cpu().numpy(), v_quats=eng.v_quats.cpu().numpy(), v_scales=eng.v_scales.cpu().numpy(),
         v_opacities=eng.v_opacities.cpu().numpy(), v_colors=eng.v_colors.cpu().numpy(), engine=eng)
+    if depth_mode:
+        out["depth"] = eng.out_depth.cpu().numpy()
+    if pose:
+        out["v_viewmats"] = eng.v_viewmats.cpu().numpy()
     if packed:
         nnz = int(eng.nnz.item())
         out.update(nnz=nnz, camera_ids=eng.camera_ids[:nnz].cpu().numpy(),

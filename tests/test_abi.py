@@ -51,7 +51,7 @@ def test_defaults_match_oracle_constants(L):
 
 def test_status_strings_and_version(L):
     lib = L.lib()
-    assert lib.gs_abi_version() == 2
+    assert lib.gs_abi_version() == 3
     assert lib.gs_status_string(0) == b"ok"
     assert lib.gs_status_string(2) == b"unsupported"
 
@@ -65,7 +65,17 @@ def test_validation_before_device_work(L):
     assert st == 1
     # bad dimensions
     assert lib.gs_project(ct.byref(o), -1, 1, 64, 64, *([null] * 5), 1, null, null, null, null, null) == 1
-    assert lib.gs_rasterize_fwd(ct.byref(o), 0, 1, 64, 64, *([null] * 8), null) == 1
+    assert lib.gs_rasterize_fwd(ct.byref(o), 0, 1, 64, 64, *([null] * 8), null, 0, null) == 1
+    # depth output with an unknown depth mode
+    assert lib.gs_rasterize_fwd(ct.byref(o), 1, 1, 64, 64, *([null] * 8), 16, 3, null) == 1
+    # pose gradients without a workspace
+    assert lib.gs_project_bwd(ct.byref(o), 0, 1, 64, 64, *([null] * 5), 1, null, null, null, null, null, null,
+                              null, null, null, 16, null, 0, null) == 1
+    # packed entry points refuse dense options and vice versa
+    assert lib.gs_project_packed(ct.byref(o), 0, 1, 64, 64, *([null] * 5), 1, null, null, 0, 8, 8, null, null,
+                                 null, null, 256, 1 << 20, null) == 1
+    op = L.options(packed=True)
+    assert lib.gs_project(ct.byref(op), 0, 1, 64, 64, *([null] * 5), 1, null, null, null, null, null) == 1
     # unsupported tile size
     o2 = L.options(tile_size=8)
     assert lib.gs_project(ct.byref(o2), 10, 1, 64, 64, *([null] * 5), 1, null, null, null, null, null) == 2

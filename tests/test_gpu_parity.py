@@ -379,3 +379,76 @@ def test_packed_capacity_growth():
 def test_config5_aa_packed_full_scale_sampled():
     """BASELINE configs[4]: 1M Gaussians, antialiased, packed, 4 views of 1297x840."""
     _full_scale_sampled("aa_packed1m", seed=5, packed=True, antialiased=True)
+
+
+# ---- depth rendering (NEXT-2, P:241-262) and camera pose gradients (NEXT-3, P:233-239) ----
+DEPTH_RTOL = 1e-5        # depth maps: fp32 sums of z alpha T, relative to the scene depth scale
+
+
+@pytest.mark.parametrize("name,mode,packed", [("tiny_sh3_ragged", 1, False), ("mip_small", 2, False),
+                                              ("mip_small_aa", 2, True), ("rgb_direct", 1, False)])
+def test_depth_and_pose_parity(name, mode, packed):
+    """Depth channel (accumulated, mode 1; expected, mode 2) against the oracle; its gradients
+    into v_splats slot 3 and through t_z; camera pose gradients against the oracle's."""
+    sc, kw = _scene(name)
+    aa = kw.get("antialiased", 0)
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    v_img, _ = S.image_grads(7, C, H, W, l1_scale=False)
+    v_d = np.random.default_rng(8).normal(size=(C, H, W)).astype(np.float32) * 0.05
+    o = oracle.Options(sh_degree=sc["sh_degree"], antialiased=aa)
+    p = oracle.project(sc, o)
+    f = oracle.render_fwd(p, C, N, W, H, o)
+    amb = f["ambig"].astype(bool)
+    v_img[amb] = 0
+    v_d[amb] = 0
+    gpu = U.run_gpu(sc, antialiased=aa, v_img=v_img, depth_mode=mode, v_depth=v_d, pose=True, packed=packed)
+    ref_d = f["depth"] if mode == 1 else f["depth_exp"]
+    zmax = np.abs(p["depth"][p["radii"][..., 0] > 0]).max()
+    ok = ~amb
+    assert np.abs(gpu["depth"] - ref_d)[ok].max() <= DEPTH_RTOL * zmax + U.IMG_ATOL
+    assert np.abs(gpu["rgb"] - f["rgb"])[ok].max() <= U.IMG_ATOL
+    kw_d = dict(v_depth=v_d.astype(np.float64)) if mode == 1 else dict(v_depth_exp=v_d.astype(np.float64))
+    b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64), **kw_d)
+    vis = p["radii"][..., 0] > 0
+    if packed:
+        cam, gid, _ = oracle.pack(p)
+        vs = U.unpack(gpu["v_splats"], cam, gid, C, N)
+    else:
+        vs = gpu["v_splats"]
+    bad = U.check_grad2d(U.v2d_from_splats(vs), b["v2d"], b["a2d"], vis, b["s2d"])
+    assert bad.sum() == 0, bad.sum()
+    # slot 3: d L / d depth of each (c, n), same tolerance model
+    badz = U.check_grad2d(vs[..., 3:4], b["vz"][..., None], b["az"][..., None], vis, b["sz"][..., None])
+    assert badz.sum() == 0, badz.sum()
+    g = oracle.project_bwd(sc, p, b["v2d"], o, vz=b["vz"], pose=True)
+    for k in ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]:
+        badk, rel = U.check_grad3d(gpu[k], g[k], vis.any(axis=0))
+        assert rel <= U.GRAD_RTOL, (k, rel)
+    # pose: per camera, relative L2 over the 12 entries of rows 0..2
+    for c in range(C):
+        r = g["v_viewmats"][c, :3].reshape(-1)
+        d = gpu["v_viewmats"][c, :3].reshape(-1) - r
+        assert np.linalg.norm(d) <= U.GRAD_RTOL * np.linalg.norm(r) + 1e-9, (c, gpu["v_viewmats"][c], g["v_viewmats"][c])
+        assert np.all(gpu["v_viewmats"][c, 3] == 0)
+
+
+def test_render_modes_api():
+    """render_mode through the public API: RGB+ED = [RGB | expected depth] and its gradients
+    equal the engine's; viewmats.requires_grad yields the pose gradient."""
+    import torch
+    from paper_2409_06765_b200 import rasterization
+    sc = S.tiny_scene(1, N=1500, width=200, height=150, sh_degree=3, views=2)
+    dev = "cuda"
+    ts = [t.clone().requires_grad_(i < 6) for i, t in enumerate(U.to_torch(sc, dev))]
+    out, alpha, meta = rasterization(*ts, 200, 150, sh_degree=3, render_mode="RGB+ED")
+    assert out.shape == (2, 150, 200, 4)
+    v, _ = S.image_grads(3, 2, 150, 200, l1_scale=False)
+    vd = np.random.default_rng(9).normal(size=(2, 150, 200)).astype(np.float32) * 0.05
+    loss = (out[..., :3] * torch.from_numpy(v).to(dev)).sum() + (out[..., 3] * torch.from_numpy(vd).to(dev)).sum()
+    loss.backward()
+    gpu = U.run_gpu(sc, v_img=v, depth_mode=2, v_depth=vd, pose=True)
+    assert np.array_equal(out[..., 3].detach().cpu().numpy(), gpu["depth"])
+    for t, k in zip(ts[:6], ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors", "v_viewmats"]):
+        np.testing.assert_allclose(t.grad.cpu().numpy(), gpu[k], rtol=1e-4, atol=1e-5 * np.abs(gpu[k]).max())
+    d, _, _ = rasterization(*[t.detach() for t in ts], 200, 150, sh_degree=3, render_mode="D")
+    assert d.shape == (2, 150, 200, 1)
