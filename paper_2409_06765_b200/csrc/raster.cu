@@ -492,40 +492,42 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                                      xy, G, alpha);
             const unsigned vb = __ballot_sync(0xffffffffu, valid);
             if (!vb) continue;
-            float g8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // mx, my, o, A, B, C, r, g
-            float g_bl = 0.f, g_z = 0.f;
-            if (valid) {
-                const float4 rgb = s.rgb[j];
-                const float ra = rcp_approx(1.f - alpha);
-                T = T * ra;                        // B2: T_{n-1} = T_n / (1 - alpha_{n-1})
-                const float fac = alpha * T;
-                g8[6] = fac * v0;                  // B3
-                g8[7] = fac * v1;
-                g_bl = fac * v2;
-                // B4 + background / alpha-output terms (Q25, Q26):
-                // v_alpha = sum_ch (c T - S ra) v_C + kbg ra = T (c . v_C) + ra (kbg - Sv)
-                float cv = rgb.x * v0 + rgb.y * v1 + rgb.z * v2;
-                if (DEPTH) {                       // depth as a fourth channel
-                    g_z = fac * vD;
-                    cv += xyo.w * vD;
-                }
-                const float v_alpha = T * cv + ra * (kbg - Sv);
-                Sv += cv * fac;                    // B5, dotted with v_C
-                const float raw = xyo.z * G;
-                if (raw < p.alpha_max) {           // B6 (Q24)
-                    g8[2] = G * v_alpha;
-                    const float v_sigma = -raw * v_alpha;
-                    const float hv = 0.5f * v_sigma;
-                    g8[3] = hv * xx;
-                    g8[4] = v_sigma * xy;
-                    g8[5] = hv * yy;
-                    // d sigma / d mu' = Sigma'^-1 Delta, with the conic recovered from
-                    // the pre-scaled one: A = a' (-2 ln2), B = b' (-ln2), C = c' (-2 ln2)
-                    const float k2 = -kLn2 * v_sigma;
-                    g8[0] = k2 * (2.f * con.x * dx + con.y * dy);
-                    g8[1] = k2 * (con.y * dx + 2.f * con.z * dy);
-                }
+            // Branch-free from here: a lane that does not take this splat gets alpha = G = 0,
+            // which makes every gradient term below exactly 0 and leaves T and Sv unchanged.
+            G = valid ? G : 0.f;
+            alpha = valid ? alpha : 0.f;
+            float g8[8];   // mx, my, o, A, B, C, r, g
+            const float4 rgb = s.rgb[j];
+            const float ra = rcp_approx(1.f - alpha);
+            T = valid ? T * ra : T;            // B2: T_{n-1} = T_n / (1 - alpha_{n-1})
+            const float fac = alpha * T;
+            g8[6] = fac * v0;                  // B3
+            g8[7] = fac * v1;
+            const float g_bl = fac * v2;
+            // B4 + background / alpha-output terms (Q25, Q26):
+            // v_alpha = sum_ch (c T - S ra) v_C + kbg ra = T (c . v_C) + ra (kbg - Sv)
+            float cv = rgb.x * v0 + rgb.y * v1 + rgb.z * v2;
+            float g_z = 0.f;
+            if (DEPTH) {                       // depth as a fourth channel
+                g_z = fac * vD;
+                cv += xyo.w * vD;
             }
+            const float v_alpha = T * cv + ra * (kbg - Sv);
+            Sv += cv * fac;                    // B5, dotted with v_C
+            const float raw = xyo.z * G;
+            // B6 (Q24): no gradient through the alpha_max clamp
+            const float va = raw < p.alpha_max ? v_alpha : 0.f;
+            g8[2] = G * va;
+            const float v_sigma = -raw * va;
+            const float hv = 0.5f * v_sigma;
+            g8[3] = hv * xx;
+            g8[4] = v_sigma * xy;
+            g8[5] = hv * yy;
+            // d sigma / d mu' = Sigma'^-1 Delta, with the conic recovered from the
+            // pre-scaled one: A = a' (-2 ln2), B = b' (-ln2), C = c' (-2 ln2)
+            const float k2 = -kLn2 * v_sigma;
+            g8[0] = k2 * (2.f * con.x * dx + con.y * dy);
+            g8[1] = k2 * (con.y * dx + 2.f * con.z * dy);
             float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
             if (__popc(vb) <= kFewLanes) {
                 // few contributing lanes: each issues its own three 16-byte reductions -- 3 warp
