@@ -100,25 +100,38 @@ __device__ __forceinline__ bool eval_alpha_q(float mx, float my, float o, float4
 // L_r = x_-(clamp(-dy_R, slab)).  The result is a 4-bit mask of 4-pixel-wide columns per
 // row: bit 4 r + k of the returned 16-bit mask is the 4x4 block at column k, row r.
 // Ill-conditioned conics (eps >= 1e-2) fall back to the axis-aligned box of E.
+// Approximate MUFU square root / reciprocal (relative error ~2^-22): the support test
+// below only needs them inside its margins.
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx_f(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ uint32_t support_mask16(float mx, float my, float o, float A, float B, float Cc, float a,
                                                    float c, float x0, float y0, float alpha_min) {
     if (o < alpha_min * 0.9999f) return 0u;   // alpha = min(alpha_max, o G) <= o (G <= 1)
-    float tau = fmaxf(0.f, __logf(o / alpha_min));
+    float tau = fmaxf(0.f, __logf(__fdividef(o, alpha_min)));
     tau = tau * 1.004f + 4e-3f;
     const float eps = 1e-6f * a * A;
     const float grow = 1.f + eps;
-    const float hx0 = sqrtf(2.f * tau * a), hy0 = sqrtf(2.f * tau * c);
+    const float hx0 = sqrt_approx(2.f * tau * a), hy0 = sqrt_approx(2.f * tau * c);
     const float hx = hx0 * grow + 1e-2f;
     const float hy = hy0 * grow + 1e-2f;
     if (!(hx < 1e30f) || !(hy < 1e30f)) return 0xffffu;
     const float u = mx - x0, v = my - y0;
     const bool ell = eps < 1e-2f;
-    const float mfrac = 2.f * sqrtf(eps) + eps;
+    const float mfrac = 2.f * sqrt_approx(eps) + eps;
     const float mxm = hx0 * mfrac + 1e-2f, mym = hy0 * mfrac + 1e-2f;
     const float det = A * Cc - B * B;
     const float s2 = 2.f * A * tau;
-    const float iA = 1.f / A;
-    const float dyR = -B * hx0 / Cc;
+    const float iA = rcp_approx_f(A);
+    const float dyR = -B * hx0 * rcp_approx_f(Cc);
     uint32_t m = 0;
 #pragma unroll
     for (int r = 0; r < 4; r++) {
@@ -129,8 +142,8 @@ __device__ __forceinline__ uint32_t support_mask16(float mx, float my, float o, 
             const float ylo = lo - mym, yhi = hi + mym;
             const float d1 = fminf(fmaxf(dyR, ylo), yhi);
             const float d2 = fminf(fmaxf(-dyR, ylo), yhi);
-            const float R1 = (-B * d1 + sqrtf(fmaxf(0.f, s2 - det * d1 * d1))) * iA + mxm;
-            const float L1 = (-B * d2 - sqrtf(fmaxf(0.f, s2 - det * d2 * d2))) * iA - mxm;
+            const float R1 = (-B * d1 + sqrt_approx(fmaxf(0.f, s2 - det * d1 * d1))) * iA + mxm;
+            const float L1 = (-B * d2 - sqrt_approx(fmaxf(0.f, s2 - det * d2 * d2))) * iA - mxm;
             R = fminf(R, R1);
             L = fmaxf(L, L1);
         }
