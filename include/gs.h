@@ -100,7 +100,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 3
+#define GS_ABI_VERSION 4
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -149,11 +149,16 @@ GS_API gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int
  * Depth rendering (App. "Depth rendering"; NULL out_depth = off): out_depth
  *      [C,H,W] = the accumulated depth sum z alpha T (depth_mode 1) or the expected
  *      depth = that sum / sum alpha T, with sum alpha T = 1 - T_final, 0 where nothing was
- *      composited (depth_mode 2); z = record slot 3.  No background term. */
+ *      composited (depth_mode 2); z = record slot 3.  No background term.
+ * isect_masks [M] uint16 (optional, NULL to skip): per intersection, the 16-bit mask of the
+ *      4x4 pixel blocks of its tile that can take the splat with alpha >= alpha_min (the
+ *      conservative support test of DESIGN.md K6; output-invariant).  Pass it to
+ *      gs_rasterize_bwd of the same forward to save that kernel recomputing it. */
 GS_API gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, float* out_rgb, float* out_alpha, float* out_T,
-                           int32_t* last_ids, float* out_depth, int32_t depth_mode, void* stream);
+                           int32_t* last_ids, float* out_depth, int32_t depth_mode, uint16_t* isect_masks,
+                           void* stream);
 
 /* ---- Diagnostics (not on the hot path): per-pixel work counts of stage 3 ---------
  * Runs the forward walk of gs_rasterize_fwd and writes, per pixel, n_eval [C,H,W] (pairs
@@ -173,13 +178,14 @@ GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N,
  * Depth (NULL v_out_depth = off): v_out_depth [C,H,W] = dL/d out_depth of the forward
  *      with the same depth_mode; depth is composited as a fourth channel, its per-splat
  *      gradient accumulates into slot 3; mode 2 (expected depth D/A) also needs the
- *      forward's out_depth and adds -v E / A to the alpha gradient (quotient rule, Q26). */
+ *      forward's out_depth and adds -v E / A to the alpha gradient (quotient rule, Q26).
+ * isect_masks: the forward's mask output or NULL (recomputed). */
 GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
                            const float* v_out_rgb, const float* v_out_alpha, const float* out_depth,
                            const float* v_out_depth, int32_t depth_mode, int32_t absgrad,
-                           float* v_splats, void* stream);
+                           const uint16_t* isect_masks, float* v_splats, void* stream);
 
 /* ---- Stage 4b: projection backward (P1-P9) -------------------------------
  * In : the gs_project inputs, its radii output, v_splats from gs_rasterize_bwd.

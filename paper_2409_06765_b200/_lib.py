@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 
@@ -45,10 +45,10 @@ SIGNATURES = {
     "gs_project": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "gs_isect_workspace_size": (_SZ, [_I32, _I64, _I32, _I32, _I64]),
     "gs_isect_tiles": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
-    "gs_rasterize_fwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
+    "gs_rasterize_fwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
     "gs_rasterize_stats": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P,
-                                _P]),
+                                _P, _P]),
     "gs_project_bwd_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                               _P, _P, _P, _P, _SZ, _P]),
@@ -152,13 +152,13 @@ def gs_isect_tiles(o, C, N, width, height, radii, splats, cap, M, overflow, isec
 
 
 def gs_rasterize_fwd(o, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_rgb, out_alpha,
-                     out_T, last_ids, out_depth=None, depth_mode=0, stream=None):
+                     out_T, last_ids, out_depth=None, depth_mode=0, isect_masks=None, stream=None):
     check(lib().gs_rasterize_fwd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
                                  ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
                                  ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_rgb, name="out_rgb"),
                                  ptr(out_alpha, name="out_alpha"), ptr(out_T, name="out_T"),
                                  ptr(last_ids, torch.int32, "last_ids"), ptr(out_depth, name="out_depth"),
-                                 int(depth_mode), stream_ptr(stream)),
+                                 int(depth_mode), ptr(isect_masks, torch.int16, "isect_masks"), stream_ptr(stream)),
           "gs_rasterize_fwd")
 
 
@@ -172,14 +172,15 @@ def gs_rasterize_stats(o, C, N, width, height, splats, isect_ids, tile_offsets, 
 
 def gs_rasterize_bwd(o, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T, last_ids,
                      v_out_rgb, v_out_alpha, absgrad, v_splats, out_depth=None, v_out_depth=None, depth_mode=0,
-                     stream=None):
+                     isect_masks=None, stream=None):
     check(lib().gs_rasterize_bwd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
                                  ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
                                  ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_T, name="out_T"),
                                  ptr(last_ids, torch.int32, "last_ids"), ptr(v_out_rgb, name="v_out_rgb"),
                                  ptr(v_out_alpha, name="v_out_alpha"), ptr(out_depth, name="out_depth"),
                                  ptr(v_out_depth, name="v_out_depth"), int(depth_mode), int(bool(absgrad)),
-                                 ptr(v_splats, name="v_splats"), stream_ptr(stream)),
+                                 ptr(isect_masks, torch.int16, "isect_masks"), ptr(v_splats, name="v_splats"),
+                                 stream_ptr(stream)),
           "gs_rasterize_bwd")
 
 

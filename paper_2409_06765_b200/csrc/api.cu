@@ -126,7 +126,8 @@ gs_status gs_isect_tiles(const gs_options* opt, int32_t C, int64_t N, int32_t wi
 gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, float* out_rgb, float* out_alpha, float* out_T,
-                           int32_t* last_ids, float* out_depth, int32_t depth_mode, void* stream) {
+                           int32_t* last_ids, float* out_depth, int32_t depth_mode, uint16_t* isect_masks,
+                           void* stream) {
     GS_TRY(check_opts(opt));
     GS_TRY(check_dims(N, C, width, height));
     GS_REQ(tile_offsets && out_rgb && out_alpha && out_T && last_ids);
@@ -134,7 +135,7 @@ gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
     GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(backgrounds) && aligned4(out_rgb) &&
            aligned4(out_alpha) && aligned4(out_T) && aligned4(last_ids) && aligned4(out_depth));
     return gsb::launch_raster_fwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_rgb,
-                                  out_alpha, out_T, last_ids, out_depth, depth_mode,
+                                  out_alpha, out_T, last_ids, out_depth, depth_mode, isect_masks,
                                   static_cast<cudaStream_t>(stream));
 }
 
@@ -153,8 +154,8 @@ gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
                            const float* v_out_rgb, const float* v_out_alpha, const float* out_depth,
-                           const float* v_out_depth, int32_t depth_mode, int32_t absgrad, float* v_splats,
-                           void* stream) {
+                           const float* v_out_depth, int32_t depth_mode, int32_t absgrad,
+                           const uint16_t* isect_masks, float* v_splats, void* stream) {
     GS_TRY(check_opts(opt));
     GS_TRY(check_dims(N, C, width, height));
     GS_REQ(tile_offsets && out_T && last_ids && v_out_rgb && (v_splats || N == 0));
@@ -164,7 +165,7 @@ gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
            aligned4(out_depth) && aligned4(v_out_depth));
     return gsb::launch_raster_bwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T,
                                   last_ids, v_out_rgb, v_out_alpha, out_depth, v_out_depth, depth_mode, absgrad,
-                                  v_splats, static_cast<cudaStream_t>(stream));
+                                  isect_masks, v_splats, static_cast<cudaStream_t>(stream));
 }
 
 size_t gs_project_bwd_workspace_size(int64_t N, int32_t C) {

@@ -68,7 +68,7 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
 gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                             const float* bg, const int32_t* ids, const int32_t* offs, float* out_rgb,
                             float* out_alpha, float* out_T, int32_t* last_ids, float* out_depth, int depth_mode,
-                            cudaStream_t s);
+                            uint16_t* isect_masks, cudaStream_t s);
 gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                               const int32_t* ids, const int32_t* offs, int32_t* n_eval, int32_t* n_contrib,
                               cudaStream_t s);
@@ -76,6 +76,6 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
                             const float* bg, const int32_t* ids, const int32_t* offs, const float* out_T,
                             const int32_t* last_ids, const float* v_rgb, const float* v_alpha,
                             const float* out_depth, const float* v_depth, int depth_mode, int absgrad,
-                            float* v_splats, cudaStream_t s);
+                            const uint16_t* isect_masks, float* v_splats, cudaStream_t s);
 
 }  // namespace gsb

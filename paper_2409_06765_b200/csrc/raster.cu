@@ -193,6 +193,9 @@ struct RasterParams {
     // diagnostics (gs_rasterize_stats)
     int32_t* n_eval;
     int32_t* n_contrib;
+    // support masks of every staged (intersection) slot, written by K6 and read back by K7
+    // (NULL: K7 recomputes them)
+    uint16_t* smask;
 };
 
 struct PixelCoord {
@@ -236,7 +239,9 @@ __device__ __forceinline__ void stage_splat(const RasterParams& p, StageT& s, in
     s.con[slot] = prescale_conic(r1.x, r1.y, r1.z);
     s.rgb[slot] = r2;
     s.id[slot] = g;
-    s.mask[slot] = (uint8_t)support_mask8(support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, p.alpha_min));
+    const uint32_t m16 = p.smask ? (uint32_t)p.smask[idx]
+                                 : support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, p.alpha_min);
+    s.mask[slot] = (uint8_t)support_mask8(m16);
 }
 
 // Order-preserving compaction of the batch slots [0, n) whose mask has this warp's bit
@@ -298,7 +303,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             s.xyo[t] = r0;
             s.con[t] = prescale_conic(r1.x, r1.y, r1.z);
             s.rgb[t] = r2;
-            s.mask[t] = (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, amin);
+            const uint16_t m16 = (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, amin);
+            s.mask[t] = m16;
+            if (!STATS && p.smask) p.smask[b0 + t] = m16;   // for K7 (every slot K7 can stage is staged here)
         }
         __syncthreads();
         if (__all_sync(0xffffffffu, done)) continue;
@@ -584,9 +591,11 @@ RasterParams make_params(const gs_options& o, int C, int64_t N, int W, int H, co
 
 gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats, const float* bg,
                             const int32_t* ids, const int32_t* offs, float* out_rgb, float* out_alpha, float* out_T,
-                            int32_t* last_ids, float* out_depth, int depth_mode, cudaStream_t s) {
+                            int32_t* last_ids, float* out_depth, int depth_mode, uint16_t* isect_masks,
+                            cudaStream_t s) {
     RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
     p.out_rgb = out_rgb; p.out_alpha = out_alpha; p.out_T = out_T; p.last_ids = last_ids;
+    p.smask = isect_masks;
     p.out_depth = out_depth; p.depth_mode = out_depth ? depth_mode : 0;
     dim3 grid(p.TX * p.TY, C);
     if (p.depth_mode)
@@ -611,8 +620,10 @@ gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int 
 gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats, const float* bg,
                             const int32_t* ids, const int32_t* offs, const float* out_T, const int32_t* last_ids,
                             const float* v_rgb, const float* v_alpha, const float* out_depth, const float* v_depth,
-                            int depth_mode, int absgrad, float* v_splats, cudaStream_t s) {
+                            int depth_mode, int absgrad, const uint16_t* isect_masks, float* v_splats,
+                            cudaStream_t s) {
     RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
+    p.smask = const_cast<uint16_t*>(isect_masks);
     p.out_T = const_cast<float*>(out_T); p.last_ids = const_cast<int32_t*>(last_ids);
     p.v_rgb = v_rgb; p.v_alpha = v_alpha; p.v_splats = v_splats; p.absgrad = absgrad;
     p.out_depth = const_cast<float*>(out_depth); p.v_depth = v_depth;

@@ -112,6 +112,8 @@ class Engine:
             return
         self.cap = cap
         self.isect_ids = torch.zeros(max(cap, 1), dtype=torch.int32, device=self.device)
+        # per-intersection support masks: written by the forward raster, read by the backward
+        self.isect_masks = torch.zeros(max(cap, 1), dtype=torch.int16, device=self.device)
         self.isect_keys = torch.zeros(max(cap, 1), dtype=torch.int64, device=self.device) if self.with_keys else None
         if self.packed:
             ws = L.gs_isect_packed_workspace_size(self.C, self.nnz_cap, self.W, self.H, cap)
@@ -171,14 +173,15 @@ class Engine:
     def rasterize_fwd(self, backgrounds=None, stream=None):
         L.gs_rasterize_fwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
                            self.isect_ids, self.tile_offsets, self.out_rgb, self.out_alpha, self.out_T,
-                           self.last_ids, self.out_depth, self.depth_mode, stream=stream)
+                           self.last_ids, self.out_depth, self.depth_mode, isect_masks=self.isect_masks,
+                           stream=stream)
 
     def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None):
         L.gs_rasterize_bwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
                            self.isect_ids, self.tile_offsets, self.out_T, self.last_ids, v_rgb, v_alpha,
                            self.absgrad, self.v_splats, out_depth=self.out_depth,
                            v_out_depth=v_depth if self.depth_mode else None, depth_mode=self.depth_mode,
-                           stream=stream)
+                           isect_masks=self.isect_masks, stream=stream)
 
     def project_bwd(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
         if self.packed:

@@ -96,13 +96,14 @@ class _Rasterize(torch.autograd.Function):
         last_ids = torch.empty((C, H, W), dtype=torch.int32, device=dev)
         depth_mode = cfg["depth_mode"]
         out_depth = torch.empty((C, H, W) if depth_mode else (0,), dtype=torch.float32, device=dev)
+        masks = torch.empty(max(cap, 1), dtype=torch.int16, device=dev)
         L.gs_rasterize_fwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_rgb, out_alpha, out_T, last_ids,
-                           out_depth if depth_mode else None, depth_mode)
+                           out_depth if depth_mode else None, depth_mode, isect_masks=masks)
         if not packed:
             cam_ids = gid = torch.empty(0, dtype=torch.int32, device=dev)
             nnz_dev = torch.full((1,), C * N, dtype=torch.int64, device=dev)
         ctx.save_for_backward(means, quats, scales, opacities, colors, viewmats, Ks, backgrounds, radii, splats,
-                              ids, offs, out_T, last_ids, cam_ids, gid, nnz_dev, out_depth)
+                              ids, offs, out_T, last_ids, cam_ids, gid, nnz_dev, out_depth, masks)
         ctx.cfg = cfg
         ctx.n_rec = n_rec
         ctx.absgrad_out = absgrad_out
@@ -112,7 +113,7 @@ class _Rasterize(torch.autograd.Function):
     @staticmethod
     def backward(ctx, v_rgb, v_alpha, v_depth, *unused):
         (means, quats, scales, opacities, colors, viewmats, Ks, backgrounds, radii, splats, ids, offs, out_T,
-         last_ids, cam_ids, gid, nnz_dev, out_depth) = ctx.saved_tensors
+         last_ids, cam_ids, gid, nnz_dev, out_depth, masks) = ctx.saved_tensors
         depth_mode = ctx.cfg["depth_mode"]
         if depth_mode and v_depth is not None:
             v_depth = v_depth.contiguous()
@@ -131,7 +132,7 @@ class _Rasterize(torch.autograd.Function):
         absgrad = ctx.absgrad_out is not None
         L.gs_rasterize_bwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_T, last_ids, v_rgb, v_alpha,
                            absgrad, v_splats, out_depth=out_depth if depth_mode else None, v_out_depth=v_depth,
-                           depth_mode=depth_mode)
+                           depth_mode=depth_mode, isect_masks=masks)
         if absgrad:
             ag = torch.stack([v_splats[..., 7], v_splats[..., 11]], dim=-1)
             if packed:

@@ -51,7 +51,7 @@ def test_defaults_match_oracle_constants(L):
 
 def test_status_strings_and_version(L):
     lib = L.lib()
-    assert lib.gs_abi_version() == 3
+    assert lib.gs_abi_version() == 4
     assert lib.gs_status_string(0) == b"ok"
     assert lib.gs_status_string(2) == b"unsupported"
 
@@ -65,9 +65,9 @@ def test_validation_before_device_work(L):
     assert st == 1
     # bad dimensions
     assert lib.gs_project(ct.byref(o), -1, 1, 64, 64, *([null] * 5), 1, null, null, null, null, null) == 1
-    assert lib.gs_rasterize_fwd(ct.byref(o), 0, 1, 64, 64, *([null] * 8), null, 0, null) == 1
+    assert lib.gs_rasterize_fwd(ct.byref(o), 0, 1, 64, 64, *([null] * 8), null, 0, null, null) == 1
     # depth output with an unknown depth mode
-    assert lib.gs_rasterize_fwd(ct.byref(o), 1, 1, 64, 64, *([null] * 8), 16, 3, null) == 1
+    assert lib.gs_rasterize_fwd(ct.byref(o), 1, 1, 64, 64, *([null] * 8), 16, 3, null, null) == 1
     # pose gradients without a workspace
     assert lib.gs_project_bwd(ct.byref(o), 0, 1, 64, 64, *([null] * 5), 1, null, null, null, null, null, null,
                               null, null, null, 16, null, 0, null) == 1
