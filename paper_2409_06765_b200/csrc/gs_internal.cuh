@@ -24,6 +24,29 @@ void set_last_error(const char* where, cudaError_t e);
 
 namespace gsb {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl() may be
+// scheduled while its predecessor in the stream is still running; it calls pdl_trigger()
+// (let ITS successor launch early) and pdl_wait() (block until the predecessor grid has
+// completed and its memory is visible) before touching anything the predecessor wrote.
+// This hides the launch / ramp-up latency of the many short kernels of stage 2.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __host__ __device__ inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 inline int tile_bits(int ntiles) {

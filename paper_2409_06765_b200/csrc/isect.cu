@@ -86,6 +86,8 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* tot
 __global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, int tile, const int* d_n, int64_t n_host,
                                                                int64_t cap, int* total_i32, int64_t* total_i64,
                                                                int32_t* overflow, int64_t ovf_cap, int* clamped_n) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_warp[33];
     const int n = (int)min(d_n ? (int64_t)*d_n : n_host, cap);
     const int nb = div_up(n, tile);
@@ -111,6 +113,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, int 
 // contiguous slice [base + 512 w, base + 512 (w+1)) and walks it in 16 coalesced rounds of
 // 32; its ballots give every visible item its rank inside the slice without block syncs.
 __global__ void __launch_bounds__(kT) k_vis_count(const int2* __restrict__ radii, int64_t n_items, int* blocksum) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_warp[33];
     const int64_t base = (int64_t)blockIdx.x * kTile;
     int cnt = 0;
@@ -130,6 +134,8 @@ __global__ void __launch_bounds__(kT) k_vis_count(const int2* __restrict__ radii
 __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ radii, const float* __restrict__ splats,
                                                    int64_t n_items, const int* __restrict__ blockoff,
                                                    uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_wtot[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = (int64_t)blockIdx.x * kTile + warp * (kTile / kWarps);
@@ -167,6 +173,8 @@ __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ rad
 // count V = min(*nnz, cap) (Q29).
 __global__ void k_packed_items(const float* __restrict__ splats, const int64_t* d_nnz, int64_t cap, int* d_V,
                                uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+    pdl_trigger();
+    pdl_wait();
     const int V = (int)min(*d_nnz, cap);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) *d_V = V;
@@ -194,6 +202,8 @@ __device__ __forceinline__ unsigned warp_peers(unsigned d) {
 
 __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
                                                    int shift, int* hist, int nb_max) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_hist[256];
     const int n = (int)min((int64_t)*d_n, cap);
     const int nb = div_up(n, kSortTile);
@@ -226,6 +236,8 @@ constexpr int kRowItems = 16;   // rows up to 4096 blocks (4 M keys) in one pass
 
 __global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, const int* d_n, int64_t cap,
                                                         int* rowtot) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_warp[33];
     const int n = (int)min((int64_t)*d_n, cap);
     const int nb = div_up(n, kSortTile);
@@ -257,6 +269,8 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
                                                       int32_t* __restrict__ vals_out, const int* d_n, int64_t cap,
                                                       int shift, const int* __restrict__ hist, int nb_max,
                                                       const int* __restrict__ rowtot) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_cnt[kWarps][256];    // per-warp running digit counts, then per-warp offsets
     __shared__ int s_dstart[256];         // start of digit d inside this block's sorted tile
     __shared__ int s_goff[256];           // global start of digit d for this block
@@ -351,6 +365,8 @@ __global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ rad
                                                     const int32_t* __restrict__ vis_val, const int* d_V, TileGeom g,
                                                     int4* __restrict__ ent_rect, int* __restrict__ ent_cnt,
                                                     int* blocksum) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_warp[33];
     const int V = *d_V;
     const int nb = div_up(V, kSortTile);
@@ -393,6 +409,8 @@ __global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ rad
 __global__ void __launch_bounds__(kT) k_tiles_offsets(const int* __restrict__ ent_cnt, const int* d_V,
                                                       const int* __restrict__ blockoff, int* __restrict__ ent_off,
                                                       int* __restrict__ first_item, int n_emit_blocks) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_warp[33];
     const int V = *d_V;
     const int nb = div_up(V, kSortTile);
@@ -428,6 +446,8 @@ __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_
                                                    const int32_t* __restrict__ vis_val, const int* d_V,
                                                    const int* d_nsort, const int* __restrict__ first_item, TileGeom g,
                                                    uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_off[kEmit + 1];
     const int n = *d_nsort;
     const int V = *d_V;
@@ -464,11 +484,15 @@ __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_
 
 // K5: tile ranges.  offsets[b] = first sorted index with key >= b; offsets[nbins] = M.
 __global__ void k_ranges_fill(int32_t* offsets, int nbins, const int* d_n) {
+    pdl_trigger();
+    pdl_wait();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b <= nbins) offsets[b] = *d_n;
 }
 
 __global__ void k_ranges(const uint32_t* __restrict__ keys, const int* d_n, int32_t* offsets) {
+    pdl_trigger();
+    pdl_wait();
     const int n = *d_n;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -479,6 +503,8 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, const int* d_n, int3
 
 __global__ void k_keys64(const uint32_t* __restrict__ keys32, const int32_t* __restrict__ ids,
                          const float* __restrict__ splats, const int* d_n, int TT, int B, uint64_t* out) {
+    pdl_trigger();
+    pdl_wait();
     const int n = *d_n;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -536,9 +562,9 @@ KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int 
     KV in = a, out = b;
     for (int p = 0; p < passes; p++) {
         int32_t* vdst = (p == passes - 1 && final_vals) ? final_vals : out.v;
-        k_radix_hist<<<nb_max, kT, 0, s>>>(in.k, d_n, cap, 8 * p, hist, nb_max);
-        k_radix_scan_rows<<<256, kT, 0, s>>>(hist, nb_max, d_n, cap, rowtot);
-        k_radix_scatter<<<nb_max, kT, 0, s>>>(in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max, rowtot);
+        launch_pdl(k_radix_hist, dim3(nb_max), dim3(kT), s, in.k, d_n, cap, 8 * p, hist, nb_max);
+        launch_pdl(k_radix_scan_rows, dim3(256), dim3(kT), s, hist, nb_max, d_n, cap, rowtot);
+        launch_pdl(k_radix_scatter, dim3(nb_max), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max, rowtot);
         KV next_in{out.k, vdst};
         out = in;
         in = next_in;
@@ -582,13 +608,13 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
 
     // 1. stable compaction of the visible (c,n) items (K2a, K2b); identity when packed
     if (d_nnz) {
-        k_packed_items<<<div_up(n_items > 0 ? n_items : 1, 256), 256, 0, s>>>(splats, d_nnz, n_items, d_V, vis.k,
+        launch_pdl(k_packed_items, dim3(div_up(n_items > 0 ? n_items : 1, 256)), dim3(256), s, splats, d_nnz, n_items, d_V, vis.k,
                                                                              vis.v);
     } else {
-        k_vis_count<<<nb_items, kT, 0, s>>>(r2, n_items, blocksum);
-        k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, kTile, nullptr, n_items, INT64_MAX, d_V, nullptr,
+        launch_pdl(k_vis_count, dim3(nb_items), dim3(kT), s, r2, n_items, blocksum);
+        launch_pdl(k_scan_blocksums, dim3(1), dim3(kScanThreads), s, blocksum, kTile, nullptr, n_items, INT64_MAX, d_V, nullptr,
                                                      nullptr, 0, nullptr);
-        k_vis_compact<<<nb_items, kT, 0, s>>>(r2, splats, n_items, blocksum, vis.k, vis.v);
+        launch_pdl(k_vis_compact, dim3(nb_items), dim3(kT), s, r2, splats, n_items, blocksum, vis.k, vis.v);
     }
     GS_LAUNCH_CHECK("isect/compact");
     // 2. stable sort by fp32 depth bits (K4, 4 passes)
@@ -596,13 +622,13 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     GS_LAUNCH_CHECK("isect/depth-sort");
     // 3. tile rectangles, counts, offsets, M, overflow, clamped count (K2c, K2d)
     const int nb_v = div_up(n_items > 0 ? n_items : 1, kSortTile);
-    k_tiles_count<<<nb_v, kT, 0, s>>>(r2, splats, dsorted.v, d_V, g, ent_rect, ent_cnt, blocksum);
-    k_scan_blocksums<<<1, kScanThreads, 0, s>>>(blocksum, kSortTile, d_V, 0, INT64_MAX, nullptr, M, overflow, cap,
+    launch_pdl(k_tiles_count, dim3(nb_v), dim3(kT), s, r2, splats, dsorted.v, d_V, g, ent_rect, ent_cnt, blocksum);
+    launch_pdl(k_scan_blocksums, dim3(1), dim3(kScanThreads), s, blocksum, kSortTile, d_V, 0, INT64_MAX, nullptr, M, overflow, cap,
                                                  d_nsort);
-    k_tiles_offsets<<<nb_v, kT, 0, s>>>(ent_cnt, d_V, blocksum, ent_off, first_item, div_up(cap, kEmit));
+    launch_pdl(k_tiles_offsets, dim3(nb_v), dim3(kT), s, ent_cnt, d_V, blocksum, ent_off, first_item, div_up(cap, kEmit));
     // 4. load-balanced emission in depth order (K3)
     if (cap > 0)
-        k_tiles_emit<<<div_up(cap, kEmit), kT, 0, s>>>(ent_rect, ent_off, dsorted.v, d_V, d_nsort, first_item, g,
+        launch_pdl(k_tiles_emit, dim3(div_up(cap, kEmit)), dim3(kT), s, ent_rect, ent_off, dsorted.v, d_V, d_nsort, first_item, g,
                                                        ia.k, ia.v);
     GS_LAUNCH_CHECK("isect/emit");
     // 5. stable sort by (camera, tile) (K4); values land in the caller's isect_ids
@@ -610,9 +636,9 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     KV sorted = radix_sort(ia, ib, ids, d_nsort, cap, kbits, hist, rowtot, L.nb_sort_max, s);
     GS_LAUNCH_CHECK("isect/tile-sort");
     // 6. tile ranges (K5)
-    k_ranges_fill<<<div_up(nbins + 1, 256), 256, 0, s>>>(tile_offsets, nbins, d_nsort);
-    if (cap > 0) k_ranges<<<div_up(cap, 256), 256, 0, s>>>(sorted.k, d_nsort, tile_offsets);
-    if (keys && cap > 0) k_keys64<<<div_up(cap, 256), 256, 0, s>>>(sorted.k, sorted.v, splats, d_nsort, TT, B, keys);
+    launch_pdl(k_ranges_fill, dim3(div_up(nbins + 1, 256)), dim3(256), s, tile_offsets, nbins, d_nsort);
+    if (cap > 0) launch_pdl(k_ranges, dim3(div_up(cap, 256)), dim3(256), s, sorted.k, d_nsort, tile_offsets);
+    if (keys && cap > 0) launch_pdl(k_keys64, dim3(div_up(cap, 256)), dim3(256), s, sorted.k, sorted.v, splats, d_nsort, TT, B, keys);
     GS_LAUNCH_CHECK("isect/ranges");
     return GS_OK;
 }

@@ -79,6 +79,8 @@ __device__ __forceinline__ float reduce_scatter16(const float (&v)[16], int lane
 // as one per-(block, camera) partial; k_pose_reduce sums the partials in a fixed order.
 template <int DEG, bool POSE>
 __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t n0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const bool active = n0 < p.N;
     if (!POSE && !active) return;   // without POSE there is no block-level synchronisation below
@@ -469,11 +471,11 @@ template <bool POSE>
 void launch_pb_t(int deg, const PBParams& p, cudaStream_t s) {
     const int grid = div_up(p.N, kThreads);
     switch (deg) {
-        case -1: k_project_bwd<-1, POSE><<<grid, kThreads, 0, s>>>(p); break;
-        case 0: k_project_bwd<0, POSE><<<grid, kThreads, 0, s>>>(p); break;
-        case 1: k_project_bwd<1, POSE><<<grid, kThreads, 0, s>>>(p); break;
-        case 2: k_project_bwd<2, POSE><<<grid, kThreads, 0, s>>>(p); break;
-        default: k_project_bwd<3, POSE><<<grid, kThreads, 0, s>>>(p); break;
+        case -1: launch_pdl(k_project_bwd<-1, POSE>, dim3(grid), dim3(kThreads), s, p); break;
+        case 0: launch_pdl(k_project_bwd<0, POSE>, dim3(grid), dim3(kThreads), s, p); break;
+        case 1: launch_pdl(k_project_bwd<1, POSE>, dim3(grid), dim3(kThreads), s, p); break;
+        case 2: launch_pdl(k_project_bwd<2, POSE>, dim3(grid), dim3(kThreads), s, p); break;
+        default: launch_pdl(k_project_bwd<3, POSE>, dim3(grid), dim3(kThreads), s, p); break;
     }
 }
 
@@ -482,6 +484,8 @@ void launch_pb_t(int deg, const PBParams& p, cudaStream_t s) {
 constexpr int kPoseT = 120;   // 12 values x 10 lanes each
 __global__ void __launch_bounds__(kPoseT) k_pose_reduce(const float* __restrict__ part, int nblk, int C,
                                                       float* __restrict__ v_viewmats) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float s_acc[kPoseT];
     const int c = blockIdx.x, v = threadIdx.x / 10, r = threadIdx.x % 10;
     float t = 0.f;
@@ -503,13 +507,15 @@ gs_status launch_pb(int deg, PBParams p, float* v_viewmats, void* pose_ws, cudaS
     }
     p.pose_part = static_cast<float*>(pose_ws);
     launch_pb_t<true>(deg, p, s);
-    k_pose_reduce<<<p.C, kPoseT, 0, s>>>(p.pose_part, div_up(p.N, kThreads), p.C, v_viewmats);
+    launch_pdl(k_pose_reduce, dim3(p.C), dim3(kPoseT), s, p.pose_part, div_up(p.N, kThreads), p.C, v_viewmats);
     return GS_OK;
 }
 
 // map[camera_ids[i] * N + gaussian_ids[i]] = i for the live packed items (map pre-set to -1)
 __global__ void k_pack_map(const int32_t* __restrict__ cam, const int32_t* __restrict__ gid, const int64_t* d_nnz,
                            int64_t cap, int64_t N, int32_t* __restrict__ map) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t n = min(*d_nnz, cap);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) map[(int64_t)cam[i] * N + gid[i]] = (int32_t)i;
@@ -563,7 +569,7 @@ gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W
         GS_LAUNCH_CHECK("packed map memset");
         return GS_ERR_CUDA;
     }
-    if (cap > 0) k_pack_map<<<div_up(cap, 256), 256, 0, s>>>(camera_ids, gaussian_ids, nnz, cap, N, map);
+    if (cap > 0) launch_pdl(k_pack_map, dim3(div_up(cap, 256)), dim3(256), s, camera_ids, gaussian_ids, nnz, cap, N, map);
     PBParams p = make_pb_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii, v_splats,
                                 v_means, v_quats, v_scales, v_opac, v_colors);
     p.map = map;

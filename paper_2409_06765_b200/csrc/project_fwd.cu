@@ -77,6 +77,8 @@ __device__ __forceinline__ void setup_cam(const ProjParams& p, int c, CamConst& 
 
 template <int DEG, int MODE>
 __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ CamConst s_cam[kCamChunk];
     __shared__ int s_wcnt[kThreads / 32];
     const int64_t n = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -289,6 +291,8 @@ namespace {
 constexpr int kScanT = 1024, kScanItems = 16;
 __global__ void __launch_bounds__(kScanT) k_pack_scan(int* cnt, int64_t n, int64_t cap, int64_t* nnz,
                                                       int32_t* overflow) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_w[kScanT / 32 + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t carry = 0;
@@ -352,11 +356,11 @@ ProjParams make_proj_params(const gs_options& o, int64_t N, int C, int W, int H,
 template <int MODE>
 void launch_mode(int deg, int grid, const ProjParams& p, cudaStream_t s) {
     switch (deg) {
-        case -1: k_project_fwd<-1, MODE><<<grid, kThreads, 0, s>>>(p); break;
-        case 0: k_project_fwd<0, MODE><<<grid, kThreads, 0, s>>>(p); break;
-        case 1: k_project_fwd<1, MODE><<<grid, kThreads, 0, s>>>(p); break;
-        case 2: k_project_fwd<2, MODE><<<grid, kThreads, 0, s>>>(p); break;
-        default: k_project_fwd<3, MODE><<<grid, kThreads, 0, s>>>(p); break;
+        case -1: launch_pdl(k_project_fwd<-1, MODE>, dim3(grid), dim3(kThreads), s, p); break;
+        case 0: launch_pdl(k_project_fwd<0, MODE>, dim3(grid), dim3(kThreads), s, p); break;
+        case 1: launch_pdl(k_project_fwd<1, MODE>, dim3(grid), dim3(kThreads), s, p); break;
+        case 2: launch_pdl(k_project_fwd<2, MODE>, dim3(grid), dim3(kThreads), s, p); break;
+        default: launch_pdl(k_project_fwd<3, MODE>, dim3(grid), dim3(kThreads), s, p); break;
     }
 }
 
@@ -391,7 +395,7 @@ gs_status launch_project_packed(const gs_options& o, int64_t N, int C, int W, in
     p.camera_ids = camera_ids;
     p.gaussian_ids = gaussian_ids;
     if (N > 0) launch_mode<kCount>(o.sh_degree, grid, p, s);
-    k_pack_scan<<<1, kScanT, 0, s>>>(p.blockcnt, N > 0 ? (int64_t)C * grid : 0, cap, nnz, overflow);
+    launch_pdl(k_pack_scan, dim3(1), dim3(kScanT), s, p.blockcnt, N > 0 ? (int64_t)C * grid : 0, cap, nnz, overflow);
     if (N > 0) launch_mode<kPacked>(o.sh_degree, grid, p, s);
     GS_LAUNCH_CHECK("k_project_fwd<packed>");
     return GS_OK;

@@ -271,6 +271,8 @@ struct StageFwd {
 
 template <bool STATS, bool DEPTH>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ StageFwd s;
     const int tile = blockIdx.x, cam = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -449,6 +451,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 template <bool ABSGRAD, bool DEPTH>
 __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ Stage<kBatchBwd> s;
     __shared__ int s_maxlast;
     const int tile = blockIdx.x, cam = blockIdx.y;
@@ -577,6 +581,14 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     }
 }
 
+constexpr int kZeroBlocks = 148 * 8;
+__global__ void __launch_bounds__(256) k_zero4(float4* __restrict__ p, int64_t n4) {
+    pdl_trigger();
+    pdl_wait();
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n4; i += (int64_t)gridDim.x * 256) p[i] = z;
+}
+
 RasterParams make_params(const gs_options& o, int C, int64_t N, int W, int H, const float* splats, const float* bg,
                          const int32_t* ids, const int32_t* offs) {
     RasterParams p{};
@@ -599,9 +611,9 @@ gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H,
     p.out_depth = out_depth; p.depth_mode = out_depth ? depth_mode : 0;
     dim3 grid(p.TX * p.TY, C);
     if (p.depth_mode)
-        k_raster_fwd<false, true><<<grid, kThreads, 0, s>>>(p);
+        launch_pdl(k_raster_fwd<false, true>, dim3(grid), dim3(kThreads), s, p);
     else
-        k_raster_fwd<false, false><<<grid, kThreads, 0, s>>>(p);
+        launch_pdl(k_raster_fwd<false, false>, dim3(grid), dim3(kThreads), s, p);
     GS_LAUNCH_CHECK("k_raster_fwd");
     return GS_OK;
 }
@@ -612,7 +624,7 @@ gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int 
     RasterParams p = make_params(o, C, N, W, H, splats, nullptr, ids, offs);
     p.n_eval = n_eval; p.n_contrib = n_contrib;
     dim3 grid(p.TX * p.TY, C);
-    k_raster_fwd<true, false><<<grid, kThreads, 0, s>>>(p);
+    launch_pdl(k_raster_fwd<true, false>, dim3(grid), dim3(kThreads), s, p);
     GS_LAUNCH_CHECK("k_raster_fwd<stats>");
     return GS_OK;
 }
@@ -629,17 +641,17 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
     p.out_depth = const_cast<float*>(out_depth); p.v_depth = v_depth;
     p.depth_mode = v_depth ? depth_mode : 0;
     const size_t nrec = o.packed ? (size_t)N : (size_t)C * (size_t)N;   // packed: N records in total (Q29)
-    if (N > 0 && cudaMemsetAsync(v_splats, 0, sizeof(float) * GS_SPLAT_FLOATS * nrec, s) != cudaSuccess) {
-        GS_LAUNCH_CHECK("v_splats memset");
-        return GS_ERR_CUDA;
-    }
+    // zero-fill as a kernel (not cudaMemsetAsync) so the chain keeps programmatic dependent launch
+    if (N > 0)
+        launch_pdl(k_zero4, dim3(kZeroBlocks), dim3(256), s, reinterpret_cast<float4*>(v_splats),
+                   (int64_t)(nrec * GS_SPLAT_FLOATS / 4));
     dim3 grid(p.TX * p.TY, C);
     if (absgrad) {
-        if (p.depth_mode) k_raster_bwd<true, true><<<grid, kThreads, 0, s>>>(p);
-        else k_raster_bwd<true, false><<<grid, kThreads, 0, s>>>(p);
+        if (p.depth_mode) launch_pdl(k_raster_bwd<true, true>, dim3(grid), dim3(kThreads), s, p);
+        else launch_pdl(k_raster_bwd<true, false>, dim3(grid), dim3(kThreads), s, p);
     } else {
-        if (p.depth_mode) k_raster_bwd<false, true><<<grid, kThreads, 0, s>>>(p);
-        else k_raster_bwd<false, false><<<grid, kThreads, 0, s>>>(p);
+        if (p.depth_mode) launch_pdl(k_raster_bwd<false, true>, dim3(grid), dim3(kThreads), s, p);
+        else launch_pdl(k_raster_bwd<false, false>, dim3(grid), dim3(kThreads), s, p);
     }
     GS_LAUNCH_CHECK("k_raster_bwd");
     return GS_OK;
