@@ -38,7 +38,7 @@ class OrOpts(ct.Structure):
         ("alpha_max", ct.c_double), ("alpha_min", ct.c_double), ("t_min", ct.c_double),
         ("amb_rel_alpha", ct.c_double), ("amb_rel_t", ct.c_double),
         ("tile_size", ct.c_int32), ("antialiased", ct.c_int32), ("sh_degree", ct.c_int32),
-        ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("pad_", ct.c_int32),
+        ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("channels", ct.c_int32),
     ]
 
 
@@ -58,12 +58,13 @@ class Options:
     antialiased: int = 0
     sh_degree: int = 3
     bbox_mode: int = 0
+    channels: int = 0              # 0: RGB from the projection; D > 0: N-D features (render_*_nd)
     fov_clamp: int = 1
 
     def c(self) -> OrOpts:
         return OrOpts(self.near_plane, self.far_plane, self.eps2d, self.alpha_max, self.alpha_min,
                       self.t_min, self.amb_rel_alpha, self.amb_rel_t, self.tile_size, self.antialiased,
-                      self.sh_degree, self.bbox_mode, self.fov_clamp, 0)
+                      self.sh_degree, self.bbox_mode, self.fov_clamp, int(self.channels))
 
 
 _lib = None
@@ -79,7 +80,7 @@ def lib():
         _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
         _lib.or_isect.restype = i64
         _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6 + [P] * 2
-        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 5
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 6
         _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6 + [P] * 2
         _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
@@ -225,8 +226,59 @@ def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
-                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz))
+                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz), None)
     return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vz=vz, az=az, sz=sz)
+
+
+def _nd_opts(opts: Options, D: int) -> Options:
+    from dataclasses import replace
+    return replace(opts, channels=int(D))
+
+
+def render_fwd_nd(proj, feats, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None):
+    """N-dimensional rasterization: the same R1-R3 composite with the per-Gaussian
+    D-channel features feats [N, D] (camera independent) in place of the projected RGB.
+    Returns feats image "feat" [C,H,W,D] plus alpha, T, last_gid, ambig as render_fwd."""
+    feats = _f64(feats)
+    D = feats.shape[1]
+    rows = np.ascontiguousarray(np.broadcast_to(feats[None], (C, N, D)).reshape(C * N, D))
+    p2 = dict(proj)
+    p2["rgb"] = rows
+    o = _nd_opts(opts, D).c()
+    bg = None if backgrounds is None else _f64(backgrounds)
+    tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
+    out = dict(feat=np.zeros((C, H, W, D)), alpha=np.zeros((C, H, W)), T=np.zeros((C, H, W)),
+               last_gid=np.zeros((C, H, W), np.int64), ambig=np.zeros((C, H, W), np.uint8),
+               ncontrib=np.zeros((C, H, W), np.int32))
+    lib().or_render_fwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
+                        _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(rows), _p(bg),
+                        _p(tm), _p(out["feat"]), _p(out["alpha"]), _p(out["T"]), _p(out["last_gid"]),
+                        _p(out["ambig"]), _p(out["ncontrib"]), None, None)
+    return out
+
+
+def render_bwd_nd(proj, feats, C, N, W, H, opts: Options, v_feat, v_alpha=None, backgrounds=None, tile_mask=None):
+    """B1-B6 with D-channel features: v2d (mean2d, conic, opac_eff slots; the rgb slots 0),
+    vfeat [C,N,D] = dL/d(features of each (c,n)), and the tolerance models a2d, s2d.
+    The per-Gaussian feature gradient is vfeat summed over cameras (features are
+    camera independent)."""
+    feats = _f64(feats)
+    D = feats.shape[1]
+    rows = np.ascontiguousarray(np.broadcast_to(feats[None], (C, N, D)).reshape(C * N, D))
+    o = _nd_opts(opts, D).c()
+    bg = None if backgrounds is None else _f64(backgrounds)
+    tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
+    va = None if v_alpha is None else _f64(v_alpha)
+    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9))
+    vfeat = np.zeros((C, N, D))
+    amb = np.zeros((C, N), np.uint8)
+    err = ct.c_double(0)
+    lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
+                        _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(rows), _p(bg),
+                        _p(tm), _p(_f64(v_feat)), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
+                        None, None, None, None, None, _p(vfeat))
+    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vfeat=vfeat,
+                v_colors=vfeat.sum(axis=0))
 
 
 def project_bwd(scene, proj, v2d, opts: Options, vz=None, pose=False):

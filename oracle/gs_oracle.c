@@ -49,8 +49,12 @@ typedef struct {
     int32_t sh_degree;   /* -1 direct RGB colors | 0..3 spherical harmonics               */
     int32_t bbox_mode;   /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3*sqrt(lambda_max)   */
     int32_t fov_clamp;   /* 1 clamp t_x/t_z, t_y/t_z for J only (Q27)                     */
-    int32_t pad_;
+    int32_t channels;    /* 0: RGB from the projection | D > 0: N-D features,
+                            render inputs are [C*N, D] feature rows, images [C,H,W,D]     */
 } or_opts;
+
+#define OR_MAX_CH 64
+static int n_channels(const or_opts *o) { return o->channels > 0 ? o->channels : 3; }
 
 /* ------------------------------------------------------------------------- */
 /* Spherical harmonics, real basis up to degree 3 ([bk]).  */
@@ -587,7 +591,7 @@ typedef struct {
 
 typedef struct {
     double eT;       /* sum over composited splats of alpha qd / (1 - alpha) (tolerance model) */
-    double rgb[3], T;
+    double rgb[OR_MAX_CH], T;
     double dacc;      /* accumulated depth sum z alpha T (App. depth rendering) */
     int64_t last_li;  /* -1 if none */
     int64_t end_li;   /* exclusive end of the evaluated part of the list */
@@ -619,7 +623,10 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
                               const double *conic, const double *opac_eff, const double *rgb,
                               const double *depth, contrib_t *rec, int64_t rec_cap)
 {
-    pixres_t r = {0.0, {0, 0, 0}, 1.0, 0.0, -1, L->count, 0, 0};
+    pixres_t r;
+    memset(&r, 0, sizeof r);
+    r.T = 1.0; r.last_li = -1; r.end_li = L->count;
+    const int D = n_channels(o);
     int tx = px / o->tile_size, ty = py / o->tile_size;
     double p[2] = {px + 0.5, py + 0.5};            /* R1: pixel centre */
     const double amax = (float)o->alpha_max, amin = (float)o->alpha_min, tmin = (float)o->t_min;
@@ -655,7 +662,7 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
             e->clamped = clamped; e->delta = delta; e->qd = qd;
         }
         r.eT += alpha * qd / (1.0 - alpha);
-        for (int ch = 0; ch < 3; ch++) r.rgb[ch] += rgb[3 * g + ch] * alpha * T;   /* P:536-538 */
+        for (int ch = 0; ch < D; ch++) r.rgb[ch] += rgb[D * g + ch] * alpha * T;   /* P:536-538 */
         if (depth) r.dacc += depth[g] * alpha * T;                                 /* P:250 */
         T = T * (1.0 - alpha);
         Tdec = nT_d;
@@ -682,6 +689,7 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                   uint8_t *out_ambig, int32_t *out_ncontrib, const double *depth, double *out_depth)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
+    const int D = n_channels(o);
     for (int64_t c = 0; c < C; c++) {
         camlist_t L;
         build_camlist(o, c, N, W, H, radii, mean2d_f, depth_f, &L);
@@ -689,9 +697,9 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
         for (int64_t pix = 0; pix < (int64_t)W * H; pix++) {
             int px = (int)(pix % W), py = (int)(pix / W);
             int64_t oi = c * W * H + pix;
-            const double *b = bg ? bg + 3 * c : NULL;
+            const double *b = bg ? bg + D * c : NULL;
             if (!tile_selected(tile_mask, c, TX, TY, px, py, T)) {
-                for (int ch = 0; ch < 3; ch++) out_rgb[3 * oi + ch] = b ? b[ch] : 0.0;
+                for (int ch = 0; ch < D; ch++) out_rgb[D * oi + ch] = b ? b[ch] : 0.0;
                 out_alpha[oi] = 0; out_T[oi] = 1; out_last_gid[oi] = -1;
                 if (out_depth) out_depth[oi] = 0;
                 if (out_ambig) out_ambig[oi] = 0;
@@ -700,7 +708,7 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
             }
             pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, depth,
                                        NULL, 0);
-            for (int ch = 0; ch < 3; ch++) out_rgb[3 * oi + ch] = r.rgb[ch] + r.T * (b ? b[ch] : 0.0);  /* R3, Q25 */
+            for (int ch = 0; ch < D; ch++) out_rgb[D * oi + ch] = r.rgb[ch] + r.T * (b ? b[ch] : 0.0);  /* R3, Q25 */
             if (out_depth) out_depth[oi] = r.dacc;                                 /* no background term */
             out_alpha[oi] = 1.0 - r.T;
             out_T[oi] = r.T;
@@ -733,10 +741,12 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   const double *v_img, const double *v_alpha_img, double *v2d, double *a2d, double *s2d,
                   uint8_t *g_ambig, double *T_replay_err, const double *depth, const double *v_depth_img,
-                  double *vz, double *az, double *sz)
+                  double *vz, double *az, double *sz, double *vfeat)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
+    const int D = n_channels(o);
     memset(v2d, 0, sizeof(double) * 9 * C * N);
+    if (vfeat) memset(vfeat, 0, sizeof(double) * D * C * N);
     if (a2d) memset(a2d, 0, sizeof(double) * 9 * C * N);
     if (s2d) memset(s2d, 0, sizeof(double) * 9 * C * N);
     if (g_ambig) memset(g_ambig, 0, (size_t)C * N);
@@ -775,6 +785,8 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
         for (int64_t pix = 0; pix < P; pix++) off[pix + 1] = off[pix] + cnt[pix];
         int64_t tot = off[P];
         term_t *terms = (term_t *)malloc(sizeof(term_t) * (tot > 0 ? tot : 1));
+        /* per-term feature gradients (N-D mode: D values per term; RGB mode uses v[5..7]) */
+        double *tvf = vfeat ? (double *)malloc(sizeof(double) * D * (tot > 0 ? tot : 1)) : NULL;
         double *errs = (double *)calloc(P, sizeof(double));
         /* pass 2: per-pixel backward */
 #pragma omp parallel
@@ -792,14 +804,16 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL,
                                            rec, cap);
                 int64_t oi = c * P + pix;
-                const double *vC = &v_img[3 * oi];
+                const double *vC = &v_img[D * oi];
                 double vA = v_alpha_img ? v_alpha_img[oi] : 0.0;
-                const double *b = bg ? bg + 3 * c : NULL;
-                double bgdot = b ? (b[0] * vC[0] + b[1] * vC[1] + b[2] * vC[2]) : 0.0;
+                const double *b = bg ? bg + D * c : NULL;
+                double bgdot = 0.0;
+                if (b)
+                    for (int ch = 0; ch < D; ch++) bgdot += b[ch] * vC[ch];
                 double Tfin = r.T;
                 double vD = with_depth ? v_depth_img[oi] : 0.0;   /* d L / d (accumulated depth) */
                 double Tn = Tfin;                /* B1 */
-                double S[3] = {0, 0, 0}, Sd = 0;  /* Sd: the depth channel's S */
+                double S[OR_MAX_CH] = {0}, Sd = 0;  /* Sd: the depth channel's S */
                 double err = 0;
                 for (int64_t k = r.ncontrib - 1; k >= 0; k--) {
                     const contrib_t *e = &rec[k];
@@ -812,23 +826,25 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     double fac = alpha * Tn;
                     term_t *tm = &terms[off[pix] + k];
                     tm->g = (int32_t)g;
-                    for (int ch = 0; ch < 3; ch++) tm->v[5 + ch] = fac * vC[ch];   /* B3 */
+                    for (int ch = 0; ch < 3; ch++) tm->v[5 + ch] = D == 3 ? fac * vC[ch] : 0.0;  /* B3 */
                     for (int ch = 0; ch < 3; ch++) tm->va[5 + ch] = fabs(tm->v[5 + ch]);
+                    if (tvf)
+                        for (int ch = 0; ch < D; ch++) tvf[(off[pix] + k) * D + ch] = fac * vC[ch];
                     double z = with_depth ? depth[g] : 0.0;
                     tm->v[9] = fac * vD;                                           /* depth as a channel: B3 */
                     tm->va[9] = fabs(tm->v[9]);
                     double v_alpha = 0;                                            /* B4 */
-                    for (int ch = 0; ch < 3; ch++) v_alpha += (rgb[3 * g + ch] * Tn - S[ch] * ra) * vC[ch];
+                    for (int ch = 0; ch < D; ch++) v_alpha += (rgb[D * g + ch] * Tn - S[ch] * ra) * vC[ch];
                     v_alpha += (z * Tn - Sd * ra) * vD;                            /* depth channel */
                     v_alpha += -Tfin * ra * bgdot + Tfin * ra * vA;
                     /* magnitude of B4 before its internal cancellation (c T vs S/(1-alpha)):
                      * the condition floor a2d of the v_alpha-dependent gradients uses it */
                     double v_alpha_abs = fabs(Tfin * ra * bgdot) + fabs(Tfin * ra * vA);
-                    for (int ch = 0; ch < 3; ch++)
-                        v_alpha_abs += fabs(rgb[3 * g + ch] * Tn * vC[ch]) + fabs(S[ch] * ra * vC[ch]);
+                    for (int ch = 0; ch < D; ch++)
+                        v_alpha_abs += fabs(rgb[D * g + ch] * Tn * vC[ch]) + fabs(S[ch] * ra * vC[ch]);
                     v_alpha_abs += fabs(z * Tn * vD) + fabs(Sd * ra * vD);
 
-                    for (int ch = 0; ch < 3; ch++) S[ch] += rgb[3 * g + ch] * fac;  /* B5 */
+                    for (int ch = 0; ch < D; ch++) S[ch] += rgb[D * g + ch] * fac;  /* B5 */
                     Sd += z * fac;
                     if (!e->clamped) {                                           /* B6 (Q24) */
                         tm->v[8] = e->G * v_alpha;
@@ -877,12 +893,14 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 if (s2d) s2d[9 * (int64_t)g + j] += terms[i].vs[j];
             }
             if (vz) vz[g] += terms[i].v[9];
+            if (tvf)
+                for (int ch = 0; ch < D; ch++) vfeat[(int64_t)g * D + ch] += tvf[i * D + ch];
             if (az) az[g] += terms[i].va[9];
             if (sz) sz[g] += terms[i].vs[9];
         }
         for (int64_t pix = 0; pix < P; pix++)
             if (errs[pix] > max_err) max_err = errs[pix];
-        free(errs); free(terms); free(off); free(cnt);
+        free(errs); free(terms); free(tvf); free(off); free(cnt);
         free_camlist(&L);
     }
     if (T_replay_err) *T_replay_err = max_err;
