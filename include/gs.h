@@ -100,11 +100,12 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 4
+#define GS_ABI_VERSION 5
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
- *      colors [N,K,3] (sh_degree >= 0, K >= (d+1)^2) or [N,3] (sh_degree = -1; K ignored),
+ *      colors [N,K,3] (sh_degree >= 0, K >= (d+1)^2) or [N,3] (sh_degree = -1; K ignored;
+ *      may be NULL in N-D feature mode, then the record's rgb slots are 0),
  *      viewmats [C,4,4], Ks [C,3,3].
  * Out: radii [C,N,2] int32 (per-axis pixel radius; 0 = culled),
  *      splats [C,N,GS_SPLAT_FLOATS] (record layout above).
@@ -198,7 +199,8 @@ GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, i
  *      view-direction (campos = -W^T w) paths; row 3 is 0.  Reduced per (block, camera)
  *      into the workspace (>= gs_project_bwd_workspace_size(N, C) bytes, 256-byte aligned;
  *      unused and may be NULL when v_viewmats is NULL), then summed in block order
- *      (deterministic). */
+ *      (deterministic).
+ * v_colors (and colors) may be NULL when sh_degree == -1 (N-D feature mode). */
 GS_API size_t gs_project_bwd_workspace_size(int64_t N, int32_t C);
 GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
                          const float* means, const float* quats, const float* scales,
@@ -207,6 +209,34 @@ GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int
                          const float* v_splats, float* v_means, float* v_quats, float* v_scales,
                          float* v_opacities, float* v_colors, float* v_viewmats, void* workspace,
                          size_t workspace_bytes, void* stream);
+
+/* ==== N-dimensional features (NEXT-2) =====================================
+ * Stage 3 / 4a with D-channel per-Gaussian features feats [n_gauss, D] (camera
+ * independent, e.g. learned feature fields) composited exactly like RGB (R1-R3, B1-B6)
+ * instead of the record's rgb slots.  Channel chunking: the kernels run once per 4
+ * channels (every pass composites the same splats, so out_T / last_ids / isect_masks are
+ * those of gs_rasterize_fwd).  Dense: record id c*N+n -> feature row n, gaussian_ids NULL;
+ * packed (opt->packed): feature row gaussian_ids[id].  backgrounds: [C, D] or NULL.
+ * Out (fwd): out_feats [C,H,W,D], out_alpha, out_T, last_ids, isect_masks as gs_rasterize_fwd.
+ * Out (bwd): v_splats (record geometry gradients: slots 0-2, 4-6; absgrad 7, 11), zero-filled
+ *      then accumulated over the passes (B4's v_alpha is linear in v_C; the alpha-output term
+ *      enters once), and v_feats [n_gauss, D] = dL/d feats, summed over cameras (zero-filled
+ *      here).  For the projection backward of feature mode pass sh_degree = -1 and
+ *      v_colors = NULL to gs_project_bwd (its colour gradient is v_feats).
+ * Depth rendering is not combined with feature mode (render depth as a feature channel). */
+GS_API gs_status gs_rasterize_fwd_nd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                                     const float* splats, const float* feats, int32_t D,
+                                     const int32_t* gaussian_ids, const float* backgrounds,
+                                     const int32_t* isect_ids, const int32_t* tile_offsets, float* out_feats,
+                                     float* out_alpha, float* out_T, int32_t* last_ids, uint16_t* isect_masks,
+                                     void* stream);
+GS_API gs_status gs_rasterize_bwd_nd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                                     const float* splats, const float* feats, int32_t D,
+                                     const int32_t* gaussian_ids, int64_t n_gauss, const float* backgrounds,
+                                     const int32_t* isect_ids, const int32_t* tile_offsets, const float* out_T,
+                                     const int32_t* last_ids, const float* v_out_feats, const float* v_out_alpha,
+                                     int32_t absgrad, const uint16_t* isect_masks, float* v_splats, float* v_feats,
+                                     void* stream);
 
 /* ==== Packed mode (Q29; BASELINE configs[4]) ==========================================
  * Only the visible (c,n) pairs are stored: item i of a packed call is the pair

@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 
@@ -52,6 +52,9 @@ SIGNATURES = {
     "gs_project_bwd_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                               _P, _P, _P, _P, _SZ, _P]),
+    "gs_rasterize_fwd_nd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "gs_rasterize_bwd_nd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I32, _P, _I64, _P, _P, _P, _P, _P, _P, _P,
+                                   _I32, _P, _P, _P, _P]),
     "gs_project_packed_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_packed": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P,
                                  _P, _P, _P, _SZ, _P]),
@@ -260,3 +263,33 @@ def gs_project_bwd_packed(o, means, quats, scales, opacities, colors, K, viewmat
                                       ptr(v_colors, name="v_colors"), ptr(v_viewmats, name="v_viewmats"),
                                       ptr(workspace, torch.uint8, "ws"), workspace.numel(), stream_ptr(stream)),
           "gs_project_bwd_packed")
+
+
+# ---- N-D features -----------------------------------------------------------
+def gs_rasterize_fwd_nd(o, C, N, width, height, splats, feats, gaussian_ids, backgrounds, isect_ids, tile_offsets,
+                        out_feats, out_alpha, out_T, last_ids, isect_masks=None, stream=None):
+    D = feats.shape[1]
+    check(lib().gs_rasterize_fwd_nd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
+                                    ptr(feats, name="feats"), D, ptr(gaussian_ids, torch.int32, "gaussian_ids"),
+                                    ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
+                                    ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_feats, name="out_feats"),
+                                    ptr(out_alpha, name="out_alpha"), ptr(out_T, name="out_T"),
+                                    ptr(last_ids, torch.int32, "last_ids"),
+                                    ptr(isect_masks, torch.int16, "isect_masks"), stream_ptr(stream)),
+          "gs_rasterize_fwd_nd")
+
+
+def gs_rasterize_bwd_nd(o, C, N, width, height, splats, feats, gaussian_ids, n_gauss, backgrounds, isect_ids,
+                        tile_offsets, out_T, last_ids, v_out_feats, v_out_alpha, absgrad, isect_masks, v_splats,
+                        v_feats, stream=None):
+    D = feats.shape[1]
+    check(lib().gs_rasterize_bwd_nd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
+                                    ptr(feats, name="feats"), D, ptr(gaussian_ids, torch.int32, "gaussian_ids"),
+                                    n_gauss, ptr(backgrounds, name="backgrounds"),
+                                    ptr(isect_ids, torch.int32, "isect_ids"),
+                                    ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_T, name="out_T"),
+                                    ptr(last_ids, torch.int32, "last_ids"), ptr(v_out_feats, name="v_out_feats"),
+                                    ptr(v_out_alpha, name="v_out_alpha"), int(bool(absgrad)),
+                                    ptr(isect_masks, torch.int16, "isect_masks"), ptr(v_splats, name="v_splats"),
+                                    ptr(v_feats, name="v_feats"), stream_ptr(stream)),
+          "gs_rasterize_bwd_nd")

@@ -89,7 +89,8 @@ gs_status gs_project(const gs_options* opt, int64_t N, int32_t C, int32_t width,
     GS_REQ(opt->packed == 0);
     GS_TRY(check_dims(N, C, width, height));
     if (N == 0) return GS_OK;
-    GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && splats);
+    GS_REQ(means && quats && scales && opacities && viewmats && Ks && radii && splats);
+    GS_REQ(colors || opt->sh_degree < 0);   // NULL direct colours: N-D feature mode
     GS_REQ(aligned16(quats) && aligned16(splats) && aligned8(radii) && aligned4(means) && aligned4(scales) &&
            aligned4(opacities) && aligned4(colors) && aligned4(viewmats) && aligned4(Ks));
     if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
@@ -186,8 +187,8 @@ gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t wi
         GS_REQ(workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0 &&
                workspace_bytes >= gsb::project_bwd_workspace_bytes(N, C));
     if (N > 0) {
-        GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && radii && v_splats && v_means &&
-               v_quats && v_scales && v_opacities && v_colors);
+        GS_REQ(means && quats && scales && opacities && viewmats && Ks && radii && v_splats && v_means &&
+               v_quats && v_scales && v_opacities && (opt->sh_degree < 0 || (colors && v_colors)));
         GS_REQ(aligned16(quats) && aligned16(v_quats) && aligned16(v_splats) && aligned8(radii) && aligned4(means) &&
                aligned4(v_means) && aligned4(colors) && aligned4(v_colors) && aligned4(scales) && aligned4(v_scales));
         if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
@@ -196,6 +197,47 @@ gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t wi
                                    opt->sh_degree >= 0 ? K : 1, viewmats, Ks, radii, v_splats, v_means, v_quats,
                                    v_scales, v_opacities, v_colors, v_viewmats, workspace,
                                    static_cast<cudaStream_t>(stream));
+}
+
+// ---- N-D features ------------------------------------------------------
+
+gs_status gs_rasterize_fwd_nd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                              const float* splats, const float* feats, int32_t D, const int32_t* gaussian_ids,
+                              const float* backgrounds, const int32_t* isect_ids, const int32_t* tile_offsets,
+                              float* out_feats, float* out_alpha, float* out_T, int32_t* last_ids,
+                              uint16_t* isect_masks, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(D >= 1 && feats && tile_offsets && out_feats && out_alpha && out_T && last_ids);
+    GS_REQ(!opt->packed || gaussian_ids);
+    GS_REQ(aligned16(splats) && aligned4(feats) && aligned4(gaussian_ids) && aligned4(isect_ids) &&
+           aligned4(backgrounds) && aligned4(out_feats) && aligned4(out_alpha) && aligned4(out_T) &&
+           aligned4(last_ids));
+    return gsb::launch_raster_fwd_nd(*opt, C, N, width, height, splats, feats, D,
+                                     opt->packed ? gaussian_ids : nullptr, backgrounds, isect_ids, tile_offsets,
+                                     out_feats, out_alpha, out_T, last_ids, isect_masks,
+                                     static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_rasterize_bwd_nd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
+                              const float* splats, const float* feats, int32_t D, const int32_t* gaussian_ids,
+                              int64_t n_gauss, const float* backgrounds, const int32_t* isect_ids,
+                              const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
+                              const float* v_out_feats, const float* v_out_alpha, int32_t absgrad,
+                              const uint16_t* isect_masks, float* v_splats, float* v_feats, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(D >= 1 && n_gauss >= 0 && feats && tile_offsets && out_T && last_ids && v_out_feats);
+    GS_REQ((v_splats || N == 0) && (v_feats || n_gauss == 0));
+    GS_REQ(!opt->packed || gaussian_ids);
+    GS_REQ(opt->packed || n_gauss == N);
+    GS_REQ(aligned16(splats) && aligned16(v_splats) && aligned4(feats) && aligned4(gaussian_ids) &&
+           aligned4(isect_ids) && aligned4(backgrounds) && aligned4(out_T) && aligned4(last_ids) &&
+           aligned4(v_out_feats) && aligned4(v_out_alpha) && aligned4(v_feats));
+    return gsb::launch_raster_bwd_nd(*opt, C, N, width, height, splats, feats, D,
+                                     opt->packed ? gaussian_ids : nullptr, n_gauss, backgrounds, isect_ids,
+                                     tile_offsets, out_T, last_ids, v_out_feats, v_out_alpha, absgrad, isect_masks,
+                                     v_splats, v_feats, static_cast<cudaStream_t>(stream));
 }
 
 // ---- packed mode (Q29) ----------------------------------------------------------------
@@ -218,7 +260,7 @@ gs_status gs_project_packed(const gs_options* opt, int64_t N, int32_t C, int32_t
     GS_REQ(nnz && overflow && workspace && aligned8(nnz) && aligned4(overflow));
     GS_REQ((reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
     GS_REQ(workspace_bytes >= gsb::project_packed_workspace_bytes(N, C));
-    GS_REQ(N == 0 || (means && quats && scales && opacities && colors && viewmats && Ks));
+    GS_REQ(N == 0 || (means && quats && scales && opacities && viewmats && Ks && (colors || opt->sh_degree < 0)));
     GS_REQ(nnz_capacity == 0 || (camera_ids && gaussian_ids && radii && splats));
     GS_REQ(aligned16(quats) && aligned16(splats) && aligned8(radii) && aligned4(camera_ids) &&
            aligned4(gaussian_ids) && aligned4(means) && aligned4(scales) && aligned4(opacities) &&
@@ -281,8 +323,8 @@ gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t C, int
                                               static_cast<cudaStream_t>(stream));
     GS_REQ(nnz_capacity >= 0 && nnz && workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
     GS_REQ(workspace_bytes >= gsb::project_bwd_packed_workspace_bytes(N, C));
-    GS_REQ(means && quats && scales && opacities && colors && viewmats && Ks && v_means && v_quats && v_scales &&
-           v_opacities && v_colors);
+    GS_REQ(means && quats && scales && opacities && viewmats && Ks && v_means && v_quats && v_scales &&
+           v_opacities && (opt->sh_degree < 0 || (colors && v_colors)));
     GS_REQ(nnz_capacity == 0 || (camera_ids && gaussian_ids && radii && v_splats));
     GS_REQ(aligned8(nnz) && aligned16(quats) && aligned16(v_quats) && aligned16(v_splats) && aligned8(radii) &&
            aligned4(camera_ids) && aligned4(gaussian_ids) && aligned4(means) && aligned4(v_means) &&

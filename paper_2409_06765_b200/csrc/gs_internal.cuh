@@ -100,5 +100,14 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
                             const int32_t* last_ids, const float* v_rgb, const float* v_alpha,
                             const float* out_depth, const float* v_depth, int depth_mode, int absgrad,
                             const uint16_t* isect_masks, float* v_splats, cudaStream_t s);
+gs_status launch_raster_fwd_nd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
+                               const float* feats, int D, const int32_t* gids, const float* bg, const int32_t* ids,
+                               const int32_t* offs, float* out_feats, float* out_alpha, float* out_T,
+                               int32_t* last_ids, uint16_t* isect_masks, cudaStream_t s);
+gs_status launch_raster_bwd_nd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
+                               const float* feats, int D, const int32_t* gids, int64_t n_gauss, const float* bg,
+                               const int32_t* ids, const int32_t* offs, const float* out_T, const int32_t* last_ids,
+                               const float* v_feats_img, const float* v_alpha, int absgrad,
+                               const uint16_t* isect_masks, float* v_splats, float* v_feats, cudaStream_t s);
 
 }  // namespace gsb

@@ -419,8 +419,10 @@ __global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
     }
     p.v_opac[n] = g_op;
     if (DEG < 0) {
+        if (p.v_colors) {   // NULL in N-D feature mode: the raster backward wrote the feature gradient
 #pragma unroll
-        for (int i = 0; i < 3; i++) p.v_colors[3 * n + i] = g_rgb[i];
+            for (int i = 0; i < 3; i++) p.v_colors[3 * n + i] = g_rgb[i];
+        }
     } else {
         const int lane = threadIdx.x & 31, wslot = threadIdx.x & ~31;
         const int64_t wbase = n - lane;

@@ -242,10 +242,10 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
             }
             // F14: colour
             float r, g, bl;
-            if (DEG < 0) {
-                r = p.colors[3 * n + 0];
-                g = p.colors[3 * n + 1];
-                bl = p.colors[3 * n + 2];
+            if (DEG < 0) {   // direct RGB; NULL colors (N-D feature mode): the rgb slots are 0
+                r = p.colors ? p.colors[3 * n + 0] : 0.f;
+                g = p.colors ? p.colors[3 * n + 1] : 0.f;
+                bl = p.colors ? p.colors[3 * n + 2] : 0.f;
             } else {
                 float ex = mu0 - cc.campos[0], ey = mu1 - cc.campos[1], ez = mu2 - cc.campos[2];
                 float en = sqrtf((ex * ex + ey * ey) + ez * ez);

@@ -190,6 +190,13 @@ struct RasterParams {
     int depth_mode;
     float* out_depth;            // fwd output; bwd reads it (expected depth, mode 2)
     const float* v_depth;        // bwd: dL/d out_depth
+    // N-D features: 4 channels [c0, c0+4) of feats [n_gauss, D] per pass
+    const float* feats;
+    int D, c0, first_pass;
+    const int32_t* gids;         // packed mode: Gaussian of each record (dense: id - cam N)
+    float* out_feats;            // fwd: [C,H,W,D]
+    const float* v_feats_img;    // bwd: dL/d out_feats [C,H,W,D]
+    float* v_feats;              // bwd: [n_gauss, D] accumulated
     // diagnostics (gs_rasterize_stats)
     int32_t* n_eval;
     int32_t* n_contrib;
@@ -197,6 +204,18 @@ struct RasterParams {
     // (NULL: K7 recomputes them)
     uint16_t* smask;
 };
+
+// Gaussian of a record (dense ids are c*N + n; packed records carry it in gids)
+__device__ __forceinline__ int64_t gauss_of(const RasterParams& p, int32_t g, int cam) {
+    return p.gids ? (int64_t)p.gids[g] : (int64_t)g - (int64_t)cam * p.N;
+}
+
+// Channels [c0, c0 + 4) of a Gaussian's feature row (zeros past D)
+__device__ __forceinline__ float4 load_feat4(const RasterParams& p, int32_t g, int cam) {
+    const float* f = p.feats + gauss_of(p, g, cam) * p.D + p.c0;
+    const int m = p.D - p.c0;
+    return make_float4(__ldg(f), m > 1 ? __ldg(f + 1) : 0.f, m > 2 ? __ldg(f + 2) : 0.f, m > 3 ? __ldg(f + 3) : 0.f);
+}
 
 struct PixelCoord {
     int px, py, warp, lane;
@@ -230,14 +249,15 @@ struct Stage {
     typename std::conditional<(kBatch <= 256), uint8_t, uint16_t>::type list[kWarps][kBatch];
 };
 
-template <class StageT>
-__device__ __forceinline__ void stage_splat(const RasterParams& p, StageT& s, int slot, int idx, float x0, float y0) {
+template <bool FEAT, class StageT>
+__device__ __forceinline__ void stage_splat(const RasterParams& p, StageT& s, int slot, int idx, float x0, float y0,
+                                            int cam) {
     const int32_t g = p.ids[idx];
     const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
     const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
     s.xyo[slot] = r0;
     s.con[slot] = prescale_conic(r1.x, r1.y, r1.z);
-    s.rgb[slot] = r2;
+    s.rgb[slot] = FEAT ? load_feat4(p, g, cam) : r2;
     s.id[slot] = g;
     const uint32_t m16 = p.smask ? (uint32_t)p.smask[idx]
                                  : support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, p.alpha_min);
@@ -269,7 +289,7 @@ struct StageFwd {
     uint16_t list[2 * kWarps][kBatchFwd];
 };
 
-template <bool STATS, bool DEPTH>
+template <bool STATS, bool DEPTH, bool FEAT>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     pdl_trigger();
     pdl_wait();
@@ -287,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     const int bin = cam * p.TX * p.TY + tile;
     const int start = p.offs[bin], end = p.offs[bin + 1];
 
-    float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dacc = 0.f;
+    float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, dacc = 0.f;
     int last = start - 1;
     bool done = !inside;
     int n_eval = 0, n_contrib = 0;
@@ -304,7 +324,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
             s.xyo[t] = r0;
             s.con[t] = prescale_conic(r1.x, r1.y, r1.z);
-            s.rgb[t] = r2;
+            s.rgb[t] = FEAT ? load_feat4(p, g, cam) : r2;
             const uint16_t m16 = (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, amin);
             s.mask[t] = m16;
             if (!STATS && p.smask) p.smask[b0 + t] = m16;   // for K7 (every slot K7 can stage is staged here)
@@ -348,6 +368,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             c0 = __fmaf_rn(rgb.x, w, c0);   // C += c alpha T
             c1 = __fmaf_rn(rgb.y, w, c1);
             c2 = __fmaf_rn(rgb.z, w, c2);
+            if (FEAT) c3 = __fmaf_rn(rgb.w, w, c3);
             if (DEPTH) dacc = __fmaf_rn(xyo.w, w, dacc);   // sum z alpha T
             T = nT;
             last = b0 + (int)(j16 >> 4);
@@ -362,7 +383,15 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         }
         return;
     }
-    if (inside) {
+    if (inside && FEAT) {
+        const float cc[4] = {c0, c1, c2, c3};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int ch = p.c0 + k;
+            if (ch < p.D) p.out_feats[pix * p.D + ch] = cc[k] + (p.bg ? T * p.bg[cam * p.D + ch] : 0.f);
+        }
+    }
+    if (inside && !FEAT) {
         float g0 = 0.f, g1 = 0.f, g2 = 0.f;
         if (p.bg) {
             g0 = p.bg[3 * cam];
@@ -372,6 +401,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         p.out_rgb[3 * pix + 0] = c0 + T * g0;   // R3, Q25
         p.out_rgb[3 * pix + 1] = c1 + T * g1;
         p.out_rgb[3 * pix + 2] = c2 + T * g2;
+    }
+    if (inside) {
         p.out_alpha[pix] = 1.f - T;
         p.out_T[pix] = T;
         p.last_ids[pix] = last;
@@ -449,7 +480,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-template <bool ABSGRAD, bool DEPTH>
+template <bool ABSGRAD, bool DEPTH, bool FEAT>
 __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     pdl_trigger();
     pdl_wait();
@@ -461,17 +492,31 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     const int start = p.offs[bin];
     const int lane = q.lane;
 
-    float Tfin = 1.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, vA = 0.f, bgdot = 0.f, vD = 0.f;
+    float Tfin = 1.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, vA = 0.f, bgdot = 0.f, vD = 0.f;
     int last = start - 1;
     if (q.inside) {
         const int64_t pix = ((int64_t)cam * p.H + q.py) * p.W + q.px;
         Tfin = p.out_T[pix];
         last = p.last_ids[pix];
-        v0 = p.v_rgb[3 * pix + 0];
-        v1 = p.v_rgb[3 * pix + 1];
-        v2 = p.v_rgb[3 * pix + 2];
-        if (p.v_alpha) vA = p.v_alpha[pix];
-        if (p.bg) bgdot = p.bg[3 * cam] * v0 + p.bg[3 * cam + 1] * v1 + p.bg[3 * cam + 2] * v2;
+        if (FEAT) {
+            // channels [c0, c0+4) of this pass; B4's v_alpha is linear in v_C, so the passes'
+            // geometry gradients add up, and the alpha-output term enters in the first pass only
+            float vv[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int ch = p.c0 + k;
+                vv[k] = ch < p.D ? p.v_feats_img[pix * p.D + ch] : 0.f;
+                if (p.bg && ch < p.D) bgdot += p.bg[cam * p.D + ch] * vv[k];
+            }
+            v0 = vv[0]; v1 = vv[1]; v2 = vv[2]; v3 = vv[3];
+            if (p.v_alpha && p.first_pass) vA = p.v_alpha[pix];
+        } else {
+            v0 = p.v_rgb[3 * pix + 0];
+            v1 = p.v_rgb[3 * pix + 1];
+            v2 = p.v_rgb[3 * pix + 2];
+            if (p.v_alpha) vA = p.v_alpha[pix];
+            if (p.bg) bgdot = p.bg[3 * cam] * v0 + p.bg[3 * cam + 1] * v1 + p.bg[3 * cam + 2] * v2;
+        }
         if (DEPTH) {
             vD = p.v_depth[pix];
             if (p.depth_mode == 2) {
@@ -501,7 +546,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
         const int n = bend - bstart;
         __syncthreads();
         static_assert(kBatchBwd == kThreads, "one staged splat per thread");
-        if ((int)threadIdx.x < n) stage_splat(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0);
+        if ((int)threadIdx.x < n) stage_splat<FEAT>(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0, cam);
         __syncthreads();
         if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
         const int cnt = build_warp_list(s, n, q.warp, lane, wlast - bstart);
@@ -528,9 +573,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             g8[6] = fac * v0;                  // B3
             g8[7] = fac * v1;
             const float g_bl = fac * v2;
+            const float g_f3 = FEAT ? fac * v3 : 0.f;   // fourth feature channel of the pass
             // B4 + background / alpha-output terms (Q25, Q26):
             // v_alpha = sum_ch (c T - S ra) v_C + kbg ra = T (c . v_C) + ra (kbg - Sv)
             float cv = rgb.x * v0 + rgb.y * v1 + rgb.z * v2;
+            if (FEAT) cv += rgb.w * v3;
             float g_z = 0.f;
             if (DEPTH) {                       // depth as a fourth channel
                 g_z = fac * vD;
@@ -553,6 +600,41 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             g8[0] = k2 * (2.f * con.x * dx + con.y * dy);
             g8[1] = k2 * (con.y * dx + 2.f * con.z * dy);
             float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
+            if (FEAT) {
+                // geometry slots into the record gradient, the 4 channels into v_feats
+                float* fdst = p.v_feats + gauss_of(p, s.id[j], cam) * p.D + p.c0;
+                const bool ab = ABSGRAD && p.first_pass;
+                const int mch = p.D - p.c0;
+                if (__popc(vb) <= kFewLanes) {
+                    if (valid) {
+                        red_add_v4(dst, g8[0], g8[1], g8[2], 0.f);
+                        red_add_v4(dst + 4, g8[3], g8[4], g8[5], ab ? fabsf(g8[0]) : 0.f);
+                        if (ab) atomicAdd(dst + 11, fabsf(g8[1]));
+                        atomicAdd(fdst, g8[6]);
+                        if (mch > 1) atomicAdd(fdst + 1, g8[7]);
+                        if (mch > 2) atomicAdd(fdst + 2, g_bl);
+                        if (mch > 3) atomicAdd(fdst + 3, g_f3);
+                    }
+                    continue;
+                }
+                const float r8 = reduce_scatter8(g8, lane);
+                const int i8 = lane >> 2;
+                if ((lane & 3) == 0) {
+                    if (i8 < 6) atomicAdd(dst + slot8(i8), r8);
+                    else if (i8 - 6 < mch) atomicAdd(fdst + (i8 - 6), r8);
+                }
+                const float g4[4] = {g_bl, g_f3, ab ? fabsf(g8[0]) : 0.f, ab ? fabsf(g8[1]) : 0.f};
+                const float r4 = reduce_scatter4(g4, lane);
+                const int i4 = lane >> 3;
+                if ((lane & 7) == 0) {
+                    if (i4 < 2) {
+                        if (2 + i4 < mch) atomicAdd(fdst + 2 + i4, r4);
+                    } else if (ab) {
+                        atomicAdd(dst + (i4 == 2 ? 7 : 11), r4);
+                    }
+                }
+                continue;
+            }
             if (__popc(vb) <= kFewLanes) {
                 // few contributing lanes: each issues its own three 16-byte reductions -- 3 warp
                 // instructions instead of the ~45 of the shuffle tree
@@ -611,9 +693,9 @@ gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H,
     p.out_depth = out_depth; p.depth_mode = out_depth ? depth_mode : 0;
     dim3 grid(p.TX * p.TY, C);
     if (p.depth_mode)
-        launch_pdl(k_raster_fwd<false, true>, dim3(grid), dim3(kThreads), s, p);
+        launch_pdl(k_raster_fwd<false, true, false>, dim3(grid), dim3(kThreads), s, p);
     else
-        launch_pdl(k_raster_fwd<false, false>, dim3(grid), dim3(kThreads), s, p);
+        launch_pdl(k_raster_fwd<false, false, false>, dim3(grid), dim3(kThreads), s, p);
     GS_LAUNCH_CHECK("k_raster_fwd");
     return GS_OK;
 }
@@ -624,7 +706,7 @@ gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int 
     RasterParams p = make_params(o, C, N, W, H, splats, nullptr, ids, offs);
     p.n_eval = n_eval; p.n_contrib = n_contrib;
     dim3 grid(p.TX * p.TY, C);
-    launch_pdl(k_raster_fwd<true, false>, dim3(grid), dim3(kThreads), s, p);
+    launch_pdl(k_raster_fwd<true, false, false>, dim3(grid), dim3(kThreads), s, p);
     GS_LAUNCH_CHECK("k_raster_fwd<stats>");
     return GS_OK;
 }
@@ -647,13 +729,64 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
                    (int64_t)(nrec * GS_SPLAT_FLOATS / 4));
     dim3 grid(p.TX * p.TY, C);
     if (absgrad) {
-        if (p.depth_mode) launch_pdl(k_raster_bwd<true, true>, dim3(grid), dim3(kThreads), s, p);
-        else launch_pdl(k_raster_bwd<true, false>, dim3(grid), dim3(kThreads), s, p);
+        if (p.depth_mode) launch_pdl(k_raster_bwd<true, true, false>, dim3(grid), dim3(kThreads), s, p);
+        else launch_pdl(k_raster_bwd<true, false, false>, dim3(grid), dim3(kThreads), s, p);
     } else {
-        if (p.depth_mode) launch_pdl(k_raster_bwd<false, true>, dim3(grid), dim3(kThreads), s, p);
-        else launch_pdl(k_raster_bwd<false, false>, dim3(grid), dim3(kThreads), s, p);
+        if (p.depth_mode) launch_pdl(k_raster_bwd<false, true, false>, dim3(grid), dim3(kThreads), s, p);
+        else launch_pdl(k_raster_bwd<false, false, false>, dim3(grid), dim3(kThreads), s, p);
     }
     GS_LAUNCH_CHECK("k_raster_bwd");
+    return GS_OK;
+}
+
+gs_status launch_raster_fwd_nd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
+                               const float* feats, int D, const int32_t* gids, const float* bg, const int32_t* ids,
+                               const int32_t* offs, float* out_feats, float* out_alpha, float* out_T,
+                               int32_t* last_ids, uint16_t* isect_masks, cudaStream_t s) {
+    RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
+    p.out_alpha = out_alpha; p.out_T = out_T; p.last_ids = last_ids;
+    p.smask = isect_masks;
+    p.feats = feats; p.D = D; p.gids = gids; p.out_feats = out_feats;
+    dim3 grid(p.TX * p.TY, C);
+    // channel chunking: 4 channels per pass; every pass composites the same
+    // splats (identical T / last_ids / masks)
+    for (int c0 = 0; c0 < D; c0 += 4) {
+        p.c0 = c0;
+        p.first_pass = c0 == 0;
+        launch_pdl(k_raster_fwd<false, false, true>, dim3(grid), dim3(kThreads), s, p);
+    }
+    GS_LAUNCH_CHECK("k_raster_fwd<nd>");
+    return GS_OK;
+}
+
+gs_status launch_raster_bwd_nd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
+                               const float* feats, int D, const int32_t* gids, int64_t n_gauss, const float* bg,
+                               const int32_t* ids, const int32_t* offs, const float* out_T, const int32_t* last_ids,
+                               const float* v_feats_img, const float* v_alpha, int absgrad,
+                               const uint16_t* isect_masks, float* v_splats, float* v_feats, cudaStream_t s) {
+    RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
+    p.out_T = const_cast<float*>(out_T); p.last_ids = const_cast<int32_t*>(last_ids);
+    p.v_alpha = v_alpha; p.v_splats = v_splats; p.absgrad = absgrad;
+    p.smask = const_cast<uint16_t*>(isect_masks);
+    p.feats = feats; p.D = D; p.gids = gids; p.v_feats_img = v_feats_img; p.v_feats = v_feats;
+    const size_t nrec = o.packed ? (size_t)N : (size_t)C * (size_t)N;
+    if (N > 0)
+        launch_pdl(k_zero4, dim3(kZeroBlocks), dim3(256), s, reinterpret_cast<float4*>(v_splats),
+                   (int64_t)(nrec * GS_SPLAT_FLOATS / 4));
+    if (n_gauss > 0 && cudaMemsetAsync(v_feats, 0, sizeof(float) * (size_t)n_gauss * (size_t)D, s) != cudaSuccess) {
+        GS_LAUNCH_CHECK("v_feats memset");
+        return GS_ERR_CUDA;
+    }
+    dim3 grid(p.TX * p.TY, C);
+    for (int c0 = 0; c0 < D; c0 += 4) {
+        p.c0 = c0;
+        p.first_pass = c0 == 0;
+        if (absgrad)
+            launch_pdl(k_raster_bwd<true, false, true>, dim3(grid), dim3(kThreads), s, p);
+        else
+            launch_pdl(k_raster_bwd<false, false, true>, dim3(grid), dim3(kThreads), s, p);
+    }
+    GS_LAUNCH_CHECK("k_raster_bwd<nd>");
     return GS_OK;
 }
 

@@ -45,6 +45,8 @@ class _Rasterize(torch.autograd.Function):
         K = cfg["K"]
         dev = means.device
         packed = bool(cfg["packed"])
+        nd = bool(cfg["nd"])                  # N-D features: colors [N, D] composited as-is
+        proj_colors = None if nd else colors
         cam_ids = gid = nnz_dev = None
         if packed:
             # packed projection (Q29): one D->H read of nnz per call, like M below
@@ -58,7 +60,7 @@ class _Rasterize(torch.autograd.Function):
                 splats = torch.empty((n_rec, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
                 cam_ids = torch.empty(n_rec, dtype=torch.int32, device=dev)
                 gid = torch.empty(n_rec, dtype=torch.int32, device=dev)
-                L.gs_project_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, n_rec,
+                L.gs_project_packed(o, means, quats, scales, opacities, proj_colors, K, viewmats, Ks, W, H, n_rec,
                                     nnz_dev, novf, cam_ids, gid, radii, splats, ws)
                 nnz = int(nnz_dev.item())
                 _NNZ_CACHE[(N, C, W, H)] = math.ceil(nnz * 1.25) + 1024
@@ -69,7 +71,7 @@ class _Rasterize(torch.autograd.Function):
             n_rec = N
             radii = torch.empty((C, N, 2), dtype=torch.int32, device=dev)
             splats = torch.empty((C, N, L.SPLAT_FLOATS), dtype=torch.float32, device=dev)
-            L.gs_project(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, radii, splats)
+            L.gs_project(o, means, quats, scales, opacities, proj_colors, K, viewmats, Ks, W, H, radii, splats)
         TX, TY = L.tiles(W, H)
         offs = torch.empty(C * TX * TY + 1, dtype=torch.int32, device=dev)
         Mdev = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -90,15 +92,19 @@ class _Rasterize(torch.autograd.Function):
             if int(ovf.item()) == 0:
                 break
             cap = M + 1024
-        out_rgb = torch.empty((C, H, W, 3), dtype=torch.float32, device=dev)
+        out_rgb = torch.empty((C, H, W, colors.shape[1] if nd else 3), dtype=torch.float32, device=dev)
         out_alpha = torch.empty((C, H, W), dtype=torch.float32, device=dev)
         out_T = torch.empty((C, H, W), dtype=torch.float32, device=dev)
         last_ids = torch.empty((C, H, W), dtype=torch.int32, device=dev)
         depth_mode = cfg["depth_mode"]
         out_depth = torch.empty((C, H, W) if depth_mode else (0,), dtype=torch.float32, device=dev)
         masks = torch.empty(max(cap, 1), dtype=torch.int16, device=dev)
-        L.gs_rasterize_fwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_rgb, out_alpha, out_T, last_ids,
-                           out_depth if depth_mode else None, depth_mode, isect_masks=masks)
+        if nd:
+            L.gs_rasterize_fwd_nd(o, C, n_rec, W, H, splats, colors, gid if packed else None, backgrounds, ids, offs,
+                                  out_rgb, out_alpha, out_T, last_ids, isect_masks=masks)
+        else:
+            L.gs_rasterize_fwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_rgb, out_alpha, out_T,
+                               last_ids, out_depth if depth_mode else None, depth_mode, isect_masks=masks)
         if not packed:
             cam_ids = gid = torch.empty(0, dtype=torch.int32, device=dev)
             nnz_dev = torch.full((1,), C * N, dtype=torch.int64, device=dev)
@@ -126,13 +132,20 @@ class _Rasterize(torch.autograd.Function):
         o = cfg["opts"]
         W, H, K = cfg["width"], cfg["height"], cfg["K"]
         N, C = means.shape[0], viewmats.shape[0]
-        v_rgb = v_rgb.contiguous() if v_rgb is not None else torch.zeros((C, H, W, 3), device=means.device)
+        nd = bool(cfg["nd"])
+        v_rgb = (v_rgb.contiguous() if v_rgb is not None
+                 else torch.zeros((C, H, W, colors.shape[1] if nd else 3), device=means.device))
         v_alpha = v_alpha.contiguous() if v_alpha is not None else None
         v_splats = torch.empty_like(splats)
         absgrad = ctx.absgrad_out is not None
-        L.gs_rasterize_bwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_T, last_ids, v_rgb, v_alpha,
-                           absgrad, v_splats, out_depth=out_depth if depth_mode else None, v_out_depth=v_depth,
-                           depth_mode=depth_mode, isect_masks=masks)
+        v_colors = torch.empty_like(colors)
+        if nd:
+            L.gs_rasterize_bwd_nd(o, C, n_rec, W, H, splats, colors, gid if packed else None, N, backgrounds, ids,
+                                  offs, out_T, last_ids, v_rgb, v_alpha, absgrad, masks, v_splats, v_colors)
+        else:
+            L.gs_rasterize_bwd(o, C, n_rec, W, H, splats, backgrounds, ids, offs, out_T, last_ids, v_rgb, v_alpha,
+                               absgrad, v_splats, out_depth=out_depth if depth_mode else None, v_out_depth=v_depth,
+                               depth_mode=depth_mode, isect_masks=masks)
         if absgrad:
             ag = torch.stack([v_splats[..., 7], v_splats[..., 11]], dim=-1)
             if packed:
@@ -145,17 +158,17 @@ class _Rasterize(torch.autograd.Function):
         v_quats = torch.empty_like(quats)
         v_scales = torch.empty_like(scales)
         v_opac = torch.empty_like(opacities)
-        v_colors = torch.empty_like(colors)
+        pc, pvc = (None, None) if nd else (colors, v_colors)
         v_view = torch.empty_like(viewmats) if pose else None
         if packed:
             ws = _aligned_ws(L.gs_project_bwd_packed_workspace_size(N, C), means.device)
-            L.gs_project_bwd_packed(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, n_rec, nnz_dev,
-                                    cam_ids, gid, radii, v_splats, v_means, v_quats, v_scales, v_opac, v_colors, ws,
+            L.gs_project_bwd_packed(o, means, quats, scales, opacities, pc, K, viewmats, Ks, W, H, n_rec, nnz_dev,
+                                    cam_ids, gid, radii, v_splats, v_means, v_quats, v_scales, v_opac, pvc, ws,
                                     v_viewmats=v_view)
         else:
             ws = _aligned_ws(L.gs_project_bwd_workspace_size(N, C), means.device) if pose else None
-            L.gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, W, H, radii, v_splats,
-                             v_means, v_quats, v_scales, v_opac, v_colors, v_viewmats=v_view, workspace=ws)
+            L.gs_project_bwd(o, means, quats, scales, opacities, pc, K, viewmats, Ks, W, H, radii, v_splats,
+                             v_means, v_quats, v_scales, v_opac, pvc, v_viewmats=v_view, workspace=ws)
         cfg["v_splats"] = v_splats
         return v_means, v_quats, v_scales, v_opac, v_colors, v_view, None, None, None, None
 
@@ -167,7 +180,8 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
     """Render C views of N Gaussians.
 
     means [N,3], quats [N,4] (w,x,y,z), scales [N,3] (activated), opacities [N] (activated),
-    colors [N,3] (RGB, sh_degree None/-1) or [N,K,3] (SH), viewmats [C,4,4] (world->camera),
+    colors [N,3] (RGB, sh_degree None/-1), [N,K,3] (SH) or [N,D] with D != 3 (N-D features,
+    P:124-128: rendered as [C,H,W,D]), viewmats [C,4,4] (world->camera),
     Ks [C,3,3], backgrounds [C,3] or None.  rasterize_mode "classic" | "antialiased" (A.4).
     packed=True stores only the visible (camera, Gaussian) pairs (Q29): the per-item meta
     entries are then [nnz, ...] rows with meta["camera_ids"], meta["gaussian_ids"].
@@ -188,7 +202,11 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
     o = L.options(sh_degree=deg, antialiased=rasterize_mode == "antialiased", near_plane=near_plane,
                   far_plane=far_plane, eps2d=eps2d, alpha_max=alpha_max, tile_size=tile_size, bbox_mode=bbox_mode,
                   fov_clamp=fov_clamp, packed=packed)
-    cfg = dict(opts=o, width=int(width), height=int(height), K=K, packed=bool(packed), depth_mode=depth_mode)
+    nd = deg < 0 and colors.dim() == 2 and colors.shape[1] != 3
+    if nd and depth_mode:
+        raise ValueError("N-D features and depth rendering are not combined (render depth as a feature)")
+    cfg = dict(opts=o, width=int(width), height=int(height), K=K, packed=bool(packed), depth_mode=depth_mode,
+               nd=nd)
     C, N = viewmats.shape[0], means.shape[0]
     absgrad_out = torch.zeros((C, N, 2), device=means.device) if absgrad else None
     args = [t.contiguous() if t is not None else None for t in (means, quats, scales, opacities, colors, viewmats, Ks,
