@@ -483,22 +483,41 @@ __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_
 }
 
 // K5: tile ranges.  offsets[b] = first sorted index with key >= b; offsets[nbins] = M.
-__global__ void k_ranges_fill(int32_t* offsets, int nbins, const int* d_n) {
-    pdl_trigger();
-    pdl_wait();
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b <= nbins) offsets[b] = *d_n;
-}
-
-__global__ void k_ranges(const uint32_t* __restrict__ keys, const int* d_n, int32_t* offsets) {
+// K5: tile ranges by boundary detection over the sorted keys, 8 keys per thread (two
+// 16-byte loads): offsets[b] = first sorted index with key >= b for every b in
+// (key[i-1], key[i]], the bins past the last key and all bins of an empty list get n.
+constexpr int kRangeKeys = 8;
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, const int* d_n, int nbins,
+                                                int32_t* offsets) {
     pdl_trigger();
     pdl_wait();
     const int n = *d_n;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = keys[i];
-    const int64_t prev = i > 0 ? (int64_t)keys[i - 1] : -1;
-    for (int64_t b = prev + 1; b <= (int64_t)k; b++) offsets[b] = i;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i0 = t * kRangeKeys;
+    if (n == 0) {
+        for (int64_t b = t; b <= nbins; b += (int64_t)gridDim.x * blockDim.x) offsets[b] = 0;
+        return;
+    }
+    if (i0 >= n) return;
+    uint32_t k[kRangeKeys];
+    if (i0 + kRangeKeys <= n) {
+        const uint4 a = reinterpret_cast<const uint4*>(keys)[t * 2];
+        const uint4 c = reinterpret_cast<const uint4*>(keys)[t * 2 + 1];
+        k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = c.x; k[5] = c.y; k[6] = c.z; k[7] = c.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRangeKeys; j++) k[j] = i0 + j < n ? keys[i0 + j] : 0u;
+    }
+    int64_t prev = i0 > 0 ? (int64_t)keys[i0 - 1] : -1;
+#pragma unroll
+    for (int j = 0; j < kRangeKeys; j++) {
+        if (i0 + j < n) {
+            for (int64_t b = prev + 1; b <= (int64_t)k[j]; b++) offsets[b] = (int32_t)(i0 + j);
+            prev = k[j];
+        }
+    }
+    if (i0 + kRangeKeys >= n)   // owner of the last key: the bins past it end at n
+        for (int64_t b = prev + 1; b <= nbins; b++) offsets[b] = n;
 }
 
 __global__ void k_keys64(const uint32_t* __restrict__ keys32, const int32_t* __restrict__ ids,
@@ -636,8 +655,8 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     KV sorted = radix_sort(ia, ib, ids, d_nsort, cap, kbits, hist, rowtot, L.nb_sort_max, s);
     GS_LAUNCH_CHECK("isect/tile-sort");
     // 6. tile ranges (K5)
-    launch_pdl(k_ranges_fill, dim3(div_up(nbins + 1, 256)), dim3(256), s, tile_offsets, nbins, d_nsort);
-    if (cap > 0) launch_pdl(k_ranges, dim3(div_up(cap, 256)), dim3(256), s, sorted.k, d_nsort, tile_offsets);
+    launch_pdl(k_ranges, dim3(div_up(div_up(cap > 0 ? cap : 1, kRangeKeys), 256)), dim3(256), s, sorted.k, d_nsort,
+               nbins, tile_offsets);
     if (keys && cap > 0) launch_pdl(k_keys64, dim3(div_up(cap, 256)), dim3(256), s, sorted.k, sorted.v, splats, d_nsort, TT, B, keys);
     GS_LAUNCH_CHECK("isect/ranges");
     return GS_OK;

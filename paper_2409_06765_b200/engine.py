@@ -137,14 +137,14 @@ class Engine:
     def launches_per_step(self) -> int:
         """Kernels of the library launched by one step(): project 1; isect 3 (compaction) +
         3x4 (depth sort) + 3 (tile counts, scan, offsets) + 1 (emission) + 3P (tile sort,
-        P = ceil(bits/8)) + 2 (ranges); raster fwd 1; raster bwd 2 (zero-fill + walk);
+        P = ceil(bits/8)) + 1 (ranges); raster fwd 1; raster bwd 2 (zero-fill + walk);
         project bwd 1 (+1 pose reduction)."""
         bits = max(1, (self.C * self.TX * self.TY - 1).bit_length())
         P = (bits + 7) // 8
         pose = 1 if self.pose else 0      # k_pose_reduce
         if self.packed:   # project: count, scan, write; isect: identity items; project bwd: map + kernel
-            return 3 + (1 + 12 + 3 + 1 + 3 * P + 2) + 1 + 2 + 2 + pose
-        return 1 + (3 + 12 + 3 + 1 + 3 * P + 2) + 1 + 2 + 1 + pose
+            return 3 + (1 + 12 + 3 + 1 + 3 * P + 1) + 1 + 2 + 2 + pose
+        return 1 + (3 + 12 + 3 + 1 + 3 * P + 1) + 1 + 2 + 1 + pose
 
     @property
     def n_isect(self) -> int:
