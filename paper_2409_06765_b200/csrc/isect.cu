@@ -464,8 +464,16 @@ __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_
         for (int k = threadIdx.x; k <= ne; k += kT) s_off[k] = ent_off[e0 + k];
     __syncthreads();
     const int* offp = staged ? s_off : ent_off + e0;
+    int lo = 0;   // a thread's positions only grow, so its item index is a lower bound for the next
     for (int o = o0 + threadIdx.x; o < o1; o += kT) {
-        int lo = 0, hi = ne - 1;
+        // galloping search for the last item whose offset is <= o, starting from lo
+        int step = 1, hi = lo;
+        while (hi + step < ne && offp[hi + step] <= o) {
+            hi += step;
+            step <<= 1;
+        }
+        lo = hi;
+        hi = min(ne - 1, hi + step - 1);
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (offp[mid] <= o) lo = mid; else hi = mid - 1;
@@ -474,9 +482,11 @@ __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_
         const int kk = o - offp[lo];
         const int4 rc = ent_rect[j];
         const int w = rc.y - rc.x;
-        const int ty = rc.z + kk / w, tx = rc.x + kk % w;
+        // kk / w exactly: kk < w h <= 2^24, so floor((kk + 0.5) / w) survives the fp32 rounding
+        const int qy = (int)__fdividef((float)kk + 0.5f, (float)w);
+        const int ty = rc.z + qy, tx = rc.x + (kk - qy * w);
         const int32_t id = vis_val[j];
-        const uint32_t cam = g.cam_ids ? (uint32_t)g.cam_ids[id] : (uint32_t)(id / g.N);
+        const uint32_t cam = g.cam_ids ? (uint32_t)g.cam_ids[id] : (uint32_t)id / (uint32_t)g.N;
         out_key[o] = cam * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
         out_val[o] = id;
     }
