@@ -78,7 +78,7 @@ __device__ __forceinline__ float reduce_scatter16(const float (&v)[16], int lane
 // P:713-726): per camera, every thread's contribution is reduced over the block and written
 // as one per-(block, camera) partial; k_pose_reduce sums the partials in a fixed order.
 template <int DEG, bool POSE>
-__global__ void __launch_bounds__(kThreads) k_project_bwd(PBParams p) {
+__global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
     pdl_trigger();
     pdl_wait();
     const int64_t n0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
