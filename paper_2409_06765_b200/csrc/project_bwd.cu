@@ -139,32 +139,32 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
 #pragma unroll
         for (int i = 0; i < 12; i++) pw[i] = 0.f;
         if (vis) {
-        seen = true;
+            seen = true;
             const float4* vr = reinterpret_cast<const float4*>(p.v_splats + idx * GS_SPLAT_FLOATS);
             const float4 v0 = vr[0], v1 = vr[1], v2 = vr[2];
             const float* vm = p.viewmats + 16 * (int64_t)c;
             const float* Kc = p.Ks + 9 * (int64_t)c;
             float Wr[3][3], w[3];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++) {
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) Wr[i][j] = vm[4 * i + j];
                 w[i] = vm[4 * i + 3];
             }
             const float fx = Kc[0], fy = Kc[4], cx = Kc[2], cy = Kc[5];
             float t[3];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++) t[i] = Wr[i][0] * mu[0] + Wr[i][1] * mu[1] + Wr[i][2] * mu[2] + w[i];
             const float tz = t[2];
             // Sigma_c = Wr Sigma Wr^T
             float A[3][3], Sc[3][3];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) A[i][j] = Wr[i][0] * Sig[0][j] + Wr[i][1] * Sig[1][j] + Wr[i][2] * Sig[2][j];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) Sc[i][j] = A[i][0] * Wr[j][0] + A[i][1] * Wr[j][1] + A[i][2] * Wr[j][2];
             // J with clamp (Q27)
             float txc = t[0], tyc = t[1];
@@ -182,13 +182,13 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
             }
             const float J[2][3] = {{fx / tz, 0.f, -fx * txc / (tz * tz)}, {0.f, fy / tz, -fy * tyc / (tz * tz)}};
             float B[2][3], Sp[2][2];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 2; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) B[i][j] = J[i][0] * Sc[0][j] + J[i][1] * Sc[1][j] + J[i][2] * Sc[2][j];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 2; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 2; j++) Sp[i][j] = B[i][0] * J[j][0] + B[i][1] * J[j][1] + B[i][2] * J[j][2];
             const float a = Sp[0][0] + p.eps2d, b = Sp[0][1], cc = Sp[1][1] + p.eps2d;
             const float detb = a * cc - b * b;
@@ -220,17 +220,17 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
             // ---- P4: v_Sc = J^T vSp J; v_J = 2 vSp J Sc (Q11)
             float vSc[3][3], vJ[2][3];
             float PJ[2][3];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 2; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) PJ[i][j] = vSp[i][0] * J[0][j] + vSp[i][1] * J[1][j];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) vSc[i][j] = J[0][i] * PJ[0][j] + J[1][i] * PJ[1][j];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 2; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) vJ[i][j] = 2.f * (PJ[i][0] * Sc[0][j] + PJ[i][1] * Sc[1][j] + PJ[i][2] * Sc[2][j]);
             // ---- P5: v_t through J (exact with clamp Q27) and mu' (Q10)
             const float rz = 1.f / tz, rz2 = rz * rz, rz3 = rz2 * rz;
@@ -271,16 +271,16 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
                                          (vSc[i][2] + vSc[2][i]) * A[2][j];
             }
             // ---- P6: v_mu += W^T v_t; v_Sigma += W^T v_Sc W
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++) g_mu[i] += Wr[0][i] * vt0 + Wr[1][i] * vt1 + Wr[2][i] * vt2;
             float T1[3][3];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) T1[i][j] = vSc[i][0] * Wr[0][j] + vSc[i][1] * Wr[1][j] + vSc[i][2] * Wr[2][j];
-    #pragma unroll
+#pragma unroll
             for (int i = 0; i < 3; i++)
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < 3; j++) g_S[i][j] += Wr[0][i] * T1[0][j] + Wr[1][i] * T1[1][j] + Wr[2][i] * T1[2][j];
             // ---- P7: colour
             if (DEG < 0) {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
                 g_rgb[2] += v2.z;
             } else {
                 float campos[3];
-    #pragma unroll
+#pragma unroll
                 for (int i = 0; i < 3; i++) campos[i] = -(Wr[0][i] * w[0] + Wr[1][i] * w[1] + Wr[2][i] * w[2]);
                 const float ex = mu[0] - campos[0], ey = mu[1] - campos[1], ez = mu[2] - campos[2];
                 const float en = sqrtf(ex * ex + ey * ey + ez * ez);
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
                 sh_eval_basis<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, Yb);
                 float raw[3] = {0.5f, 0.5f, 0.5f};
                 if (vec) {
-    #pragma unroll
+#pragma unroll
                     for (int i = 0; i < NB * 3 / 4; i++) {
                         const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
                         raw[(4 * i + 0) % 3] += Yb[(4 * i + 0) / 3] * v.x;
@@ -307,18 +307,18 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
                         raw[(4 * i + 3) % 3] += Yb[(4 * i + 3) / 3] * v.w;
                     }
                 } else {
-    #pragma unroll
+#pragma unroll
                     for (int i = 0; i < NB * 3; i++) raw[i % 3] += Yb[i / 3] * __ldg(src + i);
                 }
                 const float vr[3] = {raw[0] > 0.f ? v2.x : 0.f, raw[1] > 0.f ? v2.y : 0.f, raw[2] > 0.f ? v2.z : 0.f};
-    #pragma unroll
+#pragma unroll
                 for (int i = 0; i < NB * 3; i++) s_gc[i][threadIdx.x] += Yb[i / 3] * vr[i % 3];
                 if (DEG > 0) {
                     float wj[NB];
-    #pragma unroll
+#pragma unroll
                     for (int j = 0; j < NB; j++) wj[j] = 0.f;
                     if (vec) {
-    #pragma unroll
+#pragma unroll
                         for (int i = 0; i < NB * 3 / 4; i++) {
                             const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
                             wj[(4 * i + 0) / 3] += v.x * vr[(4 * i + 0) % 3];
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
                             wj[(4 * i + 3) / 3] += v.w * vr[(4 * i + 3) % 3];
                         }
                     } else {
-    #pragma unroll
+#pragma unroll
                         for (int i = 0; i < NB * 3; i++) wj[i / 3] += __ldg(src + i) * vr[i % 3];
                     }
                     float gx = 0.f, gy = 0.f, gz = 0.f;
