@@ -78,6 +78,9 @@ typedef struct gs_options {
     int32_t packed;     /* 0 dense [C,N] records | 1 packed [nnz] records (Q29; the *_packed
                            entry points require 1, the dense ones 0; gs_rasterize_* read
                            N as the total record count when 1)                            */
+    int32_t support_cull;/* 1 (default): stages 3/4a skip (splat, 4x4-pixel block) pairs
+                           outside the conservative alpha-support of DESIGN.md K6 -- output
+                           invariant; 0: evaluate every pair of the tile (verification)   */
 } gs_options;
 
 /* ---- Projected splat record ------------------------------------------------------
@@ -100,7 +103,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 5
+#define GS_ABI_VERSION 6
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],

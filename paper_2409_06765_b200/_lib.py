@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 
@@ -26,6 +26,7 @@ class GsOptions(ct.Structure):
         ("alpha_max", ct.c_float), ("alpha_min", ct.c_float), ("t_min", ct.c_float),
         ("tile_size", ct.c_int32), ("antialiased", ct.c_int32), ("sh_degree", ct.c_int32),
         ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("packed", ct.c_int32),
+        ("support_cull", ct.c_int32),
     ]
 
 
@@ -93,7 +94,7 @@ def check(status: int, what: str) -> None:
 
 def options(sh_degree=3, antialiased=False, near_plane=0.01, far_plane=1e10, eps2d=0.3, alpha_max=0.99,
             alpha_min=1.0 / 255.0, t_min=1e-4, tile_size=16, bbox_mode=0, fov_clamp=True,
-            packed=False) -> GsOptions:
+            packed=False, support_cull=True) -> GsOptions:
     o = GsOptions()
     lib().gs_default_options(ct.byref(o))
     o.near_plane, o.far_plane, o.eps2d = near_plane, far_plane, eps2d
@@ -101,6 +102,7 @@ def options(sh_degree=3, antialiased=False, near_plane=0.01, far_plane=1e10, eps
     o.tile_size, o.antialiased, o.sh_degree = tile_size, int(bool(antialiased)), int(sh_degree)
     o.bbox_mode, o.fov_clamp = int(bbox_mode), int(bool(fov_clamp))
     o.packed = int(bool(packed))
+    o.support_cull = int(bool(support_cull))
     return o
 
 

@@ -27,6 +27,7 @@ gs_status check_opts(const gs_options* o) {
         !(o->t_min >= 0.f) || !(o->near_plane > 0.f))
         return GS_ERR_INVALID_ARGUMENT;
     if (o->bbox_mode < 0 || o->bbox_mode > 1 || o->packed < 0 || o->packed > 1) return GS_ERR_INVALID_ARGUMENT;
+    if (o->support_cull < 0 || o->support_cull > 1) return GS_ERR_INVALID_ARGUMENT;
     return GS_OK;
 }
 
@@ -66,6 +67,7 @@ void gs_default_options(gs_options* o) {
     o->bbox_mode = 0;
     o->fov_clamp = 1;
     o->packed = 0;
+    o->support_cull = 1;
 }
 
 const char* gs_status_string(int32_t s) {

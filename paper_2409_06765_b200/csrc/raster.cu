@@ -173,6 +173,7 @@ struct RasterParams {
     int C, W, H, TX, TY;
     int64_t N;
     float alpha_max, alpha_min, t_min;
+    int cull;                    // 1: conservative alpha-support test per (splat, 4x4 block); 0: every pair
     const float* splats;
     const float* bg;
     const int32_t* ids;
@@ -260,7 +261,8 @@ __device__ __forceinline__ void stage_splat(const RasterParams& p, StageT& s, in
     s.rgb[slot] = FEAT ? load_feat4(p, g, cam) : r2;
     s.id[slot] = g;
     const uint32_t m16 = p.smask ? (uint32_t)p.smask[idx]
-                                 : support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, p.alpha_min);
+                         : (p.cull ? support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, p.alpha_min)
+                                   : 0xffffu);
     s.mask[slot] = (uint8_t)support_mask8(m16);
 }
 
@@ -325,7 +327,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             s.xyo[t] = r0;
             s.con[t] = prescale_conic(r1.x, r1.y, r1.z);
             s.rgb[t] = FEAT ? load_feat4(p, g, cam) : r2;
-            const uint16_t m16 = (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, amin);
+            const uint16_t m16 =
+                p.cull ? (uint16_t)support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w, r2.w, x0, y0, amin)
+                       : (uint16_t)0xffffu;
             s.mask[t] = m16;
             if (!STATS && p.smask) p.smask[b0 + t] = m16;   // for K7 (every slot K7 can stage is staged here)
         }
@@ -677,6 +681,7 @@ RasterParams make_params(const gs_options& o, int C, int64_t N, int W, int H, co
     p.C = C; p.W = W; p.H = H; p.N = N;
     p.TX = div_up(W, GS_TILE); p.TY = div_up(H, GS_TILE);
     p.alpha_max = o.alpha_max; p.alpha_min = o.alpha_min; p.t_min = o.t_min;
+    p.cull = o.support_cull;
     p.splats = splats; p.bg = bg; p.ids = ids; p.offs = offs;
     return p;
 }
