@@ -668,6 +668,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
 }
 
 constexpr int kZeroBlocks = 148 * 8;
+#ifndef GS_FWD_PAD
+#define GS_FWD_PAD 4096
+#endif
+constexpr size_t kFwdPad = GS_FWD_PAD;   // dynamic shared-memory pad: at most 4 K6 CTAs per SM
 __global__ void __launch_bounds__(256) k_zero4(float4* __restrict__ p, int64_t n4) {
     pdl_trigger();
     pdl_wait();
@@ -700,7 +704,7 @@ gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H,
     if (p.depth_mode)
         launch_pdl(k_raster_fwd<false, true, false>, dim3(grid), dim3(kThreads), s, p);
     else
-        launch_pdl(k_raster_fwd<false, false, false>, dim3(grid), dim3(kThreads), s, p);
+        launch_pdl_smem(k_raster_fwd<false, false, false>, dim3(grid), dim3(kThreads), kFwdPad, s, p);
     GS_LAUNCH_CHECK("k_raster_fwd");
     return GS_OK;
 }
