@@ -103,7 +103,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 6
+#define GS_ABI_VERSION 7
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -292,6 +292,41 @@ GS_API gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t
                                        const int32_t* radii, const float* v_splats, float* v_means, float* v_quats,
                                        float* v_scales, float* v_opacities, float* v_colors, float* v_viewmats,
                                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* ==== Gaussian-sharded scale-out ("multi-GPU training support
+ * for large-scale scene reconstruction") ===============================================
+ * For scenes too large to replicate: rank r of R owns a contiguous shard of the Gaussians
+ * and renders a contiguous block of the views, [view_starts[r], view_starts[r+1]).  A step
+ * is
+ *   owner:  gs_project_packed over its shard and ALL C views  -> items camera-major
+ *           gs_shard_pack                                     -> send rows + per-rank counts
+ *   NCCL all-to-all of the 16-float rows (views' owners receive, source rank-major)
+ *   render: gs_shard_unpack -> gs_isect_tiles_packed / gs_rasterize_fwd / gs_rasterize_bwd
+ *           over the received items with C = its own view count
+ *   NCCL all-to-all of the per-item v_splats back along the reversed splits
+ *   owner:  gs_project_bwd_packed over its shard -> its parameter gradients (no all-reduce).
+ * Within each camera the received items are ordered by (source rank, local Gaussian index)
+ * = global Gaussian index when shards are contiguous and ascending with rank, so the sort
+ * order (camera, tile, depth, item) and hence every image bit equal the one-GPU packed
+ * (and dense) call's (Q16, Q29).
+ *
+ * gs_shard_pack.  In : camera_ids [cap] (camera-major, as gs_project_packed writes them),
+ *      *nnz (device, clamped to cap), radii [cap,2], splats [cap, GS_SPLAT_FLOATS], from
+ *      gs_project_packed; view_starts: HOST array of R+1 ascending camera indices,
+ *      view_starts[0] = 0, view_starts[R] = C; 1 <= R <= 64.
+ * Out: send [cap, GS_SHARD_ROW_FLOATS] fp32, row i = item i: the 12 record floats, the two
+ *      radii and the destination-local camera id c - view_starts[q] (int32 bit patterns in
+ *      floats 12..14), float 15 = 0.  Rows of destination q are contiguous (camera-major).
+ *      send_counts [R] int64 (device): rows per destination (sum = min(*nnz, cap)).
+ * gs_shard_unpack.  In : recv [n_recv, GS_SHARD_ROW_FLOATS] (host count n_recv).
+ * Out: camera_ids [n_recv], radii [n_recv,2], splats [n_recv, GS_SPLAT_FLOATS] and
+ *      *nnz = n_recv (device int64), ready for gs_isect_tiles_packed / gs_rasterize_*. */
+#define GS_SHARD_ROW_FLOATS 16
+GS_API gs_status gs_shard_pack(int64_t nnz_capacity, const int64_t* nnz, int32_t C, int32_t R,
+                               const int32_t* view_starts, const int32_t* camera_ids, const int32_t* radii,
+                               const float* splats, float* send, int64_t* send_counts, void* stream);
+GS_API gs_status gs_shard_unpack(int64_t n_recv, const float* recv, int32_t* camera_ids, int32_t* radii,
+                                 float* splats, int64_t* nnz, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 
@@ -65,6 +65,8 @@ SIGNATURES = {
     "gs_project_bwd_packed_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd_packed": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P, _P,
                                      _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "gs_shard_pack": (_I32, [_I64, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "gs_shard_unpack": (_I32, [_I64, _P, _P, _P, _P, _P, _P]),
 }
 
 
@@ -295,3 +297,24 @@ def gs_rasterize_bwd_nd(o, C, N, width, height, splats, feats, gaussian_ids, n_g
                                     ptr(isect_masks, torch.int16, "isect_masks"), ptr(v_splats, name="v_splats"),
                                     ptr(v_feats, name="v_feats"), stream_ptr(stream)),
           "gs_rasterize_bwd_nd")
+
+
+# ---- Gaussian-sharded scale-out (NEXT-4(i)) ---------------------------------------
+SHARD_ROW_FLOATS = 16
+
+
+def gs_shard_pack(cap_nnz, nnz, C, view_starts, camera_ids, radii, splats, send, send_counts, stream=None):
+    R = len(view_starts) - 1
+    vs = (ct.c_int32 * (R + 1))(*[int(v) for v in view_starts])
+    check(lib().gs_shard_pack(cap_nnz, ptr(nnz, torch.int64, "nnz"), C, R, ct.cast(vs, ct.c_void_p),
+                              ptr(camera_ids, torch.int32, "camera_ids"), ptr(radii, torch.int32, "radii"),
+                              ptr(splats, name="splats"), ptr(send, name="send"),
+                              ptr(send_counts, torch.int64, "send_counts"), stream_ptr(stream)),
+          "gs_shard_pack")
+
+
+def gs_shard_unpack(n_recv, recv, camera_ids, radii, splats, nnz, stream=None):
+    check(lib().gs_shard_unpack(int(n_recv), ptr(recv, name="recv"), ptr(camera_ids, torch.int32, "camera_ids"),
+                                ptr(radii, torch.int32, "radii"), ptr(splats, name="splats"),
+                                ptr(nnz, torch.int64, "nnz"), stream_ptr(stream)),
+          "gs_shard_unpack")

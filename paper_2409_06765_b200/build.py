@@ -28,6 +28,7 @@ SOURCES = {
     "project_bwd.cu": [],
     "isect.cu": ["-fmad=false"],
     "raster.cu": [],
+    "shard.cu": [],
 }
 HEADERS = ["gs_internal.cuh", "sh.cuh"]
 

@@ -104,3 +104,84 @@ def test_gloo_allreduce_equals_single_process():
     assert sorted(sum([r[1] for r in res], [])) == [0, 1, 2, 3]
     for _, _, flat in res:
         np.testing.assert_allclose(flat, ref, rtol=1e-12, atol=1e-15)
+
+
+# ---- Gaussian-sharded exchange (NEXT-4(i), paper_2409_06765_b200.gshard) ----------------
+def _shard_worker(rank, world, port, q, n_views):
+    """Each rank plays the owner of a shard with camera-major items and the renderer of its
+    views: rows encode (source rank, camera, local item); the forward all-to-all must deliver
+    exactly the rows of the renderer's cameras, source rank-major, in each source's order,
+    and the backward all-to-all must return every row to the position it came from."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2409_06765_b200 import gshard as G
+    vs = G.view_starts(n_views, world)
+    rng = np.random.default_rng(100 + rank)
+    per_cam = rng.integers(0, 7, size=n_views)          # items per camera on this owner
+    cams = np.repeat(np.arange(n_views), per_cam)       # camera-major (gs_project_packed order)
+    n = cams.size
+    send = torch.zeros((n, 16), dtype=torch.float32)
+    send[:, 0] = rank
+    send[:, 1] = torch.from_numpy(cams.astype(np.float32))
+    send[:, 2] = torch.arange(n, dtype=torch.float32)
+    counts = torch.tensor([int(((cams >= vs[d]) & (cams < vs[d + 1])).sum()) for d in range(world)],
+                          dtype=torch.int64)
+    ex = G.Exchange()
+    assert ex.world == world
+    recv_counts = ex.counts(counts)
+    rs, ss = recv_counts.tolist(), counts.tolist()
+    recv = torch.zeros((sum(rs), 16), dtype=torch.float32)
+    ex.rows(recv, send, rs, ss)
+    # "render": tag every received row, then send it back
+    back_in = recv.clone()
+    back_in[:, 3] = 1000 + rank
+    back = torch.zeros_like(send)
+    ex.rows(back, back_in, ss, rs)
+    q.put((rank, vs, cams, recv.numpy(), rs, back.numpy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_views", [(2, 4), (3, 2), (3, 7)])
+def test_gloo_sharded_exchange_routing(world, n_views):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q, n_views)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r[1:] for r in (q.get(timeout=300) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    vs = res[0][0]
+    for d in range(world):
+        _, _, recv, rs, _ = res[d]
+        # expected: for each source rank in order, its items of cameras [vs[d], vs[d+1]) in order
+        exp = []
+        for s in range(world):
+            cams = res[s][1]
+            idx = np.nonzero((cams >= vs[d]) & (cams < vs[d + 1]))[0]
+            exp += [(s, cams[i], i) for i in idx]
+            assert rs[s] == idx.size
+        got = [(int(r[0]), int(r[1]), int(r[2])) for r in recv]
+        assert got == exp
+    for s in range(world):
+        _, cams, _, _, back = res[s]
+        assert np.array_equal(back[:, 0], np.full(cams.size, s))
+        assert np.array_equal(back[:, 2], np.arange(cams.size))            # back in place
+        owner = np.searchsorted(vs, cams, side="right") - 1                 # renderer of each item
+        assert np.array_equal(back[:, 3], 1000 + owner)
+
+
+def test_view_starts_and_shards():
+    from paper_2409_06765_b200 import gshard as G
+    for V in [1, 2, 5, 32]:
+        for R in [1, 2, 3, 8]:
+            vs = G.view_starts(V, R)
+            assert vs[0] == 0 and vs[-1] == V and all(a <= b for a, b in zip(vs, vs[1:]))
+            for r in range(R):
+                assert list(range(vs[r], vs[r + 1])) == D.partition_views(V, R, r)
+            rng = [G.shard_range(1001, R, r) for r in range(R)]
+            assert rng[0][0] == 0 and rng[-1][1] == 1001
+            assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
