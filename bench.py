@@ -136,7 +136,7 @@ def run_ours(args):
     host_v = torch.from_numpy(v_img).pin_memory()
     params = tuple(host[k].to(dev) for k in keys)
     v_dev = host_v.to(dev)
-    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev)
+    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=args.bbox_mode)
     stream = torch.cuda.current_stream(dev)
 
     # size the intersection capacity once (one sync), outside any timed region
@@ -266,7 +266,8 @@ def run_ours(args):
     # timed region runs from before the first upload to after the last download.
     e2e = None
     if not args.no_e2e:
-        engs = [eng, Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, M_capacity=eng.cap)]
+        engs = [eng, Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, M_capacity=eng.cap,
+                             bbox_mode=args.bbox_mode)]
         d_in = [list(params), [t.clone() for t in params]]
         d_v = [v_dev, v_dev.clone()]
         engs[1].run_checked(tuple(d_in[1]), d_v[1])
@@ -331,11 +332,87 @@ def run_ours(args):
         "config": {"workload": f"{cfg_name}: {N} Gaussians SH{sc['sh_degree']}, {args.views_per_gpu} view(s) of "
                                f"{W}x{H} per GPU (BASELINE configs[1])", "global_batch_views": C * world,
                    "width": W, "height": H, "n_gaussians": N, "parallelism": f"views dp{world}",
+                   "bbox_mode": args.bbox_mode,
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "V_visible": V, "M_isect": M, "pairs_eval": E_f, "pairs_contrib": E_c},
         "roofline": roof, "stages": per_stage, "gpu_launches": launches * args.steps,
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
     }
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------
+def run_gshard(args):
+    """--shard gaussians: the Gaussian-sharded step (paper_2409_06765_b200.gshard, NEXT-4(i)).
+    Rank r owns Gaussians [N r/R, N (r+1)/R) of the scene and renders views_per_gpu views; a
+    step is project+pack -> all-to-all -> isect/raster fwd/bwd -> all-to-all -> project bwd,
+    with the one host read of the row counts inside the timed region."""
+    import torch
+    import torch.distributed as dist
+    from paper_2409_06765_b200.gshard import Exchange, ShardedEngine, shard_range
+    from synth import scenes as S
+
+    world, rank, local = _dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    cfg = S.CONFIGS[args.config]
+    vpg = args.views_per_gpu
+    C = vpg * world
+    sc = S.mipnerf_like_scene(cfg["N"], cfg["width"], cfg["height"], views=C, sh_degree=cfg["sh_degree"],
+                              seed=cfg["seed"])
+    N, W, H = sc["means"].shape[0], sc["width"], sc["height"]
+    n0, n1 = shard_range(N, world, rank)
+    keys = ["means", "quats", "scales", "opacities", "colors"]
+    params = tuple(torch.from_numpy(np.ascontiguousarray(sc[k][n0:n1], np.float32)).to(dev) for k in keys) + \
+        tuple(torch.from_numpy(np.ascontiguousarray(sc[k], np.float32)).to(dev) for k in ["viewmats", "Ks"])
+    v_img, _ = S.image_grads(cfg["seed"] + rank, vpg, H, W)
+    v_dev = torch.from_numpy(v_img).to(dev)
+    eng = ShardedEngine(n1 - n0, C, W, H, rank=rank, world=world, sh_degree=sc["sh_degree"], device=dev,
+                        bbox_mode=args.bbox_mode)
+    ex = Exchange()
+    for _ in range(args.warmup):
+        eng.step(params, v_dev, ex)
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        eng.step(params, v_dev, ex)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    tot_ms = float(np.sum([a.elapsed_time(b) for a, b in ev]))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms = tot_ms / args.steps
+    value = C * W * H / 1e6 / (ms / 1e3)
+    launches = 3 + 2 + 2 + (1 + 12 + 3 + 1 + 6 + 1) + 1 + 2 + 2
+    res = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Mip-NeRF-360-shaped scene)",
+           "config": {"workload": f"{args.config}: {N} Gaussians sharded over {world} GPU(s), {vpg} view(s) of "
+                                  f"{W}x{H} per GPU", "global_batch_views": C, "width": W, "height": H,
+                      "n_gaussians": N, "parallelism": f"gaussian-shard{world} + views{world}",
+                      "bbox_mode": args.bbox_mode, "items_sent": eng.n_send, "items_received": eng.n_recv,
+                      "l2": "flushed between steps (256 MiB write outside the per-step events)"},
+           "gpu_launches": launches * args.steps, "e2e": None, "cpu_baseline": None, "clocks": clocks}
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:
@@ -419,11 +496,18 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--bbox-mode", type=int, default=0, choices=[0, 1, 2],
+                    help="tile extent: 0 the paper's 3-sigma box (default), 2 opacity-aware (Q36)")
+    ap.add_argument("--shard", default="views", choices=["views", "gaussians"],
+                    help="views: Gaussians replicated + gradient all-reduce (default); gaussians: "
+                         "Gaussian-sharded step with record all-to-alls (NEXT-4(i))")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.shard == "gaussians":
+        run_gshard(args)
     else:
         run_ours(args)
 

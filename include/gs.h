@@ -73,7 +73,11 @@ typedef struct gs_options {
     int32_t tile_size;  /* 16 only                                                */
     int32_t antialiased;/* 0 classic | 1 opacity x sqrt(det S'/det(S'+sI))     */
     int32_t sh_degree;  /* -1: colors are RGB [N,3]; 0..3: colors are SH [N,K,3]   */
-    int32_t bbox_mode;  /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3 sqrt(lambda_max)     */
+    int32_t bbox_mode;  /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3 sqrt(lambda_max) |
+                           2 opacity-aware: per-axis extent min(3, k(o_eff)) sigma with
+                           k^2 = 2 (1.004 tau_ub + 4e-3), tau_ub >= ln(o_eff/alpha_min); o_eff
+                           < alpha_min culled (NEXT-4(ii), Q36; images and gradients equal
+                           mode 0's, fewer intersections)                              */
     int32_t fov_clamp;  /* 1 clamp t_x/t_z, t_y/t_z to the widened frustum for J only (Q27)*/
     int32_t packed;     /* 0 dense [C,N] records | 1 packed [nnz] records (Q29; the *_packed
                            entry points require 1, the dense ones 0; gs_rasterize_* read

@@ -47,7 +47,8 @@ typedef struct {
     int32_t tile_size;   /* 16                                                    */
     int32_t antialiased; /* 0 classic | 1 compensated opacity                 */
     int32_t sh_degree;   /* -1 direct RGB colors | 0..3 spherical harmonics               */
-    int32_t bbox_mode;   /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3*sqrt(lambda_max)   */
+    int32_t bbox_mode;   /* 0 per-axis 3-sigma AABB (Q12) | 1 square 3*sqrt(lambda_max) |
+                            2 opacity-aware extent (Q36)                                   */
     int32_t fov_clamp;   /* 1 clamp t_x/t_z, t_y/t_z for J only (Q27)                     */
     int32_t channels;    /* 0: RGB from the projection | D > 0: N-D features,
                             render inputs are [C*N, D] feature rows, images [C,H,W,D]     */
@@ -243,9 +244,33 @@ static keypath_t key_path_f32(const or_opts *o, int W, int H, const float *mu, c
     if (!(det > 0.f)) return kp;
     /* KP12 (F12): radii */
     int rx, ry;
-    if (o->bbox_mode == 0) {
+    if (o->bbox_mode == 0 || o->bbox_mode == 2) {
         rx = (int)ceilf(3.f * sqrtf(a));
         ry = (int)ceilf(3.f * sqrtf(c));
+        if (o->bbox_mode == 2 && o->alpha_min > 0.0) {
+            /* KP12b (DESIGN Q36): opacity-aware extent, fp32.
+             * A splat reaches alpha >= alpha_min only where sigma <= tau = ln(o_eff/alpha_min)
+             * (R1: alpha = o_eff exp(-sigma)).  Upper bound: x = o_eff/alpha_min = m 2^e,
+             * ln x = e ln2 + ln m and ln m <= 2(m-1)/(m+1) for m in (0,1].  Mahalanobis
+             * radius^2 = 2 tau (sigma = d^T conic d / 2), with the fp32 margin 1.004, 4e-3. */
+            float comp_b = 1.f;
+            if (o->antialiased) {
+                float det_raw_b = Sp[0][0] * Sp[1][1] - Sp[0][1] * Sp[0][1];
+                comp_b = sqrtf(fmaxf(0.f, det_raw_b / det));
+            }
+            float o_eff = op * comp_b;
+            float amin = (float)o->alpha_min;
+            if (!(o_eff >= amin)) return kp;               /* alpha < alpha_min at every pixel */
+            int e;
+            float m = frexpf(o_eff / amin, &e);
+            float tau_ub = (float)e * 0.693147182f + (2.f * (m - 1.f)) / (m + 1.f);
+            float k2 = 2.f * (tau_ub * 1.004f + 4e-3f);
+            float cond = (a * c) / det;                    /* 1/(1-rho^2) of Sigma'+sI */
+            if (k2 < 9.f && cond <= 1000.f) {              /* else the 3-sigma extent */
+                rx = (int)ceilf(sqrtf(k2 * a));
+                ry = (int)ceilf(sqrtf(k2 * c));
+            }
+        }
     } else {
         float m = 0.5f * (a + c);
         float lam = m + sqrtf(fmaxf(0.f, m * m - det));

@@ -26,7 +26,7 @@ gs_status check_opts(const gs_options* o) {
     if (!(o->eps2d >= 0.f) || !(o->alpha_max > 0.f) || !(o->alpha_max < 1.f) || !(o->alpha_min >= 0.f) ||
         !(o->t_min >= 0.f) || !(o->near_plane > 0.f))
         return GS_ERR_INVALID_ARGUMENT;
-    if (o->bbox_mode < 0 || o->bbox_mode > 1 || o->packed < 0 || o->packed > 1) return GS_ERR_INVALID_ARGUMENT;
+    if (o->bbox_mode < 0 || o->bbox_mode > 2 || o->packed < 0 || o->packed > 1) return GS_ERR_INVALID_ARGUMENT;
     if (o->support_cull < 0 || o->support_cull > 1) return GS_ERR_INVALID_ARGUMENT;
     return GS_OK;
 }

@@ -31,7 +31,7 @@ struct CamConst {
 struct ProjParams {
     int64_t N;
     int C, W, H, K;
-    float near_plane, far_plane, eps2d;
+    float near_plane, far_plane, eps2d, alpha_min;
     int antialiased, bbox_mode, fov_clamp;
     int vec_colors;   // colors base 16B-aligned and K*3 % 4 == 0
     const float* means;
@@ -184,9 +184,32 @@ __global__ void __launch_bounds__(kThreads) k_project_fwd(ProjParams p) {
                 det = a * c - b * b;                                   // KP11 (F9)
                 vis = det > 0.f;
                 if (vis) {
-                    if (p.bbox_mode == 0) {                           // KP12 (F12, Q12)
+                    if (p.bbox_mode != 1) {                           // KP12 (F12, Q12)
                         rx = (int)ceilf(3.f * sqrtf(a));
                         ry = (int)ceilf(3.f * sqrtf(c));
+                        if (p.bbox_mode == 2 && p.alpha_min > 0.f) {
+                            // KP12b (NEXT-4(ii), Q36): opacity-aware extent.  alpha >= alpha_min
+                            // needs sigma <= tau = ln(o_eff / alpha_min); tau_ub >= tau from
+                            // frexp (x = m 2^e) and ln m <= 2(m-1)/(m+1) on (0, 1].
+                            float comp2 = 1.f;
+                            if (p.antialiased) {
+                                const float det_raw = Sp00 * Sp11 - Sp01 * Sp01;
+                                comp2 = sqrtf(fmaxf(0.f, det_raw / det));
+                            }
+                            const float oe = op * comp2;
+                            if (!(oe >= p.alpha_min)) {
+                                vis = false;                              // never composited
+                            } else {
+                                int e2;
+                                const float m2 = frexpf(oe / p.alpha_min, &e2);
+                                const float tau = (float)e2 * 0.693147182f + (2.f * (m2 - 1.f)) / (m2 + 1.f);
+                                const float k2 = 2.f * (tau * 1.004f + 4e-3f);
+                                if (k2 < 9.f && (a * c) / det <= 1000.f) {
+                                    rx = (int)ceilf(sqrtf(k2 * a));
+                                    ry = (int)ceilf(sqrtf(k2 * c));
+                                }
+                            }
+                        }
                     } else {
                         float m = 0.5f * (a + c);
                         float lam = m + sqrtf(fmaxf(0.f, m * m - det));
@@ -345,7 +368,7 @@ ProjParams make_proj_params(const gs_options& o, int64_t N, int C, int W, int H,
                             const float* viewmats, const float* Ks, int32_t* radii, float* splats) {
     ProjParams p{};
     p.N = N; p.C = C; p.W = W; p.H = H; p.K = K;
-    p.near_plane = o.near_plane; p.far_plane = o.far_plane; p.eps2d = o.eps2d;
+    p.near_plane = o.near_plane; p.far_plane = o.far_plane; p.eps2d = o.eps2d; p.alpha_min = o.alpha_min;
     p.antialiased = o.antialiased; p.bbox_mode = o.bbox_mode; p.fov_clamp = o.fov_clamp;
     p.means = means; p.quats = quats; p.scales = scales; p.opac = opac; p.colors = colors;
     p.viewmats = viewmats; p.Ks = Ks; p.radii = radii; p.splats = splats;

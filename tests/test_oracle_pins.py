@@ -757,3 +757,61 @@ class TestNDFeatures:
                     assert abs(an - fd) <= 1e-5 * abs(fd) + 1e-7 * (1 + b["a2d"][0, n, off + j]), (name, n, j, an, fd)
                     checked += 1
         assert checked > 60
+
+
+# --------------------------------------------------------------------------- Q36 (NEXT-4(ii))
+class TestOpacityAwareExtent:
+    """bbox_mode 2: the per-axis extent min(3, k) sigma with k^2 >= 2 ln(o_eff / alpha_min)
+    (R1: alpha = o_eff exp(-sigma) >= alpha_min iff sigma <= ln(o_eff / alpha_min)).  Pinned by
+    the closed form of the alpha support for isotropic splats and by output invariance: the
+    method's images, transmittance, last splats and gradients are those of the 3-sigma box."""
+
+    def test_isotropic_extent_brackets_the_alpha_support(self, oracle_lib):
+        z, f = 2.0, 100.0
+        for s in [0.01, 0.05, 0.2]:
+            for op in [0.005, 0.02, 0.1, 0.3, 0.6, 0.99]:
+                sc = _one_gaussian([0, 0, z], [1, 0, 0, 0], [s, s, s], op, [1, 1, 1],
+                                   K=[[f, 0, 32], [0, f, 32], [0, 0, 1]])
+                p0 = oracle.project(sc, oracle.Options(sh_degree=-1, fov_clamp=0, bbox_mode=0))
+                p2 = oracle.project(sc, oracle.Options(sh_degree=-1, fov_clamp=0, bbox_mode=2))
+                sig = math.sqrt(float(np.float32(s)) ** 2 * f * f / (z * z) + 0.3)   # S:129 closed form
+                r0, r2 = p0["radii"][0, 0], p2["radii"][0, 0]
+                assert r0.tolist() == [math.ceil(3 * sig)] * 2
+                o32 = float(np.float32(op))
+                if o32 < 1 / 255:
+                    assert r2.tolist() == [0, 0]          # alpha < alpha_min everywhere: culled
+                    continue
+                k_true = math.sqrt(2 * math.log(o32 * 255))
+                assert np.all(r2 <= r0)
+                assert np.all(r2 >= min(3.0, k_true) * sig - 1e-6)             # contains the support
+                assert np.all(r2 <= math.ceil(min(3.0, k_true * 1.02 + 0.1) * sig))   # and is tight
+        # low opacity really shrinks the box (o = 0.02: k = sqrt(2 ln 5.1) = 1.81 vs 3)
+        sc = _one_gaussian([0, 0, z], [1, 0, 0, 0], [0.2] * 3, 0.02, [1, 1, 1], K=[[f, 0, 32], [0, f, 32], [0, 0, 1]])
+        r2 = oracle.project(sc, oracle.Options(sh_degree=-1, fov_clamp=0, bbox_mode=2))["radii"][0, 0]
+        assert r2[0] <= 0.65 * math.ceil(3 * math.sqrt(0.04 * 2500 + 0.3))
+
+    @pytest.mark.parametrize("name,aa", [("tiny", 0), ("tiny_sh3", 1), ("mip", 0), ("mip", 1), ("fig1", 0)])
+    def test_output_invariance(self, oracle_lib, name, aa):
+        if name == "tiny":
+            sc = S.tiny_scene(3, N=300, sh_degree=0)
+        elif name == "tiny_sh3":
+            sc = S.tiny_scene(4, N=400, width=97, height=61, sh_degree=3, views=2)
+        elif name == "mip":
+            sc = S.mipnerf_like_scene(3000, width=96, height=64, views=1, sh_degree=1, seed=5)
+        else:
+            sc = S.fig1_scene()
+        C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+        v_img = np.random.default_rng(1).normal(size=(C, H, W, 3))
+        res = {}
+        for mode in (0, 2):
+            o = oracle.Options(sh_degree=sc["sh_degree"], antialiased=aa, bbox_mode=mode)
+            res[mode] = oracle.forward_backward(sc, o, v_img)
+            res[mode]["M"] = res[mode]["keys"].size
+        a, b = res[0], res[2]
+        assert b["M"] <= a["M"]
+        for k in ("rgb", "alpha", "T", "last_gid"):
+            assert np.array_equal(a["fwd"][k], b["fwd"][k]), k
+        for k, g in a["grads"].items():
+            assert np.array_equal(g, b["grads"][k]), k
+        if name == "mip":
+            assert b["M"] < a["M"]
