@@ -321,6 +321,30 @@ def run_ours(args):
 
     launches = eng.launches_per_step() + (0 if world == 1 else 0)
 
+    # ---- variant: the opacity-aware tile extent (bbox_mode 2, Q36: same images and
+    # gradients, fewer intersections), timed the same way on the same inputs ----
+    variants = {}
+    if world == 1 and args.bbox_mode == 0 and not args.no_variants:
+        e2 = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=2)
+        e2.run_checked(params, v_dev)
+        for _ in range(args.warmup):
+            e2.step(params, v_dev)
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()
+            ev2[i][0].record(stream)
+            e2.step(params, v_dev)
+            ev2[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if int(e2.overflow.item()) != 0:
+            raise RuntimeError("intersection capacity overflowed (bbox_mode 2 variant)")
+        ms2 = float(np.sum([a.elapsed_time(b) for a, b in ev2])) / args.steps
+        variants["bbox_mode2"] = {"value": round(mp_per_step / (ms2 / 1e3), 3), "ms_per_step": round(ms2, 4),
+                                  "M_isect": e2.n_isect, "note": "opacity-aware tile extent (DESIGN Q36): "
+                                  "images and gradients identical to the 3-sigma box"}
+        del e2
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(sc, v_img, budget_s=args.cpu_budget)
@@ -336,7 +360,7 @@ def run_ours(args):
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "V_visible": V, "M_isect": M, "pairs_eval": E_f, "pairs_contrib": E_c},
         "roofline": roof, "stages": per_stage, "gpu_launches": launches * args.steps,
-        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "variants": variants,
     }
     if rank == 0:
         print(json.dumps(res), flush=True)
@@ -496,6 +520,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--bbox-mode", type=int, default=0, choices=[0, 1, 2],
                     help="tile extent: 0 the paper's 3-sigma box (default), 2 opacity-aware (Q36)")
     ap.add_argument("--shard", default="views", choices=["views", "gaussians"],

@@ -138,8 +138,9 @@ def test_sharded_equals_one_gpu_and_oracle(name, R):
     for k in ("rgb", "alpha", "T"):
         assert np.array_equal(sh[k], one[k]), f"sharded {k} must be bit-identical to the one-GPU call"
     assert np.array_equal(sh["last_gid"], U.last_gid(one, N)), "last composited splat per pixel"
-    for k in GRAD_KEYS:   # same kernels, fp32 atomic order only (cancelling sums: 1e-3 elementwise)
-        np.testing.assert_allclose(sh[k], one[k], rtol=1e-3, atol=1e-5 * max(np.abs(one[k]).max(), 1e-30))
+    for k in GRAD_KEYS:   # same kernels, fp32 atomic order only (cancelling sums: the 3D floor)
+        np.testing.assert_allclose(sh[k], one[k], rtol=U.GRAD_RTOL,
+                                   atol=U.GRAD3D_FLOOR * max(np.abs(one[k]).max(), 1e-30))
         rel = np.linalg.norm(sh[k] - one[k]) / max(np.linalg.norm(one[k]), 1e-30)
         assert rel <= 1e-5, (k, rel)
     # and the parity contract against the oracle
@@ -165,4 +166,23 @@ def test_sharded_capacity_growth():
     b = run_sharded(sc, 2, v_img, nnz_capacity=5)
     assert np.array_equal(a["rgb"], b["rgb"]) and np.array_equal(a["T"], b["T"])
     for k in GRAD_KEYS:
-        np.testing.assert_allclose(a[k], b[k], rtol=1e-4, atol=1e-5 * max(np.abs(a[k]).max(), 1e-30))
+        np.testing.assert_allclose(a[k], b[k], rtol=U.GRAD_RTOL, atol=U.GRAD3D_FLOOR * max(np.abs(a[k]).max(), 1e-30))
+
+
+@pytest.mark.slow
+def test_sharded_large_scene_full_scale():
+    """BASELINE configs[3]'s scene (6M Gaussians, SH3, 1920x1080) sharded over R = 8 simulated
+    ranks, one view each: every pixel of every view bit-identical to the one-GPU call over the
+    same 8 views, the last composited splat identical, and the sharded gradients (each rank's
+    750k Gaussians) equal to the one-GPU gradients up to fp32 atomic order."""
+    sc = S.scene_from_config("large6m", views=8)
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    v_img, _ = S.image_grads(11, C, H, W, l1_scale=False)
+    one = U.run_gpu(sc, v_img=v_img)
+    sh = run_sharded(sc, 8, v_img)
+    for k in ("rgb", "alpha", "T"):
+        assert np.array_equal(sh[k], one[k]), k
+    assert np.array_equal(sh["last_gid"], U.last_gid(one, N))
+    for k in GRAD_KEYS:
+        rel = np.linalg.norm(sh[k] - one[k]) / max(np.linalg.norm(one[k]), 1e-30)
+        assert rel <= 1e-5, (k, rel)
