@@ -106,6 +106,17 @@ def _dist_env():
     return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def _device_of(local_rank):
+    """One process per GPU.  GS_BENCH_BACKEND=gloo with more ranks than GPUs is only for
+    exercising the N > 1 code path on a one-GPU box (ranks share devices round-robin);
+    every reported multi-GPU number uses NCCL with one GPU per rank."""
+    import torch
+    n = torch.cuda.device_count()
+    if os.environ.get("GS_BENCH_BACKEND", "nccl") != "nccl" and n > 0:
+        return local_rank % n
+    return local_rank
+
+
 def build_scene(cfg_name, world, rank, views_per_gpu):
     from synth import scenes as S
     cfg = S.CONFIGS[cfg_name]
@@ -124,8 +135,9 @@ def run_ours(args):
 
     world, rank, local = _dist_env()
     if world > 1:
+        local = _device_of(local)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("GS_BENCH_BACKEND", "nccl"))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     cfg_name = args.config
@@ -381,8 +393,9 @@ def run_gshard(args):
 
     world, rank, local = _dist_env()
     if world > 1:
+        local = _device_of(local)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("GS_BENCH_BACKEND", "nccl"))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     cfg = S.CONFIGS[args.config]
