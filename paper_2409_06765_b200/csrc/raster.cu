@@ -484,6 +484,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+#ifdef GS_K7_STATS
+// debug builds only (GS_NVCC_EXTRA=-DGS_K7_STATS): visit counters of K7
+__device__ unsigned long long g_k7_stats[8];
+#define K7_STAT(i, v) \
+    do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_k7_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define K7_STAT(i, v) do { } while (0)
+#endif
+
 template <bool ABSGRAD, bool DEPTH, bool FEAT>
 __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     pdl_trigger();
@@ -564,6 +573,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 valid = eval_alpha_q(xyo.x, xyo.y, xyo.z, con, q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, xx, yy,
                                      xy, G, alpha);
             const unsigned vb = __ballot_sync(0xffffffffu, valid);
+            K7_STAT(0, 1);
+            K7_STAT(1, vb == 0);
+            K7_STAT(2, __popc(vb));
+            K7_STAT(3, (vb != 0) && __popc(vb) <= kFewLanes);
+            K7_STAT(4, ((vb & 0xffffu) == 0) != ((vb >> 16) == 0));   // only one 4x4 half takes it
             if (!vb) continue;
             // Branch-free from here: a lane that does not take this splat gets alpha = G = 0,
             // which makes every gradient term below exactly 0 and leaves T and Sv unchanged.
@@ -800,3 +814,13 @@ gs_status launch_raster_bwd_nd(const gs_options& o, int C, int64_t N, int W, int
 }
 
 }  // namespace gsb
+
+#ifdef GS_K7_STATS
+extern "C" GS_API int gs_debug_k7_stats(unsigned long long* host8, int reset) {
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        return (int)cudaMemcpyToSymbol(gsb::g_k7_stats, z, sizeof z);
+    }
+    return (int)cudaMemcpyFromSymbol(host8, gsb::g_k7_stats, 8 * sizeof(unsigned long long));
+}
+#endif
