@@ -82,7 +82,8 @@ class ShardedEngine:
     """
 
     def __init__(self, n_local, C, width, height, rank=0, world=1, sh_degree=3, K=None, antialiased=False,
-                 device="cuda", nnz_capacity=None, M_capacity=None, absgrad=False, **opt_kwargs):
+                 device="cuda", nnz_capacity=None, M_capacity=None, absgrad=False, view_starts=None, recv_capacity=None,
+                 **opt_kwargs):
         self.N, self.C, self.W, self.H = int(n_local), int(C), int(width), int(height)
         self.rank, self.world = int(rank), int(world)
         self.sh_degree = int(sh_degree)
@@ -90,7 +91,9 @@ class ShardedEngine:
         self.device = dev = torch.device(device)
         self.absgrad = bool(absgrad)
         self.opts = L.options(sh_degree=self.sh_degree, antialiased=antialiased, packed=True, **opt_kwargs)
-        self.vs = view_starts(self.C, self.world)
+        self.vs = list(view_starts) if view_starts is not None else globals()["view_starts"](self.C, self.world)
+        if len(self.vs) != self.world + 1 or self.vs[0] != 0 or self.vs[-1] != self.C:
+            raise ValueError("view_starts must be [0, ..., C] with one entry per rank + 1")
         self.c0, self.c1 = self.vs[self.rank], self.vs[self.rank + 1]
         self.C_loc = self.c1 - self.c0
         self.TX, self.TY = L.tiles(self.W, self.H)
@@ -111,7 +114,7 @@ class ShardedEngine:
         Cl = max(self.C_loc, 1)
         self.r_nnz = torch.zeros(1, dtype=torch.int64, device=dev)
         self.rcap = 0
-        self._alloc_recv(self.nnz_cap)
+        self._alloc_recv(recv_capacity if recv_capacity is not None else self.nnz_cap)
         self.M = torch.zeros(1, dtype=torch.int64, device=dev)
         self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
         self.tile_offsets = torch.zeros(Cl * self.TX * self.TY + 1, dtype=torch.int32, device=dev)

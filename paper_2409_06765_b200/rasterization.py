@@ -173,10 +173,93 @@ class _Rasterize(torch.autograd.Function):
         return v_means, v_quats, v_scales, v_opac, v_colors, v_view, None, None, None, None
 
 
+# last (items, received items, intersections) per problem shape of the distributed call
+_DIST_CACHE: dict = {}
+
+
+def _gather_cameras(viewmats, Ks, group):
+    """All ranks' cameras in rank order (counts may differ) and the view_starts of the
+    partition: rank r renders views [vs[r], vs[r+1]).  Small host-side collectives."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([viewmats.shape[0]], dtype=torch.int64)
+    cnts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    cnts = [int(c.item()) for c in cnts]
+    cmax = max(cnts)
+    cam = torch.zeros((cmax, 25), dtype=torch.float32)
+    cam[:viewmats.shape[0], :16] = viewmats.detach().reshape(-1, 16).cpu()
+    cam[:viewmats.shape[0], 16:] = Ks.detach().reshape(-1, 9).cpu()
+    allc = [torch.zeros_like(cam) for _ in range(world)]
+    dist.all_gather(allc, cam, group=group)
+    rows = torch.cat([a[:c] for a, c in zip(allc, cnts)])
+    vs = [0]
+    for c in cnts:
+        vs.append(vs[-1] + c)
+    dev = viewmats.device
+    return (rows[:, :16].reshape(-1, 4, 4).contiguous().to(dev), rows[:, 16:].reshape(-1, 3, 3).contiguous().to(dev),
+            vs)
+
+
+class _RasterizeDistributed(torch.autograd.Function):
+    """Gaussian-sharded rasterization (NEXT-4(i)): this rank holds a shard of the
+    Gaussians and its own cameras; projected records travel to the cameras' ranks and their
+    gradients back through two all-to-alls (gshard.py, include/gs.h).  Collective: every rank
+    of the group calls forward and backward."""
+
+    @staticmethod
+    def forward(ctx, means, quats, scales, opacities, colors, viewmats, Ks, backgrounds, cfg):
+        from .gshard import Exchange, ShardedEngine
+        import torch.distributed as dist
+        group = cfg["group"]
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        vm_all, K_all, vs = _gather_cameras(viewmats, Ks, group)
+        W, H = cfg["width"], cfg["height"]
+        N, C = means.shape[0], vm_all.shape[0]
+        key = (N, C, W, H, rank, world)
+        nnz_cap, rcap, mcap = _DIST_CACHE.get(key, (max(1024, C * N // 2), None, None))
+        eng = ShardedEngine(N, C, W, H, rank=rank, world=world, sh_degree=cfg["deg"], K=cfg["K"],
+                            antialiased=cfg["antialiased"], device=means.device, nnz_capacity=nnz_cap,
+                            recv_capacity=rcap, M_capacity=mcap, view_starts=vs, **cfg["opt_kwargs"])
+        ex = Exchange(group)
+        params = (means, quats, scales, opacities, colors, vm_all, K_all)
+        while True:
+            eng.project_and_pack(*params)
+            if eng.read_send_counts():
+                break
+        eng.exchange_forward(ex)
+        while True:
+            eng.render_forward(backgrounds)
+            if not eng.check_isect_capacity():
+                break
+        M = int(eng.M.item()) if eng.C_loc else 0
+        _DIST_CACHE[key] = (math.ceil(eng.n_send * 1.25) + 1024, math.ceil(eng.n_recv * 1.25) + 1024,
+                            math.ceil(M * 1.25) + 1024)
+        ctx.eng, ctx.ex = eng, ex
+        ctx.save_for_backward(means, quats, scales, opacities, colors, vm_all, K_all, backgrounds)
+        Cl = eng.C_loc
+        return eng.out_rgb[:Cl].clone(), eng.out_alpha[:Cl].clone()
+
+    @staticmethod
+    def backward(ctx, v_rgb, v_alpha):
+        means, quats, scales, opacities, colors, vm_all, K_all, backgrounds = ctx.saved_tensors
+        eng, ex = ctx.eng, ctx.ex
+        Cl = eng.C_loc
+        if v_rgb is None:
+            v_rgb = torch.zeros((Cl, eng.H, eng.W, 3), device=means.device)
+        eng.render_backward(v_rgb.contiguous() if Cl else None,
+                            v_alpha.contiguous() if (v_alpha is not None and Cl) else None, backgrounds)
+        eng.exchange_backward(ex)
+        eng.project_backward(means, quats, scales, opacities, colors, vm_all, K_all)
+        ctx.eng = None
+        return (eng.v_means.clone(), eng.v_quats.clone(), eng.v_scales.clone(), eng.v_opacities.clone(),
+                eng.v_colors.clone(), None, None, None, None)
+
+
 def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, height, *, sh_degree=None,
                   near_plane=0.01, far_plane=1e10, eps2d=0.3, rasterize_mode="classic", tile_size=16,
                   backgrounds=None, alpha_max=0.99, absgrad=False, fov_clamp=True, bbox_mode=0, packed=False,
-                  render_mode="RGB"):
+                  render_mode="RGB", distributed=False, group=None):
     """Render C views of N Gaussians.
 
     means [N,3], quats [N,4] (w,x,y,z), scales [N,3] (activated), opacities [N] (activated),
@@ -189,6 +272,12 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
     (expected depth) | "RGB+D" | "RGB+ED"; depth is rendered in the same kernels as colour and
     is the last channel of render_colors.  Gradients w.r.t. viewmats (camera pose)
     are computed when viewmats.requires_grad.
+    distributed=True (NEXT-4(i); needs torch.distributed initialised, `group` or the
+    default group): this rank's means..colors are ITS shard of the scene's Gaussians (shards
+    ascending with rank) and viewmats/Ks ITS cameras; the returned images are those cameras'
+    views of the WHOLE scene, and the gradients flow back to this rank's shard.  Collective in
+    forward and backward.  Supports SH or RGB colours, classic/antialiased, backgrounds and an
+    alpha loss; not combined with packed meta, depth, N-D features, absgrad or pose gradients.
     Returns render_colors [C,H,W,3], render_alphas [C,H,W,1] and a meta dict.
     """
     if rasterize_mode not in ("classic", "antialiased"):
@@ -199,6 +288,19 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
     depth_mode = modes[render_mode]
     deg = _sh_degree_of(colors, sh_degree)
     K = colors.shape[1] if deg >= 0 else 1
+    if distributed:
+        if depth_mode or absgrad or (deg < 0 and colors.shape[-1] != 3) or viewmats.requires_grad:
+            raise ValueError("distributed=True renders RGB / SH colours only (no depth, N-D features, absgrad "
+                             "or pose gradients)")
+        cfg = dict(width=int(width), height=int(height), K=K, deg=deg, antialiased=rasterize_mode == "antialiased",
+                   group=group, opt_kwargs=dict(near_plane=near_plane, far_plane=far_plane, eps2d=eps2d,
+                                                alpha_max=alpha_max, tile_size=tile_size, bbox_mode=bbox_mode,
+                                                fov_clamp=fov_clamp))
+        args = [t.contiguous() if t is not None else None for t in (means, quats, scales, opacities, colors, viewmats,
+                                                                  Ks, backgrounds)]
+        out_rgb, out_alpha = _RasterizeDistributed.apply(*args, cfg)
+        return out_rgb, out_alpha.unsqueeze(-1), dict(width=int(width), height=int(height), distributed=True,
+                                                      n_cameras=out_rgb.shape[0])
     o = L.options(sh_degree=deg, antialiased=rasterize_mode == "antialiased", near_plane=near_plane,
                   far_plane=far_plane, eps2d=eps2d, alpha_max=alpha_max, tile_size=tile_size, bbox_mode=bbox_mode,
                   fov_clamp=fov_clamp, packed=packed)
