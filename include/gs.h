@@ -332,6 +332,23 @@ GS_API gs_status gs_shard_pack(int64_t nnz_capacity, const int64_t* nnz, int32_t
 GS_API gs_status gs_shard_unpack(int64_t n_recv, const float* recv, int32_t* camera_ids, int32_t* radii,
                                  float* splats, int64_t* nnz, void* stream);
 
+/* ==== Densification statistics (App. ADC, Absgrad P:204-206)
+ * After gs_rasterize_bwd, per Gaussian n over the cameras c where (c,n) is visible
+ * (radii > 0), ACCUMULATED IN PLACE (not zero-filled: callers sum over training steps):
+ *   grad2d[n]    += || (sx g_x, sy g_y) ||, g = dL/dmu' of that view (v_splats slots 0, 1) or,
+ *                   absgrad != 0, its per-pixel absolute sums (slots 7, 11, written by
+ *                   gs_rasterize_bwd with absgrad = 1)
+ *   count[n]     += 1
+ *   max_radii[n]  = max(max_radii[n], max(rx, ry) * radius_scale)   (radius_scale >= 0)
+ * Dense (opt->packed == 0): radii [C,N,2], v_splats [C,N,12]; deterministic (one thread per
+ * Gaussian sums its cameras in order).  Packed: the per-item rows with gaussian_ids, *nnz
+ * clamped to nnz_capacity; fp32 atomics (sum order unspecified).  grad2d, max_radii [N] fp32,
+ * count [N] int32. */
+GS_API gs_status gs_densify_stats(const gs_options* opt, int64_t N, int32_t C, int64_t nnz_capacity,
+                                  const int64_t* nnz, const int32_t* gaussian_ids, const int32_t* radii,
+                                  const float* v_splats, int32_t absgrad, float sx, float sy, float radius_scale,
+                                  float* grad2d, int32_t* count, float* max_radii, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,7 +80,7 @@ def lib():
         _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
         _lib.or_isect.restype = i64
         _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6 + [P] * 2
-        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 6
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 7
         _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6 + [P] * 2
         _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
@@ -204,7 +204,8 @@ def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds
     Depth rendering: v_depth = dL/d(accumulated depth) [C,H,W] and/or
     v_depth_exp = dL/d(expected depth); the expected depth D/A (A = 1 - T_final = sum alpha T)
     enters by the quotient rule, dL/dD += v_exp / A and dL/dA += -v_exp D / A^2 (the alpha
-    output's gradient, Q26).  vz [C,N] = dL/d(depth of each (c,n)) (+ az, sz floors)."""
+    output's gradient, Q26).  vz [C,N] = dL/d(depth of each (c,n)) (+ az, sz floors).
+    absgrad [C,N,2] = sum over pixels of |dL_pixel/dmu'| per axis (App. Absgrad)."""
     o = opts.c()
     bg = None if backgrounds is None else _f64(backgrounds)
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
@@ -219,15 +220,15 @@ def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds
         ve = _f64(v_depth_exp)
         vD = (np.zeros((C, H, W)) if vD is None else vD) + np.where(ok, ve / Ar, 0.0)
         va = (np.zeros((C, H, W)) if va is None else va.copy()) + np.where(ok, -ve * f["depth"] / (Ar * Ar), 0.0)
-    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9))
+    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9)); absg = np.zeros((C, N, 2))
     vz = np.zeros((C, N)); az = np.zeros((C, N)); sz = np.zeros((C, N))
     amb = np.zeros((C, N), np.uint8)
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
-                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz), None)
-    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vz=vz, az=az, sz=sz)
+                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz), None, _p(absg))
+    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vz=vz, az=az, sz=sz, absgrad=absg)
 
 
 def _nd_opts(opts: Options, D: int) -> Options:
@@ -269,15 +270,15 @@ def render_bwd_nd(proj, feats, C, N, W, H, opts: Options, v_feat, v_alpha=None, 
     bg = None if backgrounds is None else _f64(backgrounds)
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
     va = None if v_alpha is None else _f64(v_alpha)
-    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9))
+    v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9)); absg = np.zeros((C, N, 2))
     vfeat = np.zeros((C, N, D))
     amb = np.zeros((C, N), np.uint8)
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(rows), _p(bg),
                         _p(tm), _p(_f64(v_feat)), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
-                        None, None, None, None, None, _p(vfeat))
-    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vfeat=vfeat,
+                        None, None, None, None, None, _p(vfeat), _p(absg))
+    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vfeat=vfeat, absgrad=absg,
                 v_colors=vfeat.sum(axis=0))
 
 
@@ -328,3 +329,19 @@ def forward_backward(scene, opts: Options, v_img, v_alpha=None, backgrounds=None
     res["bwd"] = render_bwd(proj, C, N, W, H, opts, v_img, v_alpha, backgrounds, tile_mask)
     res["grads"] = project_bwd(scene, proj, res["bwd"]["v2d"], opts)
     return res
+
+
+def densify_stats(radii, v_mean2d, scale=(1.0, 1.0), radius_scale=1.0):
+    """Densification statistics (App. ADC P:196-200 and Absgrad P:204-206):
+    per Gaussian n, over the cameras c where it is visible (radii > 0),
+        grad2d[n] = sum_c || (sx g_x, sy g_y) ||,  g = that view's dL/dmu' (or its Absgrad sums)
+        count[n]  = number of such cameras,  max_radii[n] = max_c max(rx, ry) * radius_scale.
+    radii [C,N,2], v_mean2d [C,N,2].  The definition written out (Q37)."""
+    radii = np.asarray(radii)
+    vis = (radii[..., 0] > 0) & (radii[..., 1] > 0)
+    g = _f64(v_mean2d) * np.asarray(scale, np.float64)
+    norms = np.sqrt((g * g).sum(axis=-1))
+    grad2d = np.where(vis, norms, 0.0).sum(axis=0)
+    count = vis.sum(axis=0).astype(np.int64)
+    max_radii = np.where(vis, radii.max(axis=-1), 0).max(axis=0) * float(radius_scale)
+    return dict(grad2d=grad2d, count=count, max_radii=max_radii.astype(np.float64))

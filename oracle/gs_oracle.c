@@ -756,6 +756,8 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
 /* a2d: same layout, sum over pixels of |term| with B4's v_alpha replaced by the */
 /* sum of the magnitudes of its parts (the fp32 condition floor)    */
 /* g_ambig[g] = 1 if g was evaluated at an ambiguous pixel.                     */
+/* absg (optional) [C,N,2]: sum over pixels of |d L_pixel / d mu'| per axis (the  */
+/* Absgrad statistic).                                                */
 /* T_replay_err (optional) = max |T_replayed - T_forward| over all steps.      */
 /* ------------------------------------------------------------------------- */
 typedef struct { int32_t g; double v[10], va[10], vs[10]; } term_t;   /* [9]: v_depth */
@@ -766,7 +768,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   const double *v_img, const double *v_alpha_img, double *v2d, double *a2d, double *s2d,
                   uint8_t *g_ambig, double *T_replay_err, const double *depth, const double *v_depth_img,
-                  double *vz, double *az, double *sz, double *vfeat)
+                  double *vz, double *az, double *sz, double *vfeat, double *absg)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
     const int D = n_channels(o);
@@ -778,6 +780,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
     if (vz) memset(vz, 0, sizeof(double) * C * N);
     if (az) memset(az, 0, sizeof(double) * C * N);
     if (sz) memset(sz, 0, sizeof(double) * C * N);
+    if (absg) memset(absg, 0, sizeof(double) * 2 * C * N);
     const int with_depth = depth && v_depth_img;
     double max_err = 0;
     for (int64_t c = 0; c < C; c++) {
@@ -918,6 +921,11 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 if (s2d) s2d[9 * (int64_t)g + j] += terms[i].vs[j];
             }
             if (vz) vz[g] += terms[i].v[9];
+            /* Absgrad (App. Absgrad): per-pixel absolute view-space gradients */
+            if (absg) {
+                absg[2 * (int64_t)g + 0] += fabs(terms[i].v[0]);
+                absg[2 * (int64_t)g + 1] += fabs(terms[i].v[1]);
+            }
             if (tvf)
                 for (int ch = 0; ch < D; ch++) vfeat[(int64_t)g * D + ch] += tvf[i * D + ch];
             if (az) az[g] += terms[i].va[9];

@@ -67,6 +67,8 @@ SIGNATURES = {
                                      _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "gs_shard_pack": (_I32, [_I64, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "gs_shard_unpack": (_I32, [_I64, _P, _P, _P, _P, _P, _P]),
+    "gs_densify_stats": (_I32, [_P, _I64, _I32, _I64, _P, _P, _P, _P, _I32, ct.c_float, ct.c_float, ct.c_float,
+                                _P, _P, _P, _P]),
 }
 
 
@@ -318,3 +320,15 @@ def gs_shard_unpack(n_recv, recv, camera_ids, radii, splats, nnz, stream=None):
                                 ptr(radii, torch.int32, "radii"), ptr(splats, name="splats"),
                                 ptr(nnz, torch.int64, "nnz"), stream_ptr(stream)),
           "gs_shard_unpack")
+
+
+# ---- densification statistics (NEXT-1; App. ADC, Absgrad P:204-206) -------------
+def gs_densify_stats(o, N, C, radii, v_splats, grad2d, count, max_radii, absgrad=False, scale=(1.0, 1.0),
+                     radius_scale=1.0, nnz_capacity=0, nnz=None, gaussian_ids=None, stream=None):
+    check(lib().gs_densify_stats(ct.byref(o), N, C, nnz_capacity, ptr(nnz, torch.int64, "nnz"),
+                                 ptr(gaussian_ids, torch.int32, "gaussian_ids"), ptr(radii, torch.int32, "radii"),
+                                 ptr(v_splats, name="v_splats"), int(bool(absgrad)), float(scale[0]),
+                                 float(scale[1]), float(radius_scale), ptr(grad2d, name="grad2d"),
+                                 ptr(count, torch.int32, "count"), ptr(max_radii, name="max_radii"),
+                                 stream_ptr(stream)),
+          "gs_densify_stats")

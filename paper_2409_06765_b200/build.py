@@ -29,6 +29,7 @@ SOURCES = {
     "isect.cu": ["-fmad=false"],
     "raster.cu": [],
     "shard.cu": [],
+    "stats.cu": [],
 }
 HEADERS = ["gs_internal.cuh", "sh.cuh"]
 

@@ -630,3 +630,51 @@ def test_opacity_aware_extent(name, packed):
         assert np.array_equal(U.last_gid(g2, N), U.last_gid(g0, N))
     for k in ("v_means", "v_quats", "v_scales", "v_opacities", "v_colors"):
         np.testing.assert_allclose(g2[k], g0[k], rtol=U.GRAD_RTOL, atol=U.GRAD3D_FLOOR * max(np.abs(g0[k]).max(), 1e-30))
+
+
+# ---- NEXT-1: Absgrad parity and densification statistics (App. ADC / Absgrad P:196-206) ---
+@pytest.mark.parametrize("name,packed", [("tiny_sh3_ragged", False), ("mip_small", False), ("mip_small_aa", True)])
+def test_absgrad_parity_and_densify_stats(name, packed):
+    import torch
+    from paper_2409_06765_b200 import _lib as L
+    sc, kw = _scene(name)
+    aa = kw.get("antialiased", 0)
+    C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
+    v_img, _ = S.image_grads(12, C, H, W, l1_scale=False)
+    o = oracle.Options(sh_degree=sc["sh_degree"], antialiased=aa)
+    p = oracle.project(sc, o)
+    f = oracle.render_fwd(p, C, N, W, H, o)
+    v_img[f["ambig"].astype(bool)] = 0
+    b = oracle.render_bwd(p, C, N, W, H, o, v_img.astype(np.float64))
+    gpu = U.run_gpu(sc, antialiased=aa, v_img=v_img, absgrad=True, packed=packed)
+    vis = (p["radii"][..., 0] > 0)
+    if packed:
+        cam, gid, _ = oracle.pack(p)
+        vs = U.unpack(gpu["v_splats"], cam, gid, C, N)
+        radii_dense = U.unpack(gpu["radii"], cam, gid, C, N)
+    else:
+        vs, radii_dense = gpu["v_splats"], gpu["radii"]
+    ag = np.stack([vs[..., 7], vs[..., 11]], axis=-1)
+    bad = U.check_grad2d(ag, b["absgrad"], b["a2d"][..., 0:2], vis, b["s2d"][..., 0:2])
+    assert bad.sum() == 0, bad.sum()
+    # statistics from the GPU's own radii / v_splats (inputs), both flavours, accumulated twice
+    eng = gpu["engine"]
+    dev = "cuda"
+    for absgrad in (False, True):
+        g2 = torch.zeros(N, device=dev)
+        cnt = torch.zeros(N, dtype=torch.int32, device=dev)
+        mr = torch.zeros(N, device=dev)
+        for _ in range(2):
+            if packed:
+                L.gs_densify_stats(eng.opts, N, C, eng.radii, eng.v_splats, g2, cnt, mr, absgrad=absgrad,
+                                   scale=(W / 2, H / 2), radius_scale=1 / max(W, H), nnz_capacity=eng.nnz_cap,
+                                   nnz=eng.nnz, gaussian_ids=eng.gaussian_ids)
+            else:
+                L.gs_densify_stats(eng.opts, N, C, eng.radii, eng.v_splats, g2, cnt, mr, absgrad=absgrad,
+                                   scale=(W / 2, H / 2), radius_scale=1 / max(W, H))
+        torch.cuda.synchronize()
+        g_in = ag if absgrad else vs[..., 0:2]
+        ref = oracle.densify_stats(radii_dense, g_in, scale=(W / 2, H / 2), radius_scale=1 / max(W, H))
+        np.testing.assert_allclose(g2.cpu().numpy(), 2 * ref["grad2d"], rtol=1e-5, atol=1e-30)
+        assert np.array_equal(cnt.cpu().numpy(), 2 * ref["count"])
+        np.testing.assert_allclose(mr.cpu().numpy(), ref["max_radii"], rtol=1e-6)

@@ -815,3 +815,47 @@ class TestOpacityAwareExtent:
             assert np.array_equal(g, b["grads"][k]), k
         if name == "mip":
             assert b["M"] < a["M"]
+
+
+# --------------------------------------------------------------------------- NEXT-1
+class TestDensificationStats:
+    """Absgrad (App. Absgrad) and the ADC statistics."""
+
+    def test_absgrad_equals_sum_of_single_pixel_gradients(self, oracle_lib):
+        """Brute force: the per-pixel absolute view-space gradient sums equal the sum over
+        pixels p of |v_mean2d| of the loss that keeps only pixel p (linearity of B1-B6 in v_C)."""
+        sc = S.tiny_scene(6, N=40, width=20, height=18, sh_degree=0)
+        o = oracle.Options(sh_degree=0)
+        p = oracle.project(sc, o)
+        v_img = np.random.default_rng(2).normal(size=(1, 18, 20, 3))
+        full = oracle.render_bwd(p, 1, 40, 20, 18, o, v_img)
+        acc = np.zeros((1, 40, 2))
+        for y in range(18):
+            for x in range(20):
+                vp = np.zeros_like(v_img)
+                vp[0, y, x] = v_img[0, y, x]
+                acc += np.abs(oracle.render_bwd(p, 1, 40, 20, 18, o, vp)["v2d"][..., 0:2])
+        assert np.allclose(full["absgrad"], acc, rtol=1e-12, atol=1e-18)
+        assert np.all(full["absgrad"] >= np.abs(full["v2d"][..., 0:2]) - 1e-15)
+        assert (full["absgrad"] > np.abs(full["v2d"][..., 0:2]) * (1 + 1e-9)).any()   # cancellation exists
+
+    def test_stats_special_cases(self, oracle_lib):
+        rng = np.random.default_rng(3)
+        C, N = 4, 50
+        radii = rng.integers(0, 9, size=(C, N, 2)).astype(np.int32)
+        radii[rng.uniform(size=(C, N)) < 0.3] = 0
+        g = rng.normal(size=(C, N, 2))
+        st = oracle.densify_stats(radii, g)
+        vis = (radii[..., 0] > 0) & (radii[..., 1] > 0)
+        # one camera: the norm of that view's gradient (library routine)
+        one = oracle.densify_stats(radii[:1], g[:1])
+        assert np.allclose(one["grad2d"], np.where(vis[0], np.linalg.norm(g[0], axis=-1), 0))
+        # camera order does not matter; counts are the visible views; homogeneity in the scale
+        perm = oracle.densify_stats(radii[::-1], g[::-1])
+        assert np.allclose(perm["grad2d"], st["grad2d"]) and np.array_equal(perm["count"], st["count"])
+        assert np.array_equal(st["count"], vis.sum(0))
+        sc2 = oracle.densify_stats(radii, g, scale=(2.0, 2.0), radius_scale=0.5)
+        assert np.allclose(sc2["grad2d"], 2 * st["grad2d"]) and np.allclose(sc2["max_radii"], 0.5 * st["max_radii"])
+        # invisible everywhere -> zeros
+        none = oracle.densify_stats(np.zeros_like(radii), g)
+        assert not none["grad2d"].any() and not none["count"].any() and not none["max_radii"].any()
