@@ -29,6 +29,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+CFG_INDEX = {"garden1m": "configs[1]", "batch3m": "configs[2]", "large6m": "configs[3]", "aa_packed1m": "configs[4]"}
 METRIC = "megapixels/sec fwd+bwd at 1/2/4/8 B200; fraction of HBM roofline"
 UNIT = "MP/s"
 SMS = 148
@@ -148,7 +149,10 @@ def run_ours(args):
     host_v = torch.from_numpy(v_img).pin_memory()
     params = tuple(host[k].to(dev) for k in keys)
     v_dev = host_v.to(dev)
-    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=args.bbox_mode)
+    from synth import scenes as S
+    cfgd = S.CONFIGS[cfg_name]
+    mode_kw = dict(antialiased=bool(cfgd.get("antialiased", 0)), packed=bool(cfgd.get("packed", 0)))
+    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=args.bbox_mode, **mode_kw)
     stream = torch.cuda.current_stream(dev)
 
     # size the intersection capacity once (one sync), outside any timed region
@@ -219,7 +223,7 @@ def run_ours(args):
     # ---- work counts for the roofline (outside the timed region) ----
     n_eval = torch.zeros((C, H, W), dtype=torch.int32, device=dev)
     n_con = torch.zeros_like(n_eval)
-    L.gs_rasterize_stats(eng.opts, C, N, W, H, eng.splats, eng.isect_ids, eng.tile_offsets, n_eval, n_con)
+    L.gs_rasterize_stats(eng.opts, C, eng.n_items, W, H, eng.splats, eng.isect_ids, eng.tile_offsets, n_eval, n_con)
     torch.cuda.synchronize(dev)
     E_f = int(n_eval.sum().item())
     E_c = int(n_con.sum().item())
@@ -230,7 +234,7 @@ def run_ours(args):
     tile = (ys * TX + xs).view(1, H, W) + torch.arange(C, device=dev).view(C, 1, 1) * (TX * TY)
     start = eng.tile_offsets[tile.long()]
     E_b = int((eng.last_ids - start + 1).clamp(min=0).sum().item())
-    V = int((eng.radii[..., 0] > 0).sum().item())
+    V = int(eng.nnz.item()) if eng.packed else int((eng.radii[..., 0] > 0).sum().item())
 
     peaks = _peaks()
     clk_mhz = peaks["sm_max_mhz"]
@@ -278,7 +282,7 @@ def run_ours(args):
     # timed region runs from before the first upload to after the last download.
     e2e = None
     if not args.no_e2e:
-        engs = [eng, Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, M_capacity=eng.cap,
+        engs = [eng, Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, M_capacity=eng.cap, **mode_kw,
                              bbox_mode=args.bbox_mode)]
         d_in = [list(params), [t.clone() for t in params]]
         d_v = [v_dev, v_dev.clone()]
@@ -337,7 +341,7 @@ def run_ours(args):
     # gradients, fewer intersections), timed the same way on the same inputs ----
     variants = {}
     if world == 1 and args.bbox_mode == 0 and not args.no_variants:
-        e2 = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=2)
+        e2 = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=2, **mode_kw)
         e2.run_checked(params, v_dev)
         for _ in range(args.warmup):
             e2.step(params, v_dev)
@@ -366,7 +370,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Mip-NeRF-360-shaped scene)",
         "config": {"workload": f"{cfg_name}: {N} Gaussians SH{sc['sh_degree']}, {args.views_per_gpu} view(s) of "
-                               f"{W}x{H} per GPU (BASELINE configs[1])", "global_batch_views": C * world,
+                               f"{W}x{H} per GPU (BASELINE {CFG_INDEX.get(cfg_name, '?')})", "global_batch_views": C * world,
                    "width": W, "height": H, "n_gaussians": N, "parallelism": f"views dp{world}",
                    "bbox_mode": args.bbox_mode,
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",

@@ -4,9 +4,10 @@
 // The method orders intersections by (camera, tile, depth) (ties by flat id, Q16).
 // Instead of one 48-bit LSD sort over all M intersections, this B200 design sorts in
 // two levels, which yields the identical order:
-//   1. compact the V visible (c,n) items, in (c,n) order                   [K2a, K2b]
+//   1. compact the V visible (c,n) items, in (c,n) order, each with a 16-B record
+//      (tile rectangle I1, flat id, camera)                                  [K2a, K2b]
 //   2. stable LSD radix sort of the V items by fp32 depth bits (4 x 8 bit)   [K4]
-//   3. per sorted item: tile rectangle (I1) and count, device scan -> M      [K2c, K2d]
+//   3. per sorted item: its record (one gather) and tile count, scan -> M    [K2c, K2d]
 //   4. load-balanced emission of (cam*TT + tile, c*N+n) in depth order       [K3]
 //   5. stable LSD radix sort of the M pairs by the ceil(log2(C*TT))-bit
 //      (camera, tile) key -- 2 passes at 1-MP, <= 15 views                   [K4]
@@ -108,6 +109,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, int 
     }
 }
 
+struct TileGeom {
+    int TX, TY, TT;
+    int64_t N;
+    const int32_t* cam_ids;   // packed mode: camera of each item (else camera = id / N)
+};
+
+// Compact record of a visible item: the packed tile rectangle (Q20) (x0 | x1 << 16,
+// y0 | y1 << 16), the flat id (c*N + n, or the packed index) and the camera.  Written in item
+// order by the compaction, gathered once per item after the depth sort (16 B instead of the
+// 48 B projected record and the radii), so the later stages stream sequentially.
+__device__ __forceinline__ int4 compact_record(const float4 r0, int2 r, int32_t id, int cam, const TileGeom& g) {
+    const int4 rc = tile_rect(r0.x, r0.y, r.x, r.y, g.TX, g.TY);
+    return make_int4(rc.x | (rc.y << 16), rc.z | (rc.w << 16), id, cam);
+}
+
 // ---------------------------------------------------------------------------------------
 // K2a / K2b: stable compaction of the visible (c,n) items.  Warp w of a block owns the
 // contiguous slice [base + 512 w, base + 512 (w+1)) and walks it in 16 coalesced rounds of
@@ -132,8 +148,9 @@ __global__ void __launch_bounds__(kT) k_vis_count(const int2* __restrict__ radii
 }
 
 __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ radii, const float* __restrict__ splats,
-                                                   int64_t n_items, const int* __restrict__ blockoff,
-                                                   uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+                                                   int64_t n_items, const int* __restrict__ blockoff, TileGeom g,
+                                                   uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val,
+                                                   int4* __restrict__ crec) {
     pdl_trigger();
     pdl_wait();
     __shared__ int s_wtot[kWarps];
@@ -162,8 +179,10 @@ __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ rad
         if (ball[k] & (1u << lane)) {
             const int64_t i = base + k * 32 + lane;
             const int p = pos + __popc(ball[k] & lt);
-            out_key[p] = __float_as_uint(splats[i * GS_SPLAT_FLOATS + 3]);   // depth >= near > 0 (Q17)
-            out_val[p] = (int32_t)i;
+            const float4 r0 = reinterpret_cast<const float4*>(splats)[i * 3];   // mu'.x, mu'.y, o, depth
+            out_key[p] = __float_as_uint(r0.w);   // depth >= near > 0 (Q17)
+            out_val[p] = p;
+            crec[p] = compact_record(r0, radii[i], (int32_t)i, (int)(i / g.N), g);
         }
         pos += __popc(ball[k]);
     }
@@ -171,16 +190,19 @@ __global__ void __launch_bounds__(kT) k_vis_compact(const int2* __restrict__ rad
 
 // Packed mode: every item is visible, so the "compaction" is the identity on the live
 // count V = min(*nnz, cap) (Q29).
-__global__ void k_packed_items(const float* __restrict__ splats, const int64_t* d_nnz, int64_t cap, int* d_V,
-                               uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+__global__ void k_packed_items(const int2* __restrict__ radii, const float* __restrict__ splats, const int64_t* d_nnz,
+                               int64_t cap, int* d_V, TileGeom g, uint32_t* __restrict__ out_key,
+                               int32_t* __restrict__ out_val, int4* __restrict__ crec) {
     pdl_trigger();
     pdl_wait();
     const int V = (int)min(*d_nnz, cap);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) *d_V = V;
     if (i >= V) return;
-    out_key[i] = __float_as_uint(splats[i * GS_SPLAT_FLOATS + 3]);
+    const float4 r0 = reinterpret_cast<const float4*>(splats)[i * 3];
+    out_key[i] = __float_as_uint(r0.w);
     out_val[i] = (int32_t)i;
+    crec[i] = compact_record(r0, radii[i], (int32_t)i, g.cam_ids[i], g);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -355,16 +377,10 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
 // ---------------------------------------------------------------------------------------
 // K2c: tile rectangle and tile count of every depth-sorted visible item (stored for the
 // emission), plus per-block (kSortTile items) sums.
-struct TileGeom {
-    int TX, TY, TT;
-    int64_t N;
-    const int32_t* cam_ids;   // packed mode: camera of each item (else camera = id / N)
-};
 
-__global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ radii, const float* __restrict__ splats,
-                                                    const int32_t* __restrict__ vis_val, const int* d_V, TileGeom g,
-                                                    int4* __restrict__ ent_rect, int* __restrict__ ent_cnt,
-                                                    int* blocksum) {
+__global__ void __launch_bounds__(kT) k_tiles_count(const int4* __restrict__ crec, const int32_t* __restrict__ vis_val,
+                                                    const int* d_V, int4* __restrict__ ent_rect,
+                                                    int* __restrict__ ent_cnt, int* blocksum) {
     pdl_trigger();
     pdl_wait();
     __shared__ int s_warp[33];
@@ -372,29 +388,19 @@ __global__ void __launch_bounds__(kT) k_tiles_count(const int2* __restrict__ rad
     const int nb = div_up(V, kSortTile);
     if ((int)blockIdx.x >= nb) return;
     const int base = blockIdx.x * kSortTile;
-    int32_t id[kSortItems];
+    int4 e[kSortItems];
 #pragma unroll
     for (int k = 0; k < kSortItems; k++) {
         const int j = base + k * kT + threadIdx.x;
-        id[k] = j < V ? vis_val[j] : -1;
-    }
-    int2 r[kSortItems];
-    float2 m[kSortItems];
-#pragma unroll
-    for (int k = 0; k < kSortItems; k++) {
-        if (id[k] >= 0) {
-            r[k] = radii[id[k]];
-            m[k] = *reinterpret_cast<const float2*>(splats + (int64_t)id[k] * GS_SPLAT_FLOATS);
-        }
+        e[k] = j < V ? crec[vis_val[j]] : make_int4(0, 0, 0, 0);
     }
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < kSortItems; k++) {
-        if (id[k] >= 0) {
-            const int4 rc = tile_rect(m[k].x, m[k].y, r[k].x, r[k].y, g.TX, g.TY);
-            const int c = (rc.y - rc.x) * (rc.w - rc.z);
-            const int j = base + k * kT + threadIdx.x;
-            ent_rect[j] = rc;
+        const int j = base + k * kT + threadIdx.x;
+        if (j < V) {
+            const int c = ((e[k].x >> 16) - (e[k].x & 0xffff)) * ((e[k].y >> 16) - (e[k].y & 0xffff));
+            ent_rect[j] = e[k];
             ent_cnt[j] = c;
             cnt += c;
         }
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(kT) k_tiles_offsets(const int* __restrict__ en
 // position finds its item by binary search there, so writes are fully coalesced whatever
 // the per-splat tile counts.
 __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_rect, const int* __restrict__ ent_off,
-                                                   const int32_t* __restrict__ vis_val, const int* d_V,
+                                                   const int* d_V,
                                                    const int* d_nsort, const int* __restrict__ first_item, TileGeom g,
                                                    uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
     pdl_trigger();
@@ -480,15 +486,13 @@ __global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_
         }
         const int j = e0 + lo;
         const int kk = o - offp[lo];
-        const int4 rc = ent_rect[j];
-        const int w = rc.y - rc.x;
+        const int4 e = ent_rect[j];   // packed rectangle, flat id, camera
+        const int x0 = e.x & 0xffff, w = (e.x >> 16) - x0, y0 = e.y & 0xffff;
         // kk / w exactly: kk < w h <= 2^24, so floor((kk + 0.5) / w) survives the fp32 rounding
         const int qy = (int)__fdividef((float)kk + 0.5f, (float)w);
-        const int ty = rc.z + qy, tx = rc.x + (kk - qy * w);
-        const int32_t id = vis_val[j];
-        const uint32_t cam = g.cam_ids ? (uint32_t)g.cam_ids[id] : (uint32_t)id / (uint32_t)g.N;
-        out_key[o] = cam * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
-        out_val[o] = id;
+        const int ty = y0 + qy, tx = x0 + (kk - qy * w);
+        out_key[o] = (uint32_t)e.w * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
+        out_val[o] = e.z;
     }
 }
 
@@ -547,7 +551,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
     size_t off_scalars, off_blocksum, off_rowtot, off_hist, off_first, off_vk, off_vv, off_ak, off_av, off_rect,
-        off_cnt, off_eoff, off_ka, off_va, off_kb, off_vb, total;
+        off_cnt, off_eoff, off_ka, off_va, off_kb, off_vb, off_crec, total;
     int nb_sort_max;   // blocks of kSortTile items (radix passes, tile counts)
 };
 
@@ -567,6 +571,7 @@ WsLayout ws_layout(int64_t n_items, int64_t cap) {
     L.off_ak = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_av = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_rect = o; o = align256(o + 16 * (size_t)(n_items + 1));
+    L.off_crec = o; o = align256(o + 16 * (size_t)(n_items + 1));
     L.off_cnt = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_eoff = o; o = align256(o + 4 * (size_t)(n_items + 2));
     L.off_ka = o; o = align256(o + 4 * (size_t)(cap + 1));
@@ -623,6 +628,7 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     KV vis{reinterpret_cast<uint32_t*>(w + L.off_vk), reinterpret_cast<int32_t*>(w + L.off_vv)};
     KV alt{reinterpret_cast<uint32_t*>(w + L.off_ak), reinterpret_cast<int32_t*>(w + L.off_av)};
     int4* ent_rect = reinterpret_cast<int4*>(w + L.off_rect);
+    int4* crec = reinterpret_cast<int4*>(w + L.off_crec);
     int* ent_cnt = reinterpret_cast<int*>(w + L.off_cnt);
     int* ent_off = reinterpret_cast<int*>(w + L.off_eoff);
     KV ia{reinterpret_cast<uint32_t*>(w + L.off_ka), reinterpret_cast<int32_t*>(w + L.off_va)};
@@ -637,13 +643,13 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
 
     // 1. stable compaction of the visible (c,n) items (K2a, K2b); identity when packed
     if (d_nnz) {
-        launch_pdl(k_packed_items, dim3(div_up(n_items > 0 ? n_items : 1, 256)), dim3(256), s, splats, d_nnz, n_items, d_V, vis.k,
-                                                                             vis.v);
+        launch_pdl(k_packed_items, dim3(div_up(n_items > 0 ? n_items : 1, 256)), dim3(256), s, r2, splats, d_nnz, n_items, d_V,
+                   g, vis.k, vis.v, crec);
     } else {
         launch_pdl(k_vis_count, dim3(nb_items), dim3(kT), s, r2, n_items, blocksum);
         launch_pdl(k_scan_blocksums, dim3(1), dim3(kScanThreads), s, blocksum, kTile, nullptr, n_items, INT64_MAX, d_V, nullptr,
                                                      nullptr, 0, nullptr);
-        launch_pdl(k_vis_compact, dim3(nb_items), dim3(kT), s, r2, splats, n_items, blocksum, vis.k, vis.v);
+        launch_pdl(k_vis_compact, dim3(nb_items), dim3(kT), s, r2, splats, n_items, blocksum, g, vis.k, vis.v, crec);
     }
     GS_LAUNCH_CHECK("isect/compact");
     // 2. stable sort by fp32 depth bits (K4, 4 passes)
@@ -651,14 +657,14 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     GS_LAUNCH_CHECK("isect/depth-sort");
     // 3. tile rectangles, counts, offsets, M, overflow, clamped count (K2c, K2d)
     const int nb_v = div_up(n_items > 0 ? n_items : 1, kSortTile);
-    launch_pdl(k_tiles_count, dim3(nb_v), dim3(kT), s, r2, splats, dsorted.v, d_V, g, ent_rect, ent_cnt, blocksum);
+    launch_pdl(k_tiles_count, dim3(nb_v), dim3(kT), s, crec, dsorted.v, d_V, ent_rect, ent_cnt, blocksum);
     launch_pdl(k_scan_blocksums, dim3(1), dim3(kScanThreads), s, blocksum, kSortTile, d_V, 0, INT64_MAX, nullptr, M, overflow, cap,
                                                  d_nsort);
     launch_pdl(k_tiles_offsets, dim3(nb_v), dim3(kT), s, ent_cnt, d_V, blocksum, ent_off, first_item, div_up(cap, kEmit));
     // 4. load-balanced emission in depth order (K3)
     if (cap > 0)
-        launch_pdl(k_tiles_emit, dim3(div_up(cap, kEmit)), dim3(kT), s, ent_rect, ent_off, dsorted.v, d_V, d_nsort, first_item, g,
-                                                       ia.k, ia.v);
+        launch_pdl(k_tiles_emit, dim3(div_up(cap, kEmit)), dim3(kT), s, ent_rect, ent_off, d_V, d_nsort, first_item, g, ia.k,
+                   ia.v);
     GS_LAUNCH_CHECK("isect/emit");
     // 5. stable sort by (camera, tile) (K4); values land in the caller's isect_ids
     const int kbits = tile_bits(nbins) > 0 ? tile_bits(nbins) : 1;
