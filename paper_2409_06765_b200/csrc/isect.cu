@@ -35,7 +35,7 @@ constexpr int kT = 256;              // threads per block
 constexpr int kWarps = kT / 32;
 constexpr int kItems = 16;           // compaction: items per thread
 constexpr int kTile = kT * kItems;   // compaction: items per block (4096)
-constexpr int kSortItems = 4;        // radix passes and per-item tile counts: items per thread ...
+constexpr int kSortItems = 4;        // per-item tile counts and small radix sorts: items per thread ...
 constexpr int kSortTile = kT * kSortItems;   // ... and per block (1024: enough blocks to fill 148 SMs)
 constexpr int kScanThreads = 1024;
 constexpr int kEmit = 2048;          // output positions per emission block
@@ -222,26 +222,27 @@ __device__ __forceinline__ unsigned warp_peers(unsigned d) {
     return peers;
 }
 
+template <int IT>
 __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
                                                    int shift, int* hist, int nb_max) {
     pdl_trigger();
     pdl_wait();
     __shared__ int s_hist[256];
     const int n = (int)min((int64_t)*d_n, cap);
-    const int nb = div_up(n, kSortTile);
+    const int nb = div_up(n, (kT * IT));
     if ((int)blockIdx.x >= nb) return;
     s_hist[threadIdx.x] = 0;
     __syncthreads();
-    const int base = blockIdx.x * kSortTile;
+    const int base = blockIdx.x * (kT * IT);
     const int lane = threadIdx.x & 31;
-    uint32_t key[kSortItems];
+    uint32_t key[IT];
 #pragma unroll
-    for (int k = 0; k < kSortItems; k++) {
+    for (int k = 0; k < IT; k++) {
         const int i = base + k * kT + threadIdx.x;
         key[k] = i < n ? keys[i] : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < kSortItems; k++) {
+    for (int k = 0; k < IT; k++) {
         const int i = base + k * kT + threadIdx.x;
         const unsigned d = i < n ? (key[k] >> shift) & 255u : 256u;
         const unsigned peers = warp_peers(d);
@@ -256,13 +257,14 @@ __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ 
 // goes to rowtot[d].
 constexpr int kRowItems = 16;   // rows up to 4096 blocks (4 M keys) in one pass, more in rounds
 
+template <int IT>
 __global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, const int* d_n, int64_t cap,
                                                         int* rowtot) {
     pdl_trigger();
     pdl_wait();
     __shared__ int s_warp[33];
     const int n = (int)min((int64_t)*d_n, cap);
-    const int nb = div_up(n, kSortTile);
+    const int nb = div_up(n, (kT * IT));
     int* row = hist + (int64_t)blockIdx.x * nb_max;
     int carry = 0;
     for (int r = 0; r < nb; r += kT * kRowItems) {
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, c
     if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
 }
 
+template <int IT>
 __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict__ keys_in,
                                                       const int32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
                                                       int32_t* __restrict__ vals_out, const int* d_n, int64_t cap,
@@ -297,10 +300,10 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
     __shared__ int s_dstart[256];         // start of digit d inside this block's sorted tile
     __shared__ int s_goff[256];           // global start of digit d for this block
     __shared__ int s_warp[33];
-    __shared__ uint32_t s_k[kSortTile];
-    __shared__ int32_t s_v[kSortTile];
+    __shared__ uint32_t s_k[(kT * IT)];
+    __shared__ int32_t s_v[(kT * IT)];
     const int n = (int)min((int64_t)*d_n, cap);
-    const int nb = div_up(n, kSortTile);
+    const int nb = div_up(n, (kT * IT));
     if ((int)blockIdx.x >= nb) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -308,19 +311,19 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
     for (int w = 0; w < kWarps; w++) s_cnt[w][threadIdx.x] = 0;
     __syncthreads();
     // 1. per-warp stable ranks over the warp's contiguous slice of 128 items
-    const int base = blockIdx.x * kSortTile + warp * (kSortTile / kWarps);
-    uint32_t key[kSortItems];
-    int32_t val[kSortItems];
-    int rank[kSortItems];
+    const int base = blockIdx.x * (kT * IT) + warp * ((kT * IT) / kWarps);
+    uint32_t key[IT];
+    int32_t val[IT];
+    int rank[IT];
 #pragma unroll
-    for (int k = 0; k < kSortItems; k++) {
+    for (int k = 0; k < IT; k++) {
         const int i = base + k * 32 + lane;
         const bool valid = i < n;
         key[k] = valid ? keys_in[i] : 0u;
         val[k] = valid ? vals_in[i] : 0;
     }
 #pragma unroll
-    for (int k = 0; k < kSortItems; k++) {
+    for (int k = 0; k < IT; k++) {
         const bool valid = base + k * 32 + lane < n;
         const unsigned d = valid ? (key[k] >> shift) & 255u : 256u;
         const unsigned peers = warp_peers(d);
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
     __syncthreads();
     // 3. reorder the tile by digit in shared memory
 #pragma unroll
-    for (int k = 0; k < kSortItems; k++) {
+    for (int k = 0; k < IT; k++) {
         if (rank[k] >= 0) {
             const unsigned d = (key[k] >> shift) & 255u;
             const int p = s_dstart[d] + s_cnt[warp][d] + rank[k];
@@ -360,9 +363,9 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
     }
     __syncthreads();
     // 4. coalesced write-out of the digit runs
-    const int nloc = min(kSortTile, n - blockIdx.x * kSortTile);
+    const int nloc = min((kT * IT), n - blockIdx.x * (kT * IT));
 #pragma unroll
-    for (int k = 0; k < kSortItems; k++) {
+    for (int k = 0; k < IT; k++) {
         const int j = k * kT + threadIdx.x;
         if (j < nloc) {
             const uint32_t kk = s_k[j];
@@ -590,20 +593,34 @@ struct KV {
 // ceil(bits/8) stable 8-bit LSD passes over `a` (live count *d_n <= cap), ping-ponging with
 // `b`.  The last pass writes its values to `final_vals` when given.  Returns the buffers
 // holding the sorted result.
-KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
-              int nb_max, cudaStream_t s) {
+// Keys per block: 1024 below kBigSort keys (enough blocks to fill 148 SMs at 0.6-3 M keys),
+// 2048 above (half the blocks and histogram rows; measured at 14-45 M keys: configs[2]
+// isect 3.69 -> 2.94 ms; 4096 was slower at both sizes).
+constexpr int64_t kBigSort = 1 << 22;
+
+template <int IT>
+KV radix_sort_t(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
+                int nb_max, cudaStream_t s) {
     const int passes = bits <= 0 ? 0 : div_up(bits, 8);
+    const int nb = div_up(cap > 0 ? cap : 1, kT * IT);   // <= nb_max (sized for 1024-key blocks)
     KV in = a, out = b;
     for (int p = 0; p < passes; p++) {
         int32_t* vdst = (p == passes - 1 && final_vals) ? final_vals : out.v;
-        launch_pdl(k_radix_hist, dim3(nb_max), dim3(kT), s, in.k, d_n, cap, 8 * p, hist, nb_max);
-        launch_pdl(k_radix_scan_rows, dim3(256), dim3(kT), s, hist, nb_max, d_n, cap, rowtot);
-        launch_pdl(k_radix_scatter, dim3(nb_max), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max, rowtot);
+        launch_pdl(k_radix_hist<IT>, dim3(nb), dim3(kT), s, in.k, d_n, cap, 8 * p, hist, nb_max);
+        launch_pdl(k_radix_scan_rows<IT>, dim3(256), dim3(kT), s, hist, nb_max, d_n, cap, rowtot);
+        launch_pdl(k_radix_scatter<IT>, dim3(nb), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max,
+                   rowtot);
         KV next_in{out.k, vdst};
         out = in;
         in = next_in;
     }
     return in;
+}
+
+KV radix_sort(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
+              int nb_max, cudaStream_t s) {
+    if (cap >= kBigSort) return radix_sort_t<8>(a, b, final_vals, d_n, cap, bits, hist, rowtot, nb_max, s);
+    return radix_sort_t<4>(a, b, final_vals, d_n, cap, bits, hist, rowtot, nb_max, s);
 }
 
 }  // namespace
