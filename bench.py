@@ -151,7 +151,7 @@ def run_ours(args):
     v_dev = host_v.to(dev)
     from synth import scenes as S
     cfgd = S.CONFIGS[cfg_name]
-    mode_kw = dict(antialiased=bool(cfgd.get("antialiased", 0)), packed=bool(cfgd.get("packed", 0)))
+    mode_kw = dict(antialiased=bool(cfgd.get("antialiased", 0)), packed=bool(cfgd.get("packed", 0)) or args.packed)
     eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=args.bbox_mode, **mode_kw)
     stream = torch.cuda.current_stream(dev)
 
@@ -372,7 +372,7 @@ def run_ours(args):
         "config": {"workload": f"{cfg_name}: {N} Gaussians SH{sc['sh_degree']}, {args.views_per_gpu} view(s) of "
                                f"{W}x{H} per GPU (BASELINE {CFG_INDEX.get(cfg_name, '?')})", "global_batch_views": C * world,
                    "width": W, "height": H, "n_gaussians": N, "parallelism": f"views dp{world}",
-                   "bbox_mode": args.bbox_mode,
+                   "bbox_mode": args.bbox_mode, "packed": mode_kw["packed"],
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "V_visible": V, "M_isect": M, "pairs_eval": E_f, "pairs_contrib": E_c},
         "roofline": roof, "stages": per_stage, "gpu_launches": launches * args.steps,
@@ -538,6 +538,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--packed", action="store_true", help="packed (visible-only) per-item layout (Q29)")
     ap.add_argument("--bbox-mode", type=int, default=0, choices=[0, 1, 2],
                     help="tile extent: 0 the paper's 3-sigma box (default), 2 opacity-aware (Q36)")
     ap.add_argument("--shard", default="views", choices=["views", "gaussians"],
