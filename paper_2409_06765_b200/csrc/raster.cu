@@ -356,7 +356,53 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         const uint32_t a_rgb = (uint32_t)__cvta_generic_to_shared(s.rgb);
         // the two halves of the warp walk their own lists in lockstep; each lane leaves on its
         // own at termination or at the end of its half's list
-        for (int k = 0; k < cnt; k++) {
+        int k = 0;
+        if (!STATS) {
+            // two splats per step: both alphas are evaluated up front (independent MUFU / LDS
+            // chains in flight), then composited in list order; a termination at the first
+            // stops before the second (Q15), so the result equals the one-at-a-time walk
+            for (; k + 1 < cnt; k += 2) {
+                const uint32_t ja = (uint32_t)list[k] << 4, jb = (uint32_t)list[k + 1] << 4;
+                const float4 xa = lds4(a_xyo + ja), xb = lds4(a_xyo + jb);
+                float dxa, dya, Ga, aa, dxb, dyb, Gb, ab;
+                const bool oka = eval_alpha(xa.x, xa.y, xa.z, lds4(a_con + ja), fpx, fpy, amax, amin, dxa, dya, Ga, aa);
+                const bool okb = eval_alpha(xb.x, xb.y, xb.z, lds4(a_con + jb), fpx, fpy, amax, amin, dxb, dyb, Gb, ab);
+                if (oka) {
+                    const float nT = __fmul_rn(T, __fsub_rn(1.f, aa));
+                    if (nT <= tmin) {
+                        done = true;
+                        break;
+                    }
+                    const float w = __fmul_rn(aa, T);
+                    const float4 rgb = lds4(a_rgb + ja);
+                    c0 = __fmaf_rn(rgb.x, w, c0);
+                    c1 = __fmaf_rn(rgb.y, w, c1);
+                    c2 = __fmaf_rn(rgb.z, w, c2);
+                    if (FEAT) c3 = __fmaf_rn(rgb.w, w, c3);
+                    if (DEPTH) dacc = __fmaf_rn(xa.w, w, dacc);
+                    T = nT;
+                    last = b0 + (int)(ja >> 4);
+                }
+                if (okb) {
+                    const float nT = __fmul_rn(T, __fsub_rn(1.f, ab));
+                    if (nT <= tmin) {
+                        done = true;
+                        break;
+                    }
+                    const float w = __fmul_rn(ab, T);
+                    const float4 rgb = lds4(a_rgb + jb);
+                    c0 = __fmaf_rn(rgb.x, w, c0);
+                    c1 = __fmaf_rn(rgb.y, w, c1);
+                    c2 = __fmaf_rn(rgb.z, w, c2);
+                    if (FEAT) c3 = __fmaf_rn(rgb.w, w, c3);
+                    if (DEPTH) dacc = __fmaf_rn(xb.w, w, dacc);
+                    T = nT;
+                    last = b0 + (int)(jb >> 4);
+                }
+            }
+            if (done) continue;
+        }
+        for (; k < cnt; k++) {
             const uint32_t j16 = (uint32_t)list[k] << 4;
             const float4 xyo = lds4(a_xyo + j16);
             float dx, dy, G, alpha;
