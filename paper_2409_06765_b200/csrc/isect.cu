@@ -8,7 +8,8 @@
 //      (tile rectangle I1, flat id, camera)                                  [K2a, K2b]
 //   2. stable LSD radix sort of the V items by fp32 depth bits (4 x 8 bit)   [K4]
 //   3. per sorted item: its record (one gather) and tile count, scan -> M    [K2c, K2d]
-//   4. load-balanced emission of (cam*TT + tile, c*N+n) in depth order       [K3]
+//   4. emission of (cam*TT + tile, c*N+n) in depth order, one warp per 32
+//      items, coalesced writes                                               [K3]
 //   5. stable LSD radix sort of the M pairs by the ceil(log2(C*TT))-bit
 //      (camera, tile) key -- 2 passes at 1-MP, <= 15 views                   [K4]
 //   6. tile ranges by boundary detection                                     [K5]
@@ -38,7 +39,6 @@ constexpr int kTile = kT * kItems;   // compaction: items per block (4096)
 constexpr int kSortItems = 4;        // per-item tile counts and small radix sorts: items per thread ...
 constexpr int kSortTile = kT * kSortItems;   // ... and per block (1024: enough blocks to fill 148 SMs)
 constexpr int kScanThreads = 1024;
-constexpr int kEmit = 2048;          // output positions per emission block
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -413,11 +413,9 @@ __global__ void __launch_bounds__(kT) k_tiles_count(const int4* __restrict__ cre
     if (threadIdx.x == 0) blocksum[blockIdx.x] = tot;
 }
 
-// K2d: exclusive offsets of the per-item counts (ent_off[V] = M), in item order, and the
-// first item of every emission block (the item owning position b * kEmit).
+// K2d: exclusive offsets of the per-item counts (ent_off[V] = M), in item order.
 __global__ void __launch_bounds__(kT) k_tiles_offsets(const int* __restrict__ ent_cnt, const int* d_V,
-                                                      const int* __restrict__ blockoff, int* __restrict__ ent_off,
-                                                      int* __restrict__ first_item, int n_emit_blocks) {
+                                                      const int* __restrict__ blockoff, int* __restrict__ ent_off) {
     pdl_trigger();
     pdl_wait();
     __shared__ int s_warp[33];
@@ -437,65 +435,53 @@ __global__ void __launch_bounds__(kT) k_tiles_offsets(const int* __restrict__ en
 #pragma unroll
     for (int k = 0; k < kSortItems; k++) {
         const int j = j0 + k;
-        if (j < V) {
-            ent_off[j] = run;
-            // emission blocks whose first position falls in [run, run + c)
-            for (int b = div_up(run, kEmit); b * kEmit < run + c[k] && b < n_emit_blocks; b++) first_item[b] = j;
-        }
+        if (j < V) ent_off[j] = run;
         run += c[k];
     }
     if (j0 <= V - 1 && V - 1 < j0 + kSortItems) ent_off[V] = run;   // owner of the last item: run = M
 }
 
-// K3: load-balanced emission.  Block b writes output positions [b*kEmit, (b+1)*kEmit):
-// the owning items [first_item[b], first_item[b+1]] are staged in shared memory and every
-// position finds its item by binary search there, so writes are fully coalesced whatever
-// the per-splat tile counts.
-__global__ void __launch_bounds__(kT) k_tiles_emit(const int4* __restrict__ ent_rect, const int* __restrict__ ent_off,
-                                                   const int* d_V,
-                                                   const int* d_nsort, const int* __restrict__ first_item, TileGeom g,
-                                                   uint32_t* __restrict__ out_key, int32_t* __restrict__ out_val) {
+// K3 (warp form): each warp emits the intersections of 32 consecutive depth-sorted items.
+// The items' offsets sit in the lanes' registers; every output position t of the warp's
+// range finds its item by a 5-step binary search over the lanes (shuffles), so the writes
+// are coalesced and there is no shared-memory staging or block synchronisation.
+__global__ void __launch_bounds__(kT) k_tiles_emit_warp(const int4* __restrict__ ent_rect,
+                                                        const int* __restrict__ ent_off, const int* d_V,
+                                                        const int* d_nsort, TileGeom g, uint32_t* __restrict__ out_key,
+                                                        int32_t* __restrict__ out_val) {
     pdl_trigger();
     pdl_wait();
-    __shared__ int s_off[kEmit + 1];
-    const int n = *d_nsort;
-    const int V = *d_V;
-    const int o0 = blockIdx.x * kEmit;
-    if (o0 >= n) return;
-    const int o1 = min(n, o0 + kEmit);
-    const int nblocks = div_up(n, kEmit);
-    const int e0 = first_item[blockIdx.x];
-    const int e1 = (int)blockIdx.x + 1 < nblocks ? first_item[blockIdx.x + 1] : V - 1;
-    // ne <= kEmit unless zero-count items (empty rectangles) interleave; then search globally
-    const int ne = e1 - e0 + 1;
-    const bool staged = ne <= kEmit;
-    if (staged)
-        for (int k = threadIdx.x; k <= ne; k += kT) s_off[k] = ent_off[e0 + k];
-    __syncthreads();
-    const int* offp = staged ? s_off : ent_off + e0;
-    int lo = 0;   // a thread's positions only grow, so its item index is a lower bound for the next
-    for (int o = o0 + threadIdx.x; o < o1; o += kT) {
-        // galloping search for the last item whose offset is <= o, starting from lo
-        int step = 1, hi = lo;
-        while (hi + step < ne && offp[hi + step] <= o) {
-            hi += step;
-            step <<= 1;
+    const int V = *d_V, n = *d_nsort;
+    const int lane = threadIdx.x & 31;
+    const int j0 = (blockIdx.x * kT + threadIdx.x) & ~31;   // first item of this warp
+    if (j0 >= V) return;
+    const int j = j0 + lane;
+    const int myoff = ent_off[min(j, V)];                      // ent_off[V] = M (past-the-end)
+    const int4 e = j < V ? ent_rect[j] : make_int4(0, 0, 0, 0);
+    const int first = __shfl_sync(0xffffffffu, myoff, 0);
+    const int end = ent_off[min(j0 + 32, V)];
+    const int x0 = e.x & 0xffff, w = (e.x >> 16) - x0, y0 = e.y & 0xffff;
+    const int lim = min(end, n);
+    for (int base = first; base < lim; base += 32) {   // warp-uniform trip count
+        const int t = base + lane;
+        // last lane whose offset is <= t (lanes past V hold M > t)
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, myoff, lo + step);
+            if (v <= t) lo += step;
         }
-        lo = hi;
-        hi = min(ne - 1, hi + step - 1);
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (offp[mid] <= o) lo = mid; else hi = mid - 1;
+        const int kk = t - __shfl_sync(0xffffffffu, myoff, lo);
+        const int ex0 = __shfl_sync(0xffffffffu, x0, lo), ew = __shfl_sync(0xffffffffu, w, lo);
+        const int ey0 = __shfl_sync(0xffffffffu, y0, lo);
+        const int cam = __shfl_sync(0xffffffffu, e.w, lo), id = __shfl_sync(0xffffffffu, e.z, lo);
+        if (t < lim) {
+            // kk / w exactly: kk < w h <= 2^24, so floor((kk + 0.5) / w) survives the fp32 rounding
+            const int qy = (int)__fdividef((float)kk + 0.5f, (float)ew);
+            const int ty = ey0 + qy, tx = ex0 + (kk - qy * ew);
+            out_key[t] = (uint32_t)cam * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
+            out_val[t] = id;
         }
-        const int j = e0 + lo;
-        const int kk = o - offp[lo];
-        const int4 e = ent_rect[j];   // packed rectangle, flat id, camera
-        const int x0 = e.x & 0xffff, w = (e.x >> 16) - x0, y0 = e.y & 0xffff;
-        // kk / w exactly: kk < w h <= 2^24, so floor((kk + 0.5) / w) survives the fp32 rounding
-        const int qy = (int)__fdividef((float)kk + 0.5f, (float)w);
-        const int ty = y0 + qy, tx = x0 + (kk - qy * w);
-        out_key[o] = (uint32_t)e.w * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
-        out_val[o] = e.z;
     }
 }
 
@@ -553,7 +539,7 @@ __global__ void k_keys64(const uint32_t* __restrict__ keys32, const int32_t* __r
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-    size_t off_scalars, off_blocksum, off_rowtot, off_hist, off_first, off_vk, off_vv, off_ak, off_av, off_rect,
+    size_t off_scalars, off_blocksum, off_rowtot, off_hist, off_vk, off_vv, off_ak, off_av, off_rect,
         off_cnt, off_eoff, off_ka, off_va, off_kb, off_vb, off_crec, total;
     int nb_sort_max;   // blocks of kSortTile items (radix passes, tile counts)
 };
@@ -562,13 +548,11 @@ WsLayout ws_layout(int64_t n_items, int64_t cap) {
     WsLayout L;
     const int64_t big = n_items > cap ? n_items : cap;
     L.nb_sort_max = div_up(big > 0 ? big : 1, kSortTile);
-    const int64_t nb_emit = div_up(cap > 0 ? cap : 1, kEmit) + 1;
     size_t o = 0;
     L.off_scalars = o; o = align256(o + 64);
     L.off_blocksum = o; o = align256(o + sizeof(int) * (size_t)(L.nb_sort_max + 1));
     L.off_rowtot = o; o = align256(o + sizeof(int) * 256);
     L.off_hist = o; o = align256(o + sizeof(int) * 256 * (size_t)L.nb_sort_max);
-    L.off_first = o; o = align256(o + sizeof(int) * (size_t)nb_emit);
     L.off_vk = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_vv = o; o = align256(o + 4 * (size_t)(n_items + 1));
     L.off_ak = o; o = align256(o + 4 * (size_t)(n_items + 1));
@@ -641,7 +625,6 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     int* blocksum = reinterpret_cast<int*>(w + L.off_blocksum);
     int* rowtot = reinterpret_cast<int*>(w + L.off_rowtot);
     int* hist = reinterpret_cast<int*>(w + L.off_hist);
-    int* first_item = reinterpret_cast<int*>(w + L.off_first);
     KV vis{reinterpret_cast<uint32_t*>(w + L.off_vk), reinterpret_cast<int32_t*>(w + L.off_vv)};
     KV alt{reinterpret_cast<uint32_t*>(w + L.off_ak), reinterpret_cast<int32_t*>(w + L.off_av)};
     int4* ent_rect = reinterpret_cast<int4*>(w + L.off_rect);
@@ -677,11 +660,11 @@ gs_status launch_isect(const gs_options& o, int C, int64_t N, int W, int H, cons
     launch_pdl(k_tiles_count, dim3(nb_v), dim3(kT), s, crec, dsorted.v, d_V, ent_rect, ent_cnt, blocksum);
     launch_pdl(k_scan_blocksums, dim3(1), dim3(kScanThreads), s, blocksum, kSortTile, d_V, 0, INT64_MAX, nullptr, M, overflow, cap,
                                                  d_nsort);
-    launch_pdl(k_tiles_offsets, dim3(nb_v), dim3(kT), s, ent_cnt, d_V, blocksum, ent_off, first_item, div_up(cap, kEmit));
+    launch_pdl(k_tiles_offsets, dim3(nb_v), dim3(kT), s, ent_cnt, d_V, blocksum, ent_off);
     // 4. load-balanced emission in depth order (K3)
     if (cap > 0)
-        launch_pdl(k_tiles_emit, dim3(div_up(cap, kEmit)), dim3(kT), s, ent_rect, ent_off, d_V, d_nsort, first_item, g, ia.k,
-                   ia.v);
+        launch_pdl(k_tiles_emit_warp, dim3(div_up(n_items > 0 ? n_items : 1, kT)), dim3(kT), s, ent_rect, ent_off, d_V,
+                   d_nsort, g, ia.k, ia.v);
     GS_LAUNCH_CHECK("isect/emit");
     // 5. stable sort by (camera, tile) (K4); values land in the caller's isect_ids
     const int kbits = tile_bits(nbins) > 0 ? tile_bits(nbins) : 1;
