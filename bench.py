@@ -484,8 +484,8 @@ def cpu_baseline(sc, v_img, budget_s=15.0):
         return time.perf_counter() - t0
 
     t1 = run(1)
-    t4 = run(4)
-    per_tile = max((t4 - t1) / 3.0, 1e-4)
+    t16 = run(16)
+    per_tile = max((t16 - t1) / 15.0, 1e-4)
     fixed = max(t1 - per_tile, 0.0)
     n = int(min(TT, max(4, (budget_s - fixed) / per_tile)))
     dt = run(n)
