@@ -67,22 +67,6 @@ __device__ __forceinline__ bool eval_alpha(float mx, float my, float o, float4 c
     return alpha >= alpha_min;
 }
 
-// Same decision, also returning the products dx^2, dy^2, dx dy it formed (reused by B6).
-__device__ __forceinline__ bool eval_alpha_q(float mx, float my, float o, float4 con, float fpx, float fpy,
-                                             float alpha_max, float alpha_min, float& dx, float& dy, float& xx,
-                                             float& yy, float& xy, float& G, float& alpha) {
-    dx = __fsub_rn(mx, fpx);
-    dy = __fsub_rn(my, fpy);
-    xx = __fmul_rn(dx, dx);
-    yy = __fmul_rn(dy, dy);
-    xy = __fmul_rn(dx, dy);
-    const float p = __fmaf_rn(con.y, xy, __fmaf_rn(con.x, xx, __fmul_rn(con.z, yy)));
-    if (p > 0.f) return false;
-    G = ex2_approx(p);
-    alpha = fminf(alpha_max, __fmul_rn(o, G));
-    return alpha >= alpha_min;
-}
-
 // Conservative support of a splat inside its tile.  The set a pixel can take the splat
 // from is the ellipse E: sigma(d) = 1/2 (A dx^2 + C dy^2) + B dx dy <= tau, tau =
 // ln(o / alpha_min) (alpha = min(alpha_max, o G) < alpha_min outside it, Q14), with
@@ -600,6 +584,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     // S only ever enters B4 contracted with this pixel's v_C, so the three channel
     // recurrences are carried as the single scalar Sv = S . v_C (same recurrence, dotted)
     float T = Tfin, Sv = 0.f;
+    const float amax = p.alpha_max, amin = p.alpha_min;
     for (int bend = max_last + 1; bend > start; bend -= kBatchBwd) {
         const int bstart = max(start, bend - kBatchBwd);
         const int n = bend - bstart;
@@ -611,13 +596,18 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
         const int cnt = build_warp_list(s, n, q.warp, lane, wlast - bstart);
         for (int k = cnt - 1; k >= 0; k--) {
             const int j = s.list[q.warp][k];
-            bool valid = q.inside && bstart + j <= last;
             const float4 xyo = s.xyo[j];
             const float4 con = s.con[j];
-            float dx = 0.f, dy = 0.f, xx = 0.f, yy = 0.f, xy = 0.f, G = 0.f, alpha = 0.f;
-            if (valid)
-                valid = eval_alpha_q(xyo.x, xyo.y, xyo.z, con, q.fpx, q.fpy, p.alpha_max, p.alpha_min, dx, dy, xx, yy,
-                                     xy, G, alpha);
+            // the alpha of eval_alpha (same operations, bit-identical decisions as K6), evaluated
+            // by every lane without a branch, keeping the products dx^2, dy^2, dx dy for B6: they
+            // are finite for any staged record, and a lane that does not take the splat has its
+            // G and alpha zeroed below
+            const float dx = __fsub_rn(xyo.x, q.fpx), dy = __fsub_rn(xyo.y, q.fpy);
+            const float xx = __fmul_rn(dx, dx), yy = __fmul_rn(dy, dy), xy = __fmul_rn(dx, dy);
+            const float pe = __fmaf_rn(con.y, xy, __fmaf_rn(con.x, xx, __fmul_rn(con.z, yy)));
+            float G = ex2_approx(pe);
+            float alpha = fminf(amax, __fmul_rn(xyo.z, G));
+            bool valid = q.inside && bstart + j <= last && !(pe > 0.f) && alpha >= amin;
             const unsigned vb = __ballot_sync(0xffffffffu, valid);
             K7_STAT(0, 1);
             K7_STAT(1, vb == 0);
@@ -651,7 +641,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             Sv += cv * fac;                    // B5, dotted with v_C
             const float raw = xyo.z * G;
             // B6 (Q24): no gradient through the alpha_max clamp
-            const float va = raw < p.alpha_max ? v_alpha : 0.f;
+            const float va = raw < amax ? v_alpha : 0.f;
             g8[2] = G * va;
             const float v_sigma = -raw * va;
             const float hv = 0.5f * v_sigma;
