@@ -97,17 +97,19 @@ typedef struct gs_options {
  *   k=7    a = (Sigma' + s I)_xx  (blurred variance along x, F8; bounds the alpha support)
  *   k=8..10 rgb (F14)
  *   k=11   c = (Sigma' + s I)_yy
- * Culled records (radii == 0) are all zeros.  gs_rasterize_bwd writes gradients in the
- * SAME slot layout (v_mean2d in 0,1; v_opac_eff in 2; v_conic in 4..6; v_rgb in 8..10;
- * slot 3 = d/d depth (0 unless depth rendering), slots 7 and 11 = absgrad |v_mean2d|
- * sums (NEXT-1, 0 unless requested)). */
+ * Culled records (radii == 0) are all zeros.  gs_rasterize_bwd writes the record
+ * GRADIENTS v_splats [.., GS_SPLAT_FLOATS] in their own slot order, chosen so the 8-value
+ * group of every (pixel, splat) contribution is two aligned float4 (two vector reductions):
+ *   0,1 dL/dmean2d   2 dL/dopac_eff   3,4,5 dL/dconic (A, B, C)   6,7,8 dL/drgb
+ *   9 dL/ddepth (0 unless depth rendering)   10,11 absgrad sums |dL/dmean2d| (NEXT-1, 0
+ *   unless requested). */
 #define GS_SPLAT_FLOATS 12
 
 GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 7
+#define GS_ABI_VERSION 8
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -182,10 +184,10 @@ GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N,
  * In : as gs_rasterize_fwd plus out_T, last_ids, v_out_rgb [C,H,W,3],
  *      v_out_alpha [C,H,W] or NULL.
  * Out: v_splats [C,N,GS_SPLAT_FLOATS] ([N,...] when opt->packed; zero-filled here, then accumulated; slot layout
- *      above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 7, 11.
+ *      above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 10, 11.
  * Depth (NULL v_out_depth = off): v_out_depth [C,H,W] = dL/d out_depth of the forward
  *      with the same depth_mode; depth is composited as a fourth channel, its per-splat
- *      gradient accumulates into slot 3; mode 2 (expected depth D/A) also needs the
+ *      gradient accumulates into gradient slot 9; mode 2 (expected depth D/A) also needs the
  *      forward's out_depth and adds -v E / A to the alpha gradient (quotient rule, Q26).
  * isect_masks: the forward's mask output or NULL (recomputed). */
 GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
@@ -200,7 +202,7 @@ GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, i
  * Out: v_means [N,3], v_quats [N,4], v_scales [N,3], v_opacities [N],
  *      v_colors (same shape as colors).  Summed over the C cameras inside one thread per
  *      Gaussian (deterministic; Q30); Gaussians culled in every camera get zeros.
- *      Slot 3 of v_splats (dL/d depth, depth rendering) enters through t_z (F4).
+ *      Gradient slot 9 of v_splats (dL/d depth, depth rendering) enters through t_z (F4).
  * Pose (NEXT-3; NULL v_viewmats = off): v_viewmats [C,4,4] = dL/d viewmats (App. pose
  *      optimisation): the t = W mu + w, Sigma_c = W Sigma W^T and SH
  *      view-direction (campos = -W^T w) paths; row 3 is 0.  Reduced per (block, camera)
@@ -225,7 +227,7 @@ GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int
  * those of gs_rasterize_fwd).  Dense: record id c*N+n -> feature row n, gaussian_ids NULL;
  * packed (opt->packed): feature row gaussian_ids[id].  backgrounds: [C, D] or NULL.
  * Out (fwd): out_feats [C,H,W,D], out_alpha, out_T, last_ids, isect_masks as gs_rasterize_fwd.
- * Out (bwd): v_splats (record geometry gradients: slots 0-2, 4-6; absgrad 7, 11), zero-filled
+ * Out (bwd): v_splats (record geometry gradients: slots 0-5; absgrad 10, 11), zero-filled
  *      then accumulated over the passes (B4's v_alpha is linear in v_C; the alpha-output term
  *      enters once), and v_feats [n_gauss, D] = dL/d feats, summed over cameras (zero-filled
  *      here).  For the projection backward of feature mode pass sh_degree = -1 and
@@ -336,7 +338,7 @@ GS_API gs_status gs_shard_unpack(int64_t n_recv, const float* recv, int32_t* cam
  * After gs_rasterize_bwd, per Gaussian n over the cameras c where (c,n) is visible
  * (radii > 0), ACCUMULATED IN PLACE (not zero-filled: callers sum over training steps):
  *   grad2d[n]    += || (sx g_x, sy g_y) ||, g = dL/dmu' of that view (v_splats slots 0, 1) or,
- *                   absgrad != 0, its per-pixel absolute sums (slots 7, 11, written by
+ *                   absgrad != 0, its per-pixel absolute sums (slots 10, 11, written by
  *                   gs_rasterize_bwd with absgrad = 1)
  *   count[n]     += 1
  *   max_radii[n]  = max(max_radii[n], max(rx, ry) * radius_scale)   (radius_scale >= 0)

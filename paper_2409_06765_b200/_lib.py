@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 

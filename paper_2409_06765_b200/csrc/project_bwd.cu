@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
             g_op += v_oeff * comp;
             const float v_comp = v_oeff * op;
             // ---- P2: v_Spb = -Y G_Y Y, G_Y = [[vA, vB/2],[vB/2, vC]]
-            const float gA = v1.x, gB = 0.5f * v1.y, gC = v1.z;
+            const float gA = v0.w, gB = 0.5f * v1.x, gC = v1.y;   // gradient slots 3-5 (include/gs.h)
             const float YG00 = Y00 * gA + Y01 * gB, YG01 = Y00 * gB + Y01 * gC;
             const float YG10 = Y01 * gA + Y11 * gB, YG11 = Y01 * gB + Y11 * gC;
             float vS00 = -(YG00 * Y00 + YG01 * Y01);
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
             vt0 += fx * rz * v0.x;
             vt1 += fy * rz * v0.y;
             vt2 -= fx * t[0] * rz2 * v0.x + fy * t[1] * rz2 * v0.y;
-            vt2 += v0.w;   // depth = t_z (F4), the depth-rendering gradient (slot 3)
+            vt2 += v2.y;   // depth = t_z (F4), the depth-rendering gradient (slot 9)
             if constexpr (POSE) {
                 // t = W mu + w: dL/dW += v_t mu^T, dL/dw += v_t
                 const float vt[3] = {vt0, vt1, vt2};
@@ -284,9 +284,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
                 for (int j = 0; j < 3; j++) g_S[i][j] += Wr[0][i] * T1[0][j] + Wr[1][i] * T1[1][j] + Wr[2][i] * T1[2][j];
             // ---- P7: colour
             if (DEG < 0) {
-                g_rgb[0] += v2.x;
-                g_rgb[1] += v2.y;
-                g_rgb[2] += v2.z;
+                g_rgb[0] += v1.z;   // gradient slots 6-8
+                g_rgb[1] += v1.w;
+                g_rgb[2] += v2.x;
             } else {
                 float campos[3];
 #pragma unroll
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
 #pragma unroll
                     for (int i = 0; i < NB * 3; i++) raw[i % 3] += Yb[i / 3] * __ldg(src + i);
                 }
-                const float vr[3] = {raw[0] > 0.f ? v2.x : 0.f, raw[1] > 0.f ? v2.y : 0.f, raw[2] > 0.f ? v2.z : 0.f};
+                const float vr[3] = {raw[0] > 0.f ? v1.z : 0.f, raw[1] > 0.f ? v1.w : 0.f, raw[2] > 0.f ? v2.x : 0.f};
 #pragma unroll
                 for (int i = 0; i < NB * 3; i++) s_gc[i][threadIdx.x] += Yb[i / 3] * vr[i % 3];
                 if (DEG > 0) {

@@ -495,18 +495,24 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// v_splats slot of value i of the 8-value group (v_mean2d.x, .y, v_opac, v_conic A, B, C,
-// v_r, v_g) is i + i/3 = {0, 1, 2, 4, 5, 6, 8, 9}; of the 4-value absgrad group (v_b,
-// |v_mean2d.x|, |v_mean2d.y|) it is {10, 7, 11}.
-__device__ __forceinline__ int slot8(int i) { return i + i / 3; }
-__device__ __forceinline__ int slot4(int i) { return i == 0 ? 10 : (i == 1 ? 7 : (i == 2 ? 11 : 3)); }
+// Gradient slots (include/gs.h): 0-7 = the 8-value group (v_mean2d.x, .y, v_opac, v_conic A,
+// B, C, v_r, v_g), 8 v_b, 9 v_depth, 10-11 absgrad: the 8-value group is two aligned float4
+// (two vector reductions), and the 4-value group (v_b, |v_mean2d.x|, |v_mean2d.y|, v_depth)
+// maps to slots {8, 10, 11, 9}.
+__device__ __forceinline__ int slot4(int i) { return i == 0 ? 8 : (i == 1 ? 10 : (i == 2 ? 11 : 9)); }
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
+__device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
+}
 
-constexpr int kFewLanes = 16;  // <= this many contributing lanes: per-lane vector reductions (measured optimum)
+#ifndef GS_FEW_LANES
+#define GS_FEW_LANES 16
+#endif
+constexpr int kFewLanes = GS_FEW_LANES;  // <= this many contributing lanes: per-lane vector reductions (measured optimum)
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
@@ -661,9 +667,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 const int mch = p.D - p.c0;
                 if (__popc(vb) <= kFewLanes) {
                     if (valid) {
-                        red_add_v4(dst, g8[0], g8[1], g8[2], 0.f);
-                        red_add_v4(dst + 4, g8[3], g8[4], g8[5], ab ? fabsf(g8[0]) : 0.f);
-                        if (ab) atomicAdd(dst + 11, fabsf(g8[1]));
+                        red_add_v4(dst, g8[0], g8[1], g8[2], g8[3]);
+                        red_add_v2(dst + 4, g8[4], g8[5]);
+                        if (ab) red_add_v2(dst + 10, fabsf(g8[0]), fabsf(g8[1]));
                         atomicAdd(fdst, g8[6]);
                         if (mch > 1) atomicAdd(fdst + 1, g8[7]);
                         if (mch > 2) atomicAdd(fdst + 2, g_bl);
@@ -674,7 +680,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 const float r8 = reduce_scatter8(g8, lane);
                 const int i8 = lane >> 2;
                 if ((lane & 3) == 0) {
-                    if (i8 < 6) atomicAdd(dst + slot8(i8), r8);
+                    if (i8 < 6) atomicAdd(dst + i8, r8);
                     else if (i8 - 6 < mch) atomicAdd(fdst + (i8 - 6), r8);
                 }
                 const float g4[4] = {g_bl, g_f3, ab ? fabsf(g8[0]) : 0.f, ab ? fabsf(g8[1]) : 0.f};
@@ -684,7 +690,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                     if (i4 < 2) {
                         if (2 + i4 < mch) atomicAdd(fdst + 2 + i4, r4);
                     } else if (ab) {
-                        atomicAdd(dst + (i4 == 2 ? 7 : 11), r4);
+                        atomicAdd(dst + (i4 == 2 ? 10 : 11), r4);
                     }
                 }
                 continue;
@@ -693,24 +699,26 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 // few contributing lanes: each issues its own three 16-byte reductions -- 3 warp
                 // instructions instead of the ~45 of the shuffle tree
                 if (valid) {
-                    red_add_v4(dst, g8[0], g8[1], g8[2], g_z);
-                    red_add_v4(dst + 4, g8[3], g8[4], g8[5], ABSGRAD ? fabsf(g8[0]) : 0.f);
-                    red_add_v4(dst + 8, g8[6], g8[7], g_bl, ABSGRAD ? fabsf(g8[1]) : 0.f);
+                    red_add_v4(dst, g8[0], g8[1], g8[2], g8[3]);
+                    red_add_v4(dst + 4, g8[4], g8[5], g8[6], g8[7]);
+                    if (ABSGRAD) red_add_v4(dst + 8, g_bl, g_z, fabsf(g8[0]), fabsf(g8[1]));
+                    else if (DEPTH) red_add_v2(dst + 8, g_bl, g_z);
+                    else atomicAdd(dst + 8, g_bl);
                 }
                 continue;
             }
             const float r8 = reduce_scatter8(g8, lane);
-            if ((lane & 3) == 0) atomicAdd(dst + slot8(lane >> 2), r8);
+            if ((lane & 3) == 0) atomicAdd(dst + (lane >> 2), r8);
             if (ABSGRAD) {
                 const float g4[4] = {g_bl, fabsf(g8[0]), fabsf(g8[1]), g_z};
                 const float r4 = reduce_scatter4(g4, lane);
                 if ((lane & 7) == 0 && (DEPTH || (lane >> 3) < 3)) atomicAdd(dst + slot4(lane >> 3), r4);
             } else {
                 const float rb = warp_sum(g_bl);
-                if (lane == 0) atomicAdd(dst + 10, rb);
+                if (lane == 0) atomicAdd(dst + 8, rb);
                 if (DEPTH) {
                     const float rz = warp_sum(g_z);
-                    if (lane == 0) atomicAdd(dst + 3, rz);
+                    if (lane == 0) atomicAdd(dst + 9, rz);
                 }
             }
         }

@@ -1,7 +1,7 @@
 // Densification statistics (App. ADC, Absgrad P:204-206):
 // per Gaussian, over the cameras where it is visible, the accumulated norm of the
 // view-space positional gradient (signed, or the Absgrad per-pixel absolute sums that
-// gs_rasterize_bwd writes into v_splats slots 7 and 11), the visible-view count and the
+// gs_rasterize_bwd writes into v_splats slots 10 and 11), the visible-view count and the
 // largest screen radius.  In-place accumulators across calls (training steps).
 //
 // Dense: one thread per Gaussian sums its C cameras in order (deterministic, no atomics).
@@ -12,7 +12,7 @@ namespace gsb {
 namespace {
 
 __device__ __forceinline__ float view_norm(const float* row, int absgrad, float sx, float sy) {
-    const float gx = sx * row[absgrad ? 7 : 0], gy = sy * row[absgrad ? 11 : 1];
+    const float gx = sx * row[absgrad ? 10 : 0], gy = sy * row[absgrad ? 11 : 1];
     return sqrtf(gx * gx + gy * gy);
 }
 

@@ -147,7 +147,7 @@ class _Rasterize(torch.autograd.Function):
                                absgrad, v_splats, out_depth=out_depth if depth_mode else None, v_out_depth=v_depth,
                                depth_mode=depth_mode, isect_masks=masks)
         if absgrad:
-            ag = torch.stack([v_splats[..., 7], v_splats[..., 11]], dim=-1)
+            ag = torch.stack([v_splats[..., 10], v_splats[..., 11]], dim=-1)
             if packed:
                 nnz = int(nnz_dev.item())
                 ctx.absgrad_out.zero_()

@@ -84,9 +84,10 @@ def last_gid(gpu, N):
 
 
 def v2d_from_splats(v_splats):
-    """GPU v_splats slot layout -> the oracle's 9-value layout (mean2d 2, conic 3, rgb 3, opac 1)."""
+    """GPU v_splats gradient slots (include/gs.h: mean2d 0-1, opac 2, conic 3-5, rgb 6-8) -> the
+    oracle's 9-value layout (mean2d 2, conic 3, rgb 3, opac 1)."""
     vs = v_splats
-    return np.concatenate([vs[..., 0:2], vs[..., 4:7], vs[..., 8:11], vs[..., 2:3]], axis=-1)
+    return np.concatenate([vs[..., 0:2], vs[..., 3:6], vs[..., 6:9], vs[..., 2:3]], axis=-1)
 
 
 GRAD2D_ULP = 2.0          # ... plus this multiple of the 1-ulp(mu') sensitivity s2d

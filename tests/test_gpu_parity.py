@@ -259,7 +259,7 @@ def test_absgrad():
     v, _ = S.image_grads(3, 1, 150, 200, l1_scale=False)
     gpu = U.run_gpu(sc, v_img=v, absgrad=True)
     vs = gpu["v_splats"]
-    assert np.all(vs[..., 7] >= np.abs(vs[..., 0]) * (1 - 1e-5) - 1e-7)
+    assert np.all(vs[..., 10] >= np.abs(vs[..., 0]) * (1 - 1e-5) - 1e-7)
     assert np.all(vs[..., 11] >= np.abs(vs[..., 1]) * (1 - 1e-5) - 1e-7)
 
 
@@ -423,7 +423,7 @@ def test_depth_and_pose_parity(name, mode, packed):
     bad = U.check_grad2d(U.v2d_from_splats(vs), b["v2d"], b["a2d"], vis, b["s2d"])
     assert bad.sum() == 0, bad.sum()
     # slot 3: d L / d depth of each (c, n), same tolerance model
-    badz = U.check_grad2d(vs[..., 3:4], b["vz"][..., None], b["az"][..., None], vis, b["sz"][..., None])
+    badz = U.check_grad2d(vs[..., 9:10], b["vz"][..., None], b["az"][..., None], vis, b["sz"][..., None])
     assert badz.sum() == 0, badz.sum()
     g = oracle.project_bwd(sc, p, b["v2d"], o, vz=b["vz"], pose=True)
     for k in ["v_means", "v_quats", "v_scales", "v_opacities", "v_colors"]:
@@ -654,7 +654,7 @@ def test_absgrad_parity_and_densify_stats(name, packed):
         radii_dense = U.unpack(gpu["radii"], cam, gid, C, N)
     else:
         vs, radii_dense = gpu["v_splats"], gpu["radii"]
-    ag = np.stack([vs[..., 7], vs[..., 11]], axis=-1)
+    ag = np.stack([vs[..., 10], vs[..., 11]], axis=-1)
     bad = U.check_grad2d(ag, b["absgrad"], b["a2d"][..., 0:2], vis, b["s2d"][..., 0:2])
     assert bad.sum() == 0, bad.sum()
     # statistics from the GPU's own radii / v_splats (inputs), both flavours, accumulated twice
