@@ -335,7 +335,7 @@ def run_ours(args):
                "d2h_bytes_per_step": bo, "ms_per_step": round(e_ms / K, 4),
                "pipeline": "H2D(i+1) | kernels(i) | D2H(i-1) on three streams, two buffer sets"}
 
-    launches = eng.launches_per_step() + (0 if world == 1 else 0)
+    launches = eng.launches_per_step()   # library kernels per step (31 at configs[1], = the ncu launch list)
 
     # ---- variant: the opacity-aware tile extent (bbox_mode 2, Q36: same images and
     # gradients, fewer intersections), timed the same way on the same inputs ----

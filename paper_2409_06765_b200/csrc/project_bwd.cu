@@ -14,6 +14,9 @@ namespace gsb {
 namespace {
 
 constexpr int kThreads = 128;
+#ifndef GS_PBWD_MINB
+#define GS_PBWD_MINB 5   // 96 registers: 5 CTAs/SM (measured best of 4, 5, 6)
+#endif
 
 struct PBParams {
     int64_t N;
@@ -78,7 +81,7 @@ __device__ __forceinline__ float reduce_scatter16(const float (&v)[16], int lane
 // P:713-726): per camera, every thread's contribution is reduced over the block and written
 // as one per-(block, camera) partial; k_pose_reduce sums the partials in a fixed order.
 template <int DEG, bool POSE>
-__global__ void __launch_bounds__(kThreads, 5) k_project_bwd(PBParams p) {
+__global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams p) {
     pdl_trigger();
     pdl_wait();
     const int64_t n0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
