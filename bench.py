@@ -444,7 +444,11 @@ def run_gshard(args):
         tot_ms = float(t.item())
     ms = tot_ms / args.steps
     value = C * W * H / 1e6 / (ms / 1e3)
-    launches = 3 + 2 + 2 + (1 + 12 + 3 + 1 + 6 + 1) + 1 + 2 + 2
+    bits = max(1, (eng.C_loc * eng.TX * eng.TY - 1).bit_length())
+    # project (count, scan, write) + pack (counts, rows) + unpack + isect (items, depth sort,
+    # counts/scan/offsets, emission, tile sort, ranges) + raster fwd + raster bwd (zero, walk)
+    # + project bwd (map, kernel)
+    launches = 3 + 2 + 1 + (1 + 12 + 3 + 1 + 3 * ((bits + 7) // 8) + 1) + 1 + 2 + 2
     res = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Mip-NeRF-360-shaped scene)",
