@@ -234,13 +234,15 @@ struct Stage {
     typename std::conditional<(kBatch <= 256), uint8_t, uint16_t>::type list[kWarps][kBatch];
 };
 
-template <bool FEAT, class StageT>
+// ID_IN_W: the record id replaces the (unused) depth in the staged xyo.w, so the walk gets it
+// with the position load instead of a separate shared-memory access
+template <bool FEAT, bool ID_IN_W = false, class StageT>
 __device__ __forceinline__ void stage_splat(const RasterParams& p, StageT& s, int slot, int idx, float x0, float y0,
                                             int cam) {
     const int32_t g = p.ids[idx];
     const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
     const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
-    s.xyo[slot] = r0;
+    s.xyo[slot] = ID_IN_W ? make_float4(r0.x, r0.y, r0.z, __int_as_float(g)) : r0;
     s.con[slot] = prescale_conic(r1.x, r1.y, r1.z);
     s.rgb[slot] = FEAT ? load_feat4(p, g, cam) : r2;
     s.id[slot] = g;
@@ -596,7 +598,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
         const int n = bend - bstart;
         __syncthreads();
         static_assert(kBatchBwd == kThreads, "one staged splat per thread");
-        if ((int)threadIdx.x < n) stage_splat<FEAT>(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0, cam);
+        if ((int)threadIdx.x < n) stage_splat<FEAT, !DEPTH>(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0, cam);
         __syncthreads();
         if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
         const int cnt = build_warp_list(s, n, q.warp, lane, wlast - bstart);
@@ -659,10 +661,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             const float k2 = -kLn2 * v_sigma;
             g8[0] = k2 * (2.f * con.x * dx + con.y * dy);
             g8[1] = k2 * (con.y * dx + 2.f * con.z * dy);
-            float* dst = p.v_splats + (int64_t)s.id[j] * GS_SPLAT_FLOATS;
+            const int32_t sid = DEPTH ? s.id[j] : __float_as_int(xyo.w);
+            float* dst = p.v_splats + (int64_t)sid * GS_SPLAT_FLOATS;
             if (FEAT) {
                 // geometry slots into the record gradient, the 4 channels into v_feats
-                float* fdst = p.v_feats + gauss_of(p, s.id[j], cam) * p.D + p.c0;
+                float* fdst = p.v_feats + gauss_of(p, sid, cam) * p.D + p.c0;
                 const bool ab = ABSGRAD && p.first_pass;
                 const int mch = p.D - p.c0;
                 if (__popc(vb) <= kFewLanes) {
