@@ -345,11 +345,13 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         int k = 0;
         if (!STATS) {
             // U splats per step: their alphas are evaluated up front (independent LDS / MUFU
-            // chains in flight), then composited in list order; a termination stops before the
-            // next one (Q15), so the result equals the one-at-a-time walk.  U swept on B200:
-            // 1, 2, 3, 4, 6 -> K6 0.246, 0.224, 0.222, 0.220, 0.221 ms
+            // chains in flight), then composited in list order with predicates instead of
+            // branches (a skipped splat changes nothing; a termination stops the rest, Q15), so
+            // the result equals the one-at-a-time walk.  Swept on B200: branchy composite U = 1,
+            // 2, 3, 4, 6 -> K6 0.246, 0.224, 0.222, 0.220, 0.221 ms; predicated U = 2, 4, 6, 8
+            // -> 0.200, 0.198, 0.195, 0.196 ms
 #ifndef GS_FWD_UNROLL
-#define GS_FWD_UNROLL 4
+#define GS_FWD_UNROLL 6
 #endif
             constexpr int U = GS_FWD_UNROLL;
             for (; k + U - 1 < cnt; k += U) {
@@ -365,26 +367,30 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
                     ok[u] = eval_alpha(xv[u].x, xv[u].y, xv[u].z, lds4(a_con + jj[u]), fpx, fpy, amax, amin, dxu, dyu,
                                        Gu, av[u]);
                 }
+                bool stop = false;
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    if (ok[u]) {
-                        const float nT = __fmul_rn(T, __fsub_rn(1.f, av[u]));
-                        if (nT <= tmin) {   // Q15: stop without compositing this splat
-                            done = true;
-                            break;
-                        }
-                        const float w = __fmul_rn(av[u], T);
-                        const float4 rgb = lds4(a_rgb + jj[u]);
-                        c0 = __fmaf_rn(rgb.x, w, c0);
-                        c1 = __fmaf_rn(rgb.y, w, c1);
-                        c2 = __fmaf_rn(rgb.z, w, c2);
-                        if (FEAT) c3 = __fmaf_rn(rgb.w, w, c3);
-                        if (DEPTH) dacc = __fmaf_rn(xv[u].w, w, dacc);
-                        T = nT;
-                        last = b0 + (int)(jj[u] >> 4);
-                    }
+                    // predicated composite: a skipped splat adds exactly 0 (w = 0) and leaves T
+                    const bool take = ok[u] && !stop;
+                    const float nT = __fmul_rn(T, __fsub_rn(1.f, av[u]));
+                    const bool term = take && nT <= tmin;   // Q15: stop without compositing
+                    const bool comp = take && !term;
+                    const float w = comp ? __fmul_rn(av[u], T) : 0.f;
+                    const float4 rgb = lds4(a_rgb + jj[u]);
+                    c0 = comp ? __fmaf_rn(rgb.x, w, c0) : c0;
+                    c1 = comp ? __fmaf_rn(rgb.y, w, c1) : c1;
+                    c2 = comp ? __fmaf_rn(rgb.z, w, c2) : c2;
+                    if (FEAT) c3 = comp ? __fmaf_rn(rgb.w, w, c3) : c3;
+                    if (DEPTH) dacc = comp ? __fmaf_rn(xv[u].w, w, dacc) : dacc;
+                    T = comp ? nT : T;
+                    last = comp ? b0 + (int)(jj[u] >> 4) : last;
+                    stop = stop || term;
                 }
-                if (done) break;
+                if (stop) {
+                    done = true;
+                    break;
+                }
+
             }
             if (done) continue;
         }
