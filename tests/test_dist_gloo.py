@@ -185,3 +185,24 @@ def test_view_starts_and_shards():
             rng = [G.shard_range(1001, R, r) for r in range(R)]
             assert rng[0][0] == 0 and rng[-1][1] == 1001
             assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+
+
+def test_exchange_world1_and_distributed_api_validation():
+    """Host logic without a process group: the world-size-1 exchange degenerates to copies,
+    and rasterization(distributed=True) rejects the options it does not combine with."""
+    from paper_2409_06765_b200 import gshard as G
+    ex = G.Exchange()
+    assert ex.world == 1
+    c = torch.tensor([5], dtype=torch.int64)
+    assert ex.counts(c).tolist() == [5]
+    src = torch.arange(10, dtype=torch.float32).reshape(5, 2)
+    dst = torch.zeros_like(src)
+    ex.rows(dst, src, [5], [5])
+    assert torch.equal(dst, src)
+    from paper_2409_06765_b200 import rasterization
+    z = torch.zeros
+    args = (z(4, 3), z(4, 4), z(4, 3), z(4), z(4, 3), z(1, 4, 4), z(1, 3, 3), 16, 16)
+    with pytest.raises(ValueError):
+        rasterization(*args, distributed=True, render_mode="RGB+D")
+    with pytest.raises(ValueError):
+        rasterization(*args, distributed=True, absgrad=True)
