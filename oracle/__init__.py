@@ -36,7 +36,7 @@ class OrOpts(ct.Structure):
     _fields_ = [
         ("near_plane", ct.c_double), ("far_plane", ct.c_double), ("eps2d", ct.c_double),
         ("alpha_max", ct.c_double), ("alpha_min", ct.c_double), ("t_min", ct.c_double),
-        ("amb_rel_alpha", ct.c_double), ("amb_rel_t", ct.c_double),
+        ("amb_safety", ct.c_double), ("amb_rel_floor", ct.c_double),
         ("tile_size", ct.c_int32), ("antialiased", ct.c_int32), ("sh_degree", ct.c_int32),
         ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("channels", ct.c_int32),
     ]
@@ -45,15 +45,15 @@ class OrOpts(ct.Structure):
 @dataclass
 class Options:
     """Constants of the method.  Duplicated, not shared, with the
-    CUDA path's gs_options; tests/test_constants.py cross-checks the two tables."""
+    CUDA path's gs_options; tests/test_abi.py cross-checks the two tables."""
     near_plane: float = 0.01       # S:196, Q18
     far_plane: float = 1e10
     eps2d: float = 0.3             # P:285
     alpha_max: float = 0.99        # north_star "opacity saturation at 0.99" (Q13)
     alpha_min: float = 1.0 / 255.0  # Q14
     t_min: float = 1e-4            # Q15
-    amb_rel_alpha: float = 1e-6    # ambiguity margins for parity masks (DESIGN.md Q28b):
-    amb_rel_t: float = 1e-3        #   ex2.approx ulps on alpha; fp32 T product on T
+    amb_safety: float = 1.5        # ambiguity flags (DESIGN.md Q28b): factor on the derived fp32
+    amb_rel_floor: float = 0.0     #   error bound of each decision; minimum relative margin
     tile_size: int = 16            # P:534
     antialiased: int = 0
     sh_degree: int = 3
@@ -63,7 +63,7 @@ class Options:
 
     def c(self) -> OrOpts:
         return OrOpts(self.near_plane, self.far_plane, self.eps2d, self.alpha_max, self.alpha_min,
-                      self.t_min, self.amb_rel_alpha, self.amb_rel_t, self.tile_size, self.antialiased,
+                      self.t_min, self.amb_safety, self.amb_rel_floor, self.tile_size, self.antialiased,
                       self.sh_degree, self.bbox_mode, self.fov_clamp, int(self.channels))
 
 
@@ -80,8 +80,8 @@ def lib():
         _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
         _lib.or_isect.restype = i64
         _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6 + [P] * 2
-        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 7
-        _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6 + [P] * 2
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 8
+        _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6 + [P] * 2 + [i32]
         _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_quat_to_rotmat.argtypes = [P, P]
@@ -227,7 +227,7 @@ def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
-                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz), None, _p(absg))
+                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz), None, _p(absg), None)
     return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vz=vz, az=az, sz=sz, absgrad=absg)
 
 
@@ -260,7 +260,8 @@ def render_fwd_nd(proj, feats, C, N, W, H, opts: Options, backgrounds=None, tile
 
 def render_bwd_nd(proj, feats, C, N, W, H, opts: Options, v_feat, v_alpha=None, backgrounds=None, tile_mask=None):
     """B1-B6 with D-channel features: v2d (mean2d, conic, opac_eff slots; the rgb slots 0),
-    vfeat [C,N,D] = dL/d(features of each (c,n)), and the tolerance models a2d, s2d.
+    vfeat [C,N,D] = dL/d(features of each (c,n)), and the tolerance models a2d, s2d and
+    afeat (the sum over pixels of |per-pixel feature term|; a_colors its sum over cameras).
     The per-Gaussian feature gradient is vfeat summed over cameras (features are
     camera independent)."""
     feats = _f64(feats)
@@ -271,15 +272,15 @@ def render_bwd_nd(proj, feats, C, N, W, H, opts: Options, v_feat, v_alpha=None, 
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
     va = None if v_alpha is None else _f64(v_alpha)
     v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9)); absg = np.zeros((C, N, 2))
-    vfeat = np.zeros((C, N, D))
+    vfeat = np.zeros((C, N, D)); afeat = np.zeros((C, N, D))
     amb = np.zeros((C, N), np.uint8)
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(rows), _p(bg),
                         _p(tm), _p(_f64(v_feat)), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
-                        None, None, None, None, None, _p(vfeat), _p(absg))
+                        None, None, None, None, None, _p(vfeat), _p(absg), _p(afeat))
     return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vfeat=vfeat, absgrad=absg,
-                v_colors=vfeat.sum(axis=0))
+                v_colors=vfeat.sum(axis=0), afeat=afeat, a_colors=afeat.sum(axis=0))
 
 
 def project_bwd(scene, proj, v2d, opts: Options, vz=None, pose=False):
@@ -299,7 +300,31 @@ def project_bwd(scene, proj, v2d, opts: Options, vz=None, pose=False):
     lib().or_project_bwd(ct.byref(o), N, C, W, H, _p(means), _p(quats), _p(scales), _p(opac), _p(colors), K,
                          _p(viewmats), _p(Ks), _p(proj["radii"]), _p(_f64(v2d)), _p(out["v_means"]),
                          _p(out["v_quats"]), _p(out["v_scales"]), _p(out["v_opacities"]), _p(out["v_colors"]),
-                         _p(None if vz is None else _f64(vz)), _p(out.get("v_viewmats")))
+                         _p(None if vz is None else _f64(vz)), _p(out.get("v_viewmats")), 0)
+    return out
+
+
+def project_bwd_bound(scene, proj, e2d, opts: Options, ez=None, pose=False):
+    """Tolerance model (not a result): the projection backward P1-P9 with every operand
+    replaced by its magnitude and every subtraction by an addition, applied to the
+    non-negative per-(c,n) bounds e2d [C,N,9] (and ez [C,N] for the depth slot).  Because
+    P1-P9 are linear in (v2d, vz), this is |Jacobian| e, an upper bound on the change of each
+    parameter gradient when every 2D gradient element moves by at most e; with e = |v2d| it
+    is the sum of the magnitudes of the terms of each output (its fp32 rounding floor)."""
+    means, quats, scales, opac, colors, viewmats, Ks = _scene_arrays(scene)
+    N, C = means.shape[0], viewmats.shape[0]
+    W, H = int(scene["width"]), int(scene["height"])
+    K = colors.shape[1] if colors.ndim == 3 else 1
+    o = opts.c()
+    out = dict(v_means=np.zeros((N, 3)), v_quats=np.zeros((N, 4)), v_scales=np.zeros((N, 3)),
+               v_opacities=np.zeros(N), v_colors=np.zeros(colors.shape))
+    if pose:
+        out["v_viewmats"] = np.zeros((C, 4, 4))
+    e2d = np.abs(_f64(e2d))
+    lib().or_project_bwd(ct.byref(o), N, C, W, H, _p(means), _p(quats), _p(scales), _p(opac), _p(colors), K,
+                         _p(viewmats), _p(Ks), _p(proj["radii"]), _p(e2d), _p(out["v_means"]),
+                         _p(out["v_quats"]), _p(out["v_scales"]), _p(out["v_opacities"]), _p(out["v_colors"]),
+                         _p(None if ez is None else np.abs(_f64(ez))), _p(out.get("v_viewmats")), 1)
     return out
 
 

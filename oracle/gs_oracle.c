@@ -42,8 +42,8 @@ typedef struct {
     double alpha_max;    /* 0.99 : opacity saturation (north_star; Q13)                   */
     double alpha_min;    /* 1/255: skip iff alpha < alpha_min (Q14)                       */
     double t_min;        /* 1e-4 : stop iff T*(1-alpha) <= t_min, exclusive (Q15)         */
-    double amb_rel_alpha;/* ambiguity margin (relative) around alpha_min / alpha_max      */
-    double amb_rel_t;    /* ambiguity margin (relative) around t_min                      */
+    double amb_safety;   /* factor on the derived fp32 error bounds of the decisions (Q28b) */
+    double amb_rel_floor;/* minimum relative ambiguity margin (FD scene sampling)          */
     int32_t tile_size;   /* 16                                                    */
     int32_t antialiased; /* 0 classic | 1 compensated opacity                 */
     int32_t sh_degree;   /* -1 direct RGB colors | 0..3 spherical harmonics               */
@@ -172,8 +172,8 @@ typedef struct {
     int   visible;
     int   rx, ry;
     float mx, my, depth;
-    /* decision path (Q28b): the fp32 conic and effective opacity the kernel's threshold
-     * decisions are taken from */
+    /* fp32 evaluation of F10 / F15 (the conic and o_eff): sizes the ambiguity margin of the
+     * threshold decisions (Q28b); decides nothing */
     float conic[3], opac;
 } keypath_t;
 
@@ -285,7 +285,7 @@ static keypath_t key_path_f32(const or_opts *o, int W, int H, const float *mu, c
         return kp;
     if (!isfinite(mx) || !isfinite(my)) return kp;
     kp.visible = 1; kp.rx = rx; kp.ry = ry; kp.mx = mx; kp.my = my; kp.depth = tz;
-    /* KP15 (F9, F10, F15 in fp32): conic and effective opacity for the decisions */
+    /* KP15 (F9, F10, F15 in fp32): conic and effective opacity, for the error bound of Q28b */
     kp.conic[0] = c / det;
     kp.conic[1] = -b / det;
     kp.conic[2] = a / det;
@@ -438,6 +438,21 @@ static void project64(const or_opts *o, int W, int H, const float *mu, const flo
     (void)K;
     /* F15 */
     P->opac_eff = P->o * P->comp;
+}
+
+/* Magnitudes of every forward quantity the projection backward uses (absmode of
+ * or_project_bwd; a tolerance model, not a result). */
+static void abs_proj(proj64_t *P)
+{
+    double *blocks[] = {&P->mu[0], &P->R[0][0], &P->M[0][0], &P->Sig[0][0], &P->t[0], &P->Sc[0][0],
+                        &P->J[0][0], &P->Sp[0][0], &P->Spb[0][0], &P->conic[0], &P->campos[0], &P->e[0],
+                        &P->dir[0], &P->Wr[0][0], &P->w[0], &P->qh[0], &P->s[0]};
+    int sizes[] = {3, 9, 9, 9, 3, 9, 6, 4, 4, 3, 3, 3, 3, 9, 3, 4, 3};
+    for (int b = 0; b < (int)(sizeof sizes / sizeof sizes[0]); b++)
+        for (int i = 0; i < sizes[b]; i++) blocks[b][i] = fabs(blocks[b][i]);
+    P->txc = fabs(P->txc); P->tyc = fabs(P->tyc);
+    P->fx = fabs(P->fx); P->fy = fabs(P->fy);
+    /* raw keeps its sign: it only selects the unclamped SH channels (P7); det > 0 as well */
 }
 
 /* ------------------------------------------------------------------------- */
@@ -626,21 +641,65 @@ typedef struct {
 
 /* Decision path (reading Q28b).  The three threshold decisions of R2 -- skip when
  * alpha < alpha_min (Q14), saturate at alpha_max (Q13), stop when T(1-alpha) <= t_min
- * (Q15) -- decide which splats a pixel composites, i.e. they decide an integer.  They
- * are therefore taken in the kernel's precision: the exponent -sigma*log2(e) is formed
- * in fp32 from the fp32 conic and fp32 pixel offset with the kernel's op order (conic
- * pre-scaled by -log2(e)/2, -log2(e), -log2(e)/2; p = fma(b', dx dy, fma(a', dx^2, c' dy^2))),
- * then exponentiated exactly (the kernel's ex2.approx differs by a few ulp, which the
- * ambiguity margins cover).  Values are still fp64.  Returns o_f32 * 2^p, or -1 when
- * p > 0 (sigma < 0, skipped). */
-static double decision_raw(const float *dec4, const float *m2f, int px, int py)
+ * (Q15) -- decide an integer (which splats a pixel composites).  They are taken with the
+ * paper's formulas evaluated in fp64: sigma = 1/2 (A dx^2 + C dy^2) + B dx dy,
+ * alpha = min(alpha_max, o_eff e^-sigma), T(1-alpha) -- on the projected
+ * geometry the method works with, i.e. the fp32 projection (as for the tile keys, Q28):
+ * mu' from the fp32 key path and the conic (F10) and o_eff (F15) evaluated in fp32 by
+ * key_path_f32.  (Taking the fp64 geometry instead moves sigma by |grad sigma| |mu'_f32 -
+ * mu'_f64| ~ 1e-4 for a 1-px splat at x ~ 1000 px, and 1.4 % of the pixels of configs[1]
+ * would hold a decision that the fp32 projection and the fp64 one take differently.)
+ * A pixel is flagged AMBIGUOUS when a decision lies within the error bound of evaluating
+ * the same formulas in fp32 (the kernel's precision) instead of fp64.  First-order bound,
+ * u = 2^-24, for sigma as a sum of the three terms t_A = 1/2 A dx^2, t_C = 1/2 C dy^2,
+ * t_B = B dx dy, s_abs = |t_A| + |t_C| + |t_B|:
+ *   each offset dx = fl(mu'_x - p_x) carries u, its square or product 3u, the coefficient
+ *   (the conic scaled by a constant) 1.5u, the product with it u: <= 5.5u per term;
+ *   the two sums 2u s_abs; in all E_sigma = 8u s_abs (the oracle's fp32 conic, F10, is
+ *   the one the kernel is given: tests assert it bit-exact);
+ *   r_alpha = E_sigma + 2^-22 + 2u   relative bound on alpha: ex2.approx.f32 (relative
+ *             error <= 2^-22, measured on B200 by tools/ubench.cu), the product o_eff G
+ *             and the fp32 constant;
+ *   r_T     = sum over the composited splats so far of alpha r_alpha / (1 - alpha) + 2u per
+ *             step (relative bound on T(1-alpha), a product of fp32 factors 1 - alpha);
+ *   ambiguous iff  sigma <= S E_sigma                    (the rounding guard "skip iff sigma < 0")
+ *             or   |o_eff e^-sigma - alpha_max| <= S r_alpha alpha_max
+ *             or   |alpha - alpha_min|          <= S r_alpha alpha_min
+ *             or   |T(1-alpha) - t_min|         <= S r_T t_min
+ *   with S = amb_safety (1.5 by default: second-order terms) and every relative margin at
+ *   least amb_rel_floor (0 by default; the FD scene sampler asks for 2e-3).
+ * The thresholds are the method's constants in fp64; the kernel is given their fp32
+ * roundings, a relative change <= u that the 2u terms cover.  The VALUES (colours, T,
+ * gradients) stay fp64 on the fp64 projection. */
+typedef struct {
+    double sigma, dx, dy;   /* fp64 evaluation on the fp32 projected geometry */
+    double raw;             /* o_eff e^-sigma */
+    double E_sigma;         /* error bound of an fp32 evaluation of sigma */
+    double r_alpha;         /* relative error bound of an fp32 evaluation of alpha */
+} pairdec_t;
+
+static const double OR_U = 5.9604644775390625e-08;   /* 2^-24 */
+
+static pairdec_t pair_decision(const float *dec4, const float *m2f, double px, double py)
 {
-    const float ka = -0.5f * 1.4426950408889634f, kb = -1.4426950408889634f;
-    float a = ka * dec4[0], b = kb * dec4[1], cc = ka * dec4[2];
-    float dx = m2f[0] - ((float)px + 0.5f), dy = m2f[1] - ((float)py + 0.5f);
-    float p = fmaf(b, dx * dy, fmaf(a, dx * dx, cc * (dy * dy)));
-    if (p > 0.f) return -1.0;
-    return (double)dec4[3] * exp2((double)p);
+    pairdec_t d;
+    const double A = dec4[0], B = dec4[1], Cc = dec4[2], o_eff = dec4[3];
+    d.dx = (double)m2f[0] - px;                                  /* Delta = mu' - p (Q21) */
+    d.dy = (double)m2f[1] - py;
+    d.sigma = 0.5 * (A * d.dx * d.dx + Cc * d.dy * d.dy) + B * d.dx * d.dy;
+    d.raw = o_eff * exp(-d.sigma);
+    double adx = fabs(d.dx), ady = fabs(d.dy);
+    double s_abs = 0.5 * fabs(A) * adx * adx + 0.5 * fabs(Cc) * ady * ady + fabs(B) * adx * ady;
+    d.E_sigma = 8 * OR_U * s_abs;
+    d.r_alpha = d.E_sigma + ldexp(1.0, -22) + 2 * OR_U;
+    return d;
+}
+
+static int near_thr(double v, double thr, double rel, const or_opts *o)
+{
+    double m = o->amb_safety * rel;
+    if (m < o->amb_rel_floor) m = o->amb_rel_floor;
+    return fabs(v - thr) <= m * thr;
 }
 
 static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, int64_t N, int px, int py,
@@ -654,29 +713,32 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
     const int D = n_channels(o);
     int tx = px / o->tile_size, ty = py / o->tile_size;
     double p[2] = {px + 0.5, py + 0.5};            /* R1: pixel centre */
-    const double amax = (float)o->alpha_max, amin = (float)o->alpha_min, tmin = (float)o->t_min;
-    double T = 1.0, Tdec = 1.0;
+    const double amax = o->alpha_max, amin = o->alpha_min, tmin = o->t_min;
+    double T = 1.0, rT = 0.0;
     for (int64_t i = 0; i < L->count; i++) {
         const int32_t *rc = &L->rect[4 * i];
         if (tx < rc[0] || tx >= rc[1] || ty < rc[2] || ty >= rc[3]) continue;   /* tile predicate */
         int64_t g = c * N + L->n[i];
-        /* decisions (kernel precision) */
-        double raw_d = decision_raw(&dec[4 * g], &mean2d_f[2 * g], px, py);
-        if (raw_d < 0) continue;                                              /* sigma < 0 */
-        if (fabs(raw_d - amin) <= o->amb_rel_alpha * amin) r.ambig = 1;
-        if (fabs(raw_d - amax) <= o->amb_rel_alpha * amax) r.ambig = 1;
-        int clamped = !(raw_d < amax);
-        double alpha_d = clamped ? amax : raw_d;
-        if (alpha_d < amin) continue;                                         /* Q14 */
-        double nT_d = Tdec * (1.0 - alpha_d);
-        if (fabs(nT_d - tmin) <= o->amb_rel_t * tmin) r.ambig = 1;
-        if (nT_d <= tmin) { r.end_li = i + 1; break; }                        /* Q15 */
-        /* values (fp64) */
-        double dx = mean2d[2 * g] - p[0], dy = mean2d[2 * g + 1] - p[1];     /* Delta = mu' - p (Q21) */
         const double *Y = &conic[3 * g];
-        double sigma = 0.5 * (Y[0] * dx * dx + Y[2] * dy * dy) + Y[1] * dx * dy;   /* P:543 */
+        pairdec_t pd = pair_decision(&dec[4 * g], &mean2d_f[2 * g], p[0], p[1]);
+        /* rounding guard of Q14: an fp32 sigma may come out negative near sigma = 0 */
+        if (pd.sigma <= o->amb_safety * pd.E_sigma) r.ambig = 1;
+        if (pd.sigma < 0) continue;                                           /* Q14 */
+        if (near_thr(pd.raw, amax, pd.r_alpha, o)) r.ambig = 1;
+        int clamped = !(pd.raw < amax);                                       /* Q13, Q24 */
+        double alpha = clamped ? amax : pd.raw;
+        if (!clamped && near_thr(alpha, amin, pd.r_alpha, o)) r.ambig = 1;
+        if (alpha < amin) continue;                                           /* Q14 */
+        double nT = T * (1.0 - alpha);
+        double rT_next = rT + alpha * (clamped ? 2 * OR_U : pd.r_alpha) / (1.0 - alpha) + 2 * OR_U;
+        if (near_thr(nT, tmin, rT_next, o)) r.ambig = 1;
+        if (nT <= tmin) { r.end_li = i + 1; break; }                          /* Q15 */
+        /* values (fp64 projection): Delta, sigma, G; alpha = o_eff G unless clamped */
+        double dx = mean2d[2 * g] - p[0], dy = mean2d[2 * g + 1] - p[1];
+        double sigma = 0.5 * (Y[0] * dx * dx + Y[2] * dy * dy) + Y[1] * dx * dy;
         double G = exp(-sigma);
-        double alpha = clamped ? o->alpha_max : opac_eff[g] * G;
+        alpha = clamped ? amax : opac_eff[g] * G;
+        nT = T * (1.0 - alpha);
         /* tolerance model only (not part of the result): 1 ulp of the fp32 mu' */
         double mm = fabs(mean2d[2 * g]) > fabs(mean2d[2 * g + 1]) ? fabs(mean2d[2 * g]) : fabs(mean2d[2 * g + 1]);
         double delta = ldexp(mm > 1.0 ? mm : 1.0, -23);
@@ -689,8 +751,8 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
         r.eT += alpha * qd / (1.0 - alpha);
         for (int ch = 0; ch < D; ch++) r.rgb[ch] += rgb[D * g + ch] * alpha * T;   /* P:536-538 */
         if (depth) r.dacc += depth[g] * alpha * T;                                 /* P:250 */
-        T = T * (1.0 - alpha);
-        Tdec = nT_d;
+        T = nT;
+        rT = rT_next;
         r.last_li = i;
         r.ncontrib++;
     }
@@ -768,12 +830,13 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   const double *v_img, const double *v_alpha_img, double *v2d, double *a2d, double *s2d,
                   uint8_t *g_ambig, double *T_replay_err, const double *depth, const double *v_depth_img,
-                  double *vz, double *az, double *sz, double *vfeat, double *absg)
+                  double *vz, double *az, double *sz, double *vfeat, double *absg, double *afeat)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
     const int D = n_channels(o);
     memset(v2d, 0, sizeof(double) * 9 * C * N);
     if (vfeat) memset(vfeat, 0, sizeof(double) * D * C * N);
+    if (afeat) memset(afeat, 0, sizeof(double) * D * C * N);
     if (a2d) memset(a2d, 0, sizeof(double) * 9 * C * N);
     if (s2d) memset(s2d, 0, sizeof(double) * 9 * C * N);
     if (g_ambig) memset(g_ambig, 0, (size_t)C * N);
@@ -928,6 +991,8 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
             }
             if (tvf)
                 for (int ch = 0; ch < D; ch++) vfeat[(int64_t)g * D + ch] += tvf[i * D + ch];
+            if (tvf && afeat)   /* tolerance model: sum over pixels of |fac v_C| per channel */
+                for (int ch = 0; ch < D; ch++) afeat[(int64_t)g * D + ch] += fabs(tvf[i * D + ch]);
             if (az) az[g] += terms[i].va[9];
             if (sz) sz[g] += terms[i].vs[9];
         }
@@ -950,8 +1015,15 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
                    const float *quats, const float *scales, const float *opacities, const float *colors,
                    int32_t K, const float *viewmats, const float *Ks, const int32_t *radii, const double *v2d,
                    double *v_means, double *v_quats, double *v_scales, double *v_opac, double *v_colors,
-                   const double *vz, double *v_viewmats)
+                   const double *vz, double *v_viewmats, int32_t absmode)
 {
+    /* absmode (tolerance model, not a result): the same chain with every operand replaced by
+     * its magnitude and every subtraction by an addition, i.e. |Jacobian| applied to the
+     * (non-negative) inputs v2d, vz -- the running bound sum |terms| of each output, used to
+     * propagate per-element error bounds of the 2D gradients to the parameter gradients and
+     * to size the fp32 rounding floor of the projection backward (DESIGN.md parity contract). */
+    const double sg = absmode ? 1.0 : -1.0;     /* sign of every subtracted term */
+#define AV(x) (absmode ? fabs(x) : (x))
     int64_t stride = o->sh_degree >= 0 ? (int64_t)K * 3 : 3;
     /* pose gradients (App. pose optimisation): per-thread partial sums
      * over Gaussians, summed in thread order after the loop */
@@ -972,10 +1044,12 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
         for (int64_t c = 0; c < C; c++) {
             int64_t idx = c * N + n;
             if (radii[2 * idx] <= 0 || radii[2 * idx + 1] <= 0) continue;
-            const double *vg = &v2d[9 * idx];
+            double vg[9];
+            for (int j = 0; j < 9; j++) vg[j] = AV(v2d[9 * idx + j]);
             proj64_t P;
             project64(o, W, H, means + 3 * n, quats + 4 * n, scales + 3 * n, opacities[n],
                       colors + stride * n, K, viewmats + 16 * c, Ks + 9 * c, &P);
+            if (absmode) abs_proj(&P);
             /* P1: o_eff = o * comp */
             go += vg[8] * P.comp;
             double v_comp = vg[8] * P.o;
@@ -986,13 +1060,13 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
             for (int i = 0; i < 2; i++)
                 for (int j = 0; j < 2; j++) YG[i][j] = Y[i][0] * GY[0][j] + Y[i][1] * GY[1][j];
             for (int i = 0; i < 2; i++)
-                for (int j = 0; j < 2; j++) vSp[i][j] = -(YG[i][0] * Y[0][j] + YG[i][1] * Y[1][j]);
+                for (int j = 0; j < 2; j++) vSp[i][j] = sg * (YG[i][0] * Y[0][j] + YG[i][1] * Y[1][j]);
             /* P3 (AA only): d comp / d Sigma' = comp/2 (Sigma'^-1 - Spb^-1) (derived from P:281) */
             if (o->antialiased && P.det > 0) {
-                double Si[2][2] = {{P.Sp[1][1] / P.det, -P.Sp[0][1] / P.det},
-                                   {-P.Sp[1][0] / P.det, P.Sp[0][0] / P.det}};
+                double Si[2][2] = {{P.Sp[1][1] / P.det, sg * P.Sp[0][1] / P.det},
+                                   {sg * P.Sp[1][0] / P.det, P.Sp[0][0] / P.det}};
                 for (int i = 0; i < 2; i++)
-                    for (int j = 0; j < 2; j++) vSp[i][j] += v_comp * 0.5 * P.comp * (Si[i][j] - Y[i][j]);
+                    for (int j = 0; j < 2; j++) vSp[i][j] += v_comp * 0.5 * P.comp * (Si[i][j] + sg * Y[i][j]);
             }
             /* P4: v_Sc = J^T vSp J; v_J = vSp J Sc^T + vSp^T J Sc (Q11) */
             double vSc[3][3], vJ[2][3];
@@ -1016,23 +1090,23 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
             double tx = P.t[0], ty = P.t[1], tz = P.t[2];
             double fx = P.fx, fy = P.fy, tz2 = tz * tz, tz3 = tz2 * tz;
             double vt[3] = {0, 0, 0};
-            vt[2] += -fx / tz2 * vJ[0][0] - fy / tz2 * vJ[1][1];
+            vt[2] += sg * fx / tz2 * vJ[0][0] + sg * fy / tz2 * vJ[1][1];
             if (!P.clamp_x) {
-                vt[0] += -fx / tz2 * vJ[0][2];
+                vt[0] += sg * fx / tz2 * vJ[0][2];
                 vt[2] += 2.0 * fx * tx / tz3 * vJ[0][2];
             } else {
                 vt[2] += fx * P.txc / tz3 * vJ[0][2];
             }
             if (!P.clamp_y) {
-                vt[1] += -fy / tz2 * vJ[1][2];
+                vt[1] += sg * fy / tz2 * vJ[1][2];
                 vt[2] += 2.0 * fy * ty / tz3 * vJ[1][2];
             } else {
                 vt[2] += fy * P.tyc / tz3 * vJ[1][2];
             }
             vt[0] += fx / tz * vg[0];
             vt[1] += fy / tz * vg[1];
-            vt[2] += -(fx * tx / tz2) * vg[0] - (fy * ty / tz2) * vg[1];
-            if (vz) vt[2] += vz[idx];                  /* depth = t_z (F4; depth rendering P:250) */
+            vt[2] += sg * (fx * tx / tz2) * vg[0] + sg * (fy * ty / tz2) * vg[1];
+            if (vz) vt[2] += AV(vz[idx]);                  /* depth = t_z (F4; depth rendering P:250) */
             double *vW = vpart ? vpart + ((size_t)tid * C + c) * 16 : NULL;
             if (vW) {
                 /* t = W mu + w: dL/dW += v_t mu^T, dL/dw += v_t */
@@ -1073,15 +1147,15 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
                 for (int j = 0; j < nb; j++) {
                     double shv = 0;
                     for (int ch = 0; ch < 3; ch++) {
-                        gc[3 * j + ch] += Yb[j] * vraw[ch];
-                        shv += (double)colors[stride * n + 3 * j + ch] * vraw[ch];
+                        gc[3 * j + ch] += AV(Yb[j]) * vraw[ch];
+                        shv += AV((double)colors[stride * n + 3 * j + ch]) * vraw[ch];
                     }
-                    for (int d = 0; d < 3; d++) vdir[d] += dY[j][d] * shv;
+                    for (int d = 0; d < 3; d++) vdir[d] += AV(dY[j][d]) * shv;
                 }
                 /* dir = e/|e|, d dir/d mu = (I - dir dir^T)/|e| */
                 double dd = P.dir[0] * vdir[0] + P.dir[1] * vdir[1] + P.dir[2] * vdir[2];
                 double ve[3];
-                for (int i = 0; i < 3; i++) ve[i] = (vdir[i] - P.dir[i] * dd) / P.enorm;
+                for (int i = 0; i < 3; i++) ve[i] = (vdir[i] + sg * P.dir[i] * dd) / P.enorm;
                 for (int i = 0; i < 3; i++) gm[i] += ve[i];
                 /* e = mu - campos, campos = -W^T w: dL/dW_ki += ve_i w_k, dL/dw_k += (W ve)_k */
                 double *vW = vpart ? vpart + ((size_t)tid * C + c) * 16 : NULL;
@@ -1112,10 +1186,10 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
                 for (int j = 0; j < 3; j++) vR[i][j] = vM[i][j] * P.s[j];
             /* P9: dR/d(w,x,y,z) at q_hat, then the normalisation */
             double w = P.qh[0], x = P.qh[1], y = P.qh[2], z = P.qh[3];
-            double dRw[3][3] = {{0, -z, y}, {z, 0, -x}, {-y, x, 0}};
-            double dRx[3][3] = {{0, y, z}, {y, -2 * x, -w}, {z, w, -2 * x}};
-            double dRy[3][3] = {{-2 * y, x, w}, {x, 0, z}, {-w, z, -2 * y}};
-            double dRz[3][3] = {{-2 * z, -w, x}, {w, -2 * z, y}, {x, y, 0}};
+            double dRw[3][3] = {{0, sg * z, y}, {z, 0, sg * x}, {sg * y, x, 0}};
+            double dRx[3][3] = {{0, y, z}, {y, sg * 2 * x, sg * w}, {z, w, sg * 2 * x}};
+            double dRy[3][3] = {{sg * 2 * y, x, w}, {x, 0, z}, {sg * w, z, sg * 2 * y}};
+            double dRz[3][3] = {{sg * 2 * z, sg * w, x}, {w, sg * 2 * z, y}, {x, y, 0}};
             double vqh[4] = {0, 0, 0, 0};
             for (int i = 0; i < 3; i++)
                 for (int j = 0; j < 3; j++) {
@@ -1125,7 +1199,7 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
                     vqh[3] += 2.0 * dRz[i][j] * vR[i][j];
                 }
             double dot = vqh[0] * P.qh[0] + vqh[1] * P.qh[1] + vqh[2] * P.qh[2] + vqh[3] * P.qh[3];
-            for (int i = 0; i < 4; i++) gq[i] += (vqh[i] - dot * P.qh[i]) / P.qn;
+            for (int i = 0; i < 4; i++) gq[i] += (vqh[i] + sg * dot * P.qh[i]) / P.qn;
         }
         for (int i = 0; i < 3; i++) v_means[3 * n + i] = gm[i], v_scales[3 * n + i] = gs[i];
         for (int i = 0; i < 4; i++) v_quats[4 * n + i] = gq[i];
@@ -1137,6 +1211,7 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
             for (int64_t k = 0; k < 16 * (int64_t)C; k++) v_viewmats[k] += vpart[(size_t)t * C * 16 + k];
         free(vpart);
     }
+#undef AV
     return 0;
 }
 

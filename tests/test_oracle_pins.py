@@ -190,6 +190,90 @@ class TestProjection:
         assert not np.allclose(a["conic"], b["conic"])
 
 
+    def test_fov_clamp_sigma_equals_fd_jacobian_at_clamped_point(self, oracle_lib):
+        """Q27: for a splat deep inside the clamp, Sigma' is the sandwich
+        with the pinhole Jacobian evaluated at the CLAMPED camera point
+        t_c = (t_z u_c, t_z v_c, t_z), u_c = the widened-frustum limit; FD Jacobian of the
+        pinhole map there, 3D covariance from scipy's rotation."""
+        rng = np.random.default_rng(3)
+        f, W, H = 40.0, 64, 48
+        cx, cy = 30.0, 26.0
+        lim_xp = (W - cx) / f + 0.3 * (W / 2) / f
+        lim_xn = cx / f + 0.3 * (W / 2) / f
+        lim_yp = (H - cy) / f + 0.3 * (H / 2) / f
+        lim_yn = cy / f + 0.3 * (H / 2) / f
+        n_checked = 0
+        for k in range(12):
+            z = rng.uniform(1.0, 3.0)
+            u = rng.choice([-1, 1]) * rng.uniform(1.1, 1.6)          # far outside [-0.99, 1.2]
+            v = rng.uniform(-0.3, 0.3) if k % 2 else rng.choice([-1, 1]) * rng.uniform(1.1, 1.5)
+            q = rng.normal(size=4)
+            s = rng.uniform(0.4, 1.2, 3)
+            sc = _one_gaussian([u * z, v * z, z], q, s, 0.5, [1, 1, 1],
+                               K=[[f, 0, cx], [0, f, cy], [0, 0, 1]], W=W, H=H)
+            p = oracle.project(sc, oracle.Options(sh_degree=-1, fov_clamp=1))
+            if p["radii"][0, 0, 0] == 0:
+                continue
+            m32 = sc["means"][0].astype(np.float64)
+            uc = min(lim_xp, max(-lim_xn, m32[0] / m32[2]))
+            vc = min(lim_yp, max(-lim_yn, m32[1] / m32[2]))
+            assert uc != m32[0] / m32[2]                        # the clamp is active
+            tc = np.array([m32[2] * uc, m32[2] * vc, m32[2]])
+            J = _fd_jacobian(tc, f, f, cx, cy)
+            Sig = _cov3d_ref(sc["quats"][0].astype(np.float64), sc["scales"][0].astype(np.float64))
+            want = J @ Sig @ J.T + 0.3 * np.eye(2)
+            Y = p["conic"][0, 0]
+            got = np.linalg.inv(np.array([[Y[0], Y[1]], [Y[1], Y[2]]]))
+            assert np.allclose(got, want, rtol=1e-6, atol=1e-6), (got, want)
+            # mu' is never clamped (Q27)
+            assert np.allclose(p["mean2d"][0, 0], _pinhole(m32, f, f, cx, cy), rtol=1e-12)
+            n_checked += 1
+        assert n_checked >= 6
+
+    def test_bbox_mode1_square_lambda_max(self, oracle_lib):
+        """Q12 option bbox_mode 1: r_x = r_y = ceil(3 sqrt(lambda_max)) of
+        Sigma'+sI.  Closed form on a rotated anisotropic splat on the optical axis: Sigma' =
+        (f/z)^2 R2 diag(sx^2, sy^2) R2^T, so lambda_max = (f/z)^2 max(sx, sy)^2 + 0.3 for every
+        rotation angle about the view axis, while the per-axis box (mode 0) changes with it."""
+        f, z = 100.0, 4.0
+        sx, sy, sz = 0.3, 0.1, 0.05
+        seen0 = set()
+        for th in [0.0, 0.35, 0.6, 1.1, 2.0]:
+            q = [math.cos(th / 2), 0, 0, math.sin(th / 2)]
+            sc = _one_gaussian([0, 0, z], q, [sx, sy, sz], 0.5, [1, 1, 1],
+                               K=[[f, 0, 50], [0, f, 50], [0, 0, 1]], W=100, H=100)
+            p1 = oracle.project(sc, oracle.Options(sh_degree=-1, bbox_mode=1))
+            s32 = float(np.float32(sx))
+            lam = (f / z) ** 2 * s32 ** 2 + 0.3
+            assert p1["radii"][0, 0].tolist() == [math.ceil(3 * math.sqrt(lam))] * 2 == [23, 23]
+            p0 = oracle.project(sc, oracle.Options(sh_degree=-1, bbox_mode=0))
+            c, s_ = math.cos(th), math.sin(th)
+            sxx = (f / z) ** 2 * (c * c * s32 ** 2 + s_ * s_ * float(np.float32(sy)) ** 2) + 0.3
+            syy = (f / z) ** 2 * (s_ * s_ * s32 ** 2 + c * c * float(np.float32(sy)) ** 2) + 0.3
+            assert p0["radii"][0, 0].tolist() == [math.ceil(3 * math.sqrt(sxx)), math.ceil(3 * math.sqrt(syy))]
+            seen0.add(tuple(p0["radii"][0, 0].tolist()))
+        assert len(seen0) >= 3
+
+    def test_bbox_mode1_equals_eigvalsh(self, oracle_lib):
+        """bbox_mode 1 on random poses: r = ceil(3 sqrt(max eigenvalue)) of the fp64 Sigma'+sI
+        (numpy eigvalsh), skipping the few whose 3 sqrt(lambda) lies within 1e-4 of an integer
+        (the radii are an fp32 key-path decision, Q28)."""
+        sc = S.tiny_scene(21, N=300, width=96, height=80, sh_degree=-1)
+        p = oracle.project(sc, oracle.Options(sh_degree=-1, bbox_mode=1))
+        vis = p["radii"][0, :, 0] > 0
+        assert vis.sum() > 200
+        checked = 0
+        for n in np.nonzero(vis)[0]:
+            Y = p["conic"][0, n]
+            cov = np.linalg.inv(np.array([[Y[0], Y[1]], [Y[1], Y[2]]]))
+            r = 3 * math.sqrt(np.linalg.eigvalsh(cov).max())
+            if abs(r - round(r)) < 1e-4:
+                continue
+            assert p["radii"][0, n].tolist() == [math.ceil(r)] * 2
+            checked += 1
+        assert checked > 200
+
+
 # --------------------------------------------------------------------------- SH
 class TestSH:
     def test_orthonormal_quadrature(self, oracle_lib):
@@ -403,7 +487,7 @@ class TestComposite:
 def _clean_scene(seed, N=24, W=32, H=32, sh_degree=1, views=1, antialiased=0, max_tries=400):
     """Rejection-sample a small scene with no pixel within 1e-3 (relative) of the alpha_min,
     alpha_max or T_min decisions (SURVEY 8c FD protocol)."""
-    o = oracle.Options(sh_degree=sh_degree, antialiased=antialiased, amb_rel_alpha=2e-3, amb_rel_t=2e-3)
+    o = oracle.Options(sh_degree=sh_degree, antialiased=antialiased, amb_rel_floor=2e-3)
     for k in range(max_tries):
         sc = S.tiny_scene(seed * 1000 + k, N=N, width=W, height=H, sh_degree=sh_degree, views=views)
         sc["scales"] *= 1.5
@@ -530,6 +614,88 @@ class TestBackward:
                     assert abs(an - fd) <= 2e-4 * abs(fd) + 1e-6, (name, n, j, an, fd)
                     checked += 1
         assert checked > 80, checked
+
+    @pytest.mark.parametrize("seed,sh", [(0, 0), (1, 2)])
+    def test_clamped_J_gradient_matches_fd(self, oracle_lib, seed, sh):
+        """Q27 gradient branch (the clamped coordinate gets no gradient
+        through J, and t_z enters J through t_c = t_z u_c): splats deep inside the clamp
+        (|t_x/t_z| 1.1-1.5 against a 0.65 limit) whose 3-sigma boxes still reach the image;
+        every parameter gradient of those splats = central FD over the fp32 inputs."""
+        o = oracle.Options(sh_degree=sh, amb_rel_floor=2e-3)
+        W = H = 32
+        found = None
+        for k in range(300):
+            sc = S.tiny_scene(seed * 1000 + 500 + k, N=20, width=W, height=H, sh_degree=sh)
+            rng = np.random.default_rng(seed * 1000 + k)
+            m = 4
+            z = rng.uniform(1.2, 2.0, m)
+            u = rng.choice([-1, 1], m) * rng.uniform(1.1, 1.5, m)
+            v = rng.uniform(-0.3, 0.3, m)
+            sc["means"][:m] = np.stack([u * z, v * z, z], 1)
+            sc["scales"][:m] = rng.uniform(0.35, 0.6, (m, 3))
+            sc["opacities"][:m] = rng.uniform(0.3, 0.8, m)
+            p = oracle.project(sc, o)
+            r = oracle.render_fwd(p, 1, 20, W, H, o)
+            vis = p["radii"][0, :m, 0] > 0
+            if vis.sum() >= 2 and not r["ambig"].any():
+                found = (sc, np.nonzero(vis)[0])
+                break
+        assert found is not None
+        sc, clamped = found
+        N = sc["means"].shape[0]
+        rng = np.random.default_rng(seed)
+        v_img = rng.normal(size=(1, H, W, 3)); v_a = rng.normal(size=(1, H, W))
+        p = oracle.project(sc, o)
+        _, ids0, offs0 = oracle.isect(p, 1, N, W, H, o)
+        b = oracle.render_bwd(p, 1, N, W, H, o, v_img, v_a)
+        g = oracle.project_bwd(sc, p, b["v2d"], o)
+        grads = {"means": g["v_means"], "quats": g["v_quats"], "scales": g["v_scales"],
+                 "opacities": g["v_opacities"]}
+        checked = 0
+        for name, G in grads.items():
+            flatG = G.reshape(N, -1)
+            for n in clamped:
+                for j in range(flatG.shape[1]):
+                    x0 = sc[name].reshape(N, -1)[n, j]
+                    h = np.float32(1e-5 * max(1.0, abs(float(x0))))
+                    vals, steps = [], []
+                    for sgn in (+1, -1):
+                        sc2 = {kk: (vv.copy() if isinstance(vv, np.ndarray) else vv) for kk, vv in sc.items()}
+                        arr = sc2[name].reshape(N, -1)
+                        arr[n, j] = np.float32(x0 + sgn * h)
+                        steps.append(float(arr[n, j]) - float(x0))
+                        l, (ids1, offs1) = _loss(sc2, o, v_img, v_a)
+                        if not (np.array_equal(ids1, ids0) and np.array_equal(offs1, offs0)):
+                            vals = None
+                            break
+                        vals.append(l)
+                    if vals is None:
+                        continue
+                    fd = (vals[0] - vals[1]) / (steps[0] - steps[1])
+                    an = flatG[n, j]
+                    assert abs(an - fd) <= 2e-4 * abs(fd) + 1e-6, (name, n, j, an, fd)
+                    checked += 1
+        assert checked >= 16, checked
+
+    def test_projection_backward_bound_dominates(self, oracle_lib):
+        """The absmode tolerance model is |Jacobian| e: for any perturbation d of the 2D
+        gradients, |project_bwd(v + d) - project_bwd(v)| <= project_bwd_bound(|d|), and
+        |project_bwd(v)| <= project_bwd_bound(|v|) (triangle inequality, linearity)."""
+        for sh, aa in [(0, 0), (3, 1)]:
+            sc = S.tiny_scene(31 + sh, N=80, width=48, height=40, sh_degree=sh, views=2)
+            o = oracle.Options(sh_degree=sh, antialiased=aa)
+            p = oracle.project(sc, o)
+            rng = np.random.default_rng(sh)
+            v = rng.normal(size=(2, 80, 9)); d = rng.normal(size=(2, 80, 9)) * 1e-3
+            vz = rng.normal(size=(2, 80)); dz = rng.normal(size=(2, 80)) * 1e-3
+            g0 = oracle.project_bwd(sc, p, v, o, vz=vz, pose=True)
+            g1 = oracle.project_bwd(sc, p, v + d, o, vz=vz + dz, pose=True)
+            bd = oracle.project_bwd_bound(sc, p, d, o, ez=dz, pose=True)
+            bv = oracle.project_bwd_bound(sc, p, v, o, ez=vz, pose=True)
+            for k in g0:
+                assert np.all(np.abs(g1[k] - g0[k]) <= bd[k] * (1 + 1e-9) + 1e-300), k
+                assert np.all(np.abs(g0[k]) <= bv[k] * (1 + 1e-9) + 1e-300), k
+                assert bv[k].max() > 0
 
     def test_dp_linearity(self, oracle_lib):
         """Q30 / 8(e): gradients of two views = sum of per-view gradients (sharding invariant)."""
