@@ -130,7 +130,9 @@ GS_API gs_status gs_project(const gs_options* opt, int64_t N, int32_t C, int32_t
  * Each visible (c,n) is binned into every 16x16 tile its 3-sigma rectangle touches
  * (Q20).  The result is ordered by (camera, tile, depth, c*N+n) ascending (Q16).
  * In : radii, splats from gs_project (reads mean2d and depth).
- * Out: *M (device int64)        total number of intersections (may exceed M_capacity)
+ * Out: *M (device int64)        total number of intersections (may exceed M_capacity;
+ *                               summed in int64, so a call whose M passes 2^31 - 1 still
+ *                               reports it and sets *overflow: M_capacity < 2^31 - 1)
  *      *overflow (device int32) 1 iff *M > M_capacity (then the outputs are truncated
  *                               and must be recomputed with a larger capacity)
  *      isect_ids [M_capacity]   flat id c*N+n of each intersection, in sorted order
@@ -232,7 +234,9 @@ GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int
  *      enters once), and v_feats [n_gauss, D] = dL/d feats, summed over cameras (zero-filled
  *      here).  For the projection backward of feature mode pass sh_degree = -1 and
  *      v_colors = NULL to gs_project_bwd (its colour gradient is v_feats).
- * Depth rendering is not combined with feature mode (render depth as a feature channel). */
+ * Depth rendering is not combined with feature mode (render depth as a feature channel).
+ * absgrad != 0 requires D <= 4 (else GS_ERR_UNSUPPORTED): slots 10, 11 hold per-pixel sums of
+ * |dL/dmean2d| over ALL channels, which one 4-channel pass sees only when D <= 4. */
 GS_API gs_status gs_rasterize_fwd_nd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                                      const float* splats, const float* feats, int32_t D,
                                      const int32_t* gaussian_ids, const float* backgrounds,

@@ -715,6 +715,7 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
     double p[2] = {px + 0.5, py + 0.5};            /* R1: pixel centre */
     const double amax = o->alpha_max, amin = o->alpha_min, tmin = o->t_min;
     double T = 1.0, rT = 0.0;
+    double Tdec = 1.0;   /* transmittance of the decision path: product of the decision alphas */
     for (int64_t i = 0; i < L->count; i++) {
         const int32_t *rc = &L->rect[4 * i];
         if (tx < rc[0] || tx >= rc[1] || ty < rc[2] || ty >= rc[3]) continue;   /* tile predicate */
@@ -729,10 +730,11 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
         double alpha = clamped ? amax : pd.raw;
         if (!clamped && near_thr(alpha, amin, pd.r_alpha, o)) r.ambig = 1;
         if (alpha < amin) continue;                                           /* Q14 */
-        double nT = T * (1.0 - alpha);
+        double nT = Tdec * (1.0 - alpha);
         double rT_next = rT + alpha * (clamped ? 2 * OR_U : pd.r_alpha) / (1.0 - alpha) + 2 * OR_U;
         if (near_thr(nT, tmin, rT_next, o)) r.ambig = 1;
         if (nT <= tmin) { r.end_li = i + 1; break; }                          /* Q15 */
+        Tdec = nT;
         /* values (fp64 projection): Delta, sigma, G; alpha = o_eff G unless clamped */
         double dx = mean2d[2 * g] - p[0], dy = mean2d[2 * g + 1] - p[1];
         double sigma = 0.5 * (Y[0] * dx * dx + Y[2] * dy * dy) + Y[1] * dx * dy;

@@ -16,6 +16,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
 ABI_VERSION = 8
+# largest item / record count of one call: ids and capacities are int32 (include/gs.h)
+MAX_ITEMS = (1 << 31) - 2048
 
 GS_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "capacity exceeded", 4: "cuda error"}
 

@@ -39,6 +39,16 @@ gs_status check_dims(int64_t N, int32_t C, int32_t W, int32_t H) {
     return GS_OK;
 }
 
+// Raster calls: in packed mode N is the total record count and record ids are packed indices
+// < N, so only N itself (not C*N) must fit the int32 ids (Q29)
+gs_status check_raster_dims(const gs_options* o, int64_t N, int32_t C, int32_t W, int32_t H) {
+    if (o->packed) {
+        gs_status s = check_dims(N, 1, W, H);
+        return s != GS_OK ? s : check_dims(0, C, W, H);
+    }
+    return check_dims(N, C, W, H);
+}
+
 }  // namespace
 
 #define GS_TRY(x)                     \
@@ -132,7 +142,7 @@ gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
                            int32_t* last_ids, float* out_depth, int32_t depth_mode, uint16_t* isect_masks,
                            void* stream) {
     GS_TRY(check_opts(opt));
-    GS_TRY(check_dims(N, C, width, height));
+    GS_TRY(check_raster_dims(opt, N, C, width, height));
     GS_REQ(tile_offsets && out_rgb && out_alpha && out_T && last_ids);
     GS_REQ(!out_depth || depth_mode == 1 || depth_mode == 2);
     GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(backgrounds) && aligned4(out_rgb) &&
@@ -146,7 +156,7 @@ gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N, int32_
                              const float* splats, const int32_t* isect_ids, const int32_t* tile_offsets,
                              int32_t* n_eval, int32_t* n_contrib, void* stream) {
     GS_TRY(check_opts(opt));
-    GS_TRY(check_dims(N, C, width, height));
+    GS_TRY(check_raster_dims(opt, N, C, width, height));
     GS_REQ(tile_offsets && n_eval && n_contrib);
     GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(n_eval) && aligned4(n_contrib));
     return gsb::launch_raster_stats(*opt, C, N, width, height, splats, isect_ids, tile_offsets, n_eval, n_contrib,
@@ -160,7 +170,7 @@ gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
                            const float* v_out_depth, int32_t depth_mode, int32_t absgrad,
                            const uint16_t* isect_masks, float* v_splats, void* stream) {
     GS_TRY(check_opts(opt));
-    GS_TRY(check_dims(N, C, width, height));
+    GS_TRY(check_raster_dims(opt, N, C, width, height));
     GS_REQ(tile_offsets && out_T && last_ids && v_out_rgb && (v_splats || N == 0));
     GS_REQ(!v_out_depth || depth_mode == 1 || (depth_mode == 2 && out_depth));
     GS_REQ(aligned16(splats) && aligned16(v_splats) && aligned4(isect_ids) && aligned4(backgrounds) &&
@@ -209,7 +219,7 @@ gs_status gs_rasterize_fwd_nd(const gs_options* opt, int32_t C, int64_t N, int32
                               float* out_feats, float* out_alpha, float* out_T, int32_t* last_ids,
                               uint16_t* isect_masks, void* stream) {
     GS_TRY(check_opts(opt));
-    GS_TRY(check_dims(N, C, width, height));
+    GS_TRY(check_raster_dims(opt, N, C, width, height));
     GS_REQ(D >= 1 && feats && tile_offsets && out_feats && out_alpha && out_T && last_ids);
     GS_REQ(!opt->packed || gaussian_ids);
     GS_REQ(aligned16(splats) && aligned4(feats) && aligned4(gaussian_ids) && aligned4(isect_ids) &&
@@ -228,8 +238,9 @@ gs_status gs_rasterize_bwd_nd(const gs_options* opt, int32_t C, int64_t N, int32
                               const float* v_out_feats, const float* v_out_alpha, int32_t absgrad,
                               const uint16_t* isect_masks, float* v_splats, float* v_feats, void* stream) {
     GS_TRY(check_opts(opt));
-    GS_TRY(check_dims(N, C, width, height));
+    GS_TRY(check_raster_dims(opt, N, C, width, height));
     GS_REQ(D >= 1 && n_gauss >= 0 && feats && tile_offsets && out_T && last_ids && v_out_feats);
+    if (absgrad && D > 4) return GS_ERR_UNSUPPORTED;   // |v_mean2d| per pixel needs every channel in one pass
     GS_REQ((v_splats || N == 0) && (v_feats || n_gauss == 0));
     GS_REQ(!opt->packed || gaussian_ids);
     GS_REQ(opt->packed || n_gauss == N);
@@ -257,7 +268,7 @@ gs_status gs_project_packed(const gs_options* opt, int64_t N, int32_t C, int32_t
                             size_t workspace_bytes, void* stream) {
     GS_TRY(check_opts(opt));
     GS_REQ(opt->packed == 1);
-    GS_TRY(check_dims(N, C, width, height));
+    GS_TRY(check_raster_dims(opt, N, C, width, height));   // packed: item ids < 2^31, not C*N
     GS_REQ(nnz_capacity >= 0 && nnz_capacity < ((int64_t)1 << 31) - 1);
     GS_REQ(nnz && overflow && workspace && aligned8(nnz) && aligned4(overflow));
     GS_REQ((reinterpret_cast<uintptr_t>(workspace) & 255u) == 0);
@@ -316,7 +327,7 @@ gs_status gs_project_bwd_packed(const gs_options* opt, int64_t N, int32_t C, int
                                 float* v_viewmats, void* workspace, size_t workspace_bytes, void* stream) {
     GS_TRY(check_opts(opt));
     GS_REQ(opt->packed == 1);
-    GS_TRY(check_dims(N, C, width, height));
+    GS_TRY(check_raster_dims(opt, N, C, width, height));   // packed: item ids < 2^31, not C*N
     GS_REQ(aligned4(v_viewmats));
     if (N == 0)
         return gsb::launch_project_bwd_packed(*opt, 0, C, width, height, nullptr, nullptr, nullptr, nullptr, nullptr, 1,

@@ -92,20 +92,24 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, int 
     __shared__ int s_warp[33];
     const int n = (int)min(d_n ? (int64_t)*d_n : n_host, cap);
     const int nb = div_up(n, tile);
-    int carry = 0;
+    // the total (M can exceed 2^31 when a call overflows its capacity) is summed in int64; the
+    // int32 block offsets saturate just past the capacity, so every position they lead to is
+    // >= the clamped count and nothing is emitted there (the overflow flag reports it)
+    const int64_t sat = min(ovf_cap, (int64_t)INT32_MAX - 1) + 1;
+    int64_t carry = 0;
     for (int r = 0; r < nb; r += kScanThreads) {
         const int i = r + threadIdx.x;
         const int v = i < nb ? data[i] : 0;
         int tot;
         const int ex = block_exclusive_scan(v, s_warp, &tot);
-        if (i < nb) data[i] = carry + ex;
+        if (i < nb) data[i] = (int)min(carry + ex, sat);
         carry += tot;
     }
     if (threadIdx.x == 0) {
-        if (total_i32) *total_i32 = carry;
+        if (total_i32) *total_i32 = (int)min(carry, (int64_t)INT32_MAX);
         if (total_i64) *total_i64 = carry;
-        if (overflow) *overflow = (int64_t)carry > ovf_cap ? 1 : 0;
-        if (clamped_n) *clamped_n = (int)min((int64_t)carry, ovf_cap);
+        if (overflow) *overflow = carry > ovf_cap ? 1 : 0;
+        if (clamped_n) *clamped_n = (int)min(carry, ovf_cap);
     }
 }
 

@@ -23,7 +23,7 @@ struct PBParams {
     int C, W, H, K;
     float eps2d;
     int antialiased, fov_clamp;
-    int vec_colors;   // v_colors base 16B-aligned and K*3 % 4 == 0
+    int vec_colors;   // colors and v_colors bases 16B-aligned and K*3 % 4 == 0
     const float* means;
     const float* quats;
     const float* scales;
@@ -467,7 +467,9 @@ PBParams make_pb_params(const gs_options& o, int64_t N, int C, int W, int H, con
     p.eps2d = o.eps2d; p.antialiased = o.antialiased; p.fov_clamp = o.fov_clamp;
     p.means = means; p.quats = quats; p.scales = scales; p.opac = opac; p.colors = colors;
     p.viewmats = viewmats; p.Ks = Ks; p.radii = radii; p.v_splats = v_splats; p.map = nullptr;
-    p.vec_colors = ((reinterpret_cast<uintptr_t>(v_colors) & 15u) == 0) && ((K * 3) % 4 == 0);
+    // float4 path reads colors and writes v_colors: both bases must be 16-byte aligned
+    p.vec_colors = ((reinterpret_cast<uintptr_t>(v_colors) & 15u) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(colors) & 15u) == 0) && ((K * 3) % 4 == 0);
     p.v_means = v_means; p.v_quats = v_quats; p.v_scales = v_scales; p.v_opac = v_opac; p.v_colors = v_colors;
     return p;
 }

@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kScanT) k_pack_scan(int* cnt, int64_t n, int64
         int64_t run = carry + (x - sum) + s_w[warp];
 #pragma unroll
         for (int k = 0; k < kScanItems; k++) {
-            if (i0 + k < n) cnt[i0 + k] = (int)run;
+            if (i0 + k < n) cnt[i0 + k] = (int)min(run, cap);   // positions >= cap are dropped (overflow)
             run += v[k];
         }
         carry += s_w[32];

@@ -46,7 +46,7 @@ class Engine:
         self.nnz_overflow = torch.zeros(1, dtype=torch.int32, device=dev)
         self.nnz_cap = 0
         if self.packed:
-            self._alloc_items(nnz_capacity if nnz_capacity is not None else C * N)
+            self._alloc_items(nnz_capacity if nnz_capacity is not None else min(C * N, L.MAX_ITEMS))
             pw = L.gs_project_packed_workspace_size(N, C)
             bw = L.gs_project_bwd_packed_workspace_size(N, C)
             self._proj_ws = self._aligned(pw)
@@ -126,7 +126,10 @@ class Engine:
         isect overflowed; the capacity is then grown and the caller must re-run."""
         if self.packed and int(self.nnz_overflow.item()) != 0:
             M_cap = self.cap
-            self._alloc_items(math.ceil(int(self.nnz.item()) * headroom) + 1024)
+            nnz = int(self.nnz.item())
+            if nnz > L.MAX_ITEMS:
+                raise RuntimeError(f"{nnz} visible (camera, Gaussian) pairs exceed the int32 item ids of one call")
+            self._alloc_items(min(math.ceil(nnz * headroom) + 1024, L.MAX_ITEMS))
             self._alloc_isect(M_cap)
             return True
         if int(self.overflow.item()) == 0:

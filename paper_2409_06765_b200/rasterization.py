@@ -53,7 +53,7 @@ class _Rasterize(torch.autograd.Function):
             nnz_dev = torch.zeros(1, dtype=torch.int64, device=dev)
             novf = torch.zeros(1, dtype=torch.int32, device=dev)
             ws = _aligned_ws(L.gs_project_packed_workspace_size(N, C), dev)
-            n_rec = _NNZ_CACHE.get((N, C, W, H), C * N)
+            n_rec = _NNZ_CACHE.get((N, C, W, H), min(C * N, L.MAX_ITEMS))
             while True:
                 n_rec = max(int(n_rec), 1)
                 radii = torch.empty((n_rec, 2), dtype=torch.int32, device=dev)
@@ -63,10 +63,12 @@ class _Rasterize(torch.autograd.Function):
                 L.gs_project_packed(o, means, quats, scales, opacities, proj_colors, K, viewmats, Ks, W, H, n_rec,
                                     nnz_dev, novf, cam_ids, gid, radii, splats, ws)
                 nnz = int(nnz_dev.item())
-                _NNZ_CACHE[(N, C, W, H)] = math.ceil(nnz * 1.25) + 1024
+                _NNZ_CACHE[(N, C, W, H)] = min(math.ceil(nnz * 1.25) + 1024, L.MAX_ITEMS)
                 if int(novf.item()) == 0:
                     break
-                n_rec = nnz + 1024
+                if nnz > L.MAX_ITEMS:
+                    raise RuntimeError(f"{nnz} visible (camera, Gaussian) pairs exceed the int32 item ids of one call")
+                n_rec = min(nnz + 1024, L.MAX_ITEMS)
         else:
             n_rec = N
             radii = torch.empty((C, N, 2), dtype=torch.int32, device=dev)
@@ -182,14 +184,16 @@ def _gather_cameras(viewmats, Ks, group):
     partition: rank r renders views [vs[r], vs[r+1]).  Small host-side collectives."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    cnt = torch.tensor([viewmats.shape[0]], dtype=torch.int64)
-    cnts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    # NCCL only moves device tensors; gloo takes host ones
+    cdev = viewmats.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    cnt = torch.tensor([viewmats.shape[0]], dtype=torch.int64, device=cdev)
+    cnts = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(world)]
     dist.all_gather(cnts, cnt, group=group)
     cnts = [int(c.item()) for c in cnts]
     cmax = max(cnts)
-    cam = torch.zeros((cmax, 25), dtype=torch.float32)
-    cam[:viewmats.shape[0], :16] = viewmats.detach().reshape(-1, 16).cpu()
-    cam[:viewmats.shape[0], 16:] = Ks.detach().reshape(-1, 9).cpu()
+    cam = torch.zeros((cmax, 25), dtype=torch.float32, device=cdev)
+    cam[:viewmats.shape[0], :16] = viewmats.detach().reshape(-1, 16).to(cdev)
+    cam[:viewmats.shape[0], 16:] = Ks.detach().reshape(-1, 9).to(cdev)
     allc = [torch.zeros_like(cam) for _ in range(world)]
     dist.all_gather(allc, cam, group=group)
     rows = torch.cat([a[:c] for a, c in zip(allc, cnts)])
@@ -217,7 +221,7 @@ class _RasterizeDistributed(torch.autograd.Function):
         W, H = cfg["width"], cfg["height"]
         N, C = means.shape[0], vm_all.shape[0]
         key = (N, C, W, H, rank, world)
-        nnz_cap, rcap, mcap = _DIST_CACHE.get(key, (max(1024, C * N // 2), None, None))
+        nnz_cap, rcap, mcap = _DIST_CACHE.get(key, (min(max(1024, C * N // 2), L.MAX_ITEMS), None, None))
         eng = ShardedEngine(N, C, W, H, rank=rank, world=world, sh_degree=cfg["deg"], K=cfg["K"],
                             antialiased=cfg["antialiased"], device=means.device, nnz_capacity=nnz_cap,
                             recv_capacity=rcap, M_capacity=mcap, view_starts=vs, **cfg["opt_kwargs"])
@@ -307,6 +311,9 @@ def rasterization(means, quats, scales, opacities, colors, viewmats, Ks, width, 
     nd = deg < 0 and colors.dim() == 2 and colors.shape[1] != 3
     if nd and depth_mode:
         raise ValueError("N-D features and depth rendering are not combined (render depth as a feature)")
+    if nd and absgrad and colors.shape[1] > 4:
+        # |sum over channels| is not the sum of the per-pass |partial sums| (include/gs.h)
+        raise ValueError("absgrad with N-D features needs D <= 4 (one channel pass)")
     cfg = dict(opts=o, width=int(width), height=int(height), K=K, packed=bool(packed), depth_mode=depth_mode,
                nd=nd)
     C, N = viewmats.shape[0], means.shape[0]

@@ -1,5 +1,6 @@
 """Worker of tests/test_gpu_dist_api.py (run under torch.distributed.run): Gaussian-sharded
-rasterization(distributed=True) on one GPU shared by all ranks (gloo backend), one shard of
+rasterization(distributed=True) on one GPU shared by all ranks (gloo backend; NCCL with one
+rank, since NCCL takes one GPU per rank), one shard of
 the scene and one block of cameras per rank; saves images and shard gradients to out_dir."""
 import os
 import sys
@@ -15,8 +16,10 @@ from paper_2409_06765_b200.gshard import shard_range  # noqa: E402
 from synth import scenes as S  # noqa: E402
 
 
-def main(out_dir, aa):
-    dist.init_process_group("gloo")
+def main(out_dir, aa, backend="gloo"):
+    if backend == "nccl":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dist.init_process_group(backend)
     rank, world = dist.get_rank(), dist.get_world_size()
     sc = S.tiny_scene(1, N=1500, width=200, height=150, sh_degree=3, views=3)
     C, N, W, H = 3, 1500, 200, 150
@@ -39,4 +42,4 @@ def main(out_dir, aa):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]))
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else "gloo")

@@ -82,6 +82,10 @@ def test_validation_before_device_work(L):
     # sh degree out of range
     o3 = L.options(sh_degree=4)
     assert lib.gs_project(ct.byref(o3), 10, 1, 64, 64, *([null] * 5), 1, null, null, null, null, null) == 1
+    # absgrad with N-D features needs one channel pass (D <= 4): refused before any launch
+    P = 256   # any non-NULL, aligned address: the call must return before touching it
+    assert lib.gs_rasterize_bwd_nd(ct.byref(o), 1, 10, 64, 64, P, P, 5, null, 10, null, P, P, P, P, P, null, 1,
+                                   P, P, P, null) == 2
     # misaligned workspace
     assert lib.gs_isect_tiles(ct.byref(o), 1, 0, 64, 64, null, null, 0, 8, 8, null, null, 8, 1, 0, null) == 1
 

@@ -2,7 +2,8 @@
 under torch.distributed.run sharing this box's one GPU over gloo (the product uses NCCL with
 one GPU per rank; the collectives' semantics are the same).  Images of every rank's cameras
 must be bit-identical to the one-process call over the whole scene, and the concatenated
-shard gradients equal to its gradients up to fp32 atomic order."""
+shard gradients equal to its gradients up to fp32 atomic order.  The NCCL case (one rank:
+NCCL cannot put two ranks on one GPU) runs the same path with device-side collectives."""
 import os
 import socket
 import subprocess
@@ -26,13 +27,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world,aa", [(2, 0), (3, 1)])
-def test_distributed_rasterization_matches_one_process(tmp_path, world, aa):
+@pytest.mark.parametrize("world,aa,backend", [(2, 0, "gloo"), (3, 1, "gloo"), (1, 0, "nccl")])
+def test_distributed_rasterization_matches_one_process(tmp_path, world, aa, backend):
     import torch
     from paper_2409_06765_b200 import rasterization
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "_dist_raster_worker.py"), str(tmp_path), str(aa)]
+           os.path.join(ROOT, "tests", "_dist_raster_worker.py"), str(tmp_path), str(aa), backend]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     sc = S.tiny_scene(1, N=1500, width=200, height=150, sh_degree=3, views=3)
