@@ -34,10 +34,58 @@ METRIC = "megapixels/sec fwd+bwd at 1/2/4/8 B200; fraction of HBM roofline"
 UNIT = "MP/s"
 SMS = 148
 FP32_LANES_PER_SM = 128
-# algorithmic FP32 instructions per pair
-OPS_EVAL = 13        # eval_alpha: 2 FSUB, 4 FMUL, 2 FFMA, 2 FSETP, MUFU.EX2, FMUL, FMNMX
-OPS_FWD_CONTRIB = 7  # 1-alpha, T*, compare, w, 3 FFMA
-OPS_BWD_CONTRIB = 36  # B2-B6 per composited pair
+# SURVEY 8(d) algorithmic work of the raster kernels (FP32 instructions; MUFU ex2 counted as one)
+OPS_K6_PER_EVAL = 17      # K6: per evaluated pair, ~16 FP32 + 1 ex2
+OPS_K7_PER_CONTRIB = 45   # K7: per composited pair (B2-B6, ~45 FP32 + 2 MUFU)
+OPS_K7_PER_EVAL = 10      # K7: per evaluated pair (alpha replay)
+
+
+def alg_bytes(N, C, V, N_vis, M, P, K):
+    """SURVEY 8(d) algorithmic (method-required) HBM bytes per stage.  N Gaussians, C views,
+    V visible (c,n), N_vis Gaussians visible in >= 1 view, M intersections, P pixels, K SH
+    coefficients per channel."""
+    return {
+        # 44 B params per Gaussian, SH once per visible Gaussian, 52 B record + rgb per visible
+        # (c,n), radii for all (c,n)
+        "project": N * 44 + N_vis * 12 * K + V * 52 + C * N * 8,
+        # count/scan/emit (V 20 read, C N 12, M 12 written) + sort floor 2 x 12 B x M + ranges M 8
+        "isect": V * 20 + C * N * 12 + M * 12 + 2 * 12 * M + M * 8,
+        # id + 36 B record per intersection, 24 B per pixel
+        "raster_fwd": M * 40 + P * 24,
+        # + one reduced 9-float RED per (splat, tile)
+        "raster_bwd": M * 40 + M * 36 + P * 24,
+        # 36 B record gradient per visible (c,n), params + SH of visible Gaussians read, 236 B/G written
+        "project_bwd": V * 36 + N_vis * (44 + 12 * K) + N * (44 + 12 * K),
+    }
+
+
+def workload(eng, L, C, W, H, dev):
+    """SURVEY 8(d) workload descriptors of the engine's last step: visible pairs V, Gaussians
+    visible in >= 1 view, M, tile-list length p50 / p99 / max, evaluated and composited pairs
+    per pixel, early-terminated pixel fraction (gs_rasterize_stats, outside any timed region)."""
+    import torch
+    n_eval = torch.zeros((C, H, W), dtype=torch.int32, device=dev)
+    n_con = torch.zeros_like(n_eval)
+    term = torch.zeros_like(n_eval)
+    L.gs_rasterize_stats(eng.opts, C, eng.n_items, W, H, eng.splats, eng.isect_ids, eng.tile_offsets, n_eval, n_con,
+                         term)
+    torch.cuda.synchronize(dev)
+    if eng.packed:
+        nnz = int(eng.nnz.item())
+        V = nnz
+        N_vis = int(torch.unique(eng.gaussian_ids[:nnz]).numel())
+    else:
+        vis = eng.radii[..., 0] > 0
+        V = int(vis.sum().item())
+        N_vis = int(vis.any(dim=0).sum().item())
+    lens = torch.diff(eng.tile_offsets.long()).double()
+    P = C * W * H
+    E_f, E_c = int(n_eval.sum().item()), int(n_con.sum().item())
+    return {"E_f": E_f, "E_c": E_c, "V": V, "N_vis": N_vis, "M": eng.n_isect,
+            "tile_list_p50": float(torch.quantile(lens, 0.5).item()),
+            "tile_list_p99": float(torch.quantile(lens, 0.99).item()), "tile_list_max": int(lens.max().item()),
+            "evaluated_per_pixel": round(E_f / P, 3), "contributing_per_pixel": round(E_c / P, 3),
+            "early_terminated_frac": round(float(term.double().mean().item()), 4)}
 
 
 def _peaks():
@@ -208,8 +256,9 @@ def run_ours(args):
         se[5].record(stream)
     torch.cuda.synchronize(dev)
     names = ["project", "isect", "raster_fwd", "raster_bwd", "project_bwd"]
-    stage_ms = {n: float(np.mean([stage_ev[i][j].elapsed_time(stage_ev[i][j + 1]) for i in range(args.steps)]))
-                for j, n in enumerate(names)}
+    stage_all = {n: [stage_ev[i][j].elapsed_time(stage_ev[i][j + 1]) for i in range(args.steps)]
+                 for j, n in enumerate(names)}
+    stage_ms = {n: float(np.mean(v)) for n, v in stage_all.items()}
     if int(eng.overflow.item()) != 0:
         raise RuntimeError("intersection capacity overflowed inside the timed region")
     if world > 1:
@@ -220,58 +269,50 @@ def run_ours(args):
     mp_per_step = C * W * H / 1e6 * world
     value = mp_per_step / (ms_per_step / 1e3)
 
-    # ---- work counts for the roofline (outside the timed region) ----
-    n_eval = torch.zeros((C, H, W), dtype=torch.int32, device=dev)
-    n_con = torch.zeros_like(n_eval)
-    L.gs_rasterize_stats(eng.opts, C, eng.n_items, W, H, eng.splats, eng.isect_ids, eng.tile_offsets, n_eval, n_con)
-    torch.cuda.synchronize(dev)
-    E_f = int(n_eval.sum().item())
-    E_c = int(n_con.sum().item())
-    # pairs the backward walks per pixel: from its last composited index back to the range start
-    TX, TY = L.tiles(W, H)
-    ys = torch.arange(H, device=dev).view(H, 1) // 16
-    xs = torch.arange(W, device=dev).view(1, W) // 16
-    tile = (ys * TX + xs).view(1, H, W) + torch.arange(C, device=dev).view(C, 1, 1) * (TX * TY)
-    start = eng.tile_offsets[tile.long()]
-    E_b = int((eng.last_ids - start + 1).clamp(min=0).sum().item())
-    V = int(eng.nnz.item()) if eng.packed else int((eng.radii[..., 0] > 0).sum().item())
+    # ---- work counts and workload descriptors (outside the timed region) ----
+    wl = workload(eng, L, C, W, H, dev)
+    E_f, E_c, V, N_vis = wl["E_f"], wl["E_c"], wl["V"], wl["N_vis"]
 
     peaks = _peaks()
     clk_mhz = peaks["sm_max_mhz"]
     alu_peak = SMS * FP32_LANES_PER_SM * clk_mhz * 1e6 / 1e12          # T FP32 instr/s
-    # useful (algorithmic) work: the composited pairs only -- evaluating a pair that ends up
-    # skipped (alpha < alpha_min) is overhead the kernel tries to avoid (K6/K7)
-    alu = {
-        "raster_fwd": (OPS_EVAL + OPS_FWD_CONTRIB) * E_c / 1e12,
-        "raster_bwd": (OPS_EVAL + OPS_BWD_CONTRIB) * E_c / 1e12,
-    }
-    # algorithmic HBM bytes per launch (SURVEY 8d formulas)
+    # SURVEY 8(d) algorithmic work: K6 E_f x (16 FP32 + 1 ex2); K7 E_c x 45 + E_f x 10 (the
+    # per-(splat, warp) reduction term, ~1 % at configs[1], is not counted)
+    alu = {"raster_fwd": OPS_K6_PER_EVAL * E_f / 1e12,
+           "raster_bwd": (OPS_K7_PER_CONTRIB * E_c + OPS_K7_PER_EVAL * E_f) / 1e12}
     Kc = 16 if sc["sh_degree"] == 3 else (sc["sh_degree"] + 1) ** 2
-    P = C * W * H
-    hbm = {
-        "project": N * 44 + N * 12 * Kc + C * N * (48 + 8),
-        "isect": C * N * 8 + V * 8 * 2 * 4 + M * 8 + M * 8 * 2 * 2 + M * 4,
-        "project_bwd": C * N * (48 + 8) + N * (44 + 12 * Kc) + N * (44 + 12 * Kc),
-    }
+    hbm = alg_bytes(N, C, V, N_vis, M, C * W * H, Kc)
     dom = max(stage_ms, key=stage_ms.get)
+    per_stage = {}
+    for n_, ms in stage_ms.items():
+        v = stage_all[n_]
+        d = {"ms": round(ms, 4), "p10": round(float(np.percentile(v, 10)), 4),
+             "p50": round(float(np.percentile(v, 50)), 4), "p90": round(float(np.percentile(v, 90)), 4),
+             "alg_bytes": int(hbm[n_]),
+             "hbm_frac": round(hbm[n_] / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
+        if n_ in alu:
+            d["alu_frac"] = round(alu[n_] / (ms / 1e3) / alu_peak, 4)
+        tr = _traffic(n_)
+        if tr is not None:
+            d["dram_bytes_ncu"] = tr
+        per_stage[n_] = d
+    step_bytes = sum(hbm.values())
     if dom in alu:
         ach = alu[dom] / (stage_ms[dom] / 1e3)
         roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2),
                 "unit": "T FP32 instr/s", "frac": round(ach / alu_peak, 4), "traffic": _traffic(dom),
                 "peak_src": f"{SMS} SMs x {FP32_LANES_PER_SM} FP32 lanes x {clk_mhz:.0f} MHz ({peaks['src']})",
-                "work": {"pairs_composited": E_c, "pairs_evaluated_fwd": E_f, "pairs_walked_bwd": E_b}}
+                "hbm_frac": per_stage[dom]["hbm_frac"],
+                "work": {"pairs_composited": E_c, "pairs_evaluated_fwd": E_f,
+                         "formula": "K6 17 E_f; K7 45 E_c + 10 E_f (SURVEY 8d)"}}
     else:
         ach = hbm[dom] / (stage_ms[dom] / 1e3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": _traffic(dom), "peak_src": peaks["src"]}
-    per_stage = {}
-    for n_, ms in stage_ms.items():
-        d = {"ms": round(ms, 4)}
-        if n_ in hbm:
-            d["hbm_frac"] = round(hbm[n_] / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)
-        if n_ in alu:
-            d["alu_frac"] = round(alu[n_] / (ms / 1e3) / alu_peak, 4)
-        per_stage[n_] = d
+    step_stats = {"p10": round(float(np.percentile(step_ms, 10)), 4), "p50": round(float(np.percentile(step_ms, 50)), 4),
+                  "p90": round(float(np.percentile(step_ms, 90)), 4),
+                  "alg_bytes": int(step_bytes),
+                  "hbm_frac": round(step_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
 
     # ---- end to end through the public API with HOST buffers (pinned), every step ----
     # Each step uploads that step's inputs (all Gaussian parameters, cameras, the upstream
@@ -281,6 +322,7 @@ def run_ours(args):
     # run during step i's kernels (PCIe is full duplex); events order every reuse.  The
     # timed region runs from before the first upload to after the last download.
     e2e = None
+    engs = d_in = d_v = None
     if not args.no_e2e:
         engs = [eng, Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, M_capacity=eng.cap, **mode_kw,
                              bbox_mode=args.bbox_mode)]
@@ -360,6 +402,34 @@ def run_ours(args):
                                   "M_isect": e2.n_isect, "note": "opacity-aware tile extent (DESIGN Q36): "
                                   "images and gradients identical to the 3-sigma box"}
         del e2
+        # the same step captured once into a CUDA graph and replayed (Engine.capture)
+        eng.capture(params, v_dev)
+        for _ in range(args.warmup):
+            eng.replay()
+        evg = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()
+            evg[i][0].record(stream)
+            eng.replay()
+            evg[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if int(eng.overflow.item()) != 0:
+            raise RuntimeError("intersection capacity overflowed (CUDA-graph variant)")
+        msg = float(np.sum([a.elapsed_time(b) for a, b in evg])) / args.steps
+        variants["cuda_graph"] = {"value": round(mp_per_step / (msg / 1e3), 3), "ms_per_step": round(msg, 4),
+                                  "note": "one captured step replayed (same kernels, same buffers)"}
+        eng.graph = None
+
+    # ---- BASELINE configs[2] as strong scaling: its 8 views split over the N ranks (the
+    # same total work at every N; E(R) = t(1) / (R t(R)) from the per-N records) ----
+    del engs, d_in, d_v
+    strong = None
+    if not args.no_strong:
+        del eng
+        torch.cuda.empty_cache()
+        strong = run_strong(args, world, rank, dev, flush)
+    ar = allreduce_sweep(world, dev) if world > 1 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -375,13 +445,108 @@ def run_ours(args):
                    "bbox_mode": args.bbox_mode, "packed": mode_kw["packed"],
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "V_visible": V, "M_isect": M, "pairs_eval": E_f, "pairs_contrib": E_c},
-        "roofline": roof, "stages": per_stage, "gpu_launches": launches * args.steps,
+        "workload": {k: v for k, v in wl.items() if k not in ("E_f", "E_c")},
+        "roofline": roof, "stages": per_stage, "step": step_stats, "gpu_launches": launches * args.steps,
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "variants": variants,
+        "strong_batch3m": strong, "allreduce": ar,
     }
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_strong(args, world, rank, dev, flush, cfg_name="batch3m", total_views=8):
+    """BASELINE configs[2]: 3M Gaussians SH3, 8 views of 1297x840 split over the world's ranks
+    (views [8 r / R, 8 (r + 1) / R) on rank r, Gaussians replicated), one call per rank plus the
+    NCCL all-reduce of the flat gradient; device-timed, L2 flushed between steps, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2409_06765_b200 import Engine
+    from paper_2409_06765_b200 import dist as D
+    from synth import scenes as S
+    cfg = S.CONFIGS[cfg_name]
+    views = D.partition_views(total_views, world, rank)
+    if len(views) == 0:
+        raise RuntimeError("more ranks than views")
+    sc = S.mipnerf_like_scene(cfg["N"], cfg["width"], cfg["height"], views=len(views), sh_degree=cfg["sh_degree"],
+                              seed=cfg["seed"], view_offset=views[0])
+    C, N, W, H = len(views), cfg["N"], cfg["width"], cfg["height"]
+    v_img, _ = S.image_grads(cfg["seed"], total_views, H, W)
+    keys = ["means", "quats", "scales", "opacities", "colors", "viewmats", "Ks"]
+    params = tuple(torch.from_numpy(np.ascontiguousarray(sc[k], np.float32)).to(dev) for k in keys)
+    v_dev = torch.from_numpy(np.ascontiguousarray(v_img[views[0]:views[-1] + 1])).to(dev)
+    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev)
+    eng.run_checked(params, v_dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eng.step(params, v_dev)
+        if world > 1:
+            dist.all_reduce(eng.flat_grad)
+
+    for _ in range(3):
+        step()
+    K = args.strong_steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(K):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if int(eng.overflow.item()) != 0:
+        raise RuntimeError("intersection capacity overflowed (strong-scaling leg)")
+    ms = [a.elapsed_time(b) for a, b in ev]
+    tot = float(np.sum(ms))
+    if world > 1:
+        t = torch.tensor([tot], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    ms_step = tot / K
+    out = {"workload": f"{cfg_name} (BASELINE {CFG_INDEX[cfg_name]}): {N} Gaussians SH{cfg['sh_degree']}, "
+                       f"{total_views} views of {W}x{H} split over {world} GPU(s)",
+           "scaling": "strong", "views_per_gpu": C, "steps": K, "ms_per_step": round(ms_step, 4),
+           "value": round(total_views * W * H / 1e6 / (ms_step / 1e3), 3), "unit": UNIT,
+           "allreduce_bytes": int(eng.flat_grad.numel() * 4) if world > 1 else 0, "M_isect_rank0": eng.n_isect,
+           "note": "E(R) = ms_per_step(1 GPU) / (R ms_per_step(R GPUs)), from the per-N records"}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+def allreduce_sweep(world, dev, sizes_mb=(236, 708), iters=10):
+    """Standalone NCCL all-reduce (fp32 SUM) of the flat-gradient sizes of configs[1] (1M
+    Gaussians x 236 B) and configs[2] (3M): device time per call (max over ranks), algorithm
+    bandwidth bytes / t and bus bandwidth 2 (R - 1) / R of it."""
+    import torch
+    import torch.distributed as dist
+    out = []
+    stream = torch.cuda.current_stream(dev)
+    for mb in sizes_mb:
+        n = mb * 1_000_000 // 4
+        x = torch.ones(n, dtype=torch.float32, device=dev)
+        for _ in range(3):
+            dist.all_reduce(x)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(iters):
+            dist.all_reduce(x)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([a.elapsed_time(b) / iters], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        alg = n * 4 / (ms / 1e3) / 1e9
+        out.append({"bytes": n * 4, "ms": round(ms, 4), "algbw_gbs": round(alg, 1),
+                    "busbw_gbs": round(alg * 2 * (world - 1) / world, 1)})
+        del x
+    return out
 
 
 # ------------------------------------------------------------------------------------------
@@ -542,6 +707,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="skip the configs[2] strong-scaling leg")
+    ap.add_argument("--strong-steps", type=int, default=10)
     ap.add_argument("--packed", action="store_true", help="packed (visible-only) per-item layout (Q29)")
     ap.add_argument("--bbox-mode", type=int, default=0, choices=[0, 1, 2],
                     help="tile extent: 0 the paper's 3-sigma box (default), 2 opacity-aware (Q36)")

@@ -109,7 +109,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 8
+#define GS_ABI_VERSION 9
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -175,10 +175,12 @@ GS_API gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, i
 /* ---- Diagnostics (not on the hot path): per-pixel work counts of stage 3 ---------
  * Runs the forward walk of gs_rasterize_fwd and writes, per pixel, n_eval [C,H,W] (pairs
  * whose alpha was evaluated, up to and including the terminating one) and n_contrib
- * [C,H,W] (pairs composited).  bench.py uses the sums as the algorithmic work of K6/K7. */
+ * [C,H,W] (pairs composited) and, if non-NULL, terminated [C,H,W] (1 where the walk stopped
+ * at the transmittance threshold Q15, 0 where it ran off the end of the tile's list).
+ * bench.py uses the sums as the algorithmic work of K6/K7 and the workload descriptors. */
 GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                                     const float* splats, const int32_t* isect_ids, const int32_t* tile_offsets,
-                                    int32_t* n_eval, int32_t* n_contrib, void* stream);
+                                    int32_t* n_eval, int32_t* n_contrib, int32_t* terminated, void* stream);
 
 /* ---- Stage 4a: backward composite (B1-B6) -------------------------------
  * Back to front from last_ids with T_{n-1} = T_n/(1-alpha_{n-1}) and the S

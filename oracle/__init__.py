@@ -79,8 +79,9 @@ def lib():
         _lib.or_project.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32, P, P] + [P] * 10
         _lib.or_isect.argtypes = [P, i32, i64, i32, i32, P, P, P, i64, P, P, P]
         _lib.or_isect.restype = i64
-        _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6 + [P] * 2
-        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 8
+        _lib.or_render_fwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 6 + [P] * 2 + [P]
+        _lib.or_render_bwd.argtypes = [P, i32, i64, i32, i32] + [P] * 10 + [P] * 7 + [P] * 8 + [P] * 4
+        _lib.or_render_pixels.argtypes = [P, i32, i64, i32, i32] + [P] * 9 + [i64] + [P] * 8
         _lib.or_project_bwd.argtypes = [P, i64, i32, i32, i32] + [P] * 5 + [i32] + [P] * 3 + [P] * 6 + [P] * 2 + [i32]
         _lib.or_sh_basis.argtypes = [i32, dbl, dbl, dbl, P]
         _lib.or_sh_basis_grad.argtypes = [i32, dbl, dbl, dbl, P]
@@ -175,10 +176,16 @@ def _depth64(proj):
     return _f64(proj["depth"] if "depth" in proj else proj["depth_f"])
 
 
-def render_fwd(proj, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None):
+def _flips(flips):
+    return None if flips is None else np.ascontiguousarray(flips, np.uint32)
+
+
+def render_fwd(proj, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None, flips=None):
     """R1-R3 per pixel.  Also returns the accumulated depth sum z alpha T ("depth")
     and the expected depth ("depth_exp" = that sum / sum alpha T, with
-    sum alpha T = 1 - T_final; 0 where nothing composited)."""
+    sum alpha T = 1 - T_final; 0 where nothing composited).  "ambig" [C,H,W] counts the
+    ambiguous decisions (DESIGN Q28b) met per pixel; flips [C,H,W] (uint32, optional) takes
+    the alternative outcome of the j-th of them where bit j is set (resolve_ambiguous)."""
     o = opts.c()
     bg = None if backgrounds is None else _f64(backgrounds)
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
@@ -188,14 +195,40 @@ def render_fwd(proj, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None
     lib().or_render_fwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(out["rgb"]), _p(out["alpha"]), _p(out["T"]), _p(out["last_gid"]),
-                        _p(out["ambig"]), _p(out["ncontrib"]), _p(_depth64(proj)), _p(out["depth"]))
+                        _p(out["ambig"]), _p(out["ncontrib"]), _p(_depth64(proj)), _p(out["depth"]),
+                        _p(_flips(flips)))
     A = 1.0 - out["T"]
     out["depth_exp"] = np.where(A > 0, out["depth"] / np.where(A > 0, A, 1.0), 0.0)
     return out
 
 
+def render_pixels(proj, C, N, W, H, opts: Options, cams, pxs, pys, flips, backgrounds=None, feats=None):
+    """R1-R3 for single pixels (cams[q], pxs[q], pys[q]) under the decision outcomes flips[q]
+    (see render_fwd).  Returns colour [Q, 3 or D], T [Q], last_gid [Q] and namb [Q], the number
+    of ambiguous decisions that walk met -- the enumeration of the outcomes an ambiguous pixel
+    admits (DESIGN Q28b).  feats [N, D]: N-D feature mode (render_fwd_nd)."""
+    rows, o = proj["rgb"], opts
+    D = 3
+    if feats is not None:
+        feats = _f64(feats)
+        D = feats.shape[1]
+        rows = np.ascontiguousarray(np.broadcast_to(feats[None], (C, N, D)).reshape(C * N, D))
+        o = _nd_opts(opts, D)
+    Q = len(cams)
+    out = dict(rgb=np.zeros((Q, D)), T=np.zeros(Q), last_gid=np.zeros(Q, np.int64), namb=np.zeros(Q, np.int32))
+    bg = None if backgrounds is None else _f64(backgrounds)
+    oc = o.c()
+    lib().or_render_pixels(ct.byref(oc), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
+                           _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(_f64(rows)),
+                           _p(bg), Q, _p(np.ascontiguousarray(cams, np.int32)),
+                           _p(np.ascontiguousarray(pxs, np.int32)), _p(np.ascontiguousarray(pys, np.int32)),
+                           _p(np.ascontiguousarray(flips, np.uint32)), _p(out["rgb"]), _p(out["T"]),
+                           _p(out["last_gid"]), _p(out["namb"]))
+    return out
+
+
 def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds=None, tile_mask=None,
-               v_depth=None, v_depth_exp=None):
+               v_depth=None, v_depth_exp=None, flips=None):
     """B1-B6.  Returns v2d [C,N,9] (v_mean2d 2, v_conic 3, v_rgb 3, v_opac_eff 1), and for the
     parity tolerance (not part of the result): a2d, the sum over pixels of |per-pixel term|
     with B4's v_alpha replaced by the magnitudes of its parts (fp32 cancellation floor),
@@ -213,7 +246,7 @@ def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds
     va = None if v_alpha is None else _f64(v_alpha)
     vD = None if v_depth is None else _f64(v_depth).copy()
     if v_depth_exp is not None:
-        f = render_fwd(proj, C, N, W, H, opts, backgrounds, tile_mask)
+        f = render_fwd(proj, C, N, W, H, opts, backgrounds, tile_mask, flips=flips)
         A = 1.0 - f["T"]
         ok = A > 0
         Ar = np.where(ok, A, 1.0)
@@ -223,12 +256,16 @@ def render_bwd(proj, C, N, W, H, opts: Options, v_img, v_alpha=None, backgrounds
     v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9)); absg = np.zeros((C, N, 2))
     vz = np.zeros((C, N)); az = np.zeros((C, N)); sz = np.zeros((C, N))
     amb = np.zeros((C, N), np.uint8)
+    n2d = np.zeros((C, N), np.int32)
+    d2d = np.zeros((C, N, 9))
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(proj["rgb"]), _p(bg),
                         _p(tm), _p(v_img), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
-                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz), None, _p(absg), None)
-    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vz=vz, az=az, sz=sz, absgrad=absg)
+                        _p(_depth64(proj)), _p(vD), _p(vz), _p(az), _p(sz), None, _p(absg), None, _p(_flips(flips)),
+                        _p(n2d), _p(d2d), None)
+    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vz=vz, az=az, sz=sz, absgrad=absg,
+                n2d=n2d, d2d=d2d)
 
 
 def _nd_opts(opts: Options, D: int) -> Options:
@@ -236,7 +273,7 @@ def _nd_opts(opts: Options, D: int) -> Options:
     return replace(opts, channels=int(D))
 
 
-def render_fwd_nd(proj, feats, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None):
+def render_fwd_nd(proj, feats, C, N, W, H, opts: Options, backgrounds=None, tile_mask=None, flips=None):
     """N-dimensional rasterization: the same R1-R3 composite with the per-Gaussian
     D-channel features feats [N, D] (camera independent) in place of the projected RGB.
     Returns feats image "feat" [C,H,W,D] plus alpha, T, last_gid, ambig as render_fwd."""
@@ -254,11 +291,12 @@ def render_fwd_nd(proj, feats, C, N, W, H, opts: Options, backgrounds=None, tile
     lib().or_render_fwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(rows), _p(bg),
                         _p(tm), _p(out["feat"]), _p(out["alpha"]), _p(out["T"]), _p(out["last_gid"]),
-                        _p(out["ambig"]), _p(out["ncontrib"]), None, None)
+                        _p(out["ambig"]), _p(out["ncontrib"]), None, None, _p(_flips(flips)))
     return out
 
 
-def render_bwd_nd(proj, feats, C, N, W, H, opts: Options, v_feat, v_alpha=None, backgrounds=None, tile_mask=None):
+def render_bwd_nd(proj, feats, C, N, W, H, opts: Options, v_feat, v_alpha=None, backgrounds=None, tile_mask=None,
+                  flips=None):
     """B1-B6 with D-channel features: v2d (mean2d, conic, opac_eff slots; the rgb slots 0),
     vfeat [C,N,D] = dL/d(features of each (c,n)), and the tolerance models a2d, s2d and
     afeat (the sum over pixels of |per-pixel feature term|; a_colors its sum over cameras).
@@ -272,15 +310,18 @@ def render_bwd_nd(proj, feats, C, N, W, H, opts: Options, v_feat, v_alpha=None, 
     tm = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8)
     va = None if v_alpha is None else _f64(v_alpha)
     v2d = np.zeros((C, N, 9)); a2d = np.zeros((C, N, 9)); s2d = np.zeros((C, N, 9)); absg = np.zeros((C, N, 2))
-    vfeat = np.zeros((C, N, D)); afeat = np.zeros((C, N, D))
+    vfeat = np.zeros((C, N, D)); afeat = np.zeros((C, N, D)); sfeat = np.zeros((C, N, D))
     amb = np.zeros((C, N), np.uint8)
+    n2d = np.zeros((C, N), np.int32)
+    d2d = np.zeros((C, N, 9))
     err = ct.c_double(0)
     lib().or_render_bwd(ct.byref(o), C, N, W, H, _p(proj["radii"]), _p(proj["mean2d_f"]), _p(proj["depth_f"]),
                         _p(proj["dec"]), _p(proj["mean2d"]), _p(proj["conic"]), _p(proj["opac_eff"]), _p(rows), _p(bg),
                         _p(tm), _p(_f64(v_feat)), _p(va), _p(v2d), _p(a2d), _p(s2d), _p(amb), ct.byref(err),
-                        None, None, None, None, None, _p(vfeat), _p(absg), _p(afeat))
-    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vfeat=vfeat, absgrad=absg,
-                v_colors=vfeat.sum(axis=0), afeat=afeat, a_colors=afeat.sum(axis=0))
+                        None, None, None, None, None, _p(vfeat), _p(absg), _p(afeat), _p(_flips(flips)), _p(n2d),
+                        _p(d2d), _p(sfeat))
+    return dict(v2d=v2d, a2d=a2d, s2d=s2d, g_ambig=amb, T_replay_err=err.value, vfeat=vfeat, absgrad=absg, n2d=n2d, d2d=d2d,
+                v_colors=vfeat.sum(axis=0), afeat=afeat, a_colors=afeat.sum(axis=0), s_colors=sfeat.sum(axis=0))
 
 
 def project_bwd(scene, proj, v2d, opts: Options, vz=None, pose=False):
@@ -325,6 +366,27 @@ def project_bwd_bound(scene, proj, e2d, opts: Options, ez=None, pose=False):
                          _p(viewmats), _p(Ks), _p(proj["radii"]), _p(e2d), _p(out["v_means"]),
                          _p(out["v_quats"]), _p(out["v_scales"]), _p(out["v_opacities"]), _p(out["v_colors"]),
                          _p(None if ez is None else np.abs(_f64(ez))), _p(out.get("v_viewmats")), 1)
+    return out
+
+
+def project_bwd_clamp_alt(scene, proj, v2d, opts: Options, pose=False):
+    """Tolerance model (not a result): the bound (project_bwd_bound) of the colour path of
+    every SH channel whose clamp colour = max(0, raw) (Q22) is decided within the fp32
+    rounding of raw -- both outcomes are correct there, and this is the magnitude of the
+    difference between them in each parameter gradient."""
+    means, quats, scales, opac, colors, viewmats, Ks = _scene_arrays(scene)
+    N, C = means.shape[0], viewmats.shape[0]
+    W, H = int(scene["width"]), int(scene["height"])
+    K = colors.shape[1] if colors.ndim == 3 else 1
+    o = opts.c()
+    out = dict(v_means=np.zeros((N, 3)), v_quats=np.zeros((N, 4)), v_scales=np.zeros((N, 3)),
+               v_opacities=np.zeros(N), v_colors=np.zeros(colors.shape))
+    if pose:
+        out["v_viewmats"] = np.zeros((C, 4, 4))
+    lib().or_project_bwd(ct.byref(o), N, C, W, H, _p(means), _p(quats), _p(scales), _p(opac), _p(colors), K,
+                         _p(viewmats), _p(Ks), _p(proj["radii"]), _p(np.abs(_f64(v2d))), _p(out["v_means"]),
+                         _p(out["v_quats"]), _p(out["v_scales"]), _p(out["v_opacities"]), _p(out["v_colors"]),
+                         None, _p(out.get("v_viewmats")), 2)
     return out
 
 

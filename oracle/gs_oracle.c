@@ -130,6 +130,46 @@ static void sh_basis_grad(int deg, double x, double y, double z, double dY[16][3
     dY[15][1] = SH_C3[6] * (-6.0 * x * y);
 }
 
+/* Tolerance model only (absmode of the projection backward): the same polynomials with
+ * every coefficient and monomial taken in magnitude (subtractions become additions), i.e. the
+ * scale of the rounding error of evaluating Y_j and dY_j in fp32.  Evaluated at |dir|. */
+static void sh_basis_mag(int deg, double x, double y, double z, double *Y, double dY[16][3])
+{
+    x = fabs(x); y = fabs(y); z = fabs(z);
+    memset(dY, 0, sizeof(double) * 16 * 3);
+    Y[0] = SH_C0;
+    if (deg < 1) return;
+    Y[1] = SH_C1 * y; Y[2] = SH_C1 * z; Y[3] = SH_C1 * x;
+    dY[1][1] = dY[2][2] = dY[3][0] = SH_C1;
+    if (deg < 2) return;
+    const double c2 = fabs(SH_C2[0]), c22 = fabs(SH_C2[2]), c24 = fabs(SH_C2[4]);
+    double xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = c2 * x * y; Y[5] = c2 * y * z; Y[6] = c22 * (2.0 * zz + xx + yy); Y[7] = c2 * x * z;
+    Y[8] = c24 * (xx + yy);
+    dY[4][0] = c2 * y;  dY[4][1] = c2 * x;
+    dY[5][1] = c2 * z;  dY[5][2] = c2 * y;
+    dY[6][0] = c22 * 2.0 * x;  dY[6][1] = c22 * 2.0 * y;  dY[6][2] = c22 * 4.0 * z;
+    dY[7][0] = c2 * z;  dY[7][2] = c2 * x;
+    dY[8][0] = c24 * 2.0 * x;  dY[8][1] = c24 * 2.0 * y;
+    if (deg < 3) return;
+    double k[7];
+    for (int i = 0; i < 7; i++) k[i] = fabs(SH_C3[i]);
+    Y[9]  = k[0] * y * (3.0 * xx + yy);
+    Y[10] = k[1] * x * y * z;
+    Y[11] = k[2] * y * (4.0 * zz + xx + yy);
+    Y[12] = k[3] * z * (2.0 * zz + 3.0 * xx + 3.0 * yy);
+    Y[13] = k[4] * x * (4.0 * zz + xx + yy);
+    Y[14] = k[5] * z * (xx + yy);
+    Y[15] = k[6] * x * (xx + 3.0 * yy);
+    dY[9][0] = k[0] * 6.0 * x * y;            dY[9][1] = k[0] * (3.0 * xx + 3.0 * yy);
+    dY[10][0] = k[1] * y * z;  dY[10][1] = k[1] * x * z;  dY[10][2] = k[1] * x * y;
+    dY[11][0] = k[2] * 2.0 * x * y;  dY[11][1] = k[2] * (4.0 * zz + xx + 3.0 * yy);  dY[11][2] = k[2] * 8.0 * y * z;
+    dY[12][0] = k[3] * 6.0 * x * z;  dY[12][1] = k[3] * 6.0 * y * z;  dY[12][2] = k[3] * (6.0 * zz + 3.0 * xx + 3.0 * yy);
+    dY[13][0] = k[4] * (4.0 * zz + 3.0 * xx + yy);  dY[13][1] = k[4] * 2.0 * x * y;  dY[13][2] = k[4] * 8.0 * x * z;
+    dY[14][0] = k[5] * 2.0 * x * z;  dY[14][1] = k[5] * 2.0 * y * z;  dY[14][2] = k[5] * (xx + yy);
+    dY[15][0] = k[6] * (3.0 * xx + 3.0 * yy);  dY[15][1] = k[6] * 6.0 * x * y;
+}
+
 /* exported for the quadrature / FD pins */
 void or_sh_basis(int32_t deg, double x, double y, double z, double *Y) { sh_basis(deg, x, y, z, Y); }
 void or_sh_basis_grad(int32_t deg, double x, double y, double z, double *dY)
@@ -327,6 +367,7 @@ typedef struct {
     double mean2d[2];
     double campos[3], e[3], enorm, dir[3];
     double raw[3], rgb[3];
+    double rawabs[3];   /* 0.5 + sum_j |Y_j sh_j|: scale of the fp32 rounding of raw (tolerance) */
     double opac_eff;
 } proj64_t;
 
@@ -427,13 +468,20 @@ static void project64(const or_opts *o, int W, int H, const float *mu, const flo
         int nb = (o->sh_degree + 1) * (o->sh_degree + 1);
         sh_basis(o->sh_degree, P->dir[0], P->dir[1], P->dir[2], Y);
         for (int ch = 0; ch < 3; ch++) {
-            double acc = 0.5;
-            for (int j = 0; j < nb; j++) acc += Y[j] * (double)colors[(int64_t)j * 3 + ch];
+            double acc = 0.5, aa = 0.5;
+            for (int j = 0; j < nb; j++) {
+                acc += Y[j] * (double)colors[(int64_t)j * 3 + ch];
+                aa += fabs(Y[j] * (double)colors[(int64_t)j * 3 + ch]);
+            }
             P->raw[ch] = acc;
+            P->rawabs[ch] = aa;
             P->rgb[ch] = acc > 0 ? acc : 0;
         }
     } else {
-        for (int ch = 0; ch < 3; ch++) P->raw[ch] = P->rgb[ch] = colors[ch];
+        for (int ch = 0; ch < 3; ch++) {
+            P->raw[ch] = P->rgb[ch] = colors[ch];
+            P->rawabs[ch] = 0;
+        }
     }
     (void)K;
     /* F15 */
@@ -625,17 +673,19 @@ typedef struct {
     int64_t li;      /* list index */
     double alpha, T, G, sigma, dx, dy;
     int clamped;     /* alpha saturated at alpha_max (decision path) */
+    int amb_clamp;   /* that decision was ambiguous: both B6 outcomes are correct (tolerance) */
     double delta;    /* 1 ulp of the fp32 mu' the kernel works with (tolerance model only) */
     double qd;       /* first-order relative change of alpha for a delta shift of mu' */
 } contrib_t;
 
 typedef struct {
     double eT;       /* sum over composited splats of alpha qd / (1 - alpha) (tolerance model) */
+    double rT;       /* relative fp32 error bound of the final T (decision path, tolerance model) */
     double rgb[OR_MAX_CH], T;
     double dacc;      /* accumulated depth sum z alpha T (App. depth rendering) */
     int64_t last_li;  /* -1 if none */
     int64_t end_li;   /* exclusive end of the evaluated part of the list */
-    int ambig;
+    int ambig;        /* number of ambiguous decisions met on the walk */
     int64_t ncontrib;
 } pixres_t;
 
@@ -702,10 +752,21 @@ static int near_thr(double v, double thr, double rel, const or_opts *o)
     return fabs(v - thr) <= m * thr;
 }
 
+/* An ambiguous decision admits both outcomes.  flip selects the alternative outcome: bit j
+ * set takes the other branch at the j-th ambiguous decision met on the walk (so the walk
+ * after a flip is the one a kernel taking that branch follows).  flip = 0 is the fp64
+ * decision everywhere.  Returns the decision to take. */
+static int decide(int outcome, int ambiguous, uint32_t flip, pixres_t *r)
+{
+    if (!ambiguous) return outcome;
+    int j = r->ambig++;
+    return (j < 32 && ((flip >> j) & 1u)) ? !outcome : outcome;
+}
+
 static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, int64_t N, int px, int py,
                               const float *mean2d_f, const float *dec, const double *mean2d,
                               const double *conic, const double *opac_eff, const double *rgb,
-                              const double *depth, contrib_t *rec, int64_t rec_cap)
+                              const double *depth, contrib_t *rec, int64_t rec_cap, uint32_t flip)
 {
     pixres_t r;
     memset(&r, 0, sizeof r);
@@ -723,17 +784,14 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
         const double *Y = &conic[3 * g];
         pairdec_t pd = pair_decision(&dec[4 * g], &mean2d_f[2 * g], p[0], p[1]);
         /* rounding guard of Q14: an fp32 sigma may come out negative near sigma = 0 */
-        if (pd.sigma <= o->amb_safety * pd.E_sigma) r.ambig = 1;
-        if (pd.sigma < 0) continue;                                           /* Q14 */
-        if (near_thr(pd.raw, amax, pd.r_alpha, o)) r.ambig = 1;
-        int clamped = !(pd.raw < amax);                                       /* Q13, Q24 */
+        if (decide(pd.sigma < 0, pd.sigma <= o->amb_safety * pd.E_sigma, flip, &r)) continue;   /* Q14 */
+        const int amb_clamp = near_thr(pd.raw, amax, pd.r_alpha, o);
+        int clamped = decide(!(pd.raw < amax), amb_clamp, flip, &r);                               /* Q13, Q24 */
         double alpha = clamped ? amax : pd.raw;
-        if (!clamped && near_thr(alpha, amin, pd.r_alpha, o)) r.ambig = 1;
-        if (alpha < amin) continue;                                           /* Q14 */
+        if (decide(alpha < amin, !clamped && near_thr(alpha, amin, pd.r_alpha, o), flip, &r)) continue;  /* Q14 */
         double nT = Tdec * (1.0 - alpha);
         double rT_next = rT + alpha * (clamped ? 2 * OR_U : pd.r_alpha) / (1.0 - alpha) + 2 * OR_U;
-        if (near_thr(nT, tmin, rT_next, o)) r.ambig = 1;
-        if (nT <= tmin) { r.end_li = i + 1; break; }                          /* Q15 */
+        if (decide(nT <= tmin, near_thr(nT, tmin, rT_next, o), flip, &r)) { r.end_li = i + 1; break; }  /* Q15 */
         Tdec = nT;
         /* values (fp64 projection): Delta, sigma, G; alpha = o_eff G unless clamped */
         double dx = mean2d[2 * g] - p[0], dy = mean2d[2 * g + 1] - p[1];
@@ -748,7 +806,7 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
         if (rec && r.ncontrib < rec_cap) {
             contrib_t *e = &rec[r.ncontrib];
             e->li = i; e->alpha = alpha; e->T = T; e->G = G; e->sigma = sigma; e->dx = dx; e->dy = dy;
-            e->clamped = clamped; e->delta = delta; e->qd = qd;
+            e->clamped = clamped; e->amb_clamp = amb_clamp; e->delta = delta; e->qd = qd;
         }
         r.eT += alpha * qd / (1.0 - alpha);
         for (int ch = 0; ch < D; ch++) r.rgb[ch] += rgb[D * g + ch] * alpha * T;   /* P:536-538 */
@@ -759,6 +817,7 @@ static pixres_t pixel_forward(const or_opts *o, const camlist_t *L, int64_t c, i
         r.ncontrib++;
     }
     r.T = T;
+    r.rT = rT;
     return r;
 }
 
@@ -775,7 +834,8 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                   const double *conic,
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   double *out_rgb, double *out_alpha, double *out_T, int64_t *out_last_gid,
-                  uint8_t *out_ambig, int32_t *out_ncontrib, const double *depth, double *out_depth)
+                  uint8_t *out_ambig, int32_t *out_ncontrib, const double *depth, double *out_depth,
+                  const uint32_t *flips)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
     const int D = n_channels(o);
@@ -796,14 +856,48 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 continue;
             }
             pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, depth,
-                                       NULL, 0);
+                                       NULL, 0, flips ? flips[oi] : 0u);
             for (int ch = 0; ch < D; ch++) out_rgb[D * oi + ch] = r.rgb[ch] + r.T * (b ? b[ch] : 0.0);  /* R3, Q25 */
             if (out_depth) out_depth[oi] = r.dacc;                                 /* no background term */
             out_alpha[oi] = 1.0 - r.T;
             out_T[oi] = r.T;
             out_last_gid[oi] = r.last_li >= 0 ? c * N + L.n[r.last_li] : -1;
-            if (out_ambig) out_ambig[oi] = (uint8_t)r.ambig;
+            if (out_ambig) out_ambig[oi] = (uint8_t)(r.ambig < 255 ? r.ambig : 255);
             if (out_ncontrib) out_ncontrib[oi] = (int32_t)r.ncontrib;
+        }
+        free_camlist(&L);
+    }
+    return 0;
+}
+
+/* One pixel per query (camera cams[q], pixel (pxs[q], pys[q])) under the decision
+ * outcomes flips[q] (see decide()): colour [D], T_final, the flat id of the last composited
+ * splat (-1 if none) and the number of ambiguous decisions met.  Used to enumerate every
+ * outcome an ambiguous pixel admits; the camera lists are built once per camera. */
+int or_render_pixels(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
+                     const float *mean2d_f, const float *depth_f, const float *dec, const double *mean2d,
+                     const double *conic, const double *opac_eff, const double *rgb, const double *bg,
+                     int64_t nq, const int32_t *cams, const int32_t *pxs, const int32_t *pys,
+                     const uint32_t *flips, double *out_rgb, double *out_T, int64_t *out_last_gid,
+                     int32_t *out_namb)
+{
+    const int D = n_channels(o);
+    for (int64_t c = 0; c < C; c++) {
+        int any = 0;
+        for (int64_t q = 0; q < nq; q++) any |= cams[q] == c;
+        if (!any) continue;
+        camlist_t L;
+        build_camlist(o, c, N, W, H, radii, mean2d_f, depth_f, &L);
+#pragma omp parallel for schedule(dynamic, 4)
+        for (int64_t q = 0; q < nq; q++) {
+            if (cams[q] != c) continue;
+            pixres_t r = pixel_forward(o, &L, c, N, pxs[q], pys[q], mean2d_f, dec, mean2d, conic, opac_eff, rgb,
+                                       NULL, NULL, 0, flips[q]);
+            const double *b = bg ? bg + D * c : NULL;
+            for (int ch = 0; ch < D; ch++) out_rgb[D * q + ch] = r.rgb[ch] + r.T * (b ? b[ch] : 0.0);
+            out_T[q] = r.T;
+            out_last_gid[q] = r.last_li >= 0 ? c * N + L.n[r.last_li] : -1;
+            out_namb[q] = r.ambig;
         }
         free_camlist(&L);
     }
@@ -824,7 +918,7 @@ int or_render_fwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
 /* Absgrad statistic).                                                */
 /* T_replay_err (optional) = max |T_replayed - T_forward| over all steps.      */
 /* ------------------------------------------------------------------------- */
-typedef struct { int32_t g; double v[10], va[10], vs[10]; } term_t;   /* [9]: v_depth */
+typedef struct { int32_t g; double v[10], va[10], vs[10], vd[9], rel; } term_t;   /* [9]: v_depth */
 
 int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, const int32_t *radii,
                   const float *mean2d_f, const float *depth_f, const float *dec, const double *mean2d,
@@ -832,13 +926,15 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                   const double *opac_eff, const double *rgb, const double *bg, const uint8_t *tile_mask,
                   const double *v_img, const double *v_alpha_img, double *v2d, double *a2d, double *s2d,
                   uint8_t *g_ambig, double *T_replay_err, const double *depth, const double *v_depth_img,
-                  double *vz, double *az, double *sz, double *vfeat, double *absg, double *afeat)
+                  double *vz, double *az, double *sz, double *vfeat, double *absg, double *afeat,
+                  const uint32_t *flips, int32_t *n2d, double *d2d, double *sfeat)
 {
     int T = o->tile_size, TX = (W + T - 1) / T, TY = (H + T - 1) / T;
     const int D = n_channels(o);
     memset(v2d, 0, sizeof(double) * 9 * C * N);
     if (vfeat) memset(vfeat, 0, sizeof(double) * D * C * N);
     if (afeat) memset(afeat, 0, sizeof(double) * D * C * N);
+    if (sfeat) memset(sfeat, 0, sizeof(double) * D * C * N);
     if (a2d) memset(a2d, 0, sizeof(double) * 9 * C * N);
     if (s2d) memset(s2d, 0, sizeof(double) * 9 * C * N);
     if (g_ambig) memset(g_ambig, 0, (size_t)C * N);
@@ -846,9 +942,16 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
     if (az) memset(az, 0, sizeof(double) * C * N);
     if (sz) memset(sz, 0, sizeof(double) * C * N);
     if (absg) memset(absg, 0, sizeof(double) * 2 * C * N);
+    if (n2d) memset(n2d, 0, sizeof(int32_t) * C * N);
+    if (d2d) memset(d2d, 0, sizeof(double) * 9 * C * N);
     const int with_depth = depth && v_depth_img;
     double max_err = 0;
     for (int64_t c = 0; c < C; c++) {
+        if (tile_mask) {   /* a camera without selected tiles contributes nothing */
+            int any = 0;
+            for (int64_t t = 0; t < (int64_t)TX * TY && !any; t++) any = tile_mask[c * TX * TY + t] != 0;
+            if (!any) continue;
+        }
         camlist_t L;
         build_camlist(o, c, N, W, H, radii, mean2d_f, depth_f, &L);
         int64_t P = (int64_t)W * H;
@@ -859,7 +962,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
             int px = (int)(pix % W), py = (int)(pix / W);
             if (!tile_selected(tile_mask, c, TX, TY, px, py, T)) continue;
             pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL,
-                                       NULL, 0);
+                                       NULL, 0, flips ? flips[c * P + pix] : 0u);
             cnt[pix] = (int32_t)r.ncontrib;
             if (r.ambig && g_ambig) {
                 /* mark every splat this pixel evaluated (in-tile, up to termination) */
@@ -895,7 +998,7 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     rec = (contrib_t *)realloc(rec, sizeof(contrib_t) * cap);
                 }
                 pixres_t r = pixel_forward(o, &L, c, N, px, py, mean2d_f, dec, mean2d, conic, opac_eff, rgb, NULL,
-                                           rec, cap);
+                                           rec, cap, flips ? flips[c * P + pix] : 0u);
                 int64_t oi = c * P + pix;
                 const double *vC = &v_img[D * oi];
                 double vA = v_alpha_img ? v_alpha_img[oi] : 0.0;
@@ -939,6 +1042,20 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
 
                     for (int ch = 0; ch < D; ch++) S[ch] += rgb[D * g + ch] * fac;  /* B5 */
                     Sd += z * fac;
+                    /* tolerance model: an ambiguous alpha_max decision (Q13/Q24) admits both B6
+                     * outcomes, clamped (no sigma / opacity gradient) and not; vd = the
+                     * magnitude of the difference, i.e. of the unclamped B6 terms */
+                    for (int j = 0; j < 9; j++) tm->vd[j] = 0;
+                    if (e->amb_clamp) {
+                        double vs_ = opac_eff[g] * e->G * fabs(v_alpha);
+                        const double *Y = &conic[3 * g];
+                        tm->vd[8] = e->G * fabs(v_alpha);
+                        tm->vd[2] = vs_ * 0.5 * e->dx * e->dx;
+                        tm->vd[3] = vs_ * fabs(e->dx * e->dy);
+                        tm->vd[4] = vs_ * 0.5 * e->dy * e->dy;
+                        tm->vd[0] = vs_ * fabs(Y[0] * e->dx + Y[1] * e->dy);
+                        tm->vd[1] = vs_ * fabs(Y[1] * e->dx + Y[2] * e->dy);
+                    }
                     if (!e->clamped) {                                           /* B6 (Q24) */
                         tm->v[8] = e->G * v_alpha;
                         double v_sigma = -opac_eff[g] * e->G * v_alpha;
@@ -970,8 +1087,12 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                     /* ... and through alpha (this splat's qd, all splats' via T and S) */
                     for (int j = 0; j < 10; j++) {
                         if (j >= 5) tm->vs[j] = 0;   /* rgb, opacity, depth: only the alpha path */
-                        tm->vs[j] += tm->va[j] * (e->qd + r.eT);
+                        /* + the fp32 rounding of the T recurrence (1 - alpha amplifies it near
+                         * alpha_max): every T the kernel forms, forward or recovered backward
+                         * from T_final, is within the pixel's r_T of the exact one */
+                        tm->vs[j] += tm->va[j] * (e->qd + r.eT + r.rT);
                     }
+                    tm->rel = e->qd + r.eT + r.rT;
                 }
                 errs[pix] = err;
             }
@@ -986,6 +1107,9 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 if (s2d) s2d[9 * (int64_t)g + j] += terms[i].vs[j];
             }
             if (vz) vz[g] += terms[i].v[9];
+            if (n2d) n2d[g] += 1;   /* tolerance model: terms summed into g (atomic-order bound) */
+            if (d2d)
+                for (int j = 0; j < 9; j++) d2d[9 * (int64_t)g + j] += terms[i].vd[j];
             /* Absgrad (App. Absgrad): per-pixel absolute view-space gradients */
             if (absg) {
                 absg[2 * (int64_t)g + 0] += fabs(terms[i].v[0]);
@@ -995,6 +1119,8 @@ int or_render_bwd(const or_opts *o, int32_t C, int64_t N, int32_t W, int32_t H, 
                 for (int ch = 0; ch < D; ch++) vfeat[(int64_t)g * D + ch] += tvf[i * D + ch];
             if (tvf && afeat)   /* tolerance model: sum over pixels of |fac v_C| per channel */
                 for (int ch = 0; ch < D; ch++) afeat[(int64_t)g * D + ch] += fabs(tvf[i * D + ch]);
+            if (tvf && sfeat)   /* ... times the relative sensitivity of fac = alpha T (as vs for rgb) */
+                for (int ch = 0; ch < D; ch++) sfeat[(int64_t)g * D + ch] += fabs(tvf[i * D + ch]) * terms[i].rel;
             if (az) az[g] += terms[i].va[9];
             if (sz) sz[g] += terms[i].vs[9];
         }
@@ -1048,6 +1174,8 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
             if (radii[2 * idx] <= 0 || radii[2 * idx + 1] <= 0) continue;
             double vg[9];
             for (int j = 0; j < 9; j++) vg[j] = AV(v2d[9 * idx + j]);
+            if (absmode == 2)   /* only the colour channels (the SH clamp alternative below) */
+                vg[0] = vg[1] = vg[2] = vg[3] = vg[4] = vg[8] = 0;
             proj64_t P;
             project64(o, W, H, means + 3 * n, quats + 4 * n, scales + 3 * n, opacities[n],
                       colors + stride * n, K, viewmats + 16 * c, Ks + 9 * c, &P);
@@ -1141,10 +1269,21 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
             if (o->sh_degree >= 0) {
                 int deg = o->sh_degree, nb = (deg + 1) * (deg + 1);
                 double Yb[16], dY[16][3];
-                sh_basis(deg, P.dir[0], P.dir[1], P.dir[2], Yb);
-                sh_basis_grad(deg, P.dir[0], P.dir[1], P.dir[2], dY);
+                if (absmode) {
+                    sh_basis_mag(deg, P.dir[0], P.dir[1], P.dir[2], Yb, dY);
+                } else {
+                    sh_basis(deg, P.dir[0], P.dir[1], P.dir[2], Yb);
+                    sh_basis_grad(deg, P.dir[0], P.dir[1], P.dir[2], dY);
+                }
                 double vraw[3];
-                for (int ch = 0; ch < 3; ch++) vraw[ch] = P.raw[ch] > 0 ? vrgb[ch] : 0.0;
+                for (int ch = 0; ch < 3; ch++) {
+                    int on = P.raw[ch] > 0;   /* colour = max(0, raw): no gradient where clamped (Q22) */
+                    /* absmode 2 (tolerance model): the channels whose clamp decision lies within
+                     * the fp32 rounding of raw (64 u of its term magnitudes) admit both outcomes;
+                     * the bound of the alternative is the full magnitude of their path */
+                    if (absmode == 2) on = fabs(P.raw[ch]) <= 64 * OR_U * P.rawabs[ch];
+                    vraw[ch] = on ? vrgb[ch] : 0.0;
+                }
                 double vdir[3] = {0, 0, 0};
                 for (int j = 0; j < nb; j++) {
                     double shv = 0;
@@ -1167,7 +1306,7 @@ int or_project_bwd(const or_opts *o, int64_t N, int32_t C, int32_t W, int32_t H,
                             vW[4 * k + i] += ve[i] * P.w[k];
                             vW[4 * k + 3] += P.Wr[k][i] * ve[i];
                         }
-            } else {
+            } else if (absmode != 2) {   /* direct colours: no clamp, no alternative */
                 for (int ch = 0; ch < 3; ch++) gc[ch] += vrgb[ch];
             }
             /* P8: Sigma = M M^T -> v_M = (vS + vS^T) M; M = R S -> v_R = v_M S, v_s */

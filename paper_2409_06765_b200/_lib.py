@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 8
+ABI_VERSION = 9
 # largest item / record count of one call: ids and capacities are int32 (include/gs.h)
 MAX_ITEMS = (1 << 31) - 2048
 
@@ -49,7 +49,7 @@ SIGNATURES = {
     "gs_isect_workspace_size": (_SZ, [_I32, _I64, _I32, _I32, _I64]),
     "gs_isect_tiles": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "gs_rasterize_fwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
-    "gs_rasterize_stats": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P]),
+    "gs_rasterize_stats": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P,
                                 _P, _P]),
     "gs_project_bwd_workspace_size": (_SZ, [_I64, _I32]),
@@ -173,11 +173,13 @@ def gs_rasterize_fwd(o, C, N, width, height, splats, backgrounds, isect_ids, til
           "gs_rasterize_fwd")
 
 
-def gs_rasterize_stats(o, C, N, width, height, splats, isect_ids, tile_offsets, n_eval, n_contrib, stream=None):
+def gs_rasterize_stats(o, C, N, width, height, splats, isect_ids, tile_offsets, n_eval, n_contrib, terminated=None,
+                       stream=None):
     check(lib().gs_rasterize_stats(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
                                    ptr(isect_ids, torch.int32, "isect_ids"),
                                    ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(n_eval, torch.int32, "n_eval"),
-                                   ptr(n_contrib, torch.int32, "n_contrib"), stream_ptr(stream)),
+                                   ptr(n_contrib, torch.int32, "n_contrib"), ptr(terminated, torch.int32, "terminated"),
+                                   stream_ptr(stream)),
           "gs_rasterize_stats")
 
 

@@ -154,12 +154,13 @@ gs_status gs_rasterize_fwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
 
 gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                              const float* splats, const int32_t* isect_ids, const int32_t* tile_offsets,
-                             int32_t* n_eval, int32_t* n_contrib, void* stream) {
+                             int32_t* n_eval, int32_t* n_contrib, int32_t* terminated, void* stream) {
     GS_TRY(check_opts(opt));
     GS_TRY(check_raster_dims(opt, N, C, width, height));
     GS_REQ(tile_offsets && n_eval && n_contrib);
-    GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(n_eval) && aligned4(n_contrib));
+    GS_REQ(aligned16(splats) && aligned4(isect_ids) && aligned4(n_eval) && aligned4(n_contrib) && aligned4(terminated));
     return gsb::launch_raster_stats(*opt, C, N, width, height, splats, isect_ids, tile_offsets, n_eval, n_contrib,
+                                    terminated,
                                     static_cast<cudaStream_t>(stream));
 }
 

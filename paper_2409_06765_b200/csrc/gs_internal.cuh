@@ -110,7 +110,7 @@ gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H,
                             uint16_t* isect_masks, cudaStream_t s);
 gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                               const int32_t* ids, const int32_t* offs, int32_t* n_eval, int32_t* n_contrib,
-                              cudaStream_t s);
+                              int32_t* terminated, cudaStream_t s);
 gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                             const float* bg, const int32_t* ids, const int32_t* offs, const float* out_T,
                             const int32_t* last_ids, const float* v_rgb, const float* v_alpha,

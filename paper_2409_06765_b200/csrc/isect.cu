@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocksums(int* data, int 
     // the total (M can exceed 2^31 when a call overflows its capacity) is summed in int64; the
     // int32 block offsets saturate just past the capacity, so every position they lead to is
     // >= the clamped count and nothing is emitted there (the overflow flag reports it)
-    const int64_t sat = min(ovf_cap, (int64_t)INT32_MAX - 1) + 1;
+    const int64_t sat = overflow ? min(ovf_cap, (int64_t)INT32_MAX - 1) + 1 : (int64_t)INT32_MAX;
     int64_t carry = 0;
     for (int r = 0; r < nb; r += kScanThreads) {
         const int i = r + threadIdx.x;

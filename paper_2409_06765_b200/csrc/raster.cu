@@ -185,6 +185,7 @@ struct RasterParams {
     // diagnostics (gs_rasterize_stats)
     int32_t* n_eval;
     int32_t* n_contrib;
+    int32_t* n_term;
     // support masks of every staged (intersection) slot, written by K6 and read back by K7
     // (NULL: K7 recomputes them)
     uint16_t* smask;
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, dacc = 0.f;
     int last = start - 1;
     bool done = !inside;
-    int n_eval = 0, n_contrib = 0;
+    int n_eval = 0, n_contrib = 0, terminated = 0;
     float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;   // pixel centre
     asm volatile("" : "+f"(fpx), "+f"(fpy));
     const float amax = p.alpha_max, amin = p.alpha_min, tmin = p.t_min;
@@ -403,6 +404,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             const float nT = __fmul_rn(T, __fsub_rn(1.f, alpha));
             if (nT <= tmin) {   // Q15: stop without compositing this splat
                 done = true;
+                if (STATS) terminated = 1;
                 break;
             }
             const float w = __fmul_rn(alpha, T);
@@ -422,6 +424,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         if (inside) {
             p.n_eval[pix] = n_eval;
             p.n_contrib[pix] = n_contrib;
+            if (p.n_term) p.n_term[pix] = terminated;
         }
         return;
     }
@@ -778,9 +781,9 @@ gs_status launch_raster_fwd(const gs_options& o, int C, int64_t N, int W, int H,
 
 gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                               const int32_t* ids, const int32_t* offs, int32_t* n_eval, int32_t* n_contrib,
-                              cudaStream_t s) {
+                              int32_t* terminated, cudaStream_t s) {
     RasterParams p = make_params(o, C, N, W, H, splats, nullptr, ids, offs);
-    p.n_eval = n_eval; p.n_contrib = n_contrib;
+    p.n_eval = n_eval; p.n_contrib = n_contrib; p.n_term = terminated;
     dim3 grid(p.TX * p.TY, C);
     launch_pdl(k_raster_fwd<true, false, false>, dim3(grid), dim3(kThreads), s, p);
     GS_LAUNCH_CHECK("k_raster_fwd<stats>");

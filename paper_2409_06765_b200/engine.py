@@ -9,8 +9,10 @@ the five stages of include/gs.h on a CUDA stream without any host synchronisatio
 The intersection count M is data dependent.  The engine keeps an M capacity; the
 isect stage writes M and an overflow flag on the device, and `ensure_capacity()` (one
 small device->host read) grows the capacity and tells the caller to re-run when the
-flag is set.  In steady state (bench.py, CUDA-graph replay) the flag is checked after
-the timed region only.  With packed=True (Q29) only the visible (camera, Gaussian) pairs
+flag is set.  In steady state (bench.py) the flag is checked after the timed region only.
+`capture()` records one step into a CUDA graph (every stage is a kernel launch on the
+current stream, programmatic dependent launch edges included) and `replay()` re-issues it
+with one call: the inputs are read from, and the outputs written to, the same buffers.  With packed=True (Q29) only the visible (camera, Gaussian) pairs
 are stored: the projection writes nnz device-side and the per-item buffers are sized by
 an nnz capacity handled the same way as M.  Parameter gradients land in ONE flat fp32 buffer (`flat_grad`)
 so the data-parallel gradient sum is a single collective.
@@ -214,6 +216,25 @@ class Engine:
         params = (means, quats, scales, opacities, colors, viewmats, Ks)."""
         self.forward(*params, backgrounds=backgrounds, stream=stream)
         self.backward(*params, v_rgb, v_alpha, backgrounds, v_depth, stream)
+
+    def capture(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None):
+        """Record one step() on these exact tensors into a CUDA graph (the capacities must
+        already fit: run run_checked() first).  Returns the graph; replay() launches it."""
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.step(params, v_rgb, v_alpha, backgrounds, v_depth)   # warm-up on the capture stream
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.graph(self.graph, stream=s):
+            self.step(params, v_rgb, v_alpha, backgrounds, v_depth)
+        torch.cuda.synchronize(self.device)
+        return self.graph
+
+    def replay(self):
+        """One captured step (capture()); the overflow flag must be checked as after step()."""
+        self.graph.replay()
 
     def run_checked(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None):
         """step() with capacity growth (syncs once to read the overflow flag)."""
