@@ -142,6 +142,17 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
 #pragma unroll
         for (int i = 0; i < 12; i++) pw[i] = 0.f;
         if (vis) {
+#ifndef GS_PBWD_PREFETCH
+#define GS_PBWD_PREFETCH 1
+#endif
+            if (GS_PBWD_PREFETCH && DEG > 0 && !seen) {
+                // the SH row (12K floats) is needed only after the geometry chain below: start
+                // bringing its cache lines into L2 now, so its loads overlap that arithmetic
+                const char* row = reinterpret_cast<const char*>(src);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 96));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(row + NB * 12 - 4));
+            }
             seen = true;
             const float4* vr = reinterpret_cast<const float4*>(p.v_splats + idx * GS_SPLAT_FLOATS);
             const float4 v0 = vr[0], v1 = vr[1], v2 = vr[2];
