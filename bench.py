@@ -210,8 +210,19 @@ def run_ours(args):
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
+    # the five calls of one step are captured once into a CUDA graph (Engine.capture) and
+    # replayed -- the same kernels on the same buffers, one launch call per step; the
+    # gradient all-reduce (N > 1) runs after it on the same stream.  --eager launches the
+    # calls one by one (also reported as a variant below).
+    use_graph = not args.eager
+    if use_graph:
+        eng.capture(params, v_dev)
+
     def step():
-        eng.step(params, v_dev)
+        if use_graph:
+            eng.replay()
+        else:
+            eng.step(params, v_dev)
         if world > 1:
             dist.all_reduce(eng.flat_grad)
 
@@ -402,24 +413,33 @@ def run_ours(args):
                                   "M_isect": e2.n_isect, "note": "opacity-aware tile extent (DESIGN Q36): "
                                   "images and gradients identical to the 3-sigma box"}
         del e2
-        # the same step captured once into a CUDA graph and replayed (Engine.capture)
-        eng.capture(params, v_dev)
+        # the other launch mode on the same inputs: eager (five C-ABI calls per step) when the
+        # headline replays the CUDA graph, and vice versa
+        if use_graph:
+            def other():
+                eng.step(params, v_dev)
+        else:
+            eng.capture(params, v_dev)
+
+            def other():
+                eng.replay()
         for _ in range(args.warmup):
-            eng.replay()
+            other()
         evg = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         torch.cuda.synchronize(dev)
         for i in range(args.steps):
             flush.zero_()
             evg[i][0].record(stream)
-            eng.replay()
+            other()
             evg[i][1].record(stream)
         torch.cuda.synchronize(dev)
         if int(eng.overflow.item()) != 0:
-            raise RuntimeError("intersection capacity overflowed (CUDA-graph variant)")
+            raise RuntimeError("intersection capacity overflowed (launch-mode variant)")
         msg = float(np.sum([a.elapsed_time(b) for a, b in evg])) / args.steps
-        variants["cuda_graph"] = {"value": round(mp_per_step / (msg / 1e3), 3), "ms_per_step": round(msg, 4),
-                                  "note": "one captured step replayed (same kernels, same buffers)"}
-        eng.graph = None
+        variants["eager" if use_graph else "cuda_graph"] = {
+            "value": round(mp_per_step / (msg / 1e3), 3), "ms_per_step": round(msg, 4),
+            "note": "five C-ABI calls launched per step" if use_graph else "one captured step replayed"}
+    eng.graph = None
 
     # ---- BASELINE configs[2] as strong scaling: its 8 views split over the N ranks (the
     # same total work at every N; E(R) = t(1) / (R t(R)) from the per-N records) ----
@@ -442,6 +462,7 @@ def run_ours(args):
         "config": {"workload": f"{cfg_name}: {N} Gaussians SH{sc['sh_degree']}, {args.views_per_gpu} view(s) of "
                                f"{W}x{H} per GPU (BASELINE {CFG_INDEX.get(cfg_name, '?')})", "global_batch_views": C * world,
                    "width": W, "height": H, "n_gaussians": N, "parallelism": f"views dp{world}",
+                   "launch": "cuda-graph replay of the captured step" if use_graph else "eager C-ABI calls",
                    "bbox_mode": args.bbox_mode, "packed": mode_kw["packed"],
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
                    "V_visible": V, "M_isect": M, "pairs_eval": E_f, "pairs_contrib": E_c},
@@ -707,6 +728,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="launch the five calls per step instead of replaying "
+                                                         "the captured CUDA graph")
     ap.add_argument("--no-strong", action="store_true", help="skip the configs[2] strong-scaling leg")
     ap.add_argument("--strong-steps", type=int, default=10)
     ap.add_argument("--packed", action="store_true", help="packed (visible-only) per-item layout (Q29)")

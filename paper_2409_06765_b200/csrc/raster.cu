@@ -47,9 +47,11 @@ __device__ __forceinline__ float4 lds4(uint32_t addr) {
     return v;
 }
 
-// Pre-scaled conic: p = a' dx^2 + c' dy^2 + b' dx dy = -sigma * log2(e)
+// Pre-scaled conic: p = a' dx^2 + c' dy^2 + b' dx dy = -sigma * log2(e); the w lane
+// holds b'/2, which the backward's d sigma / d mu' uses (one FFMA per component)
 __device__ __forceinline__ float4 prescale_conic(float A, float B, float C) {
-    return make_float4(__fmul_rn(-0.5f * kLog2e, A), __fmul_rn(-kLog2e, B), __fmul_rn(-0.5f * kLog2e, C), 0.f);
+    return make_float4(__fmul_rn(-0.5f * kLog2e, A), __fmul_rn(-kLog2e, B), __fmul_rn(-0.5f * kLog2e, C),
+                       __fmul_rn(-0.5f * kLog2e, B));
 }
 
 // alpha of one (pixel, splat) pair; returns false when the pair is skipped (sigma < 0 or
@@ -666,10 +668,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             g8[4] = v_sigma * xy;
             g8[5] = hv * yy;
             // d sigma / d mu' = Sigma'^-1 Delta, with the conic recovered from the
-            // pre-scaled one: A = a' (-2 ln2), B = b' (-ln2), C = c' (-2 ln2)
-            const float k2 = -kLn2 * v_sigma;
-            g8[0] = k2 * (2.f * con.x * dx + con.y * dy);
-            g8[1] = k2 * (con.y * dx + 2.f * con.z * dy);
+            // pre-scaled one: A = a' (-2 ln2), B = b' (-ln2) = (b'/2)(-2 ln2), C = c' (-2 ln2)
+            const float k2 = (-2.f * kLn2) * v_sigma;
+            g8[0] = k2 * (con.x * dx + con.w * dy);
+            g8[1] = k2 * (con.w * dx + con.z * dy);
             const int32_t sid = DEPTH ? s.id[j] : __float_as_int(xyo.w);
             float* dst = p.v_splats + (int64_t)sid * GS_SPLAT_FLOATS;
             if (FEAT) {
