@@ -181,6 +181,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2409_06765_b200 import Engine, _lib as L
+    from paper_2409_06765_b200.engine import DPEngine
 
     world, rank, local = _dist_env()
     if world > 1:
@@ -200,7 +201,17 @@ def run_ours(args):
     from synth import scenes as S
     cfgd = S.CONFIGS[cfg_name]
     mode_kw = dict(antialiased=bool(cfgd.get("antialiased", 0)), packed=bool(cfgd.get("packed", 0)) or args.packed)
-    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=args.bbox_mode, **mode_kw)
+    # N > 1: the gradient lives in buckets whose all-reduces overlap the projection backward
+    # of the next bucket (DPEngine); N = 1 has no collective
+    bucketed = world > 1 and args.buckets > 1 and not mode_kw["packed"]
+
+    def make_engine(**kw):
+        if bucketed:
+            return DPEngine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=args.bbox_mode,
+                            buckets=args.buckets, **mode_kw, **kw)
+        return Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, bbox_mode=args.bbox_mode, **mode_kw, **kw)
+
+    eng = make_engine()
     stream = torch.cuda.current_stream(dev)
 
     # size the intersection capacity once (one sync), outside any timed region
@@ -216,9 +227,17 @@ def run_ours(args):
     # calls one by one (also reported as a variant below).
     use_graph = not args.eager
     if use_graph:
-        eng.capture(params, v_dev)
+        eng.capture(params, v_dev, head_only=bucketed)
 
     def step():
+        if bucketed:
+            if use_graph:
+                eng.replay()
+            else:
+                eng.forward(*params)
+                eng.rasterize_bwd(v_dev)
+            eng.backward_allreduce(params)
+            return
         if use_graph:
             eng.replay()
         else:
@@ -335,8 +354,7 @@ def run_ours(args):
     e2e = None
     engs = d_in = d_v = None
     if not args.no_e2e:
-        engs = [eng, Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, M_capacity=eng.cap, **mode_kw,
-                             bbox_mode=args.bbox_mode)]
+        engs = [eng, make_engine(M_capacity=eng.cap)]
         d_in = [list(params), [t.clone() for t in params]]
         d_v = [v_dev, v_dev.clone()]
         engs[1].run_checked(tuple(d_in[1]), d_v[1])
@@ -366,9 +384,15 @@ def run_ours(args):
             stream.wait_event(ev_h2d[i])
             if i >= 2:
                 stream.wait_event(ev_d2h[i - 2])           # its previous results were read out
-            engs[bsel].step(tuple(d_in[bsel]), d_v[bsel])
-            if world > 1:
-                dist.all_reduce(engs[bsel].flat_grad)
+            if bucketed:
+                e_ = engs[bsel]
+                e_.forward(*d_in[bsel])
+                e_.rasterize_bwd(d_v[bsel])
+                e_.backward_allreduce(tuple(d_in[bsel]))
+            else:
+                engs[bsel].step(tuple(d_in[bsel]), d_v[bsel])
+                if world > 1:
+                    dist.all_reduce(engs[bsel].flat_grad)
             ev_cmp[i].record(stream)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev_cmp[i])
@@ -439,6 +463,37 @@ def run_ours(args):
         variants["eager" if use_graph else "cuda_graph"] = {
             "value": round(mp_per_step / (msg / 1e3), 3), "ms_per_step": round(msg, 4),
             "note": "five C-ABI calls launched per step" if use_graph else "one captured step replayed"}
+
+    # ---- N > 1: the overlap the gradient buckets achieve -- the same step with the projection
+    # backward run whole and ONE all-reduce after it (serial), device-timed, max over ranks ----
+    overlap = None
+    if bucketed:
+        def serial():
+            if use_graph:
+                eng.replay()
+            else:
+                eng.forward(*params)
+                eng.rasterize_bwd(v_dev)
+            eng.project_bwd(*params)
+            dist.all_reduce(eng.flat_grad)
+        for _ in range(args.warmup):
+            serial()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            serial()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([float(np.sum([a.elapsed_time(b) for a, b in evs]))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_serial = float(t.item()) / args.steps
+        overlap = {"buckets": args.buckets, "ms_per_step_overlapped": round(ms_per_step, 4),
+                   "ms_per_step_serial": round(ms_serial, 4), "saved_ms": round(ms_serial - ms_per_step, 4),
+                   "allreduce_bytes": int(eng.flat_grad.numel() * 4)}
+
     eng.graph = None
 
     # ---- BASELINE configs[2] as strong scaling: its 8 views split over the N ranks (the
@@ -469,7 +524,7 @@ def run_ours(args):
         "workload": {k: v for k, v in wl.items() if k not in ("E_f", "E_c")},
         "roofline": roof, "stages": per_stage, "step": step_stats, "gpu_launches": launches * args.steps,
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "variants": variants,
-        "strong_batch3m": strong, "allreduce": ar,
+        "strong_batch3m": strong, "allreduce": ar, "allreduce_overlap": overlap,
     }
     if rank == 0:
         print(json.dumps(res), flush=True)
@@ -497,13 +552,27 @@ def run_strong(args, world, rank, dev, flush, cfg_name="batch3m", total_views=8)
     keys = ["means", "quats", "scales", "opacities", "colors", "viewmats", "Ks"]
     params = tuple(torch.from_numpy(np.ascontiguousarray(sc[k], np.float32)).to(dev) for k in keys)
     v_dev = torch.from_numpy(np.ascontiguousarray(v_img[views[0]:views[-1] + 1])).to(dev)
-    eng = Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev)
+    from paper_2409_06765_b200.engine import DPEngine
+    bucketed = world > 1 and args.buckets > 1
+    eng = (DPEngine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev, buckets=args.buckets) if bucketed
+           else Engine(N, C, W, H, sh_degree=sc["sh_degree"], device=dev))
     eng.run_checked(params, v_dev)
     stream = torch.cuda.current_stream(dev)
+    if not args.eager:
+        eng.capture(params, v_dev, head_only=bucketed)
 
-    def step():
-        eng.step(params, v_dev)
-        if world > 1:
+    def step():   # the main step's launch mode: graph replay (head only when bucketed) + collective
+        if args.eager:
+            if bucketed:
+                eng.forward(*params)
+                eng.rasterize_bwd(v_dev)
+            else:
+                eng.step(params, v_dev)
+        else:
+            eng.replay()
+        if bucketed:
+            eng.backward_allreduce(params)
+        elif world > 1:
             dist.all_reduce(eng.flat_grad)
 
     for _ in range(3):
@@ -534,6 +603,7 @@ def run_strong(args, world, rank, dev, flush, cfg_name="batch3m", total_views=8)
            "value": round(total_views * W * H / 1e6 / (ms_step / 1e3), 3), "unit": UNIT,
            "allreduce_bytes": int(eng.flat_grad.numel() * 4) if world > 1 else 0, "M_isect_rank0": eng.n_isect,
            "note": "E(R) = ms_per_step(1 GPU) / (R ms_per_step(R GPUs)), from the per-N records"}
+    eng.graph = None
     del eng
     torch.cuda.empty_cache()
     return out
@@ -731,6 +801,8 @@ def main(argv=None):
     ap.add_argument("--eager", action="store_true", help="launch the five calls per step instead of replaying "
                                                          "the captured CUDA graph")
     ap.add_argument("--no-strong", action="store_true", help="skip the configs[2] strong-scaling leg")
+    ap.add_argument("--buckets", type=int, default=4, help="N > 1: gradient buckets whose all-reduces overlap "
+                                                           "the projection backward (1: one all-reduce after it)")
     ap.add_argument("--strong-steps", type=int, default=10)
     ap.add_argument("--packed", action="store_true", help="packed (visible-only) per-item layout (Q29)")
     ap.add_argument("--bbox-mode", type=int, default=0, choices=[0, 1, 2],

@@ -215,6 +215,22 @@ GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, i
  *      (deterministic).
  * v_colors (and colors) may be NULL when sh_degree == -1 (N-D feature mode). */
 GS_API size_t gs_project_bwd_workspace_size(int64_t N, int32_t C);
+
+/* ---- Stage 4b over a range of Gaussians (data-parallel gradient buckets) ----
+ * gs_project_bwd for the Gaussians [n_begin, n_end) only (0 <= n_begin <= n_end <= N):
+ * inputs are the full arrays of gs_project_bwd (means [N,3] ..., radii / v_splats [C,N,...]);
+ * the OUTPUTS are the range's own rows -- v_means[(n - n_begin)*3 ...], v_quats, v_scales,
+ * v_opacities, v_colors -- so each range can write into its own contiguous bucket and that
+ * bucket's all-reduce overlaps the next range's launch.  Per-Gaussian arithmetic, camera sum
+ * and results are gs_project_bwd's, bit for bit.  Dense layout; no pose gradients (use
+ * gs_project_bwd).  v_colors and colors must be 16-byte aligned for the vector SH path
+ * (else the scalar one). */
+GS_API gs_status gs_project_bwd_range(const gs_options* opt, int64_t N, int64_t n_begin, int64_t n_end, int32_t C,
+                                      int32_t width, int32_t height, const float* means, const float* quats,
+                                      const float* scales, const float* opacities, const float* colors, int32_t K,
+                                      const float* viewmats, const float* Ks, const int32_t* radii,
+                                      const float* v_splats, float* v_means, float* v_quats, float* v_scales,
+                                      float* v_opacities, float* v_colors, void* stream);
 GS_API gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t width, int32_t height,
                          const float* means, const float* quats, const float* scales,
                          const float* opacities, const float* colors, int32_t K,

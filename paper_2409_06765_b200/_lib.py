@@ -55,6 +55,8 @@ SIGNATURES = {
     "gs_project_bwd_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                               _P, _P, _P, _P, _SZ, _P]),
+    "gs_project_bwd_range": (_I32, [_P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P,
+                                    _P, _P, _P, _P, _P, _P]),
     "gs_rasterize_fwd_nd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "gs_rasterize_bwd_nd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _I32, _P, _I64, _P, _P, _P, _P, _P, _P, _P,
                                    _I32, _P, _P, _P, _P]),
@@ -214,6 +216,22 @@ def gs_project_bwd(o, means, quats, scales, opacities, colors, K, viewmats, Ks, 
                                ptr(workspace, torch.uint8, "ws"), 0 if workspace is None else workspace.numel(),
                                stream_ptr(stream)),
           "gs_project_bwd")
+
+
+def gs_project_bwd_range(o, n_begin, n_end, means, quats, scales, opacities, colors, K, viewmats, Ks, width, height,
+                         radii, v_splats, v_means, v_quats, v_scales, v_opacities, v_colors, stream=None):
+    """gs_project_bwd for the Gaussians [n_begin, n_end): the v_* tensors are that range's own
+    rows (e.g. one gradient bucket)."""
+    N, C = means.shape[0], viewmats.shape[0]
+    check(lib().gs_project_bwd_range(ct.byref(o), N, n_begin, n_end, C, width, height, ptr(means, name="means"),
+                                     ptr(quats, name="quats"), ptr(scales, name="scales"),
+                                     ptr(opacities, name="opacities"), ptr(colors, name="colors"), K,
+                                     ptr(viewmats, name="viewmats"), ptr(Ks, name="Ks"),
+                                     ptr(radii, torch.int32, "radii"), ptr(v_splats, name="v_splats"),
+                                     ptr(v_means, name="v_means"), ptr(v_quats, name="v_quats"),
+                                     ptr(v_scales, name="v_scales"), ptr(v_opacities, name="v_opacities"),
+                                     ptr(v_colors, name="v_colors"), stream_ptr(stream)),
+          "gs_project_bwd_range")
 
 
 # ---- packed mode (Q29) ------------------------------------------------------------------

@@ -212,6 +212,28 @@ gs_status gs_project_bwd(const gs_options* opt, int64_t N, int32_t C, int32_t wi
                                    static_cast<cudaStream_t>(stream));
 }
 
+gs_status gs_project_bwd_range(const gs_options* opt, int64_t N, int64_t n_begin, int64_t n_end, int32_t C,
+                               int32_t width, int32_t height, const float* means, const float* quats,
+                               const float* scales, const float* opacities, const float* colors, int32_t K,
+                               const float* viewmats, const float* Ks, const int32_t* radii, const float* v_splats,
+                               float* v_means, float* v_quats, float* v_scales, float* v_opacities, float* v_colors,
+                               void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_REQ(opt->packed == 0);
+    GS_TRY(check_dims(N, C, width, height));
+    GS_REQ(0 <= n_begin && n_begin <= n_end && n_end <= N);
+    if (n_end > n_begin) {
+        GS_REQ(means && quats && scales && opacities && viewmats && Ks && radii && v_splats && v_means &&
+               v_quats && v_scales && v_opacities && (opt->sh_degree < 0 || (colors && v_colors)));
+        GS_REQ(aligned16(quats) && aligned16(v_quats) && aligned16(v_splats) && aligned8(radii) && aligned4(means) &&
+               aligned4(v_means) && aligned4(colors) && aligned4(v_colors) && aligned4(scales) && aligned4(v_scales));
+        if (opt->sh_degree >= 0) GS_REQ(K >= (opt->sh_degree + 1) * (opt->sh_degree + 1));
+    }
+    return gsb::launch_project_bwd_range(*opt, N, n_begin, n_end, C, width, height, means, quats, scales, opacities,
+                                         colors, opt->sh_degree >= 0 ? K : 1, viewmats, Ks, radii, v_splats, v_means,
+                                         v_quats, v_scales, v_opacities, v_colors, static_cast<cudaStream_t>(stream));
+}
+
 // ---- N-D features ------------------------------------------------------
 
 gs_status gs_rasterize_fwd_nd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,

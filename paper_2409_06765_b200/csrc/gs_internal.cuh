@@ -90,6 +90,11 @@ gs_status launch_project_packed(const gs_options& o, int64_t N, int C, int W, in
                                 int32_t* overflow, int32_t* camera_ids, int32_t* gaussian_ids, int32_t* radii,
                                 float* splats, void* ws, cudaStream_t s);
 size_t project_bwd_packed_workspace_bytes(int64_t N, int C);
+gs_status launch_project_bwd_range(const gs_options& o, int64_t N, int64_t n_begin, int64_t n_end, int C, int W,
+                                   int H, const float* means, const float* quats, const float* scales,
+                                   const float* opac, const float* colors, int K, const float* viewmats,
+                                   const float* Ks, const int32_t* radii, const float* v_splats, float* v_means,
+                                   float* v_quats, float* v_scales, float* v_opac, float* v_colors, cudaStream_t s);
 gs_status launch_project_bwd_packed(const gs_options& o, int64_t N, int C, int W, int H, const float* means,
                                     const float* quats, const float* scales, const float* opac,
                                     const float* colors, int K, const float* viewmats, const float* Ks,

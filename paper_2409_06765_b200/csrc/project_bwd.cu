@@ -20,6 +20,7 @@ constexpr int kThreads = 128;
 
 struct PBParams {
     int64_t N;
+    int64_t n_begin, n_end;   // the Gaussians [n_begin, n_end) of this launch; outputs row n - n_begin
     int C, W, H, K;
     float eps2d;
     int antialiased, fov_clamp;
@@ -84,10 +85,11 @@ template <int DEG, bool POSE>
 __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams p) {
     pdl_trigger();
     pdl_wait();
-    const int64_t n0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    const bool active = n0 < p.N;
+    const int64_t n0 = p.n_begin + (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const bool active = n0 < p.n_end;
     if (!POSE && !active) return;   // without POSE there is no block-level synchronisation below
-    const int64_t n = active ? n0 : p.N - 1;   // POSE: idle threads read a valid row, contribute nothing
+    const int64_t n = active ? n0 : p.n_end - 1;   // POSE: idle threads read a valid row, contribute nothing
+    const int64_t no = n - p.n_begin;              // output row (a chunk's outputs start at n_begin)
     constexpr int NB = DEG < 0 ? 1 : (DEG + 1) * (DEG + 1);
     __shared__ float s_pose[POSE ? kThreads / 32 : 1][12];
 
@@ -425,23 +427,23 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
         oq = make_float4(0.f, 0.f, 0.f, 0.f);
         gsc[0] = gsc[1] = gsc[2] = 0.f;
     }
-    reinterpret_cast<float4*>(p.v_quats)[n] = oq;
+    reinterpret_cast<float4*>(p.v_quats)[no] = oq;
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-        p.v_means[3 * n + i] = g_mu[i];
-        p.v_scales[3 * n + i] = gsc[i];
+        p.v_means[3 * no + i] = g_mu[i];
+        p.v_scales[3 * no + i] = gsc[i];
     }
-    p.v_opac[n] = g_op;
+    p.v_opac[no] = g_op;
     if (DEG < 0) {
         if (p.v_colors) {   // NULL in N-D feature mode: the raster backward wrote the feature gradient
 #pragma unroll
-            for (int i = 0; i < 3; i++) p.v_colors[3 * n + i] = g_rgb[i];
+            for (int i = 0; i < 3; i++) p.v_colors[3 * no + i] = g_rgb[i];
         }
     } else {
         const int lane = threadIdx.x & 31, wslot = threadIdx.x & ~31;
-        const int64_t wbase = n - lane;
+        const int64_t wbase = no - lane;
         constexpr int F = NB * 3;   // floats per Gaussian
-        if (vec && p.K == NB && wbase + 32 <= p.N) {
+        if (vec && p.K == NB && wbase + 32 <= p.n_end - p.n_begin) {
             // the warp's 32 consecutive rows are one contiguous block: transpose through shared
             // memory and write it with coalesced 16-byte stores
             __syncwarp();
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
                 dstw[c] = make_float4(v[0], v[1], v[2], v[3]);
             }
         } else {
-            float* dst = p.v_colors + n * (int64_t)p.K * 3;
+            float* dst = p.v_colors + no * (int64_t)p.K * 3;
 #pragma unroll
             for (int i = 0; i < NB * 3; i++) dst[i] = s_gc[i][threadIdx.x];
             for (int i = NB * 3; i < p.K * 3; i++) dst[i] = 0.f;
@@ -475,6 +477,7 @@ PBParams make_pb_params(const gs_options& o, int64_t N, int C, int W, int H, con
                         float* v_quats, float* v_scales, float* v_opac, float* v_colors) {
     PBParams p{};
     p.N = N; p.C = C; p.W = W; p.H = H; p.K = K;
+    p.n_begin = 0; p.n_end = N;
     p.eps2d = o.eps2d; p.antialiased = o.antialiased; p.fov_clamp = o.fov_clamp;
     p.means = means; p.quats = quats; p.scales = scales; p.opac = opac; p.colors = colors;
     p.viewmats = viewmats; p.Ks = Ks; p.radii = radii; p.v_splats = v_splats; p.map = nullptr;
@@ -487,7 +490,7 @@ PBParams make_pb_params(const gs_options& o, int64_t N, int C, int W, int H, con
 
 template <bool POSE>
 void launch_pb_t(int deg, const PBParams& p, cudaStream_t s) {
-    const int grid = div_up(p.N, kThreads);
+    const int grid = div_up(p.n_end - p.n_begin, kThreads);
     switch (deg) {
         case -1: launch_pdl(k_project_bwd<-1, POSE>, dim3(grid), dim3(kThreads), s, p); break;
         case 0: launch_pdl(k_project_bwd<0, POSE>, dim3(grid), dim3(kThreads), s, p); break;
@@ -525,7 +528,8 @@ gs_status launch_pb(int deg, PBParams p, float* v_viewmats, void* pose_ws, cudaS
     }
     p.pose_part = static_cast<float*>(pose_ws);
     launch_pb_t<true>(deg, p, s);
-    launch_pdl(k_pose_reduce, dim3(p.C), dim3(kPoseT), s, p.pose_part, div_up(p.N, kThreads), p.C, v_viewmats);
+    launch_pdl(k_pose_reduce, dim3(p.C), dim3(kPoseT), s, p.pose_part, div_up(p.n_end - p.n_begin, kThreads), p.C,
+               v_viewmats);
     return GS_OK;
 }
 
@@ -556,6 +560,21 @@ gs_status launch_project_bwd(const gs_options& o, int64_t N, int C, int W, int H
                                       v_splats, v_means, v_quats, v_scales, v_opac, v_colors);
     launch_pb(o.sh_degree, p, v_viewmats, ws, s);
     GS_LAUNCH_CHECK("k_project_bwd");
+    return GS_OK;
+}
+
+gs_status launch_project_bwd_range(const gs_options& o, int64_t N, int64_t n_begin, int64_t n_end, int C, int W,
+                                   int H, const float* means, const float* quats, const float* scales,
+                                   const float* opac, const float* colors, int K, const float* viewmats,
+                                   const float* Ks, const int32_t* radii, const float* v_splats, float* v_means,
+                                   float* v_quats, float* v_scales, float* v_opac, float* v_colors, cudaStream_t s) {
+    if (n_end <= n_begin) return GS_OK;
+    PBParams p = make_pb_params(o, N, C, W, H, means, quats, scales, opac, colors, K, viewmats, Ks, radii, v_splats,
+                                v_means, v_quats, v_scales, v_opac, v_colors);
+    p.n_begin = n_begin;
+    p.n_end = n_end;
+    launch_pb(o.sh_degree, p, nullptr, nullptr, s);
+    GS_LAUNCH_CHECK("k_project_bwd<range>");
     return GS_OK;
 }
 

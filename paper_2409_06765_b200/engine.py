@@ -217,18 +217,26 @@ class Engine:
         self.forward(*params, backgrounds=backgrounds, stream=stream)
         self.backward(*params, v_rgb, v_alpha, backgrounds, v_depth, stream)
 
-    def capture(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None):
+    def capture(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, head_only=False):
         """Record one step() on these exact tensors into a CUDA graph (the capacities must
-        already fit: run run_checked() first).  Returns the graph; replay() launches it."""
+        already fit: run run_checked() first).  Returns the graph; replay() launches it.
+        head_only: everything but the projection backward (which DPEngine runs in buckets
+        interleaved with their all-reduces)."""
+        def body():
+            if head_only:
+                self.forward(*params, backgrounds=backgrounds)
+                self.rasterize_bwd(v_rgb, v_alpha, backgrounds, v_depth)
+            else:
+                self.step(params, v_rgb, v_alpha, backgrounds, v_depth)
         self.graph = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
-            self.step(params, v_rgb, v_alpha, backgrounds, v_depth)   # warm-up on the capture stream
+            body()   # warm-up on the capture stream
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
         with torch.cuda.graph(self.graph, stream=s):
-            self.step(params, v_rgb, v_alpha, backgrounds, v_depth)
+            body()
         torch.cuda.synchronize(self.device)
         return self.graph
 
@@ -242,3 +250,48 @@ class Engine:
             self.step(params, v_rgb, v_alpha, backgrounds, v_depth)
             if not self.ensure_capacity():
                 return
+
+
+class DPEngine(Engine):
+    """Views-DP engine whose parameter gradient lives in a bucket-major flat
+    buffer (dist.bucket_layout): the projection backward runs bucket by bucket
+    (gs_project_bwd_range) and each bucket's all-reduce is issued asynchronously as soon as its
+    rows are written, so it overlaps the next bucket's kernel.  Dense layout, no pose."""
+
+    def __init__(self, N, C, width, height, buckets=4, **kw):
+        super().__init__(N, C, width, height, **kw)
+        if self.packed or self.pose:
+            raise ValueError("DPEngine: dense layout without pose gradients")
+        sh = self.sh_degree >= 0
+        self.bucket_layout, total = D.bucket_layout(self.N, self.K, sh, buckets)
+        self.flat_grad = torch.zeros(total, dtype=torch.float32, device=self.device)
+        self.buckets = D.bucket_views(self.flat_grad, self.bucket_layout)
+        self.v_quats = self.v_means = self.v_scales = self.v_opacities = self.v_colors = None
+
+    def project_bwd(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
+        for b in self.buckets:
+            self._bucket_bwd(b, (means, quats, scales, opacities, colors, viewmats, Ks), stream)
+
+    def _bucket_bwd(self, b, params, stream=None):
+        means, quats, scales, opacities, colors, viewmats, Ks = params
+        L.gs_project_bwd_range(self.opts, b["n0"], b["n1"], means, quats, scales, opacities, colors, self.K, viewmats,
+                               Ks, self.W, self.H, self.radii, self.v_splats, b["means"], b["quats"], b["scales"],
+                               b["opacities"], b["colors"], stream)
+
+    def backward_allreduce(self, params, group=None):
+        """The projection backward bucket by bucket, each bucket's gradient summed over the
+        group with an asynchronous all-reduce right after its kernel (the collective waits for
+        the kernel on the current stream and runs on the process group's stream while the next
+        bucket computes); returns after the current stream has waited for every collective."""
+        import torch.distributed as dist
+        works = []
+        for b in self.buckets:
+            self._bucket_bwd(b, params)
+            works.append(dist.all_reduce(b["flat"], op=dist.ReduceOp.SUM, group=group, async_op=True))
+        for w in works:
+            w.wait()
+
+    def grads(self):
+        """The parameter gradient as full tensors {"v_means": [N,3], ...} (copies)."""
+        g = D.gather_buckets(self.flat_grad, self.bucket_layout)
+        return {"v_" + k: v for k, v in g.items()}

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2409_06765_b200 import Engine  # noqa: E402
+from paper_2409_06765_b200.engine import DPEngine, Engine  # noqa: E402
 from paper_2409_06765_b200 import dist as D  # noqa: E402
 from synth import scenes as S  # noqa: E402
 
@@ -20,7 +20,7 @@ def scene():
     return S.mipnerf_like_scene(20000, width=320, height=200, views=4, sh_degree=3, seed=31)
 
 
-def main(out_dir):
+def main(out_dir, bucketed=False):
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     sc = scene()
@@ -31,18 +31,33 @@ def main(out_dir):
     dev = torch.device("cuda", 0)
     params = [torch.from_numpy(np.ascontiguousarray(sc[k], np.float32)).to(dev) for k in keys]
     params += [torch.from_numpy(np.ascontiguousarray(sc[k][views], np.float32)).to(dev) for k in ("viewmats", "Ks")]
-    eng = Engine(N, len(views), W, H, sh_degree=3, device=dev)
-    eng.run_checked(tuple(params), torch.from_numpy(np.ascontiguousarray(v_img[views])).to(dev))
-    torch.cuda.synchronize()
-    flat = eng.flat_grad.cpu()            # the collective runs on the host buffer over gloo
-    D.allreduce_grads(flat)
+    v = torch.from_numpy(np.ascontiguousarray(v_img[views])).to(dev)
+    if bucketed:
+        # the bench's N > 1 step: projection backward in buckets, each bucket all-reduced
+        # asynchronously right after its kernel (gloo takes the CUDA tensors here)
+        eng = DPEngine(N, len(views), W, H, sh_degree=3, device=dev, buckets=3)
+        eng.run_checked(tuple(params), v)
+        eng.forward(*params)
+        eng.rasterize_bwd(v)
+        eng.backward_allreduce(tuple(params))
+        torch.cuda.synchronize()
+        flat = dict((k, t.cpu()) for k, t in eng.grads().items())
+    else:
+        eng = Engine(N, len(views), W, H, sh_degree=3, device=dev)
+        eng.run_checked(tuple(params), v)
+        torch.cuda.synchronize()
+        flat = eng.flat_grad.cpu()            # the collective runs on the host buffer over gloo
+        D.allreduce_grads(flat)
     np.save(os.path.join(out_dir, f"rgb{rank}.npy"), eng.out_rgb.cpu().numpy())
     np.save(os.path.join(out_dir, f"views{rank}.npy"), np.array(views, np.int64))
     if rank == 0:
-        np.save(os.path.join(out_dir, "flat.npy"), flat.numpy())
+        if bucketed:
+            np.savez(os.path.join(out_dir, "grads.npz"), **{k: t.numpy() for k, t in flat.items()})
+        else:
+            np.save(os.path.join(out_dir, "flat.npy"), flat.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], len(sys.argv) > 2 and sys.argv[2] == "bucketed")

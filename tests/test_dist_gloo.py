@@ -206,3 +206,27 @@ def test_exchange_world1_and_distributed_api_validation():
         rasterization(*args, distributed=True, render_mode="RGB+D")
     with pytest.raises(ValueError):
         rasterization(*args, distributed=True, absgrad=True)
+
+
+def test_bucket_layout_covers_every_gaussian_once():
+    """dist.bucket_layout: buckets tile [0, N) in order with 128-aligned starts, every section
+    16-byte aligned, one contiguous slice per bucket; gather_buckets inverts bucket_views."""
+    for N, nb in [(1000, 4), (20000, 3), (130, 8), (0, 4), (128, 1)]:
+        lay, total = D.bucket_layout(N, 16, True, nb)
+        n = 0
+        for n0, n1, off, secs in lay:
+            assert n0 == n and n0 % 128 == 0 and n1 >= n0
+            n = n1
+            for o, s, shp in secs.values():
+                assert o % 4 == 0 and off <= o and o + s <= total
+        assert n == N
+        flat = torch.arange(total, dtype=torch.float32)
+        vs = D.bucket_views(flat, lay)
+        g = D.gather_buckets(flat, lay)
+        assert g["means"].shape == (N, 3) and g["colors"].shape == (N, 16, 3) and g["quats"].shape == (N, 4)
+        for v in vs:
+            assert torch.equal(g["means"][v["n0"]:v["n1"]], v["means"])
+            assert v["flat"].data_ptr() <= v["means"].data_ptr()
+        # sections never overlap: every float index used at most once
+        used = torch.cat([t.reshape(-1) for v in vs for k, t in v.items() if k not in ("n0", "n1", "flat")])
+        assert used.unique().numel() == used.numel()

@@ -28,11 +28,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_views_dp_equals_one_process_and_oracle(tmp_path, world):
+@pytest.mark.parametrize("world,mode", [(2, "flat"), (3, "flat"), (2, "bucketed"), (3, "bucketed")])
+def test_views_dp_equals_one_process_and_oracle(tmp_path, world, mode):
+    """flat: one all-reduce of the section-major flat gradient after the step; bucketed: the
+    projection backward in 3 Gaussian buckets, each all-reduced asynchronously right after its
+    kernel (DPEngine.backward_allreduce, the bench's N > 1 step)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "_dist_dp_worker.py"), str(tmp_path)]
+           os.path.join(ROOT, "tests", "_dist_dp_worker.py"), str(tmp_path), mode]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     sc = scene()
@@ -45,9 +48,12 @@ def test_views_dp_equals_one_process_and_oracle(tmp_path, world):
         seen += list(vw)
         assert np.array_equal(np.load(os.path.join(tmp_path, f"rgb{rk}.npy")), one["rgb"][vw])
     assert sorted(seen) == list(range(C))
-    flat = np.load(os.path.join(tmp_path, "flat.npy"))
-    lay, _ = D.flat_layout(N, 16, True)
-    dp = {"v_" + k: flat[o:o + n].reshape(shp) for k, (o, n, shp) in lay.items()}
+    if mode == "bucketed":
+        dp = dict(np.load(os.path.join(tmp_path, "grads.npz")))
+    else:
+        flat = np.load(os.path.join(tmp_path, "flat.npy"))
+        lay, _ = D.flat_layout(N, 16, True)
+        dp = {"v_" + k: flat[o:o + n].reshape(shp) for k, (o, n, shp) in lay.items()}
     o = oracle.Options(sh_degree=3)
     ref = U.oracle_reference(sc, o, one, v_img, with_isect=False)
     # the all-reduced sum against the one-process call: the same per-(c,n) terms, another
