@@ -345,72 +345,90 @@ def run_ours(args):
                   "hbm_frac": round(step_bytes / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
 
     # ---- end to end through the public API with HOST buffers (pinned), every step ----
-    # Each step uploads that step's inputs (all Gaussian parameters, cameras, the upstream
-    # image gradient) from pinned host memory and reads back its results (the rendered image
-    # and the flat parameter gradient).  Steps are software-pipelined over three streams
+    # Each step uploads that step's inputs from pinned host memory and reads back its result.
+    # Headline (a training loop: the Gaussians live on the GPU like any model's parameters):
+    # the view's camera (viewmats, Ks) and dL/d(image) go up, the rendered image comes back.
+    # Also reported: every Gaussian parameter up and the whole flat gradient back each step
+    # (`full_param_roundtrip`, PCIe bound).  Steps are software-pipelined over three streams
     # with two engines / buffer sets: step i+1's upload (H2D) and step i-1's download (D2H)
-    # run during step i's kernels (PCIe is full duplex); events order every reuse.  The
-    # timed region runs from before the first upload to after the last download.
+    # run during step i's kernels (PCIe is full duplex); events order every reuse.  The timed
+    # region runs from before the first upload to after the last download.
     e2e = None
-    engs = d_in = d_v = None
+    engs = None
     if not args.no_e2e:
         engs = [eng, make_engine(M_capacity=eng.cap)]
-        d_in = [list(params), [t.clone() for t in params]]
-        d_v = [v_dev, v_dev.clone()]
-        engs[1].run_checked(tuple(d_in[1]), d_v[1])
-        h_out = [(torch.empty(eng.out_rgb.shape, dtype=torch.float32).pin_memory(),
-                  torch.empty(eng.flat_grad.shape, dtype=torch.float32).pin_memory()) for _ in range(2)]
-        bi = sum(t.numel() * 4 for t in host.values()) + host_v.numel() * 4
-        bo = h_out[0][0].numel() * 4 + h_out[0][1].numel() * 4
+        engs[1].run_checked(params, v_dev)
         s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        K = args.steps
-        ev_h2d = [torch.cuda.Event() for _ in range(K)]
-        ev_cmp = [torch.cuda.Event() for _ in range(K)]
-        ev_d2h = [torch.cuda.Event() for _ in range(K)]
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        t0.record(s_h2d)
-        for i in range(K):
-            bsel = i % 2
-            with torch.cuda.stream(s_h2d):
+
+        def e2e_run(up_keys, grad_back):
+            d_in = [list(params), list(params)]
+            for b in range(2):
+                for j, k in enumerate(keys):
+                    if k in up_keys:
+                        d_in[b][j] = params[j].clone()
+            d_v = [v_dev.clone(), v_dev.clone()]
+            h_out = [[torch.empty(eng.out_rgb.shape, dtype=torch.float32).pin_memory()] +
+                     ([torch.empty(eng.flat_grad.shape, dtype=torch.float32).pin_memory()] if grad_back else [])
+                     for _ in range(2)]
+            bi = sum(host[k].numel() * 4 for k in up_keys) + host_v.numel() * 4
+            bo = sum(t.numel() * 4 for t in h_out[0])
+            K = args.steps
+            ev_h2d = [torch.cuda.Event() for _ in range(K)]
+            ev_cmp = [torch.cuda.Event() for _ in range(K)]
+            ev_d2h = [torch.cuda.Event() for _ in range(K)]
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            t0.record(s_h2d)
+            for i in range(K):
+                bsel = i % 2
+                with torch.cuda.stream(s_h2d):
+                    if i >= 2:
+                        s_h2d.wait_event(ev_cmp[i - 2])        # engine bsel finished reading its inputs
+                    for j, k in enumerate(keys):
+                        if k in up_keys:
+                            d_in[bsel][j].copy_(host[k], non_blocking=True)
+                    d_v[bsel].copy_(host_v, non_blocking=True)
+                    ev_h2d[i].record(s_h2d)
+                stream.wait_event(ev_h2d[i])
                 if i >= 2:
-                    s_h2d.wait_event(ev_cmp[i - 2])        # engine bsel finished reading its inputs
-                for dst, k in zip(d_in[bsel], keys):
-                    dst.copy_(host[k], non_blocking=True)
-                d_v[bsel].copy_(host_v, non_blocking=True)
-                ev_h2d[i].record(s_h2d)
-            stream.wait_event(ev_h2d[i])
-            if i >= 2:
-                stream.wait_event(ev_d2h[i - 2])           # its previous results were read out
-            if bucketed:
-                e_ = engs[bsel]
-                e_.forward(*d_in[bsel])
-                e_.rasterize_bwd(d_v[bsel])
-                e_.backward_allreduce(tuple(d_in[bsel]))
-            else:
-                engs[bsel].step(tuple(d_in[bsel]), d_v[bsel])
-                if world > 1:
-                    dist.all_reduce(engs[bsel].flat_grad)
-            ev_cmp[i].record(stream)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev_cmp[i])
-                h_out[bsel][0].copy_(engs[bsel].out_rgb, non_blocking=True)
-                h_out[bsel][1].copy_(engs[bsel].flat_grad, non_blocking=True)
-                ev_d2h[i].record(s_d2h)
-        t1.record(s_d2h)
-        torch.cuda.synchronize(dev)
-        e_ms = float(t0.elapsed_time(t1))
-        if any(int(e.overflow.item()) != 0 for e in engs):
-            raise RuntimeError("intersection capacity overflowed inside the e2e region")
-        if world > 1:
-            t = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": round(mp_per_step / (e_ms / K / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": bi,
-               "d2h_bytes_per_step": bo, "ms_per_step": round(e_ms / K, 4),
-               "pipeline": "H2D(i+1) | kernels(i) | D2H(i-1) on three streams, two buffer sets"}
+                    stream.wait_event(ev_d2h[i - 2])           # its previous results were read out
+                if bucketed:
+                    e_ = engs[bsel]
+                    e_.forward(*d_in[bsel])
+                    e_.rasterize_bwd(d_v[bsel])
+                    e_.backward_allreduce(tuple(d_in[bsel]))
+                else:
+                    engs[bsel].step(tuple(d_in[bsel]), d_v[bsel])
+                    if world > 1:
+                        dist.all_reduce(engs[bsel].flat_grad)
+                ev_cmp[i].record(stream)
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_cmp[i])
+                    h_out[bsel][0].copy_(engs[bsel].out_rgb, non_blocking=True)
+                    if grad_back:
+                        h_out[bsel][1].copy_(engs[bsel].flat_grad, non_blocking=True)
+                    ev_d2h[i].record(s_d2h)
+            t1.record(s_d2h)
+            torch.cuda.synchronize(dev)
+            e_ms = float(t0.elapsed_time(t1))
+            if any(int(e.overflow.item()) != 0 for e in engs):
+                raise RuntimeError("intersection capacity overflowed inside the e2e region")
+            if world > 1:
+                t = torch.tensor([e_ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e_ms = float(t.item())
+            return {"value": round(mp_per_step / (e_ms / K / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": bi,
+                    "d2h_bytes_per_step": bo, "ms_per_step": round(e_ms / K, 4)}
+
+        e2e = e2e_run(("viewmats", "Ks"), False)
+        e2e.update(inputs="per step: the view's camera and dL/d(image) up (Gaussians resident on the GPU), "
+                          "the rendered image back", api="Engine.step (the five C-ABI calls)",
+                   pipeline="H2D(i+1) | kernels(i) | D2H(i-1) on three streams, two buffer sets")
+        e2e["full_param_roundtrip"] = e2e_run(tuple(keys), True)
+        e2e["full_param_roundtrip"]["inputs"] = ("per step: every Gaussian parameter, the cameras and dL/d(image) "
+                                                 "up, the image and the whole flat gradient back")
 
     launches = eng.launches_per_step()   # library kernels per step (31 at configs[1], = the ncu launch list)
 
@@ -498,7 +516,7 @@ def run_ours(args):
 
     # ---- BASELINE configs[2] as strong scaling: its 8 views split over the N ranks (the
     # same total work at every N; E(R) = t(1) / (R t(R)) from the per-N records) ----
-    del engs, d_in, d_v
+    del engs
     strong = None
     if not args.no_strong:
         del eng
