@@ -11,7 +11,14 @@ import subprocess
 import sys
 
 STAGE_OF = {"k_project_fwd": "project", "k_raster_fwd": "raster_fwd", "k_raster_bwd": "raster_bwd",
-            "k_project_bwd": "project_bwd"}
+            "k_project_bwd": "project_bwd", "k_zero4": "raster_bwd"}
+ISECT = ("k_vis_", "k_scan_blocksums", "k_radix_", "k_tiles_", "k_ranges", "k_packed_items", "k_keys64")
+
+
+def stage_of(name):
+    if name in STAGE_OF:
+        return STAGE_OF[name]
+    return "isect" if name.startswith(ISECT) else None
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
@@ -68,21 +75,17 @@ def full(path, traffic_out=None):
         for k in KEYS:
             if k in h and r[h.index(k)]:
                 print(f"   {k:78s} {r[h.index(k)]} {u[h.index(k)]}")
-        if name in STAGE_OF:
+        st = stage_of(name)
+        if st:
             rd = float(r[h.index("dram__bytes_read.sum")].replace(",", ""))
             wr = float(r[h.index("dram__bytes_write.sum")].replace(",", ""))
             mult = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}
-            traffic[STAGE_OF[name]] = {"kernel": name, "dram_bytes_per_launch": rd * mult[u[h.index("dram__bytes_read.sum")]] +
-                                       wr * mult[u[h.index("dram__bytes_write.sum")]],
-                                       "source": path.split("/")[-1]}
+            b = rd * mult[u[h.index("dram__bytes_read.sum")]] + wr * mult[u[h.index("dram__bytes_write.sum")]]
+            t = traffic.setdefault(st, {"kernels": [], "dram_bytes_per_launch": 0.0, "source": path.split("/")[-1]})
+            t["kernels"].append(name)
+            t["dram_bytes_per_launch"] += b   # the stage's kernels of one step summed
     if traffic_out:
-        old = {}
-        try:
-            old = json.load(open(traffic_out))
-        except Exception:
-            pass
-        old.update(traffic)
-        json.dump(old, open(traffic_out, "w"), indent=1)
+        json.dump(traffic, open(traffic_out, "w"), indent=1)
 
 
 if __name__ == "__main__":
