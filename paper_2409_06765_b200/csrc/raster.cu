@@ -739,182 +739,6 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// K7, per-splat form (GS_K7_PS): lane = splat instead of lane = pixel.  A warp owns two 4x4
-// pixel blocks of the tile; for each staged batch it builds each block's ordered list (the
-// K6 support masks, up to the block's largest last_id) and walks it back to front in chunks
-// of 32 list entries, one entry per lane.  For each of the block's 16 pixels (pixel state in
-// shared memory, dead pixels skipped) the lanes evaluate alpha exactly as K6 (eval_alpha's
-// operations), recover T before their splat as T_after * prod_{j >= k} 1/(1 - alpha_j) (a
-// suffix product over the lanes) and S . v_C as S_after + the suffix sum of c_j alpha_j T_j
-// . v_C (B2, B5), and accumulate their splat's B3-B6 terms in registers.  One
-// set of reductions per (splat, block, chunk) instead of one per (splat, 8x4 warp).
-struct StagePS {
-    float4 xyo[kBatchBwd];   // mean2d.x, mean2d.y, opac_eff, id bits
-    float4 con[kBatchBwd];   // pre-scaled conic, b'/2
-    float4 rgb[kBatchBwd];
-    uint16_t mask[kBatchBwd];
-    uint8_t list[kWarps][kBatchBwd];
-};
-
-__device__ __forceinline__ float shfl_down_or(float v, int d, int lane, float dflt) {
-    const float y = __shfl_down_sync(0xffffffffu, v, d);
-    return lane + d < 32 ? y : dflt;
-}
-
-__global__ void __launch_bounds__(kThreads) k_raster_bwd_ps(RasterParams p) {
-    pdl_trigger();
-    pdl_wait();
-    __shared__ StagePS s;
-    __shared__ float4 s_pa[16][16];   // per block, per pixel: T_after, Sv_after, kbg, last (int bits)
-    __shared__ float4 s_pb[16][16];   // v_C (3), unused
-    __shared__ float2 s_pc[16][16];   // pixel centre
-    __shared__ int s_blast[16];
-    __shared__ int s_maxlast;
-    const int tile = blockIdx.x, cam = blockIdx.y;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tx = tile % p.TX, ty = tile / p.TX;
-    const int bin = cam * p.TX * p.TY + tile;
-    const int start = p.offs[bin];
-    // thread t holds pixel (t & 15) of block (t >> 4); warp w owns blocks 2w, 2w + 1
-    {
-        const int b = threadIdx.x >> 4, q = threadIdx.x & 15;
-        const int px = tx * GS_TILE + (b & 3) * 4 + (q & 3), py = ty * GS_TILE + (b >> 2) * 4 + (q >> 2);
-        const bool inside = px < p.W && py < p.H;
-        float Tfin = 1.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, vA = 0.f, bgdot = 0.f;
-        int last = start - 1;
-        if (inside) {
-            const int64_t pix = ((int64_t)cam * p.H + py) * p.W + px;
-            Tfin = p.out_T[pix];
-            last = p.last_ids[pix];
-            v0 = p.v_rgb[3 * pix + 0];
-            v1 = p.v_rgb[3 * pix + 1];
-            v2 = p.v_rgb[3 * pix + 2];
-            if (p.v_alpha) vA = p.v_alpha[pix];
-            if (p.bg) bgdot = p.bg[3 * cam] * v0 + p.bg[3 * cam + 1] * v1 + p.bg[3 * cam + 2] * v2;
-        }
-        s_pa[b][q] = make_float4(Tfin, 0.f, Tfin * (vA - bgdot), __int_as_float(last));
-        s_pb[b][q] = make_float4(v0, v1, v2, 0.f);
-        s_pc[b][q] = make_float2((float)px + 0.5f, (float)py + 0.5f);
-        int bl = last;
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) bl = max(bl, __shfl_xor_sync(0xffffffffu, bl, o));
-        if (q == 0) s_blast[b] = bl;
-        if (threadIdx.x == 0) s_maxlast = start - 1;
-        __syncthreads();
-        const int wl = __reduce_max_sync(0xffffffffu, last);
-        if (lane == 0) atomicMax(&s_maxlast, wl);
-        __syncthreads();
-    }
-    const int max_last = s_maxlast;
-    const float amax = p.alpha_max, amin = p.alpha_min;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int bend = max_last + 1; bend > start; bend -= kBatchBwd) {
-        const int bstart = max(start, bend - kBatchBwd);
-        const int n = bend - bstart;
-        __syncthreads();
-        if ((int)threadIdx.x < n) {
-            const int idx = bstart + threadIdx.x;
-            const int32_t g = p.ids[idx];
-            const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
-            const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
-            s.xyo[threadIdx.x] = make_float4(r0.x, r0.y, r0.z, __int_as_float(g));
-            s.con[threadIdx.x] = prescale_conic(r1.x, r1.y, r1.z);
-            s.rgb[threadIdx.x] = r2;
-            s.mask[threadIdx.x] = p.smask ? p.smask[idx]
-                                          : (uint16_t)(p.cull ? support_mask16(r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r1.w,
-                                                                               r2.w, (float)(tx * GS_TILE),
-                                                                               (float)(ty * GS_TILE), amin)
-                                                              : 0xffffu);
-        }
-        __syncthreads();
-#pragma unroll 1
-        for (int bb = 0; bb < 2; bb++) {
-            const int b = 2 * warp + bb;
-            const int blast = s_blast[b];
-            if (blast < bstart) continue;   // warp-uniform
-            // ordered list of this block's splats in the batch (support mask, up to blast)
-            int cnt = 0;
-            for (int c = 0; c < n; c += 32) {
-                const int j = c + lane;
-                const bool keep = j < n && bstart + j <= blast && ((s.mask[j] >> b) & 1u);
-                const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (keep) s.list[warp][cnt + __popc(bal & lt)] = (uint8_t)j;
-                cnt += __popc(bal);
-            }
-            __syncwarp();
-            for (int ce = cnt; ce > 0; ce -= 32) {
-                const int k = ce - 32 + lane;   // this lane's list position (< 0: no splat)
-                const bool have = k >= 0;
-                const int j = have ? s.list[warp][k] : 0;
-                const float4 xyo = s.xyo[j];
-                const float4 con = s.con[j];
-                const float4 rgb = s.rgb[j];
-                const int idx = bstart + j;
-                const int cmin = bstart + s.list[warp][max(ce - 32, 0)];   // smallest tile index of the chunk
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f, a8 = 0.f;
-#pragma unroll 1
-                for (int q = 0; q < 16; q++) {
-                    const float4 pa = s_pa[b][q];
-                    const int lastq = __float_as_int(pa.w);
-                    if (lastq < cmin) continue;   // uniform: the pixel composited nothing of this chunk
-                    const float2 pc = s_pc[b][q];
-                    const float dx = __fsub_rn(xyo.x, pc.x), dy = __fsub_rn(xyo.y, pc.y);
-                    const float xx = __fmul_rn(dx, dx), yy = __fmul_rn(dy, dy), xy = __fmul_rn(dx, dy);
-                    const float pe = __fmaf_rn(con.y, xy, __fmaf_rn(con.x, xx, __fmul_rn(con.z, yy)));
-                    float G = ex2_approx(pe);
-                    float alpha = fminf(amax, __fmul_rn(xyo.z, G));
-                    const bool valid = have && idx <= lastq && !(pe > 0.f) && alpha >= amin;
-                    if (!__any_sync(0xffffffffu, valid)) continue;
-                    G = valid ? G : 0.f;
-                    alpha = valid ? alpha : 0.f;
-                    const float ra = rcp_approx(1.f - alpha);
-                    // T before this lane's splat: T_after * prod over this and the later lanes of 1/(1-alpha)
-                    float x = ra;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) x *= shfl_down_or(x, d, lane, 1.f);
-                    const float4 pb = s_pb[b][q];
-                    const float T = pa.x * x;
-                    const float fac = alpha * T;
-                    const float cv = rgb.x * pb.x + rgb.y * pb.y + rgb.z * pb.z;
-                    const float e = cv * fac;
-                    float qs = e;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) qs += shfl_down_or(qs, d, lane, 0.f);
-                    const float Sv = pa.y + (qs - e);
-                    const float v_alpha = T * cv + ra * (pa.z - Sv);
-                    const float raw = xyo.z * G;
-                    const float va = raw < amax ? v_alpha : 0.f;   // Q24
-                    const float v_sigma = -raw * va;
-                    const float hv = 0.5f * v_sigma;
-                    const float k2 = (-2.f * kLn2) * v_sigma;
-                    a0 += k2 * (con.x * dx + con.w * dy);
-                    a1 += k2 * (con.w * dx + con.z * dy);
-                    a2 += G * va;
-                    a3 += hv * xx;
-                    a4 += v_sigma * xy;
-                    a5 += hv * yy;
-                    a6 += fac * pb.x;
-                    a7 += fac * pb.y;
-                    a8 += fac * pb.z;
-                    const float T0 = __shfl_sync(0xffffffffu, T, 0), q0 = __shfl_sync(0xffffffffu, qs, 0);
-                    if (lane == 0) {
-                        s_pa[b][q].x = T0;
-                        s_pa[b][q].y = pa.y + q0;
-                    }
-                    __syncwarp();
-                }
-                if (have && (a0 != 0.f || a1 != 0.f || a2 != 0.f || a6 != 0.f || a7 != 0.f || a8 != 0.f)) {
-                    float* dst = p.v_splats + (int64_t)__float_as_int(xyo.w) * GS_SPLAT_FLOATS;
-                    red_add_v4(dst, a0, a1, a2, a3);
-                    red_add_v4(dst + 4, a4, a5, a6, a7);
-                    atomicAdd(dst + 8, a8);
-                }
-            }
-        }
-    }
-}
-
 constexpr int kZeroBlocks = 148 * 8;
 #ifndef GS_FWD_PAD
 #define GS_FWD_PAD 4096
@@ -985,12 +809,7 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
         launch_pdl(k_zero4, dim3(kZeroBlocks), dim3(256), s, reinterpret_cast<float4*>(v_splats),
                    (int64_t)(nrec * GS_SPLAT_FLOATS / 4));
     dim3 grid(p.TX * p.TY, C);
-#ifndef GS_K7_PS
-#define GS_K7_PS 0
-#endif
-    if (GS_K7_PS && !absgrad && !p.depth_mode) {
-        launch_pdl(k_raster_bwd_ps, dim3(grid), dim3(kThreads), s, p);
-    } else if (absgrad) {
+    if (absgrad) {
         if (p.depth_mode) launch_pdl(k_raster_bwd<true, true, false>, dim3(grid), dim3(kThreads), s, p);
         else launch_pdl(k_raster_bwd<true, false, false>, dim3(grid), dim3(kThreads), s, p);
     } else {
