@@ -46,7 +46,8 @@ struct PBParams {
 // R(q / |q|)
 __device__ __forceinline__ void quat_rot(float4 q4, float (&R)[3][3]) {
     const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
-    const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
+    const float iq = 1.f / qn;   // K8 is the values path: reciprocals instead of divisions
+    const float qw = q4.x * iq, qx = q4.y * iq, qy = q4.z * iq, qz = q4.w * iq;
     R[0][0] = 1.f - 2.f * (qy * qy + qz * qz); R[0][1] = 2.f * (qx * qy - qw * qz); R[0][2] = 2.f * (qx * qz + qw * qy);
     R[1][0] = 2.f * (qx * qy + qw * qz); R[1][1] = 1.f - 2.f * (qx * qx + qz * qz); R[1][2] = 2.f * (qy * qz - qw * qx);
     R[2][0] = 2.f * (qx * qz - qw * qy); R[2][1] = 2.f * (qy * qz + qw * qx); R[2][2] = 1.f - 2.f * (qx * qx + qy * qy);
@@ -196,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
                 txc = tz * fminf(lxp, fmaxf(-lxn, u));
                 tyc = tz * fminf(lyp, fmaxf(-lyn, v));
             }
-            const float J[2][3] = {{fx / tz, 0.f, -fx * txc / (tz * tz)}, {0.f, fy / tz, -fy * tyc / (tz * tz)}};
+            const float rz = 1.f / tz, rz2 = rz * rz, rz3 = rz2 * rz;
+            const float J[2][3] = {{fx * rz, 0.f, -fx * txc * rz2}, {0.f, fy * rz, -fy * tyc * rz2}};
             float B[2][3], Sp[2][2];
 #pragma unroll
             for (int i = 0; i < 2; i++)
@@ -208,11 +210,12 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
                 for (int j = 0; j < 2; j++) Sp[i][j] = B[i][0] * J[j][0] + B[i][1] * J[j][1] + B[i][2] * J[j][2];
             const float a = Sp[0][0] + p.eps2d, b = Sp[0][1], cc = Sp[1][1] + p.eps2d;
             const float detb = a * cc - b * b;
-            const float Y00 = cc / detb, Y01 = -b / detb, Y11 = a / detb;
+            const float idet = 1.f / detb;
+            const float Y00 = cc * idet, Y01 = -b * idet, Y11 = a * idet;
             float comp = 1.f, det_raw = 0.f;
             if (p.antialiased) {
                 det_raw = Sp[0][0] * Sp[1][1] - Sp[0][1] * Sp[0][1];
-                comp = sqrtf(fmaxf(0.f, det_raw / detb));
+                comp = sqrtf(fmaxf(0.f, det_raw * idet));
             }
             // ---- P1: o_eff = o * comp
             const float v_oeff = v0.z;
@@ -228,9 +231,10 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
             // ---- P3 (AA): + v_comp * comp/2 * (Sigma'^-1 - Spb^-1)
             if (p.antialiased && det_raw > 0.f) {
                 const float k = v_comp * 0.5f * comp;
-                vS00 += k * (Sp[1][1] / det_raw - Y00);
-                vS01 += k * (-Sp[0][1] / det_raw - Y01);
-                vS11 += k * (Sp[0][0] / det_raw - Y11);
+                const float idr = 1.f / det_raw;
+                vS00 += k * (Sp[1][1] * idr - Y00);
+                vS01 += k * (-Sp[0][1] * idr - Y01);
+                vS11 += k * (Sp[0][0] * idr - Y11);
             }
             const float vSp[2][2] = {{vS00, vS01}, {vS01, vS11}};
             // ---- P4: v_Sc = J^T vSp J; v_J = 2 vSp J Sc (Q11)
@@ -249,7 +253,6 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
 #pragma unroll
                 for (int j = 0; j < 3; j++) vJ[i][j] = 2.f * (PJ[i][0] * Sc[0][j] + PJ[i][1] * Sc[1][j] + PJ[i][2] * Sc[2][j]);
             // ---- P5: v_t through J (exact with clamp Q27) and mu' (Q10)
-            const float rz = 1.f / tz, rz2 = rz * rz, rz3 = rz2 * rz;
             float vt0 = 0.f, vt1 = 0.f, vt2 = -fx * rz2 * vJ[0][0] - fy * rz2 * vJ[1][1];
             if (!clx) {
                 vt0 += -fx * rz2 * vJ[0][2];
@@ -309,7 +312,8 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
                 for (int i = 0; i < 3; i++) campos[i] = -(Wr[0][i] * w[0] + Wr[1][i] * w[1] + Wr[2][i] * w[2]);
                 const float ex = mu[0] - campos[0], ey = mu[1] - campos[1], ez = mu[2] - campos[2];
                 const float en = sqrtf(ex * ex + ey * ey + ez * ez);
-                const float dx = ex / en, dy = ey / en, dz = ez / en;
+                const float ren = 1.f / en;
+                const float dx = ex * ren, dy = ey * ren, dz = ez * ren;
                 float Yb[NB];
                 sh_eval_basis<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, Yb);
                 float raw[3] = {0.5f, 0.5f, 0.5f};
@@ -349,7 +353,6 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
                     float gx = 0.f, gy = 0.f, gz = 0.f;
                     sh_basis_vjp<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, wj, gx, gy, gz);
                     const float dd = dx * gx + dy * gy + dz * gz;
-                    const float ren = 1.f / en;
                     const float ve[3] = {(gx - dx * dd) * ren, (gy - dy * dd) * ren, (gz - dz * dd) * ren};
                     g_mu[0] += ve[0];
                     g_mu[1] += ve[1];
@@ -389,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
 
     // ---- P8: v_M = (vS + vS^T) M; v_s_j = (R^T v_M)_jj; v_R = v_M S
     const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
-    const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
+    const float rq = 1.f / qn;
+    const float qw = q4.x * rq, qx = q4.y * rq, qy = q4.z * rq, qz = q4.w * rq;
     float R[3][3], M[3][3];
     quat_rot(q4, R);
 #pragma unroll
@@ -421,7 +425,6 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
     float vqz = 2.f * (-2.f * z_ * vR[0][0] - w_ * vR[0][1] + x_ * vR[0][2] + w_ * vR[1][0] - 2.f * z_ * vR[1][1] +
                        y_ * vR[1][2] + x_ * vR[2][0] + y_ * vR[2][1]);
     const float dot = vqw * w_ + vqx * x_ + vqy * y_ + vqz * z_;
-    const float rq = 1.f / qn;
     float4 oq = make_float4((vqw - dot * w_) * rq, (vqx - dot * x_) * rq, (vqy - dot * y_) * rq, (vqz - dot * z_) * rq);
     if (!seen) {   // culled in every camera (includes zero / non-finite quaternions): zeros
         oq = make_float4(0.f, 0.f, 0.f, 0.f);
