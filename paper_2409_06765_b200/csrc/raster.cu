@@ -604,19 +604,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     // recurrences are carried as the single scalar Sv = S . v_C (same recurrence, dotted)
     float T = Tfin, Sv = 0.f;
     const float amax = p.alpha_max, amin = p.alpha_min;
-    for (int bend = max_last + 1; bend > start; bend -= kBatchBwd) {
-        const int bstart = max(start, bend - kBatchBwd);
-        const int n = bend - bstart;
-        __syncthreads();
-        static_assert(kBatchBwd == kThreads, "one staged splat per thread");
-        if ((int)threadIdx.x < n) stage_splat<FEAT, !DEPTH>(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0, cam);
-        __syncthreads();
-        if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
-        const int cnt = build_warp_list(s, n, q.warp, lane, wlast - bstart);
-        for (int k = cnt - 1; k >= 0; k--) {
-            const int j = s.list[q.warp][k];
-            const float4 xyo = s.xyo[j];
-            const float4 con = s.con[j];
+    // one (warp, splat) visit: alpha by eval_alpha's operations, B2-B6, the reduction.  tidx is
+    // the splat's index in the tile's list (the lane takes it iff tidx <= its last_id)
+    auto visit = [&](const float4 xyo, const float4 con, const float4* prgb, const int32_t* pid, int tidx) {
             // the alpha of eval_alpha (same operations, bit-identical decisions as K6), evaluated
             // by every lane without a branch, keeping the products dx^2, dy^2, dx dy for B6: they
             // are finite for any staged record, and a lane that does not take the splat has its
@@ -626,20 +616,20 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             const float pe = __fmaf_rn(con.y, xy, __fmaf_rn(con.x, xx, __fmul_rn(con.z, yy)));
             float G = ex2_approx(pe);
             float alpha = fminf(amax, __fmul_rn(xyo.z, G));
-            bool valid = q.inside && bstart + j <= last && !(pe > 0.f) && alpha >= amin;
+            bool valid = q.inside && tidx <= last && !(pe > 0.f) && alpha >= amin;
             const unsigned vb = __ballot_sync(0xffffffffu, valid);
             K7_STAT(0, 1);
             K7_STAT(1, vb == 0);
             K7_STAT(2, __popc(vb));
             K7_STAT(3, (vb != 0) && __popc(vb) <= kFewLanes);
             K7_STAT(4, ((vb & 0xffffu) == 0) != ((vb >> 16) == 0));   // only one 4x4 half takes it
-            if (!vb) continue;
+            if (!vb) return;
             // Branch-free from here: a lane that does not take this splat gets alpha = G = 0,
             // which makes every gradient term below exactly 0 and leaves T and Sv unchanged.
             G = valid ? G : 0.f;
             alpha = valid ? alpha : 0.f;
             float g8[8];   // mx, my, o, A, B, C, r, g
-            const float4 rgb = s.rgb[j];
+            const float4 rgb = *prgb;
             const float ra = rcp_approx(1.f - alpha);
             T = valid ? T * ra : T;            // B2: T_{n-1} = T_n / (1 - alpha_{n-1})
             const float fac = alpha * T;
@@ -672,7 +662,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             const float k2 = (-2.f * kLn2) * v_sigma;
             g8[0] = k2 * (con.x * dx + con.w * dy);
             g8[1] = k2 * (con.w * dx + con.z * dy);
-            const int32_t sid = DEPTH ? s.id[j] : __float_as_int(xyo.w);
+            const int32_t sid = DEPTH ? *pid : __float_as_int(xyo.w);
             float* dst = p.v_splats + (int64_t)sid * GS_SPLAT_FLOATS;
             if (FEAT) {
                 // geometry slots into the record gradient, the 4 channels into v_feats
@@ -689,7 +679,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                         if (mch > 2) atomicAdd(fdst + 2, g_bl);
                         if (mch > 3) atomicAdd(fdst + 3, g_f3);
                     }
-                    continue;
+                    return;
                 }
                 const float r8 = reduce_scatter8(g8, lane);
                 const int i8 = lane >> 2;
@@ -707,7 +697,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                         atomicAdd(dst + (i4 == 2 ? 10 : 11), r4);
                     }
                 }
-                continue;
+                return;
             }
             if (__popc(vb) <= kFewLanes) {
                 // few contributing lanes: each issues its own three 16-byte reductions -- 3 warp
@@ -719,7 +709,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                     else if (DEPTH) red_add_v2(dst + 8, g_bl, g_z);
                     else atomicAdd(dst + 8, g_bl);
                 }
-                continue;
+                return;
             }
             const float r8 = reduce_scatter8(g8, lane);
             if ((lane & 3) == 0) atomicAdd(dst + (lane >> 2), r8);
@@ -735,6 +725,57 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                     if (lane == 0) atomicAdd(dst + 9, rz);
                 }
             }
+    };
+#ifndef GS_K7_WARP
+#define GS_K7_WARP 0
+#endif
+    if (GS_K7_WARP && p.smask) {
+        // warp-autonomous staging: the warp walks the tile's list back to front from ITS largest
+        // last_id in chunks of 32 entries, keeps the entries whose support mask has its 8x4
+        // block, gathers their records into its own shared slots and visits them -- no block
+        // barriers, a warp that is done leaves
+        __shared__ float4 w_xyo[kWarps][32], w_con[kWarps][32], w_rgb[kWarps][32];
+        __shared__ int32_t w_idx[kWarps][32], w_id[kWarps][32];
+        const int warp = q.warp;
+        const unsigned lt = (1u << lane) - 1u;
+        for (int cend = wlast + 1; cend > start; cend -= 32) {
+            const int cb = max(start, cend - 32);
+            const int jj = cb + lane;
+            const bool in = jj < cend;
+            const uint32_t m16 = in ? (uint32_t)p.smask[jj] : 0u;
+            const bool keep = in && ((support_mask8(m16) >> warp) & 1u);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (!bal) continue;
+            if (keep) {
+                const int slot = __popc(bal & lt);
+                const int32_t g = p.ids[jj];
+                const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
+                const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
+                w_xyo[warp][slot] = DEPTH ? r0 : make_float4(r0.x, r0.y, r0.z, __int_as_float(g));
+                w_con[warp][slot] = prescale_conic(r1.x, r1.y, r1.z);
+                w_rgb[warp][slot] = FEAT ? load_feat4(p, g, cam) : r2;
+                w_idx[warp][slot] = jj;
+                w_id[warp][slot] = g;
+            }
+            __syncwarp();
+            for (int k = __popc(bal) - 1; k >= 0; k--)
+                visit(w_xyo[warp][k], w_con[warp][k], &w_rgb[warp][k], &w_id[warp][k], w_idx[warp][k]);
+            __syncwarp();
+        }
+        return;
+    }
+    for (int bend = max_last + 1; bend > start; bend -= kBatchBwd) {
+        const int bstart = max(start, bend - kBatchBwd);
+        const int n = bend - bstart;
+        __syncthreads();
+        static_assert(kBatchBwd == kThreads, "one staged splat per thread");
+        if ((int)threadIdx.x < n) stage_splat<FEAT, !DEPTH>(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0, cam);
+        __syncthreads();
+        if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
+        const int cnt = build_warp_list(s, n, q.warp, lane, wlast - bstart);
+        for (int k = cnt - 1; k >= 0; k--) {
+            const int j = s.list[q.warp][k];
+            visit(s.xyo[j], s.con[j], &s.rgb[j], &s.id[j], bstart + j);
         }
     }
 }
