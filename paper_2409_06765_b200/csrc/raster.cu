@@ -726,44 +726,6 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
                 }
             }
     };
-#ifndef GS_K7_WARP
-#define GS_K7_WARP 0
-#endif
-    if (GS_K7_WARP && p.smask) {
-        // warp-autonomous staging: the warp walks the tile's list back to front from ITS largest
-        // last_id in chunks of 32 entries, keeps the entries whose support mask has its 8x4
-        // block, gathers their records into its own shared slots and visits them -- no block
-        // barriers, a warp that is done leaves
-        __shared__ float4 w_xyo[kWarps][32], w_con[kWarps][32], w_rgb[kWarps][32];
-        __shared__ int32_t w_idx[kWarps][32], w_id[kWarps][32];
-        const int warp = q.warp;
-        const unsigned lt = (1u << lane) - 1u;
-        for (int cend = wlast + 1; cend > start; cend -= 32) {
-            const int cb = max(start, cend - 32);
-            const int jj = cb + lane;
-            const bool in = jj < cend;
-            const uint32_t m16 = in ? (uint32_t)p.smask[jj] : 0u;
-            const bool keep = in && ((support_mask8(m16) >> warp) & 1u);
-            const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (!bal) continue;
-            if (keep) {
-                const int slot = __popc(bal & lt);
-                const int32_t g = p.ids[jj];
-                const float4* rec = reinterpret_cast<const float4*>(p.splats + (int64_t)g * GS_SPLAT_FLOATS);
-                const float4 r0 = __ldg(rec), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2);
-                w_xyo[warp][slot] = DEPTH ? r0 : make_float4(r0.x, r0.y, r0.z, __int_as_float(g));
-                w_con[warp][slot] = prescale_conic(r1.x, r1.y, r1.z);
-                w_rgb[warp][slot] = FEAT ? load_feat4(p, g, cam) : r2;
-                w_idx[warp][slot] = jj;
-                w_id[warp][slot] = g;
-            }
-            __syncwarp();
-            for (int k = __popc(bal) - 1; k >= 0; k--)
-                visit(w_xyo[warp][k], w_con[warp][k], &w_rgb[warp][k], &w_id[warp][k], w_idx[warp][k]);
-            __syncwarp();
-        }
-        return;
-    }
     for (int bend = max_last + 1; bend > start; bend -= kBatchBwd) {
         const int bstart = max(start, bend - kBatchBwd);
         const int n = bend - bstart;
