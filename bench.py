@@ -769,7 +769,28 @@ def cpu_baseline(sc, v_img, budget_s=15.0):
     dt = run(n)
     per_tile = max((dt - fixed) / n, 1e-6)
     full = fixed + per_tile * TT
-    return {"value": round(C * W * H / 1e6 / full, 6), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    # BASELINE configs[0] (64x64, 100 Gaussians, SH0) timed in full: all host threads and one
+    # (SURVEY 8(d) oracle timing)
+    tiny = S.tiny_scene(0)
+    tv, _ = S.image_grads(0, 1, 64, 64, l1_scale=False)
+    ot = oracle.Options(sh_degree=0)
+
+    def run_tiny():
+        t0 = time.perf_counter()
+        for _ in range(5):
+            oracle.forward_backward(tiny, ot, tv.astype(np.float64), with_isect=False)
+        return (time.perf_counter() - t0) / 5
+
+    nthr = oracle.num_threads()
+    t_all = run_tiny()
+    oracle.set_num_threads(1)
+    t_one = run_tiny()
+    oracle.set_num_threads(nthr)
+    cfg0 = {"workload": "configs[0]: 64x64, 100 Gaussians, SH0, fwd+bwd in full", "ms": round(t_all * 1e3, 3),
+            "value": round(64 * 64 / 1e6 / t_all, 4), "threads": nthr, "ms_1_thread": round(t_one * 1e3, 3),
+            "value_1_thread": round(64 * 64 / 1e6 / t_one, 4), "unit": UNIT}
+    return {"configs0": cfg0, "value": round(C * W * H / 1e6 / full, 6), "unit": UNIT, "cores": oracle.num_threads(),
+            "kind": "oracle",
             "sample": f"{n} of {TT} tiles per view composited fwd+bwd plus projection fwd+bwd of all {N} Gaussians "
                       f"in {dt:.1f} s; linear model ({fixed:.2f} s fixed + {per_tile * 1e3:.1f} ms/tile) extrapolated "
                       f"to the full {W}x{H} frame = {full:.0f} s/view"}
