@@ -748,6 +748,8 @@ def cpu_baseline(sc, v_img, budget_s=15.0):
     import oracle
     from synth import scenes as S
     oracle.build()
+    # every host core this process may run on (torchrun sets OMP_NUM_THREADS=1 per rank)
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     C, N, W, H = sc["viewmats"].shape[0], sc["means"].shape[0], sc["width"], sc["height"]
     TT = ((W + 15) // 16) * ((H + 15) // 16)
     o = oracle.Options(sh_degree=sc["sh_degree"])
