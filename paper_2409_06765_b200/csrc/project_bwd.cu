@@ -43,10 +43,22 @@ struct PBParams {
     float* v_colors;
 };
 
+// MUFU approximations (relative error ~2^-22): K8 computes values, not decisions, and its
+// tolerance is 1e-3 relative (the Q27 clamp branch keeps IEEE divisions)
+__device__ __forceinline__ float rcp_fast(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rsqrt_fast(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // R(q / |q|)
 __device__ __forceinline__ void quat_rot(float4 q4, float (&R)[3][3]) {
-    const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
-    const float iq = 1.f / qn;   // K8 is the values path: reciprocals instead of divisions
+    const float iq = rsqrt_fast(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
     const float qw = q4.x * iq, qx = q4.y * iq, qy = q4.z * iq, qz = q4.w * iq;
     R[0][0] = 1.f - 2.f * (qy * qy + qz * qz); R[0][1] = 2.f * (qx * qy - qw * qz); R[0][2] = 2.f * (qx * qz + qw * qy);
     R[1][0] = 2.f * (qx * qy + qw * qz); R[1][1] = 1.f - 2.f * (qx * qx + qz * qz); R[1][2] = 2.f * (qy * qz - qw * qx);
@@ -197,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
                 txc = tz * fminf(lxp, fmaxf(-lxn, u));
                 tyc = tz * fminf(lyp, fmaxf(-lyn, v));
             }
-            const float rz = 1.f / tz, rz2 = rz * rz, rz3 = rz2 * rz;
+            const float rz = rcp_fast(tz), rz2 = rz * rz, rz3 = rz2 * rz;
             const float J[2][3] = {{fx * rz, 0.f, -fx * txc * rz2}, {0.f, fy * rz, -fy * tyc * rz2}};
             float B[2][3], Sp[2][2];
 #pragma unroll
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
                 for (int j = 0; j < 2; j++) Sp[i][j] = B[i][0] * J[j][0] + B[i][1] * J[j][1] + B[i][2] * J[j][2];
             const float a = Sp[0][0] + p.eps2d, b = Sp[0][1], cc = Sp[1][1] + p.eps2d;
             const float detb = a * cc - b * b;
-            const float idet = 1.f / detb;
+            const float idet = rcp_fast(detb);
             const float Y00 = cc * idet, Y01 = -b * idet, Y11 = a * idet;
             float comp = 1.f, det_raw = 0.f;
             if (p.antialiased) {
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
             // ---- P3 (AA): + v_comp * comp/2 * (Sigma'^-1 - Spb^-1)
             if (p.antialiased && det_raw > 0.f) {
                 const float k = v_comp * 0.5f * comp;
-                const float idr = 1.f / det_raw;
+                const float idr = rcp_fast(det_raw);
                 vS00 += k * (Sp[1][1] * idr - Y00);
                 vS01 += k * (-Sp[0][1] * idr - Y01);
                 vS11 += k * (Sp[0][0] * idr - Y11);
@@ -311,8 +323,7 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
 #pragma unroll
                 for (int i = 0; i < 3; i++) campos[i] = -(Wr[0][i] * w[0] + Wr[1][i] * w[1] + Wr[2][i] * w[2]);
                 const float ex = mu[0] - campos[0], ey = mu[1] - campos[1], ez = mu[2] - campos[2];
-                const float en = sqrtf(ex * ex + ey * ey + ez * ez);
-                const float ren = 1.f / en;
+                const float ren = rsqrt_fast(ex * ex + ey * ey + ez * ez);
                 const float dx = ex * ren, dy = ey * ren, dz = ez * ren;
                 float Yb[NB];
                 sh_eval_basis<(DEG < 0 ? 0 : DEG)>(dx, dy, dz, Yb);
@@ -391,8 +402,7 @@ __global__ void __launch_bounds__(kThreads, GS_PBWD_MINB) k_project_bwd(PBParams
     if (!active) return;
 
     // ---- P8: v_M = (vS + vS^T) M; v_s_j = (R^T v_M)_jj; v_R = v_M S
-    const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
-    const float rq = 1.f / qn;
+    const float rq = rsqrt_fast(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
     const float qw = q4.x * rq, qx = q4.y * rq, qy = q4.z * rq, qz = q4.w * rq;
     float R[3][3], M[3][3];
     quat_rot(q4, R);
