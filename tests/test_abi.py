@@ -86,6 +86,14 @@ def test_validation_before_device_work(L):
     P = 256   # any non-NULL, aligned address: the call must return before touching it
     assert lib.gs_rasterize_bwd_nd(ct.byref(o), 1, 10, 64, 64, P, P, 5, null, 10, null, P, P, P, P, P, null, 1,
                                    P, P, P, null) == 2
+    # gs_project_bwd_range: the range must lie in [0, N] and be ordered
+    bad_ranges = [(5, 3), (-1, 4), (0, 11)]
+    for b0, b1 in bad_ranges:
+        assert lib.gs_project_bwd_range(ct.byref(o), 10, b0, b1, 1, 64, 64, *([P] * 5), 16, P, P, P, P,
+                                        *([P] * 5), null) == 1, (b0, b1)
+    # packed options are refused by the dense range call
+    assert lib.gs_project_bwd_range(ct.byref(op), 10, 0, 10, 1, 64, 64, *([P] * 5), 16, P, P, P, P,
+                                    *([P] * 5), null) == 1
     # misaligned workspace
     assert lib.gs_isect_tiles(ct.byref(o), 1, 0, 64, 64, null, null, 0, 8, 8, null, null, 8, 1, 0, null) == 1
 
