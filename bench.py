@@ -96,13 +96,27 @@ def _peaks():
     return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, src="fallback")
 
 
-def _traffic(stage):
-    """DRAM bytes (read + write) per launch of the stage's kernel from the committed
-    `ncu --set full` capture summarised in profiles/traffic.json (None if absent)."""
+def traffic_key(args, views, world):
+    """The workload a committed (single-GPU) ncu capture was taken on: config, views and the
+    non-default modes (profiles/traffic.json is keyed by it); None for N > 1."""
+    if world > 1:
+        return None
+    k = f"{args.config}/views{views}"
+    if args.bbox_mode:
+        k += f"/bbox{args.bbox_mode}"
+    if args.packed:
+        k += "/packed"
+    return k
+
+
+def _traffic(stage, key):
+    """DRAM bytes (read + write) per launch of the stage's kernels from the committed
+    `ncu --set full` capture of THIS workload summarised in profiles/traffic.json (None if
+    there is no capture of it)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p)).get(stage)
+    d = json.load(open(p)).get(key or "", {}).get(stage)
     return None if d is None else d.get("dram_bytes_per_launch")
 
 
@@ -313,6 +327,7 @@ def run_ours(args):
     Kc = 16 if sc["sh_degree"] == 3 else (sc["sh_degree"] + 1) ** 2
     hbm = alg_bytes(N, C, V, N_vis, M, C * W * H, Kc)
     dom = max(stage_ms, key=stage_ms.get)
+    tkey = traffic_key(args, C, world)
     per_stage = {}
     for n_, ms in stage_ms.items():
         v = stage_all[n_]
@@ -322,7 +337,7 @@ def run_ours(args):
              "hbm_frac": round(hbm[n_] / (ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
         if n_ in alu:
             d["alu_frac"] = round(alu[n_] / (ms / 1e3) / alu_peak, 4)
-        tr = _traffic(n_)
+        tr = _traffic(n_, tkey)
         if tr is not None:
             d["dram_bytes_ncu"] = tr
         per_stage[n_] = d
@@ -330,7 +345,7 @@ def run_ours(args):
     if dom in alu:
         ach = alu[dom] / (stage_ms[dom] / 1e3)
         roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2),
-                "unit": "T FP32 instr/s", "frac": round(ach / alu_peak, 4), "traffic": _traffic(dom),
+                "unit": "T FP32 instr/s", "frac": round(ach / alu_peak, 4), "traffic": _traffic(dom, tkey),
                 "peak_src": f"{SMS} SMs x {FP32_LANES_PER_SM} FP32 lanes x {clk_mhz:.0f} MHz ({peaks['src']})",
                 "hbm_frac": per_stage[dom]["hbm_frac"],
                 "work": {"pairs_composited": E_c, "pairs_evaluated_fwd": E_f,
@@ -338,7 +353,7 @@ def run_ours(args):
     else:
         ach = hbm[dom] / (stage_ms[dom] / 1e3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": _traffic(dom), "peak_src": peaks["src"]}
+                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": _traffic(dom, tkey), "peak_src": peaks["src"]}
     step_stats = {"p10": round(float(np.percentile(step_ms, 10)), 4), "p50": round(float(np.percentile(step_ms, 50)), 4),
                   "p90": round(float(np.percentile(step_ms, 90)), 4),
                   "alg_bytes": int(step_bytes),

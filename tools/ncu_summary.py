@@ -2,10 +2,11 @@
 brought back in gpurun_out/).
 
   python tools/ncu_summary.py launches <launches.csv> > profiles/rN_launches.txt
-  python tools/ncu_summary.py full <report.ncu-rep> [--traffic profiles/traffic.json] > profiles/rN_full.txt
+  python tools/ncu_summary.py full <report.ncu-rep> [--traffic profiles/traffic.json --workload garden1m/views1] > profiles/rN_full.txt
 """
 import csv
 import json
+import os
 import re
 import subprocess
 import sys
@@ -63,7 +64,7 @@ def launches(path):
         print(f"   {k:24s} {v / 1e3:9.1f} us  {100 * v / tot:5.1f} %")
 
 
-def full(path, traffic_out=None):
+def full(path, traffic_out=None, workload=None):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, u = rows[0], rows[1]
@@ -85,7 +86,10 @@ def full(path, traffic_out=None):
             t["kernels"].append(name)
             t["dram_bytes_per_launch"] += b   # the stage's kernels of one step summed
     if traffic_out:
-        json.dump(traffic, open(traffic_out, "w"), indent=1)
+        # keyed by the bench workload the capture was taken on (bench.traffic_key)
+        allw = json.load(open(traffic_out)) if os.path.exists(traffic_out) else {}
+        allw[workload] = traffic
+        json.dump(allw, open(traffic_out, "w"), indent=1)
 
 
 if __name__ == "__main__":
@@ -93,4 +97,7 @@ if __name__ == "__main__":
         launches(sys.argv[2])
     else:
         tr = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
-        full(sys.argv[2], tr)
+        wl = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else None
+        if tr and not wl:
+            sys.exit("--traffic needs --workload (the bench workload key, e.g. garden1m/views1)")
+        full(sys.argv[2], tr, wl)
