@@ -20,10 +20,10 @@
 //
 // Radix pass (K4) = three fully parallel kernels (no serial look-back chain, which at
 // these sizes -- 0.6 M and 2.9 M keys -- made a single-pass Onesweep latency-bound):
-// per-block digit histogram, one block per digit scanning that digit's row across blocks
-// (coalesced), and a scatter that ranks the block's 1024 keys stably in shared memory,
-// reorders them by digit there and writes each digit run with consecutive threads.
-// Warp-level multi-split uses 9 ballots per key instead of MATCH.ANY.
+// per-block digit histogram (shared-memory integer atomics), one block per digit scanning
+// that digit's row across blocks (coalesced), and a scatter that ranks the block's 1024 keys
+// stably in shared memory, reorders them by digit there and writes each digit run with
+// consecutive threads.  The scatter's stable warp-level multi-split uses 9 ballots per key.
 //
 // Compiled with -fmad=false: the tile rectangle (Q20) is evaluated in fp32 with the
 // same op order as the oracle so keys match bit for bit.
@@ -34,11 +34,17 @@ namespace {
 
 constexpr int kT = 256;              // threads per block
 constexpr int kWarps = kT / 32;
-constexpr int kItems = 16;           // compaction: items per thread
+#ifndef GS_VIS_ITEMS
+#define GS_VIS_ITEMS 16
+#endif
+constexpr int kItems = GS_VIS_ITEMS; // compaction: items per thread
 constexpr int kTile = kT * kItems;   // compaction: items per block (4096)
 constexpr int kSortItems = 4;        // per-item tile counts and small radix sorts: items per thread ...
 constexpr int kSortTile = kT * kSortItems;   // ... and per block (1024: enough blocks to fill 148 SMs)
 constexpr int kScanThreads = 1024;
+#ifndef GS_SCATTER_MATCH
+#define GS_SCATTER_MATCH 0
+#endif
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -238,7 +244,6 @@ __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ 
     s_hist[threadIdx.x] = 0;
     __syncthreads();
     const int base = blockIdx.x * (kT * IT);
-    const int lane = threadIdx.x & 31;
     uint32_t key[IT];
 #pragma unroll
     for (int k = 0; k < IT; k++) {
@@ -249,8 +254,7 @@ __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ 
     for (int k = 0; k < IT; k++) {
         const int i = base + k * kT + threadIdx.x;
         const unsigned d = i < n ? (key[k] >> shift) & 255u : 256u;
-        const unsigned peers = warp_peers(d);
-        if (d < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[d], __popc(peers));
+        if (d < 256u) atomicAdd(&s_hist[d], 1);
     }
     __syncthreads();
     hist[threadIdx.x * nb_max + blockIdx.x] = s_hist[threadIdx.x];
@@ -330,7 +334,11 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
     for (int k = 0; k < IT; k++) {
         const bool valid = base + k * 32 + lane < n;
         const unsigned d = valid ? (key[k] >> shift) & 255u : 256u;
+#if GS_SCATTER_MATCH
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+#else
         const unsigned peers = warp_peers(d);
+#endif
         int b = 0;
         if (valid) b = s_cnt[warp][d];
         __syncwarp();
@@ -465,6 +473,9 @@ __global__ void __launch_bounds__(kT) k_tiles_emit_warp(const int4* __restrict__
     const int first = __shfl_sync(0xffffffffu, myoff, 0);
     const int end = ent_off[min(j0 + 32, V)];
     const int x0 = e.x & 0xffff, w = (e.x >> 16) - x0, y0 = e.y & 0xffff;
+    // key of the item's first tile: an output's key is kbase + qy TX + qx (one shuffle instead
+    // of four for camera, x0, y0)
+    const uint32_t kbase = (uint32_t)e.w * (uint32_t)g.TT + (uint32_t)(y0 * g.TX + x0);
     const int lim = min(end, n);
     for (int base = first; base < lim; base += 32) {   // warp-uniform trip count
         const int t = base + lane;
@@ -476,14 +487,13 @@ __global__ void __launch_bounds__(kT) k_tiles_emit_warp(const int4* __restrict__
             if (v <= t) lo += step;
         }
         const int kk = t - __shfl_sync(0xffffffffu, myoff, lo);
-        const int ex0 = __shfl_sync(0xffffffffu, x0, lo), ew = __shfl_sync(0xffffffffu, w, lo);
-        const int ey0 = __shfl_sync(0xffffffffu, y0, lo);
-        const int cam = __shfl_sync(0xffffffffu, e.w, lo), id = __shfl_sync(0xffffffffu, e.z, lo);
+        const int ew = __shfl_sync(0xffffffffu, w, lo);
+        const uint32_t kb = __shfl_sync(0xffffffffu, kbase, lo);
+        const int id = __shfl_sync(0xffffffffu, e.z, lo);
         if (t < lim) {
             // kk / w exactly: kk < w h <= 2^24, so floor((kk + 0.5) / w) survives the fp32 rounding
             const int qy = (int)__fdividef((float)kk + 0.5f, (float)ew);
-            const int ty = ey0 + qy, tx = ex0 + (kk - qy * ew);
-            out_key[t] = (uint32_t)cam * (uint32_t)g.TT + (uint32_t)(ty * g.TX + tx);
+            out_key[t] = kb + (uint32_t)(qy * g.TX + (kk - qy * ew));
             out_val[t] = id;
         }
     }

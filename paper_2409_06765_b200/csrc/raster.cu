@@ -623,6 +623,16 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             K7_STAT(2, __popc(vb));
             K7_STAT(3, (vb != 0) && __popc(vb) <= kFewLanes);
             K7_STAT(4, ((vb & 0xffffu) == 0) != ((vb >> 16) == 0));   // only one 4x4 half takes it
+#ifdef GS_K7_STATS
+            {   // why lanes idle in non-empty visits: not yet composited (tidx > last) vs outside the support
+                const unsigned alive = __ballot_sync(0xffffffffu, q.inside && tidx <= last);
+                const unsigned supp = __ballot_sync(0xffffffffu, q.inside && !(pe > 0.f) && alpha >= amin);
+                K7_STAT(5, vb ? __popc(alive) : 0);
+                K7_STAT(6, vb ? __popc(supp) : 0);
+                const unsigned ins = __ballot_sync(0xffffffffu, q.inside);
+                K7_STAT(7, vb ? __popc(ins) : 0);
+            }
+#endif
             if (!vb) return;
             // Branch-free from here: a lane that does not take this splat gets alpha = G = 0,
             // which makes every gradient term below exactly 0 and leaves T and Sv unchanged.

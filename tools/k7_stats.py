@@ -29,3 +29,6 @@ for mode in (0, 2):
     s = list(buf)
     print(f"bbox{mode}: visits {s[0]/1e6:.2f}M empty {s[1]/1e6:.2f}M ({s[1]/s[0]:.1%}) lanes/visit(nonempty) {s[2]/(s[0]-s[1]):.2f} "
           f"few {s[3]/1e6:.2f}M tree {(s[0]-s[1]-s[3])/1e6:.2f}M one-half-only {s[4]/1e6:.2f}M  contributing pairs {s[2]/1e6:.1f}M")
+    ne = s[0] - s[1]
+    print(f"   per non-empty visit: lanes inside {s[7]/ne:.2f}, alive (tidx <= last) {s[5]/ne:.2f}, "
+          f"in support (alpha >= alpha_min) {s[6]/ne:.2f}, contributing {s[2]/ne:.2f}")
