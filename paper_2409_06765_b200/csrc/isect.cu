@@ -35,10 +35,10 @@ namespace {
 constexpr int kT = 256;              // threads per block
 constexpr int kWarps = kT / 32;
 #ifndef GS_VIS_ITEMS
-#define GS_VIS_ITEMS 16
+#define GS_VIS_ITEMS 4
 #endif
 constexpr int kItems = GS_VIS_ITEMS; // compaction: items per thread
-constexpr int kTile = kT * kItems;   // compaction: items per block (4096)
+constexpr int kTile = kT * kItems;   // compaction: items per block (1024: ~1000 blocks at 1 M items)
 constexpr int kSortItems = 4;        // per-item tile counts and small radix sorts: items per thread ...
 constexpr int kSortTile = kT * kSortItems;   // ... and per block (1024: enough blocks to fill 148 SMs)
 constexpr int kScanThreads = 1024;
