@@ -445,7 +445,7 @@ def run_ours(args):
         e2e["full_param_roundtrip"]["inputs"] = ("per step: every Gaussian parameter, the cameras and dL/d(image) "
                                                  "up, the image and the whole flat gradient back")
 
-    launches = eng.launches_per_step()   # library kernels per step (31 at configs[1], = the ncu launch list)
+    launches = eng.launches_per_step()   # library kernels per step (32 at configs[1], = the ncu launch list)
 
     # ---- variant: the opacity-aware tile extent (bbox_mode 2, Q36: same images and
     # gradients, fewer intersections), timed the same way on the same inputs ----

@@ -109,7 +109,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 9
+#define GS_ABI_VERSION 10
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -193,13 +193,26 @@ GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N,
  *      with the same depth_mode; depth is composited as a fourth channel, its per-splat
  *      gradient accumulates into gradient slot 9; mode 2 (expected depth D/A) also needs the
  *      forward's out_depth and adds -v E / A to the alpha gradient (quotient rule, Q26).
- * isect_masks: the forward's mask output or NULL (recomputed). */
+ * isect_masks: the forward's mask output or NULL (recomputed).
+ * tile_order [C*TY*TX] int32 or NULL: the launch order of the (camera, tile) bins
+ *      (gs_tile_order; NULL = camera-major, tile-ascending).  It changes only the order of
+ *      the fp32 atomic additions, not the value of any term. */
 GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t width, int32_t height,
                            const float* splats, const float* backgrounds, const int32_t* isect_ids,
                            const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
                            const float* v_out_rgb, const float* v_out_alpha, const float* out_depth,
                            const float* v_out_depth, int32_t depth_mode, int32_t absgrad,
-                           const uint16_t* isect_masks, float* v_splats, void* stream);
+                           const uint16_t* isect_masks, const int32_t* tile_order, float* v_splats,
+                           void* stream);
+
+/* ---- Launch order of the backward composite (scheduling only) ---------------------
+ * tile_order [C*TY*TX] int32 := every bin c*TY*TX + t of tile_offsets, camera by camera,
+ * each camera's tiles in descending order of list length (counting sort on buckets of 16
+ * intersections, arbitrary order inside a bucket) -- the longest tiles of the backward
+ * start first, so its tail holds short ones.  A permutation of the bins; pass it to
+ * gs_rasterize_bwd.  Depends on tile_offsets only. */
+GS_API gs_status gs_tile_order(const gs_options* opt, int32_t C, int32_t width, int32_t height,
+                               const int32_t* tile_offsets, int32_t* tile_order, void* stream);
 
 /* ---- Stage 4b: projection backward (P1-P9) -------------------------------
  * In : the gs_project inputs, its radii output, v_splats from gs_rasterize_bwd.

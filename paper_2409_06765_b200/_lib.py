@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 9
+ABI_VERSION = 10
 # largest item / record count of one call: ids and capacities are int32 (include/gs.h)
 MAX_ITEMS = (1 << 31) - 2048
 
@@ -51,7 +51,8 @@ SIGNATURES = {
     "gs_rasterize_fwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
     "gs_rasterize_stats": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P,
-                                _P, _P]),
+                                _P, _P, _P]),
+    "gs_tile_order": (_I32, [_P, _I32, _I32, _I32, _P, _P, _P]),
     "gs_project_bwd_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                               _P, _P, _P, _P, _SZ, _P]),
@@ -187,16 +188,22 @@ def gs_rasterize_stats(o, C, N, width, height, splats, isect_ids, tile_offsets, 
 
 def gs_rasterize_bwd(o, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T, last_ids,
                      v_out_rgb, v_out_alpha, absgrad, v_splats, out_depth=None, v_out_depth=None, depth_mode=0,
-                     isect_masks=None, stream=None):
+                     isect_masks=None, stream=None, tile_order=None):
     check(lib().gs_rasterize_bwd(ct.byref(o), C, N, width, height, ptr(splats, name="splats"),
                                  ptr(backgrounds, name="backgrounds"), ptr(isect_ids, torch.int32, "isect_ids"),
                                  ptr(tile_offsets, torch.int32, "tile_offsets"), ptr(out_T, name="out_T"),
                                  ptr(last_ids, torch.int32, "last_ids"), ptr(v_out_rgb, name="v_out_rgb"),
                                  ptr(v_out_alpha, name="v_out_alpha"), ptr(out_depth, name="out_depth"),
                                  ptr(v_out_depth, name="v_out_depth"), int(depth_mode), int(bool(absgrad)),
-                                 ptr(isect_masks, torch.int16, "isect_masks"), ptr(v_splats, name="v_splats"),
+                                 ptr(isect_masks, torch.int16, "isect_masks"),
+                                 ptr(tile_order, torch.int32, "tile_order"), ptr(v_splats, name="v_splats"),
                                  stream_ptr(stream)),
           "gs_rasterize_bwd")
+
+
+def gs_tile_order(o, C, width, height, tile_offsets, tile_order, stream=None):
+    check(lib().gs_tile_order(ct.byref(o), C, width, height, ptr(tile_offsets, torch.int32, "tile_offsets"),
+                              ptr(tile_order, torch.int32, "tile_order"), stream_ptr(stream)), "gs_tile_order")
 
 
 def gs_project_bwd_workspace_size(N, C):

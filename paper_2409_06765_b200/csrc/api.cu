@@ -169,17 +169,25 @@ gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
                            const int32_t* tile_offsets, const float* out_T, const int32_t* last_ids,
                            const float* v_out_rgb, const float* v_out_alpha, const float* out_depth,
                            const float* v_out_depth, int32_t depth_mode, int32_t absgrad,
-                           const uint16_t* isect_masks, float* v_splats, void* stream) {
+                           const uint16_t* isect_masks, const int32_t* tile_order, float* v_splats, void* stream) {
     GS_TRY(check_opts(opt));
     GS_TRY(check_raster_dims(opt, N, C, width, height));
     GS_REQ(tile_offsets && out_T && last_ids && v_out_rgb && (v_splats || N == 0));
     GS_REQ(!v_out_depth || depth_mode == 1 || (depth_mode == 2 && out_depth));
     GS_REQ(aligned16(splats) && aligned16(v_splats) && aligned4(isect_ids) && aligned4(backgrounds) &&
            aligned4(out_T) && aligned4(last_ids) && aligned4(v_out_rgb) && aligned4(v_out_alpha) &&
-           aligned4(out_depth) && aligned4(v_out_depth));
+           aligned4(out_depth) && aligned4(v_out_depth) && aligned4(tile_order));
     return gsb::launch_raster_bwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T,
                                   last_ids, v_out_rgb, v_out_alpha, out_depth, v_out_depth, depth_mode, absgrad,
-                                  isect_masks, v_splats, static_cast<cudaStream_t>(stream));
+                                  isect_masks, tile_order, v_splats, static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_tile_order(const gs_options* opt, int32_t C, int32_t width, int32_t height,
+                        const int32_t* tile_offsets, int32_t* tile_order, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_TRY(check_dims(0, C, width, height));
+    GS_REQ(tile_offsets && tile_order && aligned4(tile_offsets) && aligned4(tile_order));
+    return gsb::launch_tile_order(C, width, height, tile_offsets, tile_order, static_cast<cudaStream_t>(stream));
 }
 
 size_t gs_project_bwd_workspace_size(int64_t N, int32_t C) {

@@ -120,7 +120,9 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
                             const float* bg, const int32_t* ids, const int32_t* offs, const float* out_T,
                             const int32_t* last_ids, const float* v_rgb, const float* v_alpha,
                             const float* out_depth, const float* v_depth, int depth_mode, int absgrad,
-                            const uint16_t* isect_masks, float* v_splats, cudaStream_t s);
+                            const uint16_t* isect_masks, const int32_t* tile_order, float* v_splats,
+                            cudaStream_t s);
+gs_status launch_tile_order(int C, int W, int H, const int32_t* offs, int32_t* order, cudaStream_t s);
 gs_status launch_raster_fwd_nd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                                const float* feats, int D, const int32_t* gids, const float* bg, const int32_t* ids,
                                const int32_t* offs, float* out_feats, float* out_alpha, float* out_T,

@@ -191,7 +191,22 @@ struct RasterParams {
     // support masks of every staged (intersection) slot, written by K6 and read back by K7
     // (NULL: K7 recomputes them)
     uint16_t* smask;
+    // launch order of the (camera, tile) bins (NULL: blockIdx order; gs_tile_order)
+    const int32_t* order;
 };
+
+// (camera, tile) bin of this CTA
+__device__ __forceinline__ void cta_bin(const RasterParams& p, int& tile, int& cam) {
+    if (p.order) {
+        const int b = p.order[blockIdx.y * gridDim.x + blockIdx.x];
+        const int TT = p.TX * p.TY;
+        cam = b / TT;
+        tile = b - cam * TT;
+    } else {
+        tile = blockIdx.x;
+        cam = blockIdx.y;
+    }
+}
 
 // Gaussian of a record (dense ids are c*N + n; packed records carry it in gids)
 __device__ __forceinline__ int64_t gauss_of(const RasterParams& p, int32_t g, int cam) {
@@ -285,7 +300,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     pdl_trigger();
     pdl_wait();
     __shared__ StageFwd s;
-    const int tile = blockIdx.x, cam = blockIdx.y;
+    int tile, cam;
+    cta_bin(p, tile, cam);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // warp w: 8x4 block at (8 (w&1), 4 (w>>1)); half h = lane>>4: its left/right 4x4 block
     const int half = lane >> 4, l4 = lane & 15;
@@ -548,7 +564,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     pdl_wait();
     __shared__ Stage<kBatchBwd> s;
     __shared__ int s_maxlast;
-    const int tile = blockIdx.x, cam = blockIdx.y;
+    int tile, cam;
+    cta_bin(p, tile, cam);
     const PixelCoord q = pixel_coord(p, tile);
     const int bin = cam * p.TX * p.TY + tile;
     const int start = p.offs[bin];
@@ -756,6 +773,51 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
 }
 
 constexpr int kZeroBlocks = 148 * 8;
+
+// Launch order of the backward's (camera, tile) bins: per camera (one block each; the
+// cameras stay in sequence, so a camera's records stay hot in L2), its bins in descending
+// order of list length -- counting sort on 256 length buckets of 16 intersections -- so the
+// longest tiles start first and the launch's tail is made of short ones (the order within a
+// bucket is arbitrary: it changes only the fp32 atomic summation order of the gradients).
+__global__ void __launch_bounds__(1024) k_tile_order(const int32_t* __restrict__ offs, int TT, int32_t* order) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ int s_cnt[256];
+    const int base = blockIdx.x * TT;
+    if (threadIdx.x < 256) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < TT; t += 1024) {
+        const int len = offs[base + t + 1] - offs[base + t];
+        atomicAdd(&s_cnt[255 - min(255, len >> 4)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the 256 bucket counts, 8 per lane
+        const int lane = threadIdx.x;
+        int v[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            v[k] = s_cnt[8 * lane + k];
+            sum += v[k];
+        }
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int run = x - sum;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            s_cnt[8 * lane + k] = run;
+            run += v[k];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < TT; t += 1024) {
+        const int len = offs[base + t + 1] - offs[base + t];
+        order[base + atomicAdd(&s_cnt[255 - min(255, len >> 4)], 1)] = base + t;
+    }
+}
 #ifndef GS_FWD_PAD
 #define GS_FWD_PAD 4096
 #endif
@@ -811,14 +873,15 @@ gs_status launch_raster_stats(const gs_options& o, int C, int64_t N, int W, int 
 gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats, const float* bg,
                             const int32_t* ids, const int32_t* offs, const float* out_T, const int32_t* last_ids,
                             const float* v_rgb, const float* v_alpha, const float* out_depth, const float* v_depth,
-                            int depth_mode, int absgrad, const uint16_t* isect_masks, float* v_splats,
-                            cudaStream_t s) {
+                            int depth_mode, int absgrad, const uint16_t* isect_masks, const int32_t* tile_order,
+                            float* v_splats, cudaStream_t s) {
     RasterParams p = make_params(o, C, N, W, H, splats, bg, ids, offs);
     p.smask = const_cast<uint16_t*>(isect_masks);
     p.out_T = const_cast<float*>(out_T); p.last_ids = const_cast<int32_t*>(last_ids);
     p.v_rgb = v_rgb; p.v_alpha = v_alpha; p.v_splats = v_splats; p.absgrad = absgrad;
     p.out_depth = const_cast<float*>(out_depth); p.v_depth = v_depth;
     p.depth_mode = v_depth ? depth_mode : 0;
+    p.order = tile_order;
     const size_t nrec = o.packed ? (size_t)N : (size_t)C * (size_t)N;   // packed: N records in total (Q29)
     // zero-fill as a kernel (not cudaMemsetAsync) so the chain keeps programmatic dependent launch
     if (N > 0)
@@ -833,6 +896,13 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
         else launch_pdl(k_raster_bwd<false, false, false>, dim3(grid), dim3(kThreads), s, p);
     }
     GS_LAUNCH_CHECK("k_raster_bwd");
+    return GS_OK;
+}
+
+gs_status launch_tile_order(int C, int W, int H, const int32_t* offs, int32_t* order, cudaStream_t s) {
+    const int TT = div_up(W, GS_TILE) * div_up(H, GS_TILE);
+    launch_pdl(k_tile_order, dim3(C), dim3(1024), s, offs, TT, order);
+    GS_LAUNCH_CHECK("k_tile_order");
     return GS_OK;
 }
 

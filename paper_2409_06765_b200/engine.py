@@ -30,7 +30,7 @@ from . import dist as D
 class Engine:
     def __init__(self, N, C, width, height, sh_degree=3, K=None, antialiased=False, M_capacity=None,
                  device="cuda", absgrad=False, with_keys=False, packed=False, nnz_capacity=None, depth_mode=0,
-                 pose=False, **opt_kwargs):
+                 pose=False, tile_order=True, **opt_kwargs):
         self.N, self.C, self.W, self.H = int(N), int(C), int(width), int(height)
         self.sh_degree = int(sh_degree)
         self.K = (K if K is not None else (self.sh_degree + 1) ** 2) if self.sh_degree >= 0 else 1
@@ -60,6 +60,8 @@ class Engine:
         self.M = torch.zeros(1, dtype=torch.int64, device=dev)
         self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
         self.tile_offsets = torch.zeros(C * self.TX * self.TY + 1, dtype=torch.int32, device=dev)
+        # launch order of the backward's bins: longest tile lists first (gs_tile_order)
+        self.tile_order = torch.zeros(C * self.TX * self.TY, dtype=torch.int32, device=dev) if tile_order else None
         self.out_rgb = torch.zeros((C, H, W, 3), dtype=torch.float32, device=dev)
         self.out_alpha = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
         self.out_T = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
@@ -142,14 +144,15 @@ class Engine:
     def launches_per_step(self) -> int:
         """Kernels of the library launched by one step(): project 1; isect 3 (compaction) +
         3x4 (depth sort) + 3 (tile counts, scan, offsets) + 1 (emission) + 3P (tile sort,
-        P = ceil(bits/8)) + 1 (ranges); raster fwd 1; raster bwd 2 (zero-fill + walk);
-        project bwd 1 (+1 pose reduction)."""
+        P = ceil(bits/8)) + 1 (ranges); raster fwd 1; raster bwd 2 (zero-fill + walk) + 1
+        (tile order); project bwd 1 (+1 pose reduction)."""
         bits = max(1, (self.C * self.TX * self.TY - 1).bit_length())
         P = (bits + 7) // 8
         pose = 1 if self.pose else 0      # k_pose_reduce
+        order = 1 if self.tile_order is not None else 0   # k_tile_order
         if self.packed:   # project: count, scan, write; isect: identity items; project bwd: map + kernel
-            return 3 + (1 + 12 + 3 + 1 + 3 * P + 1) + 1 + 2 + 2 + pose
-        return 1 + (3 + 12 + 3 + 1 + 3 * P + 1) + 1 + 2 + 1 + pose
+            return 3 + (1 + 12 + 3 + 1 + 3 * P + 1) + 1 + 2 + order + 2 + pose
+        return 1 + (3 + 12 + 3 + 1 + 3 * P + 1) + 1 + 2 + order + 1 + pose
 
     @property
     def n_isect(self) -> int:
@@ -182,11 +185,13 @@ class Engine:
                            stream=stream)
 
     def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None):
+        if self.tile_order is not None:
+            L.gs_tile_order(self.opts, self.C, self.W, self.H, self.tile_offsets, self.tile_order, stream)
         L.gs_rasterize_bwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
                            self.isect_ids, self.tile_offsets, self.out_T, self.last_ids, v_rgb, v_alpha,
                            self.absgrad, self.v_splats, out_depth=self.out_depth,
                            v_out_depth=v_depth if self.depth_mode else None, depth_mode=self.depth_mode,
-                           isect_masks=self.isect_masks, stream=stream)
+                           isect_masks=self.isect_masks, stream=stream, tile_order=self.tile_order)
 
     def project_bwd(self, means, quats, scales, opacities, colors, viewmats, Ks, stream=None):
         if self.packed:

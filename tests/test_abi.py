@@ -51,7 +51,7 @@ def test_defaults_match_oracle_constants(L):
 
 def test_status_strings_and_version(L):
     lib = L.lib()
-    assert lib.gs_abi_version() == 9
+    assert lib.gs_abi_version() == 10
     assert lib.gs_status_string(0) == b"ok"
     assert lib.gs_status_string(2) == b"unsupported"
 

@@ -673,3 +673,32 @@ def test_bbox_mode1_square_box(name):
     assert np.array_equal(gpu["offsets"], ref["offsets"])
     U.assert_images(gpu, ref, label=f"bbox1/{name}")
     U.assert_grads(sc, gpu, ref, label=f"bbox1/{name}")
+
+
+def test_tile_order_is_a_permutation_and_output_invariant():
+    """gs_tile_order: a permutation of the bins, camera by camera, each camera's tiles in
+    non-increasing length bucket; gs_rasterize_bwd launched in that order gives the natural
+    order's gradients up to fp32 atomic order (same-kernel bound)."""
+    import torch
+    sc = S.mipnerf_like_scene(20000, width=320, height=200, views=2, sh_degree=3, seed=11)
+    C, N, W, H = 2, 20000, 320, 200
+    v_img, _ = S.image_grads(0, C, H, W, l1_scale=False)
+    ordered = U.run_gpu(sc, v_img=v_img)             # Engine default: tile order on
+    natural = U.run_gpu(sc, v_img=v_img, tile_order=False)
+    eng = ordered["engine"]
+    TT = eng.TX * eng.TY
+    order = eng.tile_order.cpu().numpy()
+    offs = ordered["offsets"]
+    assert np.array_equal(np.sort(order), np.arange(C * TT))
+    for c in range(C):
+        oc = order[c * TT:(c + 1) * TT]
+        assert np.all((oc >= c * TT) & (oc < (c + 1) * TT))
+        bucket = np.minimum(255, (offs[oc + 1] - offs[oc]) >> 4)
+        assert np.all(np.diff(bucket) <= 0)
+    for k in ["rgb", "T", "last_ids"]:
+        assert np.array_equal(ordered[k], natural[k]), k
+    o = oracle.Options(sh_degree=3)
+    b = oracle.render_bwd(oracle.project(sc, o), C, N, W, H, o, v_img.astype(np.float64))
+    rep = {k: natural[k] for k in U.GRAD_KEYS}
+    U.assert_same_kernel_grads(sc, o, b, rep, ordered, label="tile-order", vs_one=natural["v_splats"],
+                               vs_other=ordered["v_splats"])
