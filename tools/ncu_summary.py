@@ -12,7 +12,8 @@ import subprocess
 import sys
 
 STAGE_OF = {"k_project_fwd": "project", "k_raster_fwd": "raster_fwd", "k_raster_bwd": "raster_bwd",
-            "k_project_bwd": "project_bwd", "k_zero4": "raster_bwd"}
+            "k_project_bwd": "project_bwd", "k_zero4": "raster_bwd", "k_tile_work": "raster_bwd",
+            "k_tile_order": "raster_bwd"}
 ISECT = ("k_vis_", "k_scan_blocksums", "k_radix_", "k_tiles_", "k_ranges", "k_packed_items", "k_keys64")
 
 
