@@ -85,6 +85,9 @@ typedef struct gs_options {
     int32_t support_cull;/* 1 (default): stages 3/4a skip (splat, 4x4-pixel block) pairs
                            outside the conservative alpha-support of DESIGN.md K6 -- output
                            invariant; 0: evaluate every pair of the tile (verification)   */
+    int32_t bwd_zero_fill;/* 1 (default): gs_rasterize_bwd / _nd zero-fill v_splats before
+                           accumulating; 0: the caller has zero-filled it (gs_zero_splat_grads,
+                           e.g. on a second stream overlapping the forward)              */
 } gs_options;
 
 /* ---- Projected splat record ------------------------------------------------------
@@ -109,7 +112,7 @@ GS_API void gs_default_options(gs_options* opt);
 GS_API const char* gs_status_string(int32_t status);
 GS_API const char* gs_last_error(void);     /* last CUDA error text of this thread, "" if none */
 GS_API int32_t gs_abi_version(void);         /* = GS_ABI_VERSION */
-#define GS_ABI_VERSION 10
+#define GS_ABI_VERSION 11
 
 /* ---- Stage 1: projection (F1-F15; App. B.1, A.4 P:266-285) ---------------
  * In : means [N,3], quats [N,4] (w,x,y,z), scales [N,3], opacities [N],
@@ -187,8 +190,8 @@ GS_API gs_status gs_rasterize_stats(const gs_options* opt, int32_t C, int64_t N,
  * recurrence; per-(c,n) sums over pixels are accumulated with fp32 atomics.
  * In : as gs_rasterize_fwd plus out_T, last_ids, v_out_rgb [C,H,W,3],
  *      v_out_alpha [C,H,W] or NULL.
- * Out: v_splats [C,N,GS_SPLAT_FLOATS] ([N,...] when opt->packed; zero-filled here, then accumulated; slot layout
- *      above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 10, 11.
+ * Out: v_splats [C,N,GS_SPLAT_FLOATS] ([N,...] when opt->packed; zero-filled here unless
+ *      opt->bwd_zero_fill == 0, then accumulated; slot layout above).  absgrad != 0 also accumulates sum |v_mean2d| per pixel into slots 10, 11.
  * Depth (NULL v_out_depth = off): v_out_depth [C,H,W] = dL/d out_depth of the forward
  *      with the same depth_mode; depth is composited as a fourth channel, its per-splat
  *      gradient accumulates into gradient slot 9; mode 2 (expected depth D/A) also needs the
@@ -213,6 +216,13 @@ GS_API gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, i
  * gs_rasterize_bwd.  Depends on tile_offsets only. */
 GS_API gs_status gs_tile_order(const gs_options* opt, int32_t C, int32_t width, int32_t height,
                                const int32_t* tile_offsets, int32_t* tile_order, void* stream);
+
+/* ---- Zero-fill of the record gradients (scheduling only) ---------------------------
+ * v_splats [C,N,GS_SPLAT_FLOATS] ([N,...] when opt->packed) := 0: the zero-fill that
+ * gs_rasterize_bwd performs itself unless opt->bwd_zero_fill == 0.  It depends on nothing of
+ * the step but the previous reader of v_splats (gs_project_bwd), so a caller can run it on a
+ * second stream while the projection and intersection stages run. */
+GS_API gs_status gs_zero_splat_grads(const gs_options* opt, int32_t C, int64_t N, float* v_splats, void* stream);
 
 /* ---- Stage 4b: projection backward (P1-P9) -------------------------------
  * In : the gs_project inputs, its radii output, v_splats from gs_rasterize_bwd.

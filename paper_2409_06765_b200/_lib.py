@@ -15,7 +15,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsplat_b200.so")
 SPLAT_FLOATS = 12
-ABI_VERSION = 10
+ABI_VERSION = 11
 # largest item / record count of one call: ids and capacities are int32 (include/gs.h)
 MAX_ITEMS = (1 << 31) - 2048
 
@@ -28,7 +28,7 @@ class GsOptions(ct.Structure):
         ("alpha_max", ct.c_float), ("alpha_min", ct.c_float), ("t_min", ct.c_float),
         ("tile_size", ct.c_int32), ("antialiased", ct.c_int32), ("sh_degree", ct.c_int32),
         ("bbox_mode", ct.c_int32), ("fov_clamp", ct.c_int32), ("packed", ct.c_int32),
-        ("support_cull", ct.c_int32),
+        ("support_cull", ct.c_int32), ("bwd_zero_fill", ct.c_int32),
     ]
 
 
@@ -53,6 +53,7 @@ SIGNATURES = {
     "gs_rasterize_bwd": (_I32, [_P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P,
                                 _P, _P, _P]),
     "gs_tile_order": (_I32, [_P, _I32, _I32, _I32, _P, _P, _P]),
+    "gs_zero_splat_grads": (_I32, [_P, _I32, _I64, _P, _P]),
     "gs_project_bwd_workspace_size": (_SZ, [_I64, _I32]),
     "gs_project_bwd": (_I32, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P,
                               _P, _P, _P, _P, _SZ, _P]),
@@ -103,7 +104,7 @@ def check(status: int, what: str) -> None:
 
 def options(sh_degree=3, antialiased=False, near_plane=0.01, far_plane=1e10, eps2d=0.3, alpha_max=0.99,
             alpha_min=1.0 / 255.0, t_min=1e-4, tile_size=16, bbox_mode=0, fov_clamp=True,
-            packed=False, support_cull=True) -> GsOptions:
+            packed=False, support_cull=True, bwd_zero_fill=True) -> GsOptions:
     o = GsOptions()
     lib().gs_default_options(ct.byref(o))
     o.near_plane, o.far_plane, o.eps2d = near_plane, far_plane, eps2d
@@ -112,6 +113,7 @@ def options(sh_degree=3, antialiased=False, near_plane=0.01, far_plane=1e10, eps
     o.bbox_mode, o.fov_clamp = int(bbox_mode), int(bool(fov_clamp))
     o.packed = int(bool(packed))
     o.support_cull = int(bool(support_cull))
+    o.bwd_zero_fill = int(bool(bwd_zero_fill))
     return o
 
 
@@ -199,6 +201,11 @@ def gs_rasterize_bwd(o, C, N, width, height, splats, backgrounds, isect_ids, til
                                  ptr(tile_order, torch.int32, "tile_order"), ptr(v_splats, name="v_splats"),
                                  stream_ptr(stream)),
           "gs_rasterize_bwd")
+
+
+def gs_zero_splat_grads(o, C, N, v_splats, stream=None):
+    check(lib().gs_zero_splat_grads(ct.byref(o), C, N, ptr(v_splats, name="v_splats"), stream_ptr(stream)),
+          "gs_zero_splat_grads")
 
 
 def gs_tile_order(o, C, width, height, tile_offsets, tile_order, stream=None):

@@ -28,6 +28,7 @@ gs_status check_opts(const gs_options* o) {
         return GS_ERR_INVALID_ARGUMENT;
     if (o->bbox_mode < 0 || o->bbox_mode > 2 || o->packed < 0 || o->packed > 1) return GS_ERR_INVALID_ARGUMENT;
     if (o->support_cull < 0 || o->support_cull > 1) return GS_ERR_INVALID_ARGUMENT;
+    if (o->bwd_zero_fill < 0 || o->bwd_zero_fill > 1) return GS_ERR_INVALID_ARGUMENT;
     return GS_OK;
 }
 
@@ -78,6 +79,7 @@ void gs_default_options(gs_options* o) {
     o->fov_clamp = 1;
     o->packed = 0;
     o->support_cull = 1;
+    o->bwd_zero_fill = 1;
 }
 
 const char* gs_status_string(int32_t s) {
@@ -180,6 +182,13 @@ gs_status gs_rasterize_bwd(const gs_options* opt, int32_t C, int64_t N, int32_t 
     return gsb::launch_raster_bwd(*opt, C, N, width, height, splats, backgrounds, isect_ids, tile_offsets, out_T,
                                   last_ids, v_out_rgb, v_out_alpha, out_depth, v_out_depth, depth_mode, absgrad,
                                   isect_masks, tile_order, v_splats, static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_zero_splat_grads(const gs_options* opt, int32_t C, int64_t N, float* v_splats, void* stream) {
+    GS_TRY(check_opts(opt));
+    GS_REQ(N >= 0 && C >= 1 && (v_splats || N == 0) && aligned16(v_splats));
+    const size_t nrec = opt->packed ? (size_t)N : (size_t)C * (size_t)N;
+    return gsb::launch_zero_splat_grads(v_splats, nrec, static_cast<cudaStream_t>(stream));
 }
 
 gs_status gs_tile_order(const gs_options* opt, int32_t C, int32_t width, int32_t height,

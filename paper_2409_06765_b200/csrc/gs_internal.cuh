@@ -123,6 +123,7 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
                             const uint16_t* isect_masks, const int32_t* tile_order, float* v_splats,
                             cudaStream_t s);
 gs_status launch_tile_order(int C, int W, int H, const int32_t* offs, int32_t* order, cudaStream_t s);
+gs_status launch_zero_splat_grads(float* v_splats, size_t nrec, cudaStream_t s);
 gs_status launch_raster_fwd_nd(const gs_options& o, int C, int64_t N, int W, int H, const float* splats,
                                const float* feats, int D, const int32_t* gids, const float* bg, const int32_t* ids,
                                const int32_t* offs, float* out_feats, float* out_alpha, float* out_T,

@@ -884,7 +884,7 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
     p.order = tile_order;
     const size_t nrec = o.packed ? (size_t)N : (size_t)C * (size_t)N;   // packed: N records in total (Q29)
     // zero-fill as a kernel (not cudaMemsetAsync) so the chain keeps programmatic dependent launch
-    if (N > 0)
+    if (N > 0 && o.bwd_zero_fill)
         launch_pdl(k_zero4, dim3(kZeroBlocks), dim3(256), s, reinterpret_cast<float4*>(v_splats),
                    (int64_t)(nrec * GS_SPLAT_FLOATS / 4));
     dim3 grid(p.TX * p.TY, C);
@@ -896,6 +896,14 @@ gs_status launch_raster_bwd(const gs_options& o, int C, int64_t N, int W, int H,
         else launch_pdl(k_raster_bwd<false, false, false>, dim3(grid), dim3(kThreads), s, p);
     }
     GS_LAUNCH_CHECK("k_raster_bwd");
+    return GS_OK;
+}
+
+gs_status launch_zero_splat_grads(float* v_splats, size_t nrec, cudaStream_t s) {
+    if (nrec > 0)
+        launch_pdl(k_zero4, dim3(kZeroBlocks), dim3(256), s, reinterpret_cast<float4*>(v_splats),
+                   (int64_t)(nrec * GS_SPLAT_FLOATS / 4));
+    GS_LAUNCH_CHECK("k_zero4");
     return GS_OK;
 }
 
@@ -937,7 +945,7 @@ gs_status launch_raster_bwd_nd(const gs_options& o, int C, int64_t N, int W, int
     p.smask = const_cast<uint16_t*>(isect_masks);
     p.feats = feats; p.D = D; p.gids = gids; p.v_feats_img = v_feats_img; p.v_feats = v_feats;
     const size_t nrec = o.packed ? (size_t)N : (size_t)C * (size_t)N;
-    if (N > 0)
+    if (N > 0 && o.bwd_zero_fill)
         launch_pdl(k_zero4, dim3(kZeroBlocks), dim3(256), s, reinterpret_cast<float4*>(v_splats),
                    (int64_t)(nrec * GS_SPLAT_FLOATS / 4));
     if (n_gauss > 0 && cudaMemsetAsync(v_feats, 0, sizeof(float) * (size_t)n_gauss * (size_t)D, s) != cudaSuccess) {

@@ -30,7 +30,7 @@ from . import dist as D
 class Engine:
     def __init__(self, N, C, width, height, sh_degree=3, K=None, antialiased=False, M_capacity=None,
                  device="cuda", absgrad=False, with_keys=False, packed=False, nnz_capacity=None, depth_mode=0,
-                 pose=False, tile_order=True, **opt_kwargs):
+                 pose=False, tile_order=True, overlap_prep=True, **opt_kwargs):
         self.N, self.C, self.W, self.H = int(N), int(C), int(width), int(height)
         self.sh_degree = int(sh_degree)
         self.K = (K if K is not None else (self.sh_degree + 1) ** 2) if self.sh_degree >= 0 else 1
@@ -41,6 +41,12 @@ class Engine:
         self.depth_mode = int(depth_mode)   # 0 off | 1 accumulated | 2 expected depth
         self.pose = bool(pose)              # camera pose gradients
         self.opts = L.options(sh_degree=self.sh_degree, antialiased=antialiased, packed=self.packed, **opt_kwargs)
+        # step(): the backward's preparation -- zero-filling the record gradients, the tile
+        # launch order -- runs on a second stream while the forward runs (gs_zero_splat_grads,
+        # gs_tile_order), and gs_rasterize_bwd is told not to zero-fill (bwd_zero_fill = 0)
+        self.overlap_prep = bool(overlap_prep)
+        self._opts_prepped = L.options(sh_degree=self.sh_degree, antialiased=antialiased, packed=self.packed,
+                                       bwd_zero_fill=False, **opt_kwargs)
         self.TX, self.TY = L.tiles(self.W, self.H)
         dev = self.device
         C, N, W, H = self.C, self.N, self.W, self.H
@@ -62,6 +68,9 @@ class Engine:
         self.tile_offsets = torch.zeros(C * self.TX * self.TY + 1, dtype=torch.int32, device=dev)
         # launch order of the backward's bins: longest tile lists first (gs_tile_order)
         self.tile_order = torch.zeros(C * self.TX * self.TY, dtype=torch.int32, device=dev) if tile_order else None
+        if self.overlap_prep:
+            self._side = torch.cuda.Stream(dev)
+            self._ev = [torch.cuda.Event() for _ in range(3)]
         self.out_rgb = torch.zeros((C, H, W, 3), dtype=torch.float32, device=dev)
         self.out_alpha = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
         self.out_T = torch.zeros((C, H, W), dtype=torch.float32, device=dev)
@@ -145,7 +154,8 @@ class Engine:
         """Kernels of the library launched by one step(): project 1; isect 3 (compaction) +
         3x4 (depth sort) + 3 (tile counts, scan, offsets) + 1 (emission) + 3P (tile sort,
         P = ceil(bits/8)) + 1 (ranges); raster fwd 1; raster bwd 2 (zero-fill + walk) + 1
-        (tile order); project bwd 1 (+1 pose reduction)."""
+        (tile order); project bwd 1 (+1 pose reduction).  With overlap_prep the zero-fill and
+        the tile order run on the side stream."""
         bits = max(1, (self.C * self.TX * self.TY - 1).bit_length())
         P = (bits + 7) // 8
         pose = 1 if self.pose else 0      # k_pose_reduce
@@ -184,10 +194,13 @@ class Engine:
                            self.last_ids, self.out_depth, self.depth_mode, isect_masks=self.isect_masks,
                            stream=stream)
 
-    def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None):
-        if self.tile_order is not None:
+    def rasterize_bwd(self, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None, prepped=False):
+        """prepped: _prep_begin / _prep_order already zero-filled v_splats and wrote the tile
+        order on the side stream (and the caller's stream has waited for them)."""
+        if self.tile_order is not None and not prepped:
             L.gs_tile_order(self.opts, self.C, self.W, self.H, self.tile_offsets, self.tile_order, stream)
-        L.gs_rasterize_bwd(self.opts, self.C, self.n_items, self.W, self.H, self.splats, backgrounds,
+        L.gs_rasterize_bwd(self._opts_prepped if prepped else self.opts, self.C, self.n_items, self.W, self.H,
+                           self.splats, backgrounds,
                            self.isect_ids, self.tile_offsets, self.out_T, self.last_ids, v_rgb, v_alpha,
                            self.absgrad, self.v_splats, out_depth=self.out_depth,
                            v_out_depth=v_depth if self.depth_mode else None, depth_mode=self.depth_mode,
@@ -216,11 +229,35 @@ class Engine:
         self.rasterize_bwd(v_rgb, v_alpha, backgrounds, v_depth, stream)
         self.project_bwd(means, quats, scales, opacities, colors, viewmats, Ks, stream)
 
+    def head(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None):
+        """Everything of step() but the projection backward.  With overlap_prep the record
+        gradients are zero-filled on the side stream while the projection and intersection
+        run, and the tile order is computed there while the forward composite runs."""
+        if not self.overlap_prep:
+            self.forward(*params, backgrounds=backgrounds, stream=stream)
+            self.rasterize_bwd(v_rgb, v_alpha, backgrounds, v_depth, stream)
+            return
+        cur = stream if stream is not None else torch.cuda.current_stream(self.device)
+        side, ev = self._side, self._ev
+        ev[0].record(cur)                 # after the previous reader of v_splats (project_bwd)
+        side.wait_event(ev[0])
+        L.gs_zero_splat_grads(self.opts, self.C, self.n_items, self.v_splats, side)
+        self.project(*params, stream=stream)
+        self.isect(stream)
+        if self.tile_order is not None:
+            ev[1].record(cur)             # tile_offsets written
+            side.wait_event(ev[1])
+            L.gs_tile_order(self.opts, self.C, self.W, self.H, self.tile_offsets, self.tile_order, side)
+        ev[2].record(side)
+        self.rasterize_fwd(backgrounds, stream)
+        cur.wait_event(ev[2])
+        self.rasterize_bwd(v_rgb, v_alpha, backgrounds, v_depth, stream, prepped=True)
+
     def step(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, stream=None):
         """One pass of the whole hot path (forward + backward) over one batch of views.
         params = (means, quats, scales, opacities, colors, viewmats, Ks)."""
-        self.forward(*params, backgrounds=backgrounds, stream=stream)
-        self.backward(*params, v_rgb, v_alpha, backgrounds, v_depth, stream)
+        self.head(params, v_rgb, v_alpha, backgrounds, v_depth, stream)
+        self.project_bwd(*params, stream=stream)
 
     def capture(self, params, v_rgb, v_alpha=None, backgrounds=None, v_depth=None, head_only=False):
         """Record one step() on these exact tensors into a CUDA graph (the capacities must
@@ -229,8 +266,7 @@ class Engine:
         interleaved with their all-reduces)."""
         def body():
             if head_only:
-                self.forward(*params, backgrounds=backgrounds)
-                self.rasterize_bwd(v_rgb, v_alpha, backgrounds, v_depth)
+                self.head(params, v_rgb, v_alpha, backgrounds, v_depth)
             else:
                 self.step(params, v_rgb, v_alpha, backgrounds, v_depth)
         self.graph = torch.cuda.CUDAGraph()

@@ -51,7 +51,7 @@ def test_defaults_match_oracle_constants(L):
 
 def test_status_strings_and_version(L):
     lib = L.lib()
-    assert lib.gs_abi_version() == 10
+    assert lib.gs_abi_version() == 11
     assert lib.gs_status_string(0) == b"ok"
     assert lib.gs_status_string(2) == b"unsupported"
 
@@ -96,6 +96,15 @@ def test_validation_before_device_work(L):
                                     *([P] * 5), null) == 1
     # misaligned workspace
     assert lib.gs_isect_tiles(ct.byref(o), 1, 0, 64, 64, null, null, 0, 8, 8, null, null, 8, 1, 0, null) == 1
+    # scheduling entry points: NULL buffers, bad dimensions, a bwd_zero_fill flag outside {0, 1}
+    assert lib.gs_tile_order(ct.byref(o), 1, 64, 64, null, P, null) == 1
+    assert lib.gs_tile_order(ct.byref(o), 0, 64, 64, P, P, null) == 1
+    assert lib.gs_zero_splat_grads(ct.byref(o), 1, 10, null, null) == 1
+    assert lib.gs_zero_splat_grads(ct.byref(o), 1, 10, P + 4, null) == 1   # misaligned
+    oz = L.options()
+    oz.bwd_zero_fill = 2
+    assert lib.gs_zero_splat_grads(ct.byref(oz), 1, 0, null, null) == 1
+    assert L.options().bwd_zero_fill == 1 and L.options(bwd_zero_fill=False).bwd_zero_fill == 0
 
 
 def test_workspace_size_monotone(L):

@@ -677,14 +677,15 @@ def test_bbox_mode1_square_box(name):
 
 def test_tile_order_is_a_permutation_and_output_invariant():
     """gs_tile_order: a permutation of the bins, camera by camera, each camera's tiles in
-    non-increasing length bucket; gs_rasterize_bwd launched in that order gives the natural
-    order's gradients up to fp32 atomic order (same-kernel bound)."""
+    non-increasing length bucket; gs_rasterize_bwd launched in that order, with the record
+    gradients zero-filled on the side stream (bwd_zero_fill = 0), gives the natural order's
+    in-call zero-fill gradients up to fp32 atomic order (same-kernel bound)."""
     import torch
     sc = S.mipnerf_like_scene(20000, width=320, height=200, views=2, sh_degree=3, seed=11)
     C, N, W, H = 2, 20000, 320, 200
     v_img, _ = S.image_grads(0, C, H, W, l1_scale=False)
-    ordered = U.run_gpu(sc, v_img=v_img)             # Engine default: tile order on
-    natural = U.run_gpu(sc, v_img=v_img, tile_order=False)
+    ordered = U.run_gpu(sc, v_img=v_img)             # Engine default: tile order + side-stream prep on
+    natural = U.run_gpu(sc, v_img=v_img, tile_order=False, overlap_prep=False)
     eng = ordered["engine"]
     TT = eng.TX * eng.TY
     order = eng.tile_order.cpu().numpy()
