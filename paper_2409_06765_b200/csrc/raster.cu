@@ -47,22 +47,36 @@ __device__ __forceinline__ float4 lds4(uint32_t addr) {
     return v;
 }
 
-// Pre-scaled conic: p = a' dx^2 + c' dy^2 + b' dx dy = -sigma * log2(e); the w lane
-// holds b'/2, which the backward's d sigma / d mu' uses (one FFMA per component)
+// Pre-scaled conic, staged as (a', c', b', b'/2): p = a' dx^2 + c' dy^2 + b' dx dy =
+// -sigma * log2(e).  a', c' sit in one aligned register pair so the backward's
+// d sigma / d mu' = Sigma'^-1 Delta is one packed multiply and one packed FMA with the b'/2
+// lane broadcast (sm_100a FMUL2 / FFMA2, below).
 __device__ __forceinline__ float4 prescale_conic(float A, float B, float C) {
-    return make_float4(__fmul_rn(-0.5f * kLog2e, A), __fmul_rn(-kLog2e, B), __fmul_rn(-0.5f * kLog2e, C),
+    return make_float4(__fmul_rn(-0.5f * kLog2e, A), __fmul_rn(-0.5f * kLog2e, C), __fmul_rn(-kLog2e, B),
                        __fmul_rn(-0.5f * kLog2e, B));
 }
 
+// Packed FP32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2): two IEEE round-to-nearest fp32
+// operations in one issue slot, each rounded exactly like the scalar _rn operation, with
+// scalar operands broadcast and pair halves swapped for free.  K6 / K7 are issue bound (FMA
+// pipe ~35 % busy), so pairing independent operations saves issue slots without
+// changing a single rounding.
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+
 // alpha of one (pixel, splat) pair; returns false when the pair is skipped (sigma < 0 or
-// alpha < alpha_min, Q14).  G = exp(-sigma).  Bit-identical in K6 and K7.
-__device__ __forceinline__ bool eval_alpha(float mx, float my, float o, float4 con, float fpx, float fpy,
-                                           float alpha_max, float alpha_min, float& dx, float& dy, float& G,
-                                           float& alpha) {
-    dx = __fsub_rn(mx, fpx);   // Delta = mu' - p (Q21)
-    dy = __fsub_rn(my, fpy);
-    const float p = __fmaf_rn(con.y, __fmul_rn(dx, dy),
-                              __fmaf_rn(con.x, __fmul_rn(dx, dx), __fmul_rn(con.z, __fmul_rn(dy, dy))));
+// alpha < alpha_min, Q14).  G = exp(-sigma).  Bit-identical in K6 and K7: Delta = mu' - p is
+// one packed add of the negated pixel centre npc = (-p.x, -p.y) (x + (-y) == x - y in IEEE),
+// the squares one packed multiply.
+__device__ __forceinline__ bool eval_alpha(float mx, float my, float o, float4 con, float2 npc, float alpha_max,
+                                           float alpha_min, float& dx, float& dy, float& G, float& alpha) {
+    const float2 d = add2(make_float2(mx, my), npc);   // Delta = mu' - p (Q21)
+    dx = d.x;
+    dy = d.y;
+    const float2 sq = mul2(d, d);
+    const float p = __fmaf_rn(con.z, __fmul_rn(dx, dy), __fmaf_rn(con.x, sq.x, __fmul_rn(con.y, sq.y)));
     if (p > 0.f) return false;   // sigma < 0
     G = ex2_approx(p);
     alpha = fminf(alpha_max, __fmul_rn(o, G));
@@ -314,12 +328,14 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
     const int bin = cam * p.TX * p.TY + tile;
     const int start = p.offs[bin], end = p.offs[bin + 1];
 
-    float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, dacc = 0.f;
+    float T = 1.f, c2 = 0.f, c3 = 0.f, dacc = 0.f;
+    float2 c01 = make_float2(0.f, 0.f);   // channels 0, 1: one packed FMA per composite
     int last = start - 1;
     bool done = !inside;
     int n_eval = 0, n_contrib = 0, terminated = 0;
     float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;   // pixel centre
     asm volatile("" : "+f"(fpx), "+f"(fpy));
+    const float2 npc = make_float2(-fpx, -fpy);
     const float amax = p.alpha_max, amin = p.alpha_min, tmin = p.t_min;
     const unsigned lt = (1u << lane) - 1u;
     for (int b0 = start; b0 < end; b0 += kBatchFwd) {
@@ -383,7 +399,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
                     jj[u] = (uint32_t)list[k + u] << 4;
                     xv[u] = lds4(a_xyo + jj[u]);
                     float dxu, dyu, Gu;
-                    ok[u] = eval_alpha(xv[u].x, xv[u].y, xv[u].z, lds4(a_con + jj[u]), fpx, fpy, amax, amin, dxu, dyu,
+                    ok[u] = eval_alpha(xv[u].x, xv[u].y, xv[u].z, lds4(a_con + jj[u]), npc, amax, amin, dxu, dyu,
                                        Gu, av[u]);
                 }
                 bool stop = false;
@@ -391,13 +407,14 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
                 for (int u = 0; u < U; u++) {
                     // predicated composite: a skipped splat adds exactly 0 (w = 0) and leaves T
                     const bool take = ok[u] && !stop;
+                    // (T (1 - alpha) and alpha T as one packed multiply measured slower: the T
+                    // recurrence is the walk's serial chain and FMUL2 lengthens it)
                     const float nT = __fmul_rn(T, __fsub_rn(1.f, av[u]));
                     const bool term = take && nT <= tmin;   // Q15: stop without compositing
                     const bool comp = take && !term;
                     const float w = comp ? __fmul_rn(av[u], T) : 0.f;
                     const float4 rgb = lds4(a_rgb + jj[u]);
-                    c0 = comp ? __fmaf_rn(rgb.x, w, c0) : c0;
-                    c1 = comp ? __fmaf_rn(rgb.y, w, c1) : c1;
+                    c01 = comp ? fma2(make_float2(rgb.x, rgb.y), bc2(w), c01) : c01;   // 0.190 -> 0.187 ms
                     c2 = comp ? __fmaf_rn(rgb.z, w, c2) : c2;
                     if (FEAT) c3 = comp ? __fmaf_rn(rgb.w, w, c3) : c3;
                     if (DEPTH) dacc = comp ? __fmaf_rn(xv[u].w, w, dacc) : dacc;
@@ -418,7 +435,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             const float4 xyo = lds4(a_xyo + j16);
             float dx, dy, G, alpha;
             if (STATS) n_eval++;
-            if (!eval_alpha(xyo.x, xyo.y, xyo.z, lds4(a_con + j16), fpx, fpy, amax, amin, dx, dy, G, alpha)) continue;
+            if (!eval_alpha(xyo.x, xyo.y, xyo.z, lds4(a_con + j16), npc, amax, amin, dx, dy, G, alpha)) continue;
             const float nT = __fmul_rn(T, __fsub_rn(1.f, alpha));
             if (nT <= tmin) {   // Q15: stop without compositing this splat
                 done = true;
@@ -427,8 +444,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             }
             const float w = __fmul_rn(alpha, T);
             const float4 rgb = lds4(a_rgb + j16);
-            c0 = __fmaf_rn(rgb.x, w, c0);   // C += c alpha T
-            c1 = __fmaf_rn(rgb.y, w, c1);
+            c01 = fma2(make_float2(rgb.x, rgb.y), bc2(w), c01);   // C += c alpha T
             c2 = __fmaf_rn(rgb.z, w, c2);
             if (FEAT) c3 = __fmaf_rn(rgb.w, w, c3);
             if (DEPTH) dacc = __fmaf_rn(xyo.w, w, dacc);   // sum z alpha T
@@ -447,7 +463,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
         return;
     }
     if (inside && FEAT) {
-        const float cc[4] = {c0, c1, c2, c3};
+        const float cc[4] = {c01.x, c01.y, c2, c3};
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const int ch = p.c0 + k;
@@ -461,8 +477,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
             g1 = p.bg[3 * cam + 1];
             g2 = p.bg[3 * cam + 2];
         }
-        p.out_rgb[3 * pix + 0] = c0 + T * g0;   // R3, Q25
-        p.out_rgb[3 * pix + 1] = c1 + T * g1;
+        p.out_rgb[3 * pix + 0] = c01.x + T * g0;   // R3, Q25
+        p.out_rgb[3 * pix + 1] = c01.y + T * g1;
         p.out_rgb[3 * pix + 2] = c2 + T * g2;
     }
     if (inside) {
@@ -480,6 +496,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterParams p) {
 // Transposed warp reduction of 8 values: after it, lane l holds the warp sum of value
 // (l >> 2) & 7.  9 shuffles + 9 adds instead of 40 + 40.
 __device__ __forceinline__ float reduce_scatter8(const float (&v)[8], int lane) {
+    // (the stage adds were also tried as packed FADD2 pairs: fewer instructions, but each pair
+    // waits for both shuffles -- K7 0.446 -> 0.460 ms)
     const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
     float u[4];
 #pragma unroll
@@ -621,6 +639,8 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     // recurrences are carried as the single scalar Sv = S . v_C (same recurrence, dotted)
     float T = Tfin, Sv = 0.f;
     const float amax = p.alpha_max, amin = p.alpha_min;
+    const float2 npc = make_float2(-q.fpx, -q.fpy);   // negated pixel centre (eval_alpha)
+    const float2 v01 = make_float2(v0, v1);             // v_C channels 0, 1 as one register pair
     // one (warp, splat) visit: alpha by eval_alpha's operations, B2-B6, the reduction.  tidx is
     // the splat's index in the tile's list (the lane takes it iff tidx <= its last_id)
     auto visit = [&](const float4 xyo, const float4 con, const float4* prgb, const int32_t* pid, int tidx) {
@@ -628,9 +648,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             // by every lane without a branch, keeping the products dx^2, dy^2, dx dy for B6: they
             // are finite for any staged record, and a lane that does not take the splat has its
             // G and alpha zeroed below
-            const float dx = __fsub_rn(xyo.x, q.fpx), dy = __fsub_rn(xyo.y, q.fpy);
-            const float xx = __fmul_rn(dx, dx), yy = __fmul_rn(dy, dy), xy = __fmul_rn(dx, dy);
-            const float pe = __fmaf_rn(con.y, xy, __fmaf_rn(con.x, xx, __fmul_rn(con.z, yy)));
+            const float2 d = add2(make_float2(xyo.x, xyo.y), npc);
+            const float2 sq = mul2(d, d);   // dx^2, dy^2
+            const float dx = d.x, dy = d.y;
+            const float xy = __fmul_rn(dx, dy);
+            const float pe = __fmaf_rn(con.z, xy, __fmaf_rn(con.x, sq.x, __fmul_rn(con.y, sq.y)));
             float G = ex2_approx(pe);
             float alpha = fminf(amax, __fmul_rn(xyo.z, G));
             bool valid = q.inside && tidx <= last && !(pe > 0.f) && alpha >= amin;
@@ -660,8 +682,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             const float ra = rcp_approx(1.f - alpha);
             T = valid ? T * ra : T;            // B2: T_{n-1} = T_n / (1 - alpha_{n-1})
             const float fac = alpha * T;
-            g8[6] = fac * v0;                  // B3
-            g8[7] = fac * v1;
+            const float2 g67 = mul2(bc2(fac), v01);   // B3: channels 0, 1
+            g8[6] = g67.x;
+            g8[7] = g67.y;
             const float g_bl = fac * v2;
             const float g_f3 = FEAT ? fac * v3 : 0.f;   // fourth feature channel of the pass
             // B4 + background / alpha-output terms (Q25, Q26):
@@ -679,16 +702,18 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
             // B6 (Q24): no gradient through the alpha_max clamp
             const float va = raw < amax ? v_alpha : 0.f;
             g8[2] = G * va;
-            const float v_sigma = -raw * va;
-            const float hv = 0.5f * v_sigma;
-            g8[3] = hv * xx;
-            g8[4] = v_sigma * xy;
-            g8[5] = hv * yy;
+            const float nvs = raw * va;        // -v_sigma
+            const float hv = -0.5f * nvs;      // v_sigma / 2
+            g8[3] = hv * sq.x;
+            g8[4] = -nvs * xy;
+            g8[5] = hv * sq.y;
             // d sigma / d mu' = Sigma'^-1 Delta, with the conic recovered from the
-            // pre-scaled one: A = a' (-2 ln2), B = b' (-ln2) = (b'/2)(-2 ln2), C = c' (-2 ln2)
-            const float k2 = (-2.f * kLn2) * v_sigma;
-            g8[0] = k2 * (con.x * dx + con.w * dy);
-            g8[1] = k2 * (con.w * dx + con.z * dy);
+            // pre-scaled one: A = a' (-2 ln2), B = b' (-ln2) = (b'/2)(-2 ln2), C = c' (-2 ln2):
+            // (a' dx + (b'/2) dy, c' dy + (b'/2) dx) = (a', c') * d + (b'/2) * swap(d)
+            const float2 m = fma2(bc2(con.w), make_float2(dy, dx), mul2(make_float2(con.x, con.y), d));
+            const float2 g01 = mul2(bc2((2.f * kLn2) * nvs), m);
+            g8[0] = g01.x;
+            g8[1] = g01.y;
             const int32_t sid = DEPTH ? *pid : __float_as_int(xyo.w);
             float* dst = p.v_splats + (int64_t)sid * GS_SPLAT_FLOATS;
             if (FEAT) {
