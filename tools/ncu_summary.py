@@ -50,6 +50,8 @@ def launches(path):
           if len(r) > vi and r[mi] == "gpu__time_duration.sum"]
     starts = [j for j, k in enumerate(ks) if "k_project_fwd" in k[1]]
     st = starts[-1]
+    if st > 0 and "k_zero4" in ks[st - 1][1]:   # the side-stream zero-fill forked at the step start
+        st -= 1
     end = next(j for j in range(st, len(ks)) if "k_project_bwd" in ks[j][1])
     step = ks[st:end + 1]
     tot = sum(v for _, _, v in step)
