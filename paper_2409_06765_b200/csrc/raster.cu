@@ -17,9 +17,10 @@
 // per-pair exponent is two FMAs and one MUFU.EX2.  Forward and backward evaluate alpha with
 // the same _rn operations (K7 inlines eval_alpha's sequence), so the backward's skip
 // decisions replay the forward's bit for bit.  Independent fp32 pairs run as sm_100a packed
-// FP32x2 instructions (FADD2 / FMUL2 / FFMA2: one issue slot, identical roundings).  The backward reduces each splat's gradient values
-// across the warp with a transposed (reduce-scatter) shuffle tree -- 9 shuffles for 8
-// values instead of 40 -- and lanes holding distinct values issue one fp32 reduction each.
+// FP32x2 instructions (FADD2 / FMUL2 / FFMA2: one issue slot, identical roundings).  The
+// backward reduces each splat's gradient values across the warp with a transposed
+// (reduce-scatter) shuffle tree -- 9 shuffles for 8 values instead of 40 -- and lanes holding
+// distinct values issue one fp32 reduction each.
 #include <type_traits>
 
 #include "gs_internal.cuh"
@@ -577,11 +578,8 @@ __device__ unsigned long long g_k7_stats[8];
 #define K7_STAT(i, v) do { } while (0)
 #endif
 
-#ifndef GS_K7_MINB
-#define GS_K7_MINB 1
-#endif
 template <bool ABSGRAD, bool DEPTH, bool FEAT>
-__global__ void __launch_bounds__(kThreads, GS_K7_MINB) k_raster_bwd(RasterParams p) {
+__global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
     pdl_trigger();
     pdl_wait();
     __shared__ Stage<kBatchBwd> s;
@@ -794,19 +792,7 @@ __global__ void __launch_bounds__(kThreads, GS_K7_MINB) k_raster_bwd(RasterParam
         __syncthreads();
         if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
         const int cnt = build_warp_list(s, n, q.warp, lane, wlast - bstart);
-        int k = cnt - 1;
-#ifndef GS_K7_U2
-#define GS_K7_U2 0
-#endif
-#if GS_K7_U2
-        for (; k >= 1; k -= 2) {
-            const int j0 = s.list[q.warp][k], j1 = s.list[q.warp][k - 1];
-            const float4 xa = s.xyo[j0], ca = s.con[j0], xb = s.xyo[j1], cb = s.con[j1];
-            visit(xa, ca, &s.rgb[j0], &s.id[j0], bstart + j0);
-            visit(xb, cb, &s.rgb[j1], &s.id[j1], bstart + j1);
-        }
-#endif
-        for (; k >= 0; k--) {
+        for (int k = cnt - 1; k >= 0; k--) {
             const int j = s.list[q.warp][k];
             visit(s.xyo[j], s.con[j], &s.rgb[j], &s.id[j], bstart + j);
         }
