@@ -24,8 +24,8 @@
  *    with the tile"), which is part of the method's definition.
  *
  * Parity status of each function is stated in DESIGN.md section "Oracle pins".
- * Parity unpinned: the SH basis signs (Q22) -- only magnitudes are pinned by the
- * orthonormality quadrature test.
+ * The SH basis (Q22) is pinned, signs included, to the real spherical harmonics built
+ * from scipy's complex Y_l^m with the Condon-Shortley phase (tests/test_oracle_pins.py).
  */
 #include <math.h>
 #include <stdint.h>

@@ -290,6 +290,25 @@ class TestSH:
                 G += np.outer(Y, Y) * wt * (2 * math.pi / nphi)
         assert np.allclose(G, np.eye(16), atol=1e-12)
 
+    def test_signs_real_sh_condon_shortley(self, oracle_lib):
+        """Q22 pinned to a library routine: the 16 basis functions (signs included) are the
+        real spherical harmonics built from scipy's complex Y_l^m (Condon-Shortley phase
+        included) as sqrt(2) Im Y_l^|m| (m < 0), Y_l^0, sqrt(2) Re Y_l^m (m > 0), index
+        l^2 + l + m -- the convention whose degree-1 terms are (-C1 y, C1 z, -C1 x)."""
+        from scipy.special import sph_harm_y
+        rng = np.random.default_rng(22)
+        for _ in range(200):
+            d = rng.normal(size=3)
+            d /= np.linalg.norm(d)
+            theta, phi = math.acos(d[2]), math.atan2(d[1], d[0])
+            ref = np.zeros(16)
+            for l in range(4):
+                for m in range(-l, l + 1):
+                    y = sph_harm_y(l, abs(m), theta, phi)
+                    ref[l * l + l + m] = (math.sqrt(2) * y.imag if m < 0 else
+                                          (y.real if m == 0 else math.sqrt(2) * y.real))
+            assert np.allclose(oracle.sh_basis(3, d), ref, rtol=0, atol=1e-12)
+
     def test_degree0_colour(self, oracle_lib):
         """S:148-149: colour = 0.5 + 0.2820948 * dc."""
         sc = S.tiny_scene(3, N=10, sh_degree=0)
