@@ -703,3 +703,53 @@ def test_tile_order_is_a_permutation_and_output_invariant():
     rep = {k: natural[k] for k in U.GRAD_KEYS}
     U.assert_same_kernel_grads(sc, o, b, rep, ordered, label="tile-order", vs_one=natural["v_splats"],
                                vs_other=ordered["v_splats"])
+
+
+# seeded sweep: shapes, SH degrees 0-3 (1 and 2 appear nowhere else), classic / antialiased,
+# backgrounds and the alpha-output gradient, both scene generators -- every stage's full
+# contract (bit-exact keys, order, ranges, radii, mu', depth; images; every gradient element)
+def _sweep_cases():
+    rng = np.random.default_rng(2409)
+    cases = []
+    for i in range(32):
+        mip = i % 3 == 2
+        sh = int(rng.integers(0, 4))
+        small = i % 8 == 7   # images of one or two partial tiles
+        cases.append(dict(seed=100 + i, mip=mip, N=int(rng.integers(3000, 12000)) if mip else int(rng.integers(50, 2500)),
+                          W=int(rng.integers(5, 33)) if small else int(rng.integers(40, 260)),
+                          H=int(rng.integers(5, 33)) if small else int(rng.integers(30, 200)),
+                          views=int(rng.integers(1, 6)),
+                          sh=sh if i != 0 else 1, aa=int(rng.integers(0, 2)), bg=bool(rng.integers(0, 2))))
+    cases[1]["sh"] = 2
+    return cases
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"s{c['seed']}")
+def test_seeded_sweep_full_contract(case):
+    c = case
+    if c["mip"]:
+        sc = S.mipnerf_like_scene(c["N"], width=c["W"], height=c["H"], views=c["views"], sh_degree=c["sh"],
+                                  seed=c["seed"])
+    else:
+        sc = S.tiny_scene(c["seed"], N=c["N"], width=c["W"], height=c["H"], sh_degree=c["sh"], views=c["views"])
+    C, W, H = sc["viewmats"].shape[0], sc["width"], sc["height"]
+    v_img, v_a = S.image_grads(c["seed"], C, H, W, l1_scale=False, with_alpha=c["bg"])
+    bgs = np.random.default_rng(c["seed"]).uniform(0, 1, (C, 3)).astype(np.float32) if c["bg"] else None
+    o = oracle.Options(sh_degree=sc["sh_degree"], antialiased=c["aa"])
+    gpu = U.run_gpu(sc, antialiased=c["aa"], v_img=v_img, v_alpha=v_a, backgrounds=bgs)
+    ref = U.oracle_reference(sc, o, gpu, v_img, v_a, bgs)
+    p = ref["proj"]
+    assert np.array_equal(gpu["radii"], p["radii"])
+    vis = p["radii"][..., 0] > 0
+    sp = gpu["splats"]
+    assert np.array_equal(sp[..., 0:2][vis], p["mean2d_f"][vis])
+    assert np.array_equal(sp[..., 3][vis], p["depth_f"][vis])
+    np.testing.assert_allclose(sp[..., 8:11][vis], p["rgb"][vis], rtol=1e-5, atol=1e-5)
+    assert gpu["M"] == len(ref["keys"])
+    assert np.array_equal(gpu["keys"], ref["keys"])
+    assert np.array_equal(gpu["ids"], ref["ids"])
+    assert np.array_equal(gpu["offsets"], ref["offsets"])
+    U.assert_images(gpu, ref, label=f"sweep{c['seed']}")
+    a = ref["amb"]
+    assert a["ambiguous"] <= 1e-3 * a["pixels"] + 1, U.amb_report(ref)
+    U.assert_grads(sc, gpu, ref, label=f"sweep{c['seed']}")
