@@ -559,9 +559,11 @@ __device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
 }
 
 #ifndef GS_FEW_LANES
-#define GS_FEW_LANES 16
+#define GS_FEW_LANES 12
 #endif
-constexpr int kFewLanes = GS_FEW_LANES;  // <= this many contributing lanes: per-lane vector reductions (measured optimum)
+// <= this many contributing lanes: per-lane vector reductions (measured optimum; 16 before the
+// packed FP32x2 gradient block, 11-14 after it: DESIGN.md)
+constexpr int kFewLanes = GS_FEW_LANES;
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
