@@ -234,7 +234,7 @@ __device__ __forceinline__ unsigned warp_peers(unsigned d) {
 
 template <int IT>
 __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
-                                                   int shift, int* hist, int nb_max) {
+                                                   int shift, unsigned mask, int* hist, int nb_max) {
     pdl_trigger();
     pdl_wait();
     __shared__ int s_hist[256];
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ 
 #pragma unroll
     for (int k = 0; k < IT; k++) {
         const int i = base + k * kT + threadIdx.x;
-        const unsigned d = i < n ? (key[k] >> shift) & 255u : 256u;
+        const unsigned d = i < n ? (key[k] >> shift) & mask : 256u;
         if (d < 256u) atomicAdd(&s_hist[d], 1);
     }
     __syncthreads();
@@ -300,8 +300,8 @@ template <int IT>
 __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict__ keys_in,
                                                       const int32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
                                                       int32_t* __restrict__ vals_out, const int* d_n, int64_t cap,
-                                                      int shift, const int* __restrict__ hist, int nb_max,
-                                                      const int* __restrict__ rowtot) {
+                                                      int shift, unsigned mask, const int* __restrict__ hist,
+                                                      int nb_max, const int* __restrict__ rowtot) {
     pdl_trigger();
     pdl_wait();
     __shared__ int s_cnt[kWarps][256];    // per-warp running digit counts, then per-warp offsets
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
 #pragma unroll
     for (int k = 0; k < IT; k++) {
         const bool valid = base + k * 32 + lane < n;
-        const unsigned d = valid ? (key[k] >> shift) & 255u : 256u;
+        const unsigned d = valid ? (key[k] >> shift) & mask : 256u;
 #if GS_SCATTER_MATCH
         const unsigned peers = __match_any_sync(0xffffffffu, d);
 #else
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
 #pragma unroll
     for (int k = 0; k < IT; k++) {
         if (rank[k] >= 0) {
-            const unsigned d = (key[k] >> shift) & 255u;
+            const unsigned d = (key[k] >> shift) & mask;
             const int p = s_dstart[d] + s_cnt[warp][d] + rank[k];
             s_k[p] = key[k];
             s_v[p] = val[k];
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
         const int j = k * kT + threadIdx.x;
         if (j < nloc) {
             const uint32_t kk = s_k[j];
-            const unsigned d = (kk >> shift) & 255u;
+            const unsigned d = (kk >> shift) & mask;
             const int pos = s_goff[d] + (j - s_dstart[d]);
             keys_out[pos] = kk;
             vals_out[pos] = s_v[j];
@@ -599,15 +599,21 @@ constexpr int64_t kBigSort = 1 << 22;
 template <int IT>
 KV radix_sort_t(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
                 int nb_max, cudaStream_t s) {
+    // ceil(bits / 8) passes of (nearly) equal digit width <= 8: e.g. a 13-bit tile key is sorted
+    // as 7 + 6 bits rather than 8 + 5 (fewer digits per pass: longer runs in the scatter's
+    // coalesced write-out)
     const int passes = bits <= 0 ? 0 : div_up(bits, 8);
+    const int width = passes > 0 ? div_up(bits, passes) : 8;   // 13-bit keys: stage 2 0.197 -> 0.195 ms
     const int nb = div_up(cap > 0 ? cap : 1, kT * IT);   // <= nb_max (sized for 1024-key blocks)
     KV in = a, out = b;
     for (int p = 0; p < passes; p++) {
         int32_t* vdst = (p == passes - 1 && final_vals) ? final_vals : out.v;
-        launch_pdl(k_radix_hist<IT>, dim3(nb), dim3(kT), s, in.k, d_n, cap, 8 * p, hist, nb_max);
+        const int shift = width * p;
+        const unsigned mask = (1u << min(width, bits - shift)) - 1u;
+        launch_pdl(k_radix_hist<IT>, dim3(nb), dim3(kT), s, in.k, d_n, cap, shift, mask, hist, nb_max);
         launch_pdl(k_radix_scan_rows<IT>, dim3(256), dim3(kT), s, hist, nb_max, d_n, cap, rowtot);
-        launch_pdl(k_radix_scatter<IT>, dim3(nb), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, 8 * p, hist, nb_max,
-                   rowtot);
+        launch_pdl(k_radix_scatter<IT>, dim3(nb), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, shift, mask, hist,
+                   nb_max, rowtot);
         KV next_in{out.k, vdst};
         out = in;
         in = next_in;
