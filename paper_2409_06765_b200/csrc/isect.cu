@@ -591,10 +591,16 @@ struct KV {
 // ceil(bits/8) stable 8-bit LSD passes over `a` (live count *d_n <= cap), ping-ponging with
 // `b`.  The last pass writes its values to `final_vals` when given.  Returns the buffers
 // holding the sorted result.
-// Keys per block: 1024 below kBigSort keys (enough blocks to fill 148 SMs at 0.6-3 M keys),
-// 2048 above (half the blocks and histogram rows; measured at 14-45 M keys: configs[2]
-// isect 3.69 -> 2.94 ms; 4096 was slower at both sizes).
-constexpr int64_t kBigSort = 1 << 22;
+// Keys per block (by the sort's capacity): 1024 below kBigSort keys, 2048 above (half the
+// blocks and histogram rows; measured at 14-45 M keys: configs[2] isect 3.69 -> 2.94 ms;
+// 4096 was slower at both sizes).  The threshold was 4 M until the shared-memory-atomic
+// histograms and equal-width digits; re-swept after them (1, 2, 4 M): configs[1]'s 4 M-capacity
+// tile sort is faster with 2048-key blocks (stage 2 0.195 -> 0.187 ms), the 1 M-item depth sort
+// gains nothing from them.
+#ifndef GS_BIG_SORT_LOG2
+#define GS_BIG_SORT_LOG2 21
+#endif
+constexpr int64_t kBigSort = 1LL << GS_BIG_SORT_LOG2;
 
 template <int IT>
 KV radix_sort_t(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, int bits, int* hist, int* rowtot,
