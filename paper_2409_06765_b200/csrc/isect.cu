@@ -232,7 +232,10 @@ __device__ __forceinline__ unsigned warp_peers(unsigned d) {
     return peers;
 }
 
-template <int IT>
+// digit mask: the compile-time 255 for full 8-bit digits (a runtime mask there cost 8 % of stage
+// 2 at configs[2], measured), the runtime one only for the narrower digits of equal-width splits
+#define GS_DMASK (NARROW ? mask : 255u)
+template <int IT, bool NARROW>
 __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ keys, const int* d_n, int64_t cap,
                                                    int shift, unsigned mask, int* hist, int nb_max) {
     pdl_trigger();
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(kT) k_radix_hist(const uint32_t* __restrict__ 
 #pragma unroll
     for (int k = 0; k < IT; k++) {
         const int i = base + k * kT + threadIdx.x;
-        const unsigned d = i < n ? (key[k] >> shift) & mask : 256u;
+        const unsigned d = i < n ? (key[k] >> shift) & GS_DMASK : 256u;
         if (d < 256u) atomicAdd(&s_hist[d], 1);
     }
     __syncthreads();
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kT) k_radix_scan_rows(int* hist, int nb_max, c
     if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
 }
 
-template <int IT>
+template <int IT, bool NARROW>
 __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict__ keys_in,
                                                       const int32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
                                                       int32_t* __restrict__ vals_out, const int* d_n, int64_t cap,
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
 #pragma unroll
     for (int k = 0; k < IT; k++) {
         const bool valid = base + k * 32 + lane < n;
-        const unsigned d = valid ? (key[k] >> shift) & mask : 256u;
+        const unsigned d = valid ? (key[k] >> shift) & GS_DMASK : 256u;
 #if GS_SCATTER_MATCH
         const unsigned peers = __match_any_sync(0xffffffffu, d);
 #else
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
 #pragma unroll
     for (int k = 0; k < IT; k++) {
         if (rank[k] >= 0) {
-            const unsigned d = (key[k] >> shift) & mask;
+            const unsigned d = (key[k] >> shift) & GS_DMASK;
             const int p = s_dstart[d] + s_cnt[warp][d] + rank[k];
             s_k[p] = key[k];
             s_v[p] = val[k];
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(kT) k_radix_scatter(const uint32_t* __restrict
         const int j = k * kT + threadIdx.x;
         if (j < nloc) {
             const uint32_t kk = s_k[j];
-            const unsigned d = (kk >> shift) & mask;
+            const unsigned d = (kk >> shift) & GS_DMASK;
             const int pos = s_goff[d] + (j - s_dstart[d]);
             keys_out[pos] = kk;
             vals_out[pos] = s_v[j];
@@ -616,10 +619,15 @@ KV radix_sort_t(KV a, KV b, int32_t* final_vals, const int* d_n, int64_t cap, in
         int32_t* vdst = (p == passes - 1 && final_vals) ? final_vals : out.v;
         const int shift = width * p;
         const unsigned mask = (1u << min(width, bits - shift)) - 1u;
-        launch_pdl(k_radix_hist<IT>, dim3(nb), dim3(kT), s, in.k, d_n, cap, shift, mask, hist, nb_max);
+        if (mask == 255u) launch_pdl(k_radix_hist<IT, false>, dim3(nb), dim3(kT), s, in.k, d_n, cap, shift, mask, hist, nb_max);
+        else launch_pdl(k_radix_hist<IT, true>, dim3(nb), dim3(kT), s, in.k, d_n, cap, shift, mask, hist, nb_max);
         launch_pdl(k_radix_scan_rows<IT>, dim3(256), dim3(kT), s, hist, nb_max, d_n, cap, rowtot);
-        launch_pdl(k_radix_scatter<IT>, dim3(nb), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, shift, mask, hist,
-                   nb_max, rowtot);
+        if (mask == 255u)
+            launch_pdl(k_radix_scatter<IT, false>, dim3(nb), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, shift, mask,
+                       hist, nb_max, rowtot);
+        else
+            launch_pdl(k_radix_scatter<IT, true>, dim3(nb), dim3(kT), s, in.k, in.v, out.k, vdst, d_n, cap, shift, mask,
+                       hist, nb_max, rowtot);
         KV next_in{out.k, vdst};
         out = in;
         in = next_in;
