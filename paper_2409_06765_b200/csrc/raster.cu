@@ -31,7 +31,10 @@ namespace {
 constexpr int kThreads = GS_BLOCK_PIXELS; // one thread per pixel of the 16x16 tile
 constexpr int kWarps = kThreads / 32;
 constexpr int kBatchFwd = 512;            // splats per staged batch: forward (2 per thread) ...
-constexpr int kBatchBwd = 256;            // ... backward (1 per thread; keeps its registers at 48)
+#ifndef GS_K7_BATCH
+#define GS_K7_BATCH 256
+#endif
+constexpr int kBatchBwd = GS_K7_BATCH;            // ... backward (1 per thread; keeps its registers at 48)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -789,7 +792,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterParams p) {
         const int bstart = max(start, bend - kBatchBwd);
         const int n = bend - bstart;
         __syncthreads();
-        static_assert(kBatchBwd == kThreads, "one staged splat per thread");
+        static_assert(kBatchBwd <= kThreads, "at most one staged splat per thread");
         if ((int)threadIdx.x < n) stage_splat<FEAT, !DEPTH>(p, s, threadIdx.x, bstart + threadIdx.x, q.x0, q.y0, cam);
         __syncthreads();
         if (wlast < bstart) continue;   // warp-uniform: nothing this warp composited here
